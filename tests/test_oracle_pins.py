@@ -1,0 +1,596 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+SURVEY.md §8c "What pins each part" P1-P18.  None of these tests retypes an
+oracle formula: each checks a closed form, a value printed in the paper
+(tests/golden/, cited), an invariant, a textbook special case, or a brute force.
+All run on CPU (-m "not gpu").
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sl
+import scipy.sparse as sp
+import scipy.sparse.linalg as sla
+
+import oracle as O
+from inputs import jump27, poisson7
+from amg_testutil import golden
+
+
+def ocsr(A):
+    return O.OracleCSR.from_inputs(A)
+
+
+# --------------------------------------------------------------- P1 / P2
+@pytest.mark.parametrize("dims,k", [((9, 1, 1), (1, 1, 1)), ((6, 5, 4), (1, 1, 1)),
+                                    ((5, 4, 3), (1.0, 2.0, 0.01))])
+def test_P1_eigenpairs_closed_form(dims, k):
+    """A v = lambda v with v_m = prod_d sin(i_d m_d pi/(N_d+1)),
+    lambda = sum_d k_d (2 - 2 cos(m_d pi/(N_d+1))) (tensor-sum closed form)."""
+    nx, ny, nz = dims
+    A = ocsr(poisson7(nx, ny, nz, k))
+    i = np.arange(nx * ny * nz)
+    x, y, z = i % nx, (i // nx) % ny, i // (nx * ny)
+    for m in [(1, 1, 1), (nx, ny, nz), (max(1, nx // 2), 1, nz)]:
+        v = (np.sin((x + 1) * m[0] * np.pi / (nx + 1)) * np.sin((y + 1) * m[1] * np.pi / (ny + 1))
+             * np.sin((z + 1) * m[2] * np.pi / (nz + 1)))
+        lam = sum(kd * (2 - 2 * np.cos(md * np.pi / (Nd + 1)))
+                  for kd, md, Nd in zip(k, m, dims))
+        Av = O.spmv(A, v)
+        assert np.linalg.norm(Av - lam * v) <= 1e-13 * np.linalg.norm(lam * v)
+
+
+def test_P2_nnz_closed_forms_and_spec_examples():
+    for (nx, ny, nz) in [(16, 16, 16), (7, 3, 5), (1, 1, 1)]:
+        A = poisson7(nx, ny, nz)
+        n = nx * ny * nz
+        edges = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
+        assert A.nnz == n + 2 * edges
+    assert poisson7(16, 16, 16).nnz == 27136
+    for N in (8, 16):
+        assert jump27(N).nnz == (3 * N - 2) ** 3
+    # SPEC.md:127-129
+    A = poisson7(1, 1, 1)
+    assert A.values.tolist() == [6.0]
+    A = poisson7(2, 1, 1).to_scipy().toarray()
+    assert A.tolist() == [[6.0, -1.0], [-1.0, 6.0]]
+    A = poisson7(3, 3, 3).to_scipy().toarray()
+    assert A[13, 13] == 6 and sorted(A[13][A[13] != 0].tolist()) == [-1.0] * 6 + [6.0]
+
+
+def test_spmv_spec_examples():
+    """SPEC.md:48-50."""
+    I3 = O.OracleCSR.from_scipy(sp.identity(3, format="csr"))
+    assert O.spmv(I3, [1.0, 2.0, 3.0]).tolist() == [1.0, 2.0, 3.0]
+    T = O.OracleCSR.from_scipy(sp.diags([-1.0, 2.0, -1.0], [-1, 0, 1], shape=(3, 3)))
+    assert O.spmv(T, np.ones(3)).tolist() == [1.0, 0.0, 1.0]
+
+
+# --------------------------------------------------------------- P3 weights
+def test_P3_weights_closed_form_per_sweep():
+    """Eq. 3.2 hand-derived: level 0 c = 7/6; after x-pairing
+    (diag 5, off -0.5 x / -1 y / -1 z) c = 1.1 / 1.2 / 1.2; after x,y-pairing
+    (diag 4, -0.5/-0.5/-1) c = 1.125 / 1.125 / 1.25."""
+    A = ocsr(poisson7(8, 8, 8))
+    w = np.ones(512)
+    _, _, c = O.edge_weights(A, w)
+    assert np.allclose(c, 7 / 6, rtol=0, atol=1e-15)
+    A1, w1, agg, pv, nc = O.pairwise_sweep(A, w)
+    assert nc == 256
+    A1s = A1.to_scipy()
+    assert np.allclose(A1s.diagonal(), 5.0, atol=1e-14)
+    ei, ej, c = O.edge_weights(A1, w1)
+    # coarse grid after x-pairing is 4 x 8 x 8
+    d = ej - ei
+    assert np.allclose(c[d == 1], 1.1, atol=1e-14)
+    assert np.allclose(c[d == 4], 1.2, atol=1e-14)
+    assert np.allclose(c[d == 32], 1.2, atol=1e-14)
+    assert set(np.unique(d)) == {1, 4, 32}
+    A2, w2, agg2, pv2, nc2 = O.pairwise_sweep(A1, w1)
+    assert nc2 == 128
+    # sweep 2 pairs along y (c_y = c_z = 1.2 tie -> lowest index, R5)
+    assert all(agg2[g] == agg2[g + 4] for g in range(256) if (g // 4) % 8 % 2 == 0)
+    assert np.allclose(A2.to_scipy().diagonal(), 4.0, atol=1e-14)
+    ei, ej, c = O.edge_weights(A2, w2)
+    d = ej - ei  # grid 4 x 4 x 8
+    assert np.allclose(c[d == 1], 1.125, atol=1e-14)
+    assert np.allclose(c[d == 4], 1.125, atol=1e-14)
+    assert np.allclose(c[d == 16], 1.25, atol=1e-14)
+
+
+def test_weight_spec_examples():
+    """interior edge 7/6; a_ij = a_ii = a_jj, w_i = w_j -> c = 0 excluded."""
+    M = O.OracleCSR.from_scipy(sp.csr_matrix(np.array([[1.0, 1.0], [1.0, 1.0]])))
+    _, _, c = O.edge_weights(M, np.ones(2))
+    assert len(c) == 0
+    M = O.OracleCSR.from_scipy(sp.csr_matrix(np.array([[6.0, -1.0], [-1.0, 6.0]])))
+    _, _, c = O.edge_weights(M, np.ones(2))
+    assert c.tolist() == [1.0 + 2.0 / 12.0]
+
+
+# --------------------------------------------------------------- P4 cubes
+def cube_map(nx, ny, nz):
+    i = np.arange(nx * ny * nz)
+    x, y, z = i % nx, (i // nx) % ny, i // (nx * ny)
+    return x // 2 + (nx // 2) * (y // 2 + (ny // 2) * (z // 2))
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16), (8, 12, 6), (32, 32, 32)])
+def test_P4_level0_aggregates_are_2x2x2_cubes(dims):
+    h = O.OracleHierarchy(poisson7(*dims), max_levels=2, max_coarse_size=1)
+    assert np.array_equal(h.agg(0), cube_map(*dims))
+
+
+# --------------------------------------------------------------- P5 / P6 K
+_N16 = 4096
+
+
+def _blocks(np_):
+    q = round(np_ ** (1 / 3))
+    assert q ** 3 == np_
+    bs = 16 // q
+    i = np.arange(_N16)
+    x, y, z = i % 16, (i // 16) % 16, i // 256
+    return (x // bs) + q * ((y // bs) + q * (z // bs))
+
+
+def _smoother(Ad, kind, np_):
+    """HGS / l1-HGS (Eq. 3.4-3.5) block-lower M for the 3D block
+    distribution; within a sub-cube the lexicographic order equals the global one."""
+    b = _blocks(np_)
+    same = b[:, None] == b[None, :]
+    M = np.tril(Ad) * same
+    if kind == "l1":
+        M = M + np.diag((np.abs(Ad) * (~same)).sum(axis=1))
+    return M
+
+
+def _K(Ad, S, SAS, M):
+    """Eq. 3.8: K = 1/lambda_min[(S^T Mbar S)^{-1}(S^T A S)],
+    Mbar = M^T (M^T + M - A)^{-1} M."""
+    Mbar = M.T @ np.linalg.solve(M.T + M - Ad, M)
+    SMS = S.T @ Mbar @ S
+    mu = sla.eigsh(SMS, k=1, M=SAS, which="LA", tol=1e-12)[0][0]
+    return mu  # = 1/lambda_min of the inverse pencil
+
+
+def _two_level(smoothed):
+    h = O.OracleHierarchy(poisson7(16, 16, 16), smooth_prolongator=int(smoothed),
+                          max_levels=2, max_coarse_size=1)
+    Ad = h.A(0).to_scipy().toarray()
+    P = h.P(0).to_scipy().toarray()
+    D = np.diag(np.diag(Ad))
+    R = np.linalg.solve(P.T @ D @ P, P.T @ D)  # R = (P^T D P)^{-1} P^T D
+    assert np.abs(R @ P - np.eye(P.shape[1])).max() < 1e-12
+    S = sl.null_space(R)                        # full-rank S with R S = 0
+    assert S.shape[1] == _N16 - P.shape[1]
+    return h, Ad, S, S.T @ Ad @ S
+
+
+@pytest.fixture(scope="module")
+def unsmoothed16():
+    return _two_level(False)
+
+
+@pytest.fixture(scope="module")
+def smoothed16():
+    return _two_level(True)
+
+
+def _table(name):
+    return {int(r[0]): (r[1], r[2]) for r in golden(name)}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("np_,kind", [(1, "hgs"), (8, "hgs"), (8, "l1"), (512, "hgs"),
+                                      (512, "l1"), (64, "l1")])
+def test_P5_table1_K_unsmoothed(unsmoothed16, np_, kind):
+    h, Ad, S, SAS = unsmoothed16
+    assert h.sizes() == [4096, 512]
+    ref = _table("table1_K_unsmoothed.txt")[np_][0 if kind == "hgs" else 1]
+    K = _K(Ad, S, SAS, _smoother(Ad, kind, np_))
+    assert round(K, 4) == pytest.approx(ref, abs=1e-12)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("np_,kind", [(1, "hgs"), (8, "hgs"), (8, "l1"), (512, "l1")])
+def test_P6_tableSM1_K_smoothed(smoothed16, np_, kind):
+    h, Ad, S, SAS = smoothed16
+    assert h.omega(0) == pytest.approx(2.0 / 3.0, abs=1e-15)  # R3, P18
+    ref = _table("tableSM1_K_smoothed.txt")[np_][0 if kind == "hgs" else 1]
+    K = _K(Ad, S, SAS, _smoother(Ad, kind, np_))
+    assert round(K, 4) == pytest.approx(ref, abs=1e-12)
+
+
+def test_P6_text_omega_does_not_reproduce_tableSM1(smoothed16):
+    """Evidence for reading R3: omega = 1/||D^-1 A|| (text) misses
+    Table SM1's np=1 cell (1.3686) in the 4th digit."""
+    h = O.OracleHierarchy(poisson7(16, 16, 16), prol_omega_scale=1.0, max_levels=2,
+                          max_coarse_size=1)
+    Ad = h.A(0).to_scipy().toarray()
+    P = h.P(0).to_scipy().toarray()
+    D = np.diag(np.diag(Ad))
+    S = sl.null_space(np.linalg.solve(P.T @ D @ P, P.T @ D))
+    K = _K(Ad, S, S.T @ Ad @ S, _smoother(Ad, "hgs", 1))
+    assert abs(K - 1.3686) > 1e-3
+
+
+# --------------------------------------------------------------- P7 Table SM
+@pytest.mark.slow
+@pytest.mark.parametrize("sweeps", [3, 4])
+def test_P7_tableSM_coarsening_80cube(sweeps):
+    row = {int(r[0]): r[1:] for r in golden("tableSM_coarsening.txt")}[sweeps]
+    nl, cr, coarsest = int(row[0]), row[1], int(row[2])
+    h = O.OracleHierarchy(poisson7(80, 80, 80), sweeps_per_level=sweeps, smooth_prolongator=0,
+                          max_coarse_size=200)
+    sizes = h.sizes()
+    assert h.nlevels == nl
+    assert sizes[-1] == coarsest
+    assert round(h.avg_cr, 2) == cr
+    for a, b in zip(sizes, sizes[1:]):
+        assert a / b == 2 ** sweeps
+
+
+# --------------------------------------------------------------- P8 opc
+@pytest.mark.slow
+def test_P8_operator_complexity_smoothed_size8():
+    """opc 'about 1.9' for size-8 smoothed hierarchies; SPEC.md:315
+    band 1.9 +- 0.3; unsmoothed 3-sweep <= 1.25."""
+    A = poisson7(48, 48, 48)
+    h = O.OracleHierarchy(A)
+    assert 1.6 <= h.opc <= 2.2
+    hu = O.OracleHierarchy(A, smooth_prolongator=0)
+    assert hu.opc <= 1.25
+    assert 7.5 <= hu.avg_cr <= 8.0
+
+
+# --------------------------------------------------------------- P9 matching
+def _brute_max_weight(n, edges, wts):
+    best = 0.0
+    m = len(edges)
+
+    def rec(k, used, tot):
+        nonlocal best
+        if tot + sum(wts[k:]) <= best:
+            return
+        if k == m:
+            best = max(best, tot)
+            return
+        i, j = edges[k]
+        if not (used >> i) & 1 and not (used >> j) & 1:
+            rec(k + 1, used | (1 << i) | (1 << j), tot + wts[k])
+        rec(k + 1, used, tot)
+
+    rec(0, 0, 0.0)
+    return best
+
+
+def _ld_pointer_rounds(n, edges, keys):
+    """Independent locally-dominant matching: every free vertex points at its
+    best free neighbour under (key desc, lo asc, hi asc); mutual pointers match."""
+    mate = [-1] * n
+    adj = [[] for _ in range(n)]
+    for (i, j), k in zip(edges, keys):
+        lo, hi = min(i, j), max(i, j)
+        adj[i].append((k, lo, hi, j))
+        adj[j].append((k, lo, hi, i))
+    while True:
+        ptr = [-1] * n
+        for v in range(n):
+            if mate[v] >= 0:
+                continue
+            cand = [(-k, lo, hi, u) for (k, lo, hi, u) in adj[v] if mate[u] < 0]
+            if cand:
+                ptr[v] = min(cand)[3]
+        changed = False
+        for v in range(n):
+            u = ptr[v]
+            if u >= 0 and ptr[u] == v and v < u:
+                mate[v], mate[u] = u, v
+                changed = True
+        if not changed:
+            return mate
+
+
+def test_P9_matching_half_approx_and_locally_dominant():
+    rng = np.random.default_rng(7)
+    for t in range(200):
+        n = int(rng.integers(2, 13))
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+        m = int(rng.integers(0, min(len(pairs), 18) + 1))
+        sel = rng.choice(len(pairs), size=m, replace=False) if m else []
+        edges = [pairs[s] for s in sel]
+        if t % 2:   # tie-heavy
+            c = rng.choice([0.5, 1.1, 7 / 6, 1.2], size=m)
+        else:
+            c = rng.uniform(0.05, 3.0, size=m) * rng.choice([-1, 1], size=m)
+        ei = np.array([e[0] for e in edges], np.int64)
+        ej = np.array([e[1] for e in edges], np.int64)
+        mate = O.greedy_matching(n, ei, ej, np.asarray(c, float))
+        # involution, matched pairs are edges, maximality
+        es = set(edges)
+        for v in range(n):
+            if mate[v] >= 0:
+                assert mate[mate[v]] == v
+                assert (min(v, mate[v]), max(v, mate[v])) in es
+        for (i, j) in edges:
+            assert mate[i] >= 0 or mate[j] >= 0
+        # 1/2-approximation with SPEC's additive weights
+        if m:
+            cmin = np.abs(c).min()
+            wh = np.log(np.abs(c)) - np.log(cmin) + 1.0
+            got = sum(wh[k] for k, (i, j) in enumerate(edges) if mate[i] == j)
+            assert got >= 0.5 * _brute_max_weight(n, edges, list(wh)) - 1e-12
+        # greedy == locally dominant pointer rounds (F7, R5)
+        assert list(mate) == _ld_pointer_rounds(n, edges, list(np.abs(c)))
+
+
+def test_matching_spec_examples():
+    """SPEC.md:202-204, 211-213."""
+    m = O.greedy_matching(3, np.array([0, 1, 0]), np.array([1, 2, 2]), np.array([3.0, 2.0, 1.0]))
+    assert m.tolist() == [1, 0, -1]
+    m = O.greedy_matching(3, np.array([0, 1]), np.array([1, 2]), np.array([1.0, 1.0]))
+    assert m.tolist() == [1, 0, -1]
+    assert O.greedy_matching(4, np.zeros(0, np.int64), np.zeros(0, np.int64),
+                             np.zeros(0)).tolist() == [-1] * 4
+    # 4-cycle {1,2,1,2}: edges (0,1)=1,(1,2)=2,(2,3)=1,(0,3)=2 -> weight 4
+    m = O.greedy_matching(4, np.array([0, 1, 2, 0]), np.array([1, 2, 3, 3]),
+                          np.array([1.0, 2.0, 1.0, 2.0]))
+    assert m.tolist() == [3, 2, 1, 0]
+
+
+# --------------------------------------------------------------- P10
+@pytest.mark.parametrize("case", ["poisson", "aniso", "jump", "random_w"])
+def test_P10_aggregation_invariants(case):
+    if case == "poisson":
+        A, w = poisson7(12, 10, 8), None
+    elif case == "aniso":
+        A, w = poisson7(12, 10, 8, (1, 1, 0.01)), None
+    elif case == "jump":
+        A, w = jump27(16), None
+    else:
+        A = poisson7(10, 10, 10)
+        w = np.random.default_rng(3).uniform(0.2, 2.0, A.n_global)
+    h = O.OracleHierarchy(A, w=w, smooth_prolongator=0, max_coarse_size=20)
+    for l in range(h.nlevels - 1):
+        n, nc = h.level_n(l), h.level_n(l + 1)
+        agg = h.agg(l)
+        assert agg.min() == 0 and agg.max() == nc - 1
+        sizes = np.bincount(agg, minlength=nc)
+        assert sizes.min() >= 1 and sizes.max() <= 2 ** h.sweeps(l)
+        # coarse ids ascending by minimum member (R5)
+        first = np.full(nc, n)
+        np.minimum.at(first, agg, np.arange(n))
+        assert np.all(np.diff(first) > 0)
+        P = h.P(l).to_scipy()
+        assert abs((P.T @ P - sp.identity(nc)).toarray()).max() <= 1e-14
+        wl = h.w(l)
+        assert np.linalg.norm(P @ (P.T @ wl) - wl) <= 1e-13 * np.linalg.norm(wl)
+
+
+def test_pairwise_spec_examples():
+    """pair (1,1) -> 1/sqrt2 each, restricted w sqrt2;
+    singleton w = -2 -> entry -1, restricted value 2."""
+    M = O.OracleCSR.from_scipy(sp.csr_matrix(np.array([[6.0, -1.0], [-1.0, 6.0]])))
+    An, wn, agg, pv, nc = O.pairwise_sweep(M, np.ones(2))
+    assert nc == 1 and pv.tolist() == [1 / math.sqrt(2)] * 2
+    assert wn[0] == pytest.approx(math.sqrt(2), abs=1e-15)
+    M = O.OracleCSR.from_scipy(sp.csr_matrix(np.array([[2.0]])))
+    An, wn, agg, pv, nc = O.pairwise_sweep(M, np.array([-2.0]))
+    assert pv.tolist() == [-1.0] and wn.tolist() == [2.0]
+
+
+# --------------------------------------------------------------- P11 Galerkin
+def test_P11_galerkin_dense_triple_product_symmetry_spd():
+    A = poisson7(8, 8, 8)
+    h = O.OracleHierarchy(A, max_coarse_size=10)
+    for l in range(h.nlevels - 1):
+        Al = h.A(l).to_scipy().toarray()
+        P = h.P(l).to_scipy().toarray()
+        Ac = h.A(l + 1).to_scipy().toarray()
+        assert np.array_equal(Ac, Ac.T)                         # exact (C4)
+        assert np.abs(Ac - P.T @ Al @ P).max() <= 1e-13 * np.abs(Al).max()
+        np.linalg.cholesky(Ac)                                  # s.p.d.
+
+
+def test_galerkin_spec_examples():
+    """SPEC.md:57-59 (spgemm) and 75-77 (P = I -> A; A = I, orthonormal P -> I)."""
+    a = O.OracleCSR.from_scipy(sp.csr_matrix(np.array([[1.0, 2.0], [0.0, 3.0]])))
+    b = O.OracleCSR.from_scipy(sp.csr_matrix(np.array([[0.0, 1.0], [1.0, 0.0]])))
+    c = O.OracleCSR(O.lib().or_matmul_canonical(a.h, b.h))
+    assert c.to_scipy().toarray().tolist() == [[2.0, 1.0], [3.0, 0.0]]
+    A = poisson7(4, 3, 2)
+    Ao = ocsr(A)
+    I = O.OracleCSR.from_scipy(sp.identity(24, format="csr"))
+    assert np.array_equal(O.rap(I, Ao, I).to_scipy().toarray(), A.to_scipy().toarray())
+    Q, _ = np.linalg.qr(np.random.default_rng(1).standard_normal((24, 5)))
+    Qo = O.OracleCSR.from_scipy(sp.csr_matrix(Q))
+    assert np.abs(O.rap(Qo, I, Qo).to_scipy().toarray() - np.eye(5)).max() < 1e-14
+
+
+# --------------------------------------------------------------- P12 l1-Jacobi
+def test_P12_l1_jacobi():
+    A = poisson7(6, 6, 6)
+    m = O.l1_jacobi_inv(ocsr(A))
+    i = np.arange(216)
+    x, y, z = i % 6, (i // 6) % 6, i // 36
+    interior = (x > 0) & (x < 5) & (y > 0) & (y < 5) & (z > 0) & (z < 5)
+    assert np.all(m[interior] == 1.0 / 12.0)
+    Ad = A.to_scipy().toarray()
+    assert np.allclose(1 / m, np.abs(Ad).sum(axis=1), rtol=0, atol=1e-13)
+    # A-convergence ||I - M^-1 A||_A < 1
+    L = np.linalg.cholesky(Ad)
+    E = np.eye(216) - m[:, None] * Ad
+    nrm = np.linalg.norm(L.T @ E @ np.linalg.inv(L.T), 2)
+    assert nrm < 1.0
+
+
+# --------------------------------------------------------------- P13 V-cycle
+def _dense_B(h):
+    n = h.n
+    return np.column_stack([h.vcycle(e) for e in np.eye(n)])
+
+
+@pytest.mark.parametrize("case", ["poisson", "aniso22", "jump"])
+def test_P13_vcycle_linear_symmetric_spd_convergent(case):
+    if case == "poisson":
+        A, kw = poisson7(10, 10, 8), {}
+    elif case == "aniso22":
+        A, kw = poisson7(10, 8, 8, (1, 1, 0.01)), dict(pre_sweeps=2, post_sweeps=2)
+    else:
+        A, kw = jump27(8), {}
+    h = O.OracleHierarchy(A, max_coarse_size=20, **kw)
+    assert h.nlevels >= 3
+    n = h.n
+    rng = np.random.default_rng(11)
+    r, s = rng.standard_normal(n), rng.standard_normal(n)
+    a, b = 0.7, -1.3
+    lhs = h.vcycle(a * r + b * s)
+    rhs = a * h.vcycle(r) + b * h.vcycle(s)
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(lhs)
+    Br, Bs = h.vcycle(r), h.vcycle(s)
+    assert abs(Br @ s - r @ Bs) <= 1e-12 * np.linalg.norm(r) * np.linalg.norm(s)
+    assert r @ Br > 0
+    Ad = A.to_scipy().toarray()
+    B = _dense_B(h)
+    L = np.linalg.cholesky(Ad)
+    E = np.eye(n) - B @ Ad
+    assert np.linalg.norm(L.T @ E @ np.linalg.inv(L.T), 2) < 1.0
+    assert np.linalg.eigvalsh((B + B.T) / 2).min() > 0
+
+
+def test_P13_single_level_is_exact_inverse():
+    A = poisson7(5, 4, 3)
+    h = O.OracleHierarchy(A, max_coarse_size=1000)
+    assert h.nlevels == 1
+    r = np.random.default_rng(2).standard_normal(60)
+    z = h.vcycle(r)
+    assert np.linalg.norm(A.to_scipy() @ z - r) <= 1e-13 * np.linalg.norm(r)
+
+
+# --------------------------------------------------------------- P14 PCG
+def test_P14_pcg_exact_preconditioner_one_iteration():
+    A = poisson7(5, 4, 3)
+    h = O.OracleHierarchy(A, max_coarse_size=1000)
+    x, info = h.pcg(np.ones(60), rtol=1e-10)
+    assert info["iterations"] == 1 and info["status"] == O.OR_OK
+
+
+@pytest.mark.parametrize("n", [6, 8, 10])
+def test_P14_cg_terminates_in_n_steps(n):
+    A = poisson7(n, 1, 1)
+    h = O.OracleHierarchy(A, max_coarse_size=2, sweeps_per_level=1)
+    assert h.nlevels >= 2
+    b = np.random.default_rng(n).standard_normal(n)
+    x, info = h.pcg(b, rtol=0.0, maxit=n)
+    assert np.linalg.norm(b - A.to_scipy() @ x) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_P14_pcg_matches_textbook_pcg_iterates():
+    """Textbook Hestenes-Stiefel PCG (written here) with B = dense V-cycle matrix."""
+    A = poisson7(8, 6, 5)
+    h = O.OracleHierarchy(A, max_coarse_size=20)
+    Ad = A.to_scipy().toarray()
+    B = _dense_B(h)
+    b = np.random.default_rng(5).uniform(0, 1, h.n)
+    for k in (1, 2, 3, 5):
+        xo, info = h.pcg(b, rtol=0.0, maxit=k)
+        x = np.zeros(h.n)
+        r = b.copy()
+        z = B @ r
+        p = z.copy()
+        rz = r @ z
+        for _ in range(k):
+            q = Ad @ p
+            al = rz / (p @ q)
+            x += al * p
+            r -= al * q
+            z = B @ r
+            rz2 = r @ z
+            p = z + (rz2 / rz) * p
+            rz = rz2
+        assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(x)
+
+
+def test_P14_pcg_zero_rhs_and_true_residual():
+    A = poisson7(8, 8, 8)
+    h = O.OracleHierarchy(A, max_coarse_size=20)
+    x, info = h.pcg(np.zeros(512))
+    assert info["iterations"] == 0 and not x.any()
+    x, info = h.pcg(np.ones(512), rtol=1e-6)
+    assert info["relres"] <= 1e-6 and info["true_relres"] <= 2e-6
+    hist = h.pcg(np.ones(512), rtol=1e-6, history=True)[1]["history"]
+    assert hist[0] == 1.0 and hist[-1] <= 1e-6
+
+
+# --------------------------------------------------------------- P15 scaling
+def test_P15_scale_invariance():
+    A = poisson7(16, 16, 12)
+    A4 = poisson7(16, 16, 12)
+    A4.values = A4.values * 4.0
+    b = np.random.default_rng(9).uniform(0, 1, A.n_global)
+    h, h4 = O.OracleHierarchy(A, max_coarse_size=50), O.OracleHierarchy(A4, max_coarse_size=50)
+    assert h.sizes() == h4.sizes()
+    for l in range(h.nlevels - 1):
+        assert np.array_equal(h.agg(l), h4.agg(l))
+    assert h.pcg(b)[1]["iterations"] == h4.pcg(b)[1]["iterations"]
+    # the paper's (100,100,1) vs config 3's (1,1,0.01)
+    Aa = poisson7(16, 16, 12, (1, 1, 0.01))
+    Ab = poisson7(16, 16, 12, (100, 100, 1))
+    ha, hb = (O.OracleHierarchy(Aa, max_coarse_size=50, pre_sweeps=2, post_sweeps=2),
+              O.OracleHierarchy(Ab, max_coarse_size=50, pre_sweeps=2, post_sweeps=2))
+    # 0.01*100 is not exact in binary, so ties deeper down can break differently
+    # (reading list); level 0 is fixed by the closed form of P16 and the
+    # iteration counts agree within +-1.
+    assert np.array_equal(ha.agg(0), hb.agg(0))
+    assert abs(ha.pcg(b)[1]["iterations"] - hb.pcg(b)[1]["iterations"]) <= 1
+
+
+# --------------------------------------------------------------- P16 aniso
+def test_P16_anisotropic_bricks():
+    """(1,1,0.01): sweep 1 pairs x (c_x = c_y = 1 + 2/8.04 > c_z), sweep 2 pairs y,
+    sweep 3 pairs x: 4x2x1 bricks, z never matched (aggregates follow strong
+    couplings)."""
+    nx = ny = nz = 16
+    A = poisson7(nx, ny, nz, (1, 1, 0.01))
+    Ao = ocsr(A)
+    _, _, c = O.edge_weights(Ao, np.ones(A.n_global))
+    assert np.isclose(c.max(), 1 + 2 / 8.04, atol=1e-14)
+    assert np.isclose(c.min(), 1 + 0.02 / 8.04, atol=1e-14)
+    h = O.OracleHierarchy(A, max_levels=2, max_coarse_size=1, pre_sweeps=2, post_sweeps=2)
+    i = np.arange(A.n_global)
+    x, y, z = i % nx, (i // nx) % ny, i // (nx * ny)
+    exp = x // 4 + (nx // 4) * (y // 2 + (ny // 2) * z)
+    assert np.array_equal(h.agg(0), exp)
+
+
+# --------------------------------------------------------------- P18 omega
+def test_P18_dinv_a_norm_is_two_for_all_operators():
+    for A in (poisson7(8, 8, 8), poisson7(8, 8, 8, (1, 1, 0.01)), jump27(16)):
+        assert O.dinv_a_inf_norm(ocsr(A)) == pytest.approx(2.0, abs=1e-14)
+        h = O.OracleHierarchy(A, max_levels=2, max_coarse_size=1)
+        assert h.omega(0) == pytest.approx(2.0 / 3.0, abs=1e-15)
+
+
+def test_dinv_spec_examples():
+    """SPEC.md:84-86."""
+    I = O.OracleCSR.from_scipy(sp.identity(3, format="csr"))
+    assert O.dinv_a_inf_norm(I) == 1.0
+    M = O.OracleCSR.from_scipy(sp.csr_matrix(np.array([[2.0, 1.0], [1.0, 4.0]])))
+    assert O.dinv_a_inf_norm(M) == 1.5
+
+
+# --------------------------------------------------------------- errors
+def test_build_rejects_bad_inputs():
+    A = poisson7(4, 4, 4)
+    bad = poisson7(4, 4, 4)
+    bad.values = bad.values.copy()
+    bad.values[bad.rowptr[5]] = -6.0 if bad.colind[bad.rowptr[5]] == 5 else bad.values[bad.rowptr[5]] + 1
+    with pytest.raises(ValueError):
+        O.OracleHierarchy(bad)
+    with pytest.raises(ValueError):
+        O.OracleHierarchy(A, w=np.zeros(64))
+    with pytest.raises(ValueError):
+        O.OracleHierarchy(A, pre_sweeps=0)
