@@ -1,0 +1,184 @@
+/*
+ * amg_b200.h — C ABI of the B200-native AMG-PCG solve path (arxiv 2006.16147).
+ *
+ * The library solves A x = b for a symmetric positive-definite sparse A
+ * ("systems ... where A is symmetric and positive-definite")
+ * with preconditioned CG (north_star) whose preconditioner is
+ * one V-cycle (Eq. 3.1) over a hierarchy built by coarsening
+ * based on compatible weighted matching (Eqs. 3.2-3.3) with a
+ * Jacobi-smoothed prolongator and l1-Jacobi smoothing
+ * (nb = 1).  The hierarchy is built once per matrix (host,
+ * C++/OpenMP) and uploaded; the solve phase runs entirely in hand-written
+ * sm_100a CUDA kernels launched from CUDA graphs.
+ *
+ * Conventions shared by every entry point:
+ *  - Status codes only; no exception crosses the ABI.  amg_last_error() returns a
+ *    thread-local message describing the last failing call.
+ *  - Host arrays are BORROWED for the duration of the call; the hierarchy owns
+ *    its device copies.  Device pointers (`*_dev`) are caller-owned fp64 buffers
+ *    on the context's device (typically torch tensors' data_ptr()).
+ *  - All calls are ordered on the context's CUDA stream.  amg_solve /
+ *    amg_solve_host / amg_precond_apply return after the stream work they issued
+ *    has completed (they synchronize the context stream).
+ *  - Multi-rank: every rank passes its own contiguous row block; build, solve and
+ *    apply are collective over the ranks of the context.
+ *  - Indices: global int64 on input; rows are contiguous blocks [row_begin, row_end).
+ *  - fp64 throughout (the paper never states precision).
+ */
+#ifndef AMG_B200_H
+#define AMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    AMG_OK = 0,
+    AMG_ERR_ARG = 1,          /* bad argument: shape, ordering, asymmetry, sizes */
+    AMG_ERR_NOT_SPD = 2,      /* non-positive diagonal, w == 0, coarsest Cholesky failed */
+    AMG_ERR_CUDA = 3,         /* CUDA runtime / launch failure */
+    AMG_ERR_NCCL = 4,         /* NCCL failure (multi-rank contexts) */
+    AMG_ERR_OOM = 5,          /* host or device allocation failure */
+    AMG_NOT_CONVERGED = 6,    /* maxit reached; x and the report are valid */
+    AMG_ERR_BREAKDOWN = 7     /* p^T A p <= 0 in PCG; x holds the last iterate */
+} amg_status_t;
+
+typedef struct amg_ctx_s* amg_ctx_t;    /* one per rank = one GPU */
+typedef struct amg_hier_s* amg_hier_t;  /* a built hierarchy, owned device data */
+
+/* Hierarchy / cycle configuration.  Defaults (amg_config_default) reproduce the
+ * paper's VA3 hierarchy with the readings of SURVEY.md §8c. */
+typedef struct {
+    int32_t sweeps_per_level;     /* m pairwise-matching sweeps per level; aggregates <= 2^m
+                                     (PAPER.md:134).  Default 3. */
+    int32_t smooth_prolongator;   /* 1: P-bar = (I - omega D^-1 A) P; 0: P. */
+    double  prol_omega_scale;     /* omega = scale / ||D^-1 A||_inf.  Default 4/3 (reading R3:
+                                     reproduces Table SM1); 1.0 = text's
+                                     reading. */
+    int64_t max_coarse_size;      /* stop coarsening once n_l <= this.
+                                     Default 200; use 200*np across np GPUs. */
+    int32_t max_levels;           /* default 20 */
+    double  min_coarsening_ratio; /* a level with n_l/n_{l+1} < this is discarded (default 1.2) */
+    int32_t pre_sweeps;           /* l1-Jacobi pre-smoothing sweeps, >= 1 (default 1) */
+    int32_t post_sweeps;          /* l1-Jacobi post-smoothing sweeps, >= 1 (default 1) */
+    int64_t replicate_below_bytes;/* multi-rank: levels whose A_l + P-bar_l bytes are below
+                                     this are held whole on every rank (default 64 MiB) */
+    int32_t setup_threads;        /* host OpenMP threads for setup; 0 = all available */
+    int32_t use_graphs;           /* 1 (default): solve/apply run as CUDA graphs; 0: eager
+                                     launches (debug / per-kernel timing) */
+} amg_config_t;
+
+/* Solve report (SPEC.md:440-443 SolveReport). */
+typedef struct {
+    int32_t iterations;           /* PCG iterations performed */
+    int32_t converged;            /* 1 iff final_relres <= rtol */
+    int32_t nlevels;              /* levels in the hierarchy */
+    int32_t status;               /* amg_status_t of the solve */
+    double  final_relres;         /* ||r_k||_2 / ||b||_2 (recursive residual, reading R12) */
+    double  setup_s;              /* wall seconds of amg_hierarchy_build (host + upload) */
+    double  solve_s;              /* device seconds of the solve (CUDA events) */
+    double  opc;                  /* operator complexity sum nnz(A_l)/nnz(A_0) */
+    double  avg_cr;               /* average coarsening ratio */
+    double  vcycle_bytes_model;   /* algorithmic bytes of one V-cycle */
+    double  iteration_bytes_model;/* algorithmic bytes of one PCG iteration */
+} amg_report_t;
+
+/* Fills *cfg with the defaults listed above. */
+void amg_config_default(amg_config_t* cfg);
+
+/* Creates a context bound to CUDA device `device` and stream `cuda_stream`
+ * (a cudaStream_t; NULL = the legacy default stream).  For nranks > 1,
+ * `nccl_unique_id` points to the 128-byte ncclUniqueId produced by rank 0 and
+ * broadcast by the caller (e.g. through torch.distributed); it is ignored when
+ * nranks == 1.  Returns AMG_ERR_ARG for rank/nranks out of range, AMG_ERR_CUDA /
+ * AMG_ERR_NCCL when the device or communicator cannot be initialised. */
+int amg_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
+                   void* cuda_stream, amg_ctx_t* out);
+int amg_ctx_destroy(amg_ctx_t ctx);
+
+/* Builds the hierarchy for the s.p.d. matrix A.
+ *  n_global            global order of A
+ *  row_begin, row_end  this rank's contiguous row block; blocks of all ranks must
+ *                      be in rank order and cover [0, n_global)
+ *  rowptr   host, int64, (row_end-row_begin)+1 entries, 0-based offsets into colind
+ *  colind   host, int64 GLOBAL column indices, strictly ascending within each row
+ *  values   host, fp64; A must be exactly symmetric (pattern and values)
+ *  w        host, fp64, local rows of the matching weight vector; NULL = all ones
+ *           ("starting from a vector w of all ones")
+ *  cfg      NULL = defaults
+ * Errors: AMG_ERR_ARG (unsorted/out-of-range columns, asymmetry, bad block),
+ * AMG_ERR_NOT_SPD (a_ii <= 0, w == 0, coarsest Cholesky failure), AMG_ERR_OOM. */
+int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int64_t row_end,
+                        const int64_t* rowptr, const int64_t* colind, const double* values,
+                        const double* w, const amg_config_t* cfg, amg_hier_t* out);
+int amg_hierarchy_destroy(amg_hier_t h);
+
+/* PCG with one V-cycle per iteration (north_star):
+ * x0 = 0, stops when ||r_k||/||b|| <= rtol or after maxit iterations; rtol = 0
+ * runs exactly maxit iterations.  b_dev (read) and x_dev (written) hold this
+ * rank's local rows.  b = 0 returns x = 0 after 0 iterations.  `rep` may be NULL.
+ * Returns AMG_OK, AMG_NOT_CONVERGED or AMG_ERR_BREAKDOWN (x valid in all three). */
+int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int32_t maxit,
+              amg_report_t* rep);
+
+/* Same as amg_solve but b_host/x_host are HOST buffers (pinned or pageable):
+ * the host->device copy of b and the device->host copy of x are part of the call. */
+int amg_solve_host(amg_hier_t h, const double* b_host, double* x_host, double rtol,
+                   int32_t maxit, amg_report_t* rep);
+
+/* One application of the preconditioner z = B r, i.e. one V-cycle
+ * (Eq. 3.1).  Device buffers, local rows. */
+int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev);
+
+/* Hierarchy inspection.
+ * amg_level_info: global rows, global nnz of A_l and P-bar_l (0 at the coarsest),
+ * this rank's row block of level l and the device storage format of A_l
+ * (0 = SELL-32, 1 = CSR-vector, 2 = dense inverse (coarsest)). */
+int amg_num_levels(amg_hier_t h, int32_t* nlevels);
+int amg_level_info(amg_hier_t h, int32_t lvl, int64_t* n_global, int64_t* nnzA_global,
+                   int64_t* nnzP_global, int64_t* row_begin, int64_t* row_end, int32_t* format);
+/* Aggregate map of level lvl (lvl < nlevels-1): for each local row of level lvl the
+ * GLOBAL index of its aggregate on level lvl+1 (host int64 array of local length). */
+int amg_level_aggregates(amg_hier_t h, int32_t lvl, int64_t* agg_out);
+/* Report of the hierarchy alone (opc, avg_cr, byte models, setup_s). */
+int amg_hierarchy_report(amg_hier_t h, amg_report_t* rep);
+
+/* Kernel timing probe: runs `napply` V-cycles with CUDA events around every kernel
+ * on the context stream (eager launches) and writes, for up to `cap` kernels of
+ * one V-cycle in launch order, the average device milliseconds (ms_out), the
+ * algorithmic bytes of one launch per SURVEY.md §8d (bytes_out) and a static name
+ * (names_out, may be NULL).  *count receives the number of kernels per V-cycle. */
+int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out,
+                       double* bytes_out, const char** names_out, int32_t* count);
+
+/* ---- Host-only view of the setup phase (no device needed) -----------------
+ * Runs exactly the setup that amg_hierarchy_build runs (the same C++ code) on a
+ * whole matrix held by one process and keeps the host hierarchy, so the
+ * aggregate maps, coarse operators and prolongators can be inspected, e.g. for
+ * bit-exact comparison with an independent implementation.  Arguments as in
+ * amg_hierarchy_build with row_begin = 0, row_end = n. */
+typedef struct amg_host_hier_s* amg_host_hier_t;
+int amg_host_hierarchy_build(int64_t n, const int64_t* rowptr, const int64_t* colind,
+                             const double* values, const double* w, const amg_config_t* cfg,
+                             amg_host_hier_t* out);
+int amg_host_hierarchy_destroy(amg_host_hier_t h);
+int amg_host_num_levels(amg_host_hier_t h, int32_t* nlevels);
+/* n, nnz(A_l), nnz(P-bar_l) (0 at the coarsest), omega_l (0 if unsmoothed/coarsest) */
+int amg_host_level_sizes(amg_host_hier_t h, int32_t lvl, int64_t* n, int64_t* nnzA, int64_t* nnzP,
+                         double* omega);
+/* aggregate map of level lvl < nlevels-1, n_l int64 entries */
+int amg_host_level_aggregates(amg_host_hier_t h, int32_t lvl, int64_t* agg_out);
+/* which = 0: A_l (n_l x n_l); which = 1: P-bar_l (n_l x n_{l+1}).  Caller-allocated
+ * int64 rowptr (n_l+1), int64 colind and fp64 values (nnz entries). */
+int amg_host_level_matrix(amg_host_hier_t h, int32_t lvl, int32_t which, int64_t* rowptr,
+                          int64_t* colind, double* values);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* amg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMG_B200_H */

@@ -1,0 +1,168 @@
+"""B200-native AMG-PCG solve path of arxiv 2006.16147 (AMG4PSBLAS).
+
+Public API (same names as the C ABI in include/amg_b200.h):
+
+    ctx = Context(device=0)
+    h = Hierarchy(ctx, A, cfg=None, w=None)       # amg_hierarchy_build
+    x, rep = h.solve(b, rtol=1e-6, maxit=500)     # amg_solve (torch CUDA tensors)
+    x, rep = h.solve_host(b_np)                   # amg_solve_host (host buffers)
+    z = h.precond_apply(r)                        # amg_precond_apply (one V-cycle)
+    h.level_aggregates(l), h.level_info(l), h.report(), h.profile_vcycle(n)
+
+Everything runs in libamg_b200.so; this package only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from ._abi import (AMG_ERR_BREAKDOWN, AMG_NOT_CONVERGED, AMG_OK, AmgError, amg_config_default,  # noqa: F401
+                   amg_config_t, amg_last_error, amg_report_t, check, lib)
+
+__all__ = ["Context", "Hierarchy", "amg_config_default", "AmgError", "lib"]
+
+
+def make_config(**kw) -> amg_config_t:
+    c = amg_config_default()
+    for k, v in kw.items():
+        if not hasattr(c, k):
+            raise KeyError(k)
+        setattr(c, k, v)
+    return c
+
+
+class Context:
+    """amg_ctx_create / amg_ctx_destroy.  stream=None lets the library own a stream."""
+
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_uid: bytes | None = None,
+                 stream: int | None = None):
+        self.h = C.c_void_p()
+        uid = C.create_string_buffer(nccl_uid, 128) if nccl_uid else None
+        check(lib.amg_ctx_create(device, rank, nranks, uid, C.c_void_p(stream) if stream else None,
+                                 C.byref(self.h)), "amg_ctx_create")
+        self.device, self.rank, self.nranks = device, rank, nranks
+
+    def close(self):
+        if self.h:
+            lib.amg_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _ptr(a):
+    return C.c_void_p(a.ctypes.data)
+
+
+class Hierarchy:
+    """amg_hierarchy_build and the solve-phase calls on the built hierarchy."""
+
+    def __init__(self, ctx: Context, A, cfg: amg_config_t | None = None, w=None):
+        self.ctx = ctx
+        self.h = C.c_void_p()
+        rp = np.ascontiguousarray(A.rowptr, dtype=np.int64)
+        ci = np.ascontiguousarray(A.colind, dtype=np.int64)
+        v = np.ascontiguousarray(A.values, dtype=np.float64)
+        wv = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+        self.cfg = cfg if cfg is not None else amg_config_default()
+        check(lib.amg_hierarchy_build(ctx.h, A.n_global, A.row_begin, A.row_end, _ptr(rp), _ptr(ci),
+                                      _ptr(v), _ptr(wv) if wv is not None else None, C.byref(self.cfg),
+                                      C.byref(self.h)), "amg_hierarchy_build")
+        self.n_local = A.row_end - A.row_begin
+
+    def close(self):
+        if self.h:
+            lib.amg_hierarchy_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------- inspection
+    @property
+    def nlevels(self) -> int:
+        n = C.c_int32()
+        check(lib.amg_num_levels(self.h, C.byref(n)), "amg_num_levels")
+        return n.value
+
+    def level_info(self, l: int) -> dict:
+        vals = [C.c_int64() for _ in range(5)]
+        f = C.c_int32()
+        check(lib.amg_level_info(self.h, l, *[C.byref(x) for x in vals], C.byref(f)), "amg_level_info")
+        n, nnzA, nnzP, rb, re = (x.value for x in vals)
+        return dict(n=n, nnzA=nnzA, nnzP=nnzP, row_begin=rb, row_end=re, format=_abi.FORMATS[f.value])
+
+    def sizes(self):
+        return [self.level_info(l)["n"] for l in range(self.nlevels)]
+
+    def level_aggregates(self, l: int) -> np.ndarray:
+        info = self.level_info(l)
+        out = np.zeros(info["row_end"] - info["row_begin"], dtype=np.int64)
+        check(lib.amg_level_aggregates(self.h, l, _ptr(out)), "amg_level_aggregates")
+        return out
+
+    def report(self) -> dict:
+        r = amg_report_t()
+        check(lib.amg_hierarchy_report(self.h, C.byref(r)), "amg_hierarchy_report")
+        return r.as_dict()
+
+    # ------------------------------------------------------------- solve phase
+    def solve(self, b, x=None, rtol: float = 1e-6, maxit: int = 500):
+        """amg_solve on CUDA tensors (fp64, this rank's rows)."""
+        import torch
+        assert b.dtype == torch.float64 and b.is_cuda and b.is_contiguous()
+        if x is None:
+            x = torch.empty_like(b)
+        torch.cuda.current_stream(b.device).synchronize()
+        rep = amg_report_t()
+        code = lib.amg_solve(self.h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), float(rtol),
+                             int(maxit), C.byref(rep))
+        check(code, "amg_solve", ok=(AMG_OK, AMG_NOT_CONVERGED))
+        return x, rep.as_dict()
+
+    def solve_raw(self, b_ptr: int, x_ptr: int, rtol: float = 1e-6, maxit: int = 500) -> dict:
+        rep = amg_report_t()
+        code = lib.amg_solve(self.h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), float(rtol), int(maxit),
+                             C.byref(rep))
+        check(code, "amg_solve", ok=(AMG_OK, AMG_NOT_CONVERGED))
+        return rep.as_dict()
+
+    def solve_host(self, b: np.ndarray, x: np.ndarray | None = None, rtol: float = 1e-6, maxit: int = 500):
+        """amg_solve_host: host buffers, H2D/D2H copies inside the call."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if x is None:
+            x = np.empty_like(b)
+        rep = amg_report_t()
+        code = lib.amg_solve_host(self.h, _ptr(b), _ptr(x), float(rtol), int(maxit), C.byref(rep))
+        check(code, "amg_solve_host", ok=(AMG_OK, AMG_NOT_CONVERGED))
+        return x, rep.as_dict()
+
+    def precond_apply(self, r, z=None):
+        """amg_precond_apply: one V-cycle z = B r on CUDA tensors."""
+        import torch
+        assert r.dtype == torch.float64 and r.is_cuda and r.is_contiguous()
+        if z is None:
+            z = torch.empty_like(r)
+        torch.cuda.current_stream(r.device).synchronize()
+        check(lib.amg_precond_apply(self.h, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr())),
+              "amg_precond_apply")
+        return z
+
+    def profile_vcycle(self, napply: int = 10, cap: int = 256):
+        ms = np.zeros(cap)
+        by = np.zeros(cap)
+        names = (C.c_char_p * cap)()
+        cnt = C.c_int32()
+        check(lib.amg_profile_vcycle(self.h, napply, cap, _ptr(ms), _ptr(by), names, C.byref(cnt)),
+              "amg_profile_vcycle")
+        k = min(cnt.value, cap)
+        return [dict(name=names[i].decode(), ms=float(ms[i]), bytes=float(by[i])) for i in range(k)]

@@ -1,0 +1,63 @@
+"""Build the product library libamg_b200.so in-tree for sm_100a.
+
+g++ compiles the host setup with -ffp-contract=off (canonical arithmetic
+contract C1); nvcc compiles the device code and the ABI for
+`-gencode arch=compute_100a,code=sm_100a` only.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(PKG, "_build")
+LIB = os.path.join(PKG, "libamg_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+SOURCES_CXX = [os.path.join(CSRC, "setup", "setup.cpp")]
+SOURCES_CU = [os.path.join(CSRC, "amg_api.cu")]
+HEADERS = [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "setup", "setup.hpp"),
+           os.path.join(ROOT, "include", "amg_b200.h")]
+
+
+def _run(cmd):
+    print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_library(force: bool = False, verbose_ptxas: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    objs = []
+    for src in SOURCES_CXX:
+        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        if force or _stale(obj, [src] + HEADERS):
+            _run(["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
+                  "-Wall", "-c", src, "-o", obj])
+        objs.append(obj)
+    for src in SOURCES_CU:
+        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        if force or _stale(obj, [src] + HEADERS):
+            cmd = [NVCC] + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler",
+                                   "-fPIC,-fopenmp,-ffp-contract=off", "-c", src, "-o", obj]
+            if verbose_ptxas:
+                cmd.insert(1, "-Xptxas=-v")
+            _run(cmd)
+        objs.append(obj)
+    if force or _stale(LIB, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lgomp", "-Xlinker", "-z,defs"])
+    return LIB
+
+
+if __name__ == "__main__":
+    build_library(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)

@@ -1,0 +1,364 @@
+// kernels.cuh — sm_100a device kernels of the AMG-PCG solve phase.
+//
+// Everything on the hot path is an fp64 sparse row reduction (~0.17 flop/B, HBM
+// bound; no tensor-core contraction exists here).  One kernel
+// family covers every step of the V-cycle (Eq. 3.1) and of PCG:
+//
+//   y_i = E( i, sum_k  a_ik * G(col_k) )
+//
+// with a Gather functor G (x_j, or m_j*b_j for the first sweep from x = 0) and an
+// Epilogue functor E (residual, l1-Jacobi update, restriction store, prolongation
+// update, SpMV + dot ...).  Two storage formats:
+//   * SELL-32: slices of 32 consecutive rows stored column-major, one warp per
+//     slice, so every lane's k-th entry is one coalesced 256 B (values) + 128 B
+//     (indices) transaction; used for short rows with little padding (levels 0-1,
+//     prolongators, restrictions).
+//   * CSR-vector: VW lanes per row with a shuffle row reduction; used for the long
+//     rows of the deep levels (hundreds to thousands of entries per row).
+// Grids are persistent-style (a multiple of the SM count x resident blocks),
+// rows are visited grid-stride.  Dot products are fused into the epilogue and
+// reduced deterministically: per-block tree, then the last block to finish sums
+// the block partials in a fixed order and runs a PCG "finisher" that computes
+// alpha / beta / the convergence test on the device (and sets the CUDA-graph
+// WHILE condition), so no host round trip happens inside a solve.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace amgk {
+
+constexpr int kBlock = 256;
+
+// --------------------------------------------------------------- PCG state
+enum PcgStatus : int32_t { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXIT = 2, ST_BREAKDOWN = 3, ST_ZERO_RHS = 4 };
+
+struct PcgState {
+    double rho;     // r^T z of the current iterate
+    double alpha, beta;
+    double bnorm;   // ||b||_2
+    double relres;  // ||r_k|| / ||b||
+    double rtol;
+    int32_t iter, maxit, status, pad;
+};
+
+enum FinishKind : int32_t { FIN_NONE = 0, FIN_BNORM = 1, FIN_RZ = 2, FIN_PQ = 3, FIN_RR = 4 };
+
+struct RedCtx {
+    double* partials;     // >= gridDim.x doubles
+    unsigned int* ticket; // zero-initialised counter, reset by the last block
+    double* out;          // optional: total written here
+    PcgState* st;
+    unsigned long long cond;  // cudaGraphConditionalHandle of the PCG WHILE node (0 = none)
+    int32_t kind;
+};
+
+__device__ __forceinline__ void finish(const RedCtx& rc, double total) {
+    if (rc.out) *rc.out = total;
+    PcgState* st = rc.st;
+    if (!st) return;
+    switch (rc.kind) {
+        case FIN_BNORM: {
+            st->bnorm = sqrt(total);
+            st->iter = 0;
+            st->alpha = 0.0;
+            st->beta = 0.0;
+            st->rho = 0.0;
+            if (total == 0.0) {
+                st->status = ST_ZERO_RHS;
+                st->relres = 0.0;
+            } else {
+                st->status = (st->maxit <= 0) ? ST_MAXIT : ST_RUNNING;
+                st->relres = 1.0;
+            }
+            if (rc.cond) cudaGraphSetConditional(rc.cond, st->status == ST_RUNNING ? 1u : 0u);
+            break;
+        }
+        case FIN_RZ: {  // rho' = r^T z ; beta = rho'/rho (0 on the first iteration)
+            st->beta = (st->iter == 0) ? 0.0 : total / st->rho;
+            st->rho = total;
+            break;
+        }
+        case FIN_PQ: {  // alpha = rho / p^T q ; breakdown if p^T q <= 0
+            if (!(total > 0.0)) {
+                st->status = ST_BREAKDOWN;
+                st->alpha = 0.0;
+            } else {
+                st->alpha = st->rho / total;
+            }
+            break;
+        }
+        case FIN_RR: {  // convergence test on the recursive residual (reading R12)
+            if (st->status == ST_RUNNING) {
+                st->iter += 1;
+                st->relres = sqrt(total) / st->bnorm;
+                if (st->relres <= st->rtol) st->status = ST_CONVERGED;
+                else if (st->iter >= st->maxit) st->status = ST_MAXIT;
+            }
+            if (rc.cond) cudaGraphSetConditional(rc.cond, st->status == ST_RUNNING ? 1u : 0u);
+            break;
+        }
+        default:
+            break;
+    }
+}
+
+// Deterministic grid reduction: fixed per-block tree, fixed-order sum of the
+// block partials by the last block to arrive.
+__device__ __forceinline__ void grid_reduce(double v, const RedCtx& rc) {
+    __shared__ double wsum[kBlock / 32];
+    __shared__ bool last;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) wsum[wid] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += wsum[w];
+        rc.partials[blockIdx.x] = s;
+        __threadfence();
+        unsigned int t = atomicAdd(rc.ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s = 0.0;
+    for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+        s += ((volatile double*)rc.partials)[b];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) wsum[wid] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += wsum[w];
+        *rc.ticket = 0u;
+        finish(rc, tot);
+    }
+}
+
+// ---------------------------------------------------------------- loads
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+    int32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+// --------------------------------------------------------------- gathers
+struct GVec {  // x_j
+    const double* __restrict__ x;
+    __device__ __forceinline__ double operator()(int32_t j) const { return __ldg(x + j); }
+};
+struct GMB {   // (m o b)_j : the first l1-Jacobi sweep from x = 0 (R9)
+    const double* __restrict__ m;
+    const double* __restrict__ b;
+    __device__ __forceinline__ double operator()(int32_t j) const { return __ldg(m + j) * __ldg(b + j); }
+};
+
+// ------------------------------------------------------------- epilogues
+// r = b - s                                (residual; s = A x or A (m o b))
+struct EResid {
+    static constexpr bool kDot = false;
+    const double* __restrict__ b;
+    double* __restrict__ r;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        r[i] = b[i] - s;
+        return 0.0;
+    }
+};
+// x' = x + m (b - s)                        (l1-Jacobi sweep, out of place)
+template <bool DOT>
+struct ESweep {
+    static constexpr bool kDot = DOT;
+    const double* __restrict__ x;
+    const double* __restrict__ b;
+    const double* __restrict__ m;
+    double* __restrict__ xo;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        const double bi = b[i];
+        const double v = x[i] + m[i] * (bi - s);
+        xo[i] = v;
+        return DOT ? bi * v : 0.0;  // r^T z at the end of the level-0 V-cycle
+    }
+};
+// x' = m b + m (b - s)  with s = A (m o b)  (two sweeps from x = 0, s1 >= 2)
+struct ESweep0 {
+    static constexpr bool kDot = false;
+    const double* __restrict__ b;
+    const double* __restrict__ m;
+    double* __restrict__ xo;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        const double mi = m[i], bi = b[i];
+        xo[i] = mi * bi + mi * (bi - s);
+        return 0.0;
+    }
+};
+// y = s                                     (restriction b_{l+1} = P-bar^T r)
+struct EStore {
+    static constexpr bool kDot = false;
+    double* __restrict__ y;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        y[i] = s;
+        return 0.0;
+    }
+};
+// x = m b + s                               (prolongation after one pre-sweep from 0)
+struct EProlong0 {
+    static constexpr bool kDot = false;
+    const double* __restrict__ b;
+    const double* __restrict__ m;
+    double* __restrict__ xo;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        xo[i] = m[i] * b[i] + s;
+        return 0.0;
+    }
+};
+// x' = x + s                                (prolongation, general)
+struct EProlongAdd {
+    static constexpr bool kDot = false;
+    const double* x;
+    double* xo;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        xo[i] = x[i] + s;
+        return 0.0;
+    }
+};
+// q = s, returns p_i q_i                    (PCG: q = A p fused with p^T q)
+struct ESpmvDot {
+    static constexpr bool kDot = true;
+    const double* __restrict__ p;
+    double* __restrict__ q;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        q[i] = s;
+        return p[i] * s;
+    }
+};
+
+// ------------------------------------------------------------ SELL-32 kernel
+struct SellView {
+    const uint32_t* __restrict__ sptr;  // nslices+1, offsets in units of 32 entries
+    const int32_t* __restrict__ col;
+    const double* __restrict__ val;
+    int64_t n;
+};
+
+template <class G, class E>
+__global__ void __launch_bounds__(kBlock) k_sell(SellView A, G g, E e, RedCtx rc) {
+    const int64_t nslices = (A.n + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
+    double d = 0.0;
+    for (int64_t s = w0; s < nslices; s += nw) {
+        const uint32_t b0 = __ldg(A.sptr + s);
+        const uint32_t w = __ldg(A.sptr + s + 1) - b0;
+        const int32_t* c = A.col + (int64_t)b0 * 32 + lane;
+        const double* v = A.val + (int64_t)b0 * 32 + lane;
+        double acc = 0.0;
+#pragma unroll 8
+        for (uint32_t k = 0; k < w; ++k) acc += ld_stream(v + 32 * k) * g(ld_stream(c + 32 * k));
+        const int64_t row = (s << 5) + lane;
+        if (row < A.n) d += e(row, acc);
+    }
+    if constexpr (E::kDot) grid_reduce(d, rc);
+}
+
+// ---------------------------------------------------------- CSR-vector kernel
+struct CsrView {
+    const int32_t* __restrict__ rp;
+    const int32_t* __restrict__ ci;
+    const double* __restrict__ v;
+    int64_t n;
+};
+
+template <int VW, class G, class E>
+__global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc) {
+    const int64_t gid = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const int sub = threadIdx.x % VW;
+    const int64_t g0 = gid / VW;
+    const int64_t ng = ((int64_t)gridDim.x * kBlock) / VW;
+    double d = 0.0;
+    // every lane of a warp runs the same number of outer iterations (shuffles)
+    const int64_t iters = (A.n + ng - 1) / ng;
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t row = g0 + it * ng;
+        double acc = 0.0;
+        if (row < A.n) {
+            const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
+#pragma unroll 4
+            for (int32_t k = k0 + sub; k < k1; k += VW) acc += ld_stream(A.v + k) * g(ld_stream(A.ci + k));
+        }
+#pragma unroll
+        for (int o = VW / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, VW);
+        if (sub == 0 && row < A.n) d += e(row, acc);
+    }
+    if constexpr (E::kDot) grid_reduce(d, rc);
+}
+
+// ------------------------------------------------------------ vector kernels
+// PCG prologue: r = b, x = 0, ||b||^2 -> FIN_BNORM
+__global__ void __launch_bounds__(kBlock) k_pcg_init(const double* __restrict__ b, double* __restrict__ r,
+                                                     double* __restrict__ x, int64_t n, RedCtx rc) {
+    double d = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        const double bi = b[i];
+        r[i] = bi;
+        x[i] = 0.0;
+        d += bi * bi;
+    }
+    grid_reduce(d, rc);
+}
+
+// a^T b -> finisher (single-level hierarchies: r^T z)
+__global__ void __launch_bounds__(kBlock) k_dot(const double* __restrict__ a, const double* __restrict__ b,
+                                                int64_t n, RedCtx rc) {
+    double d = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        d += a[i] * b[i];
+    grid_reduce(d, rc);
+}
+
+// p = z (first iteration) or p = z + beta p
+__global__ void __launch_bounds__(kBlock) k_pupdate(const double* __restrict__ z, double* __restrict__ p, int64_t n,
+                                                    const PcgState* __restrict__ st) {
+    const bool first = st->iter == 0;
+    const double beta = st->beta;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        p[i] = first ? z[i] : z[i] + beta * p[i];
+}
+
+// x += alpha p ; r -= alpha q ; ||r||^2 -> FIN_RR
+__global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ x, double* __restrict__ r,
+                                                    const double* __restrict__ p, const double* __restrict__ q,
+                                                    int64_t n, RedCtx rc) {
+    const double alpha = rc.st->alpha;
+    double d = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        x[i] = x[i] + alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        d += ri * ri;
+    }
+    grid_reduce(d, rc);
+}
+
+// Coarsest level: z = A_L^{-1} b, dense row-major inverse, one warp per row.
+__global__ void __launch_bounds__(kBlock) k_dense_gemv(const double* __restrict__ Ainv, const double* __restrict__ b,
+                                                       double* __restrict__ z, int64_t n) {
+    const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
+    for (int64_t row = warp; row < n; row += nw) {
+        const double* a = Ainv + row * n;
+        double s = 0.0;
+        for (int64_t k = lane; k < n; k += 32) s += __ldg(a + k) * __ldg(b + k);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) z[row] = s;
+    }
+}
+
+}  // namespace amgk

@@ -1,0 +1,624 @@
+// setup.cpp — host hierarchy construction (C++17 + OpenMP), compiled with
+// -ffp-contract=off.  Follows PAPER.md §3.2 and SURVEY.md §8c O1-O9 with the
+// canonical arithmetic contract C1-C5 so that aggregate maps equal the oracle's
+// bit for bit, but with its own (parallel) algorithms:
+//  * matching: locally-dominant pointer rounds with a worklist (the parallel
+//    half-approximate scheme of PAPER.md:147-150) under the strict edge order
+//    (|c| desc, lo asc, hi asc) — the unique locally-dominant matching (R5);
+//  * SpGEMM: row-parallel, per-thread dense accumulators, per-entry accumulation
+//    in the canonical arrival order of C3 ("any serial sparse-matrix
+//    by sparse-matrix product code" for the local part).
+#include "setup.hpp"
+
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+
+namespace amgsetup {
+
+namespace {
+
+std::vector<double> diagonal(const Csr& A) {
+    std::vector<double> d(A.nrows, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < A.nrows; ++i) {
+        const int32_t* b = A.ci.data() + A.rp[i];
+        const int32_t* e = A.ci.data() + A.rp[i + 1];
+        const int32_t* p = std::lower_bound(b, e, (int32_t)i);
+        d[i] = (p != e && *p == i) ? A.v[p - A.ci.data()] : 0.0;
+    }
+    return d;
+}
+
+bool lookup(const Csr& A, int64_t r, int32_t c, double& val) {
+    const int32_t* b = A.ci.data() + A.rp[r];
+    const int32_t* e = A.ci.data() + A.rp[r + 1];
+    const int32_t* p = std::lower_bound(b, e, c);
+    if (p != e && *p == c) {
+        val = A.v[p - A.ci.data()];
+        return true;
+    }
+    return false;
+}
+
+// Concatenate per-thread vectors.
+template <class T>
+std::vector<T> concat(std::vector<std::vector<T>>& parts) {
+    size_t tot = 0;
+    for (auto& p : parts) tot += p.size();
+    std::vector<T> out;
+    out.reserve(tot);
+    for (auto& p : parts) out.insert(out.end(), p.begin(), p.end());
+    return out;
+}
+
+// P^T w with each coarse entry summed over its fine rows in ascending order (C3).
+std::vector<double> restrict_vec(const Csr& P, const std::vector<double>& w) {
+    Csr Pt = transpose(P);
+    std::vector<double> out(Pt.nrows);
+#pragma omp parallel for schedule(static)
+    for (int64_t G = 0; G < Pt.nrows; ++G) {
+        double s = 0.0;
+        for (int64_t k = Pt.rp[G]; k < Pt.rp[G + 1]; ++k) s += Pt.v[k] * w[Pt.ci[k]];
+        out[G] = s;
+    }
+    return out;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ sparse
+Csr transpose(const Csr& X) {
+    Csr T;
+    T.nrows = X.ncols;
+    T.ncols = X.nrows;
+    const int64_t nnz = X.nnz();
+    T.rp.assign(T.nrows + 1, 0);
+    T.ci.resize(nnz);
+    T.v.resize(nnz);
+    for (int64_t k = 0; k < nnz; ++k) T.rp[X.ci[k] + 1]++;
+    for (int64_t c = 0; c < T.nrows; ++c) T.rp[c + 1] += T.rp[c];
+    std::vector<int64_t> pos(T.rp.begin(), T.rp.end() - 1);
+    for (int64_t i = 0; i < X.nrows; ++i)
+        for (int64_t k = X.rp[i]; k < X.rp[i + 1]; ++k) {
+            int64_t c = X.ci[k];
+            T.ci[pos[c]] = (int32_t)i;
+            T.v[pos[c]] = X.v[k];
+            ++pos[c];
+        }
+    return T;
+}
+
+Csr spgemm_canonical(const Csr& A, const Csr& Y) {
+    Csr C;
+    C.nrows = A.nrows;
+    C.ncols = Y.ncols;
+    const int64_t n = A.nrows, m = Y.ncols;
+    const int nt = omp_get_max_threads();
+    const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)nt * 32));
+    std::vector<std::vector<int32_t>> ccol(nchunk);
+    std::vector<std::vector<double>> cval(nchunk);
+    std::vector<int64_t> cnt(n + 1, 0);
+#pragma omp parallel
+    {
+        std::vector<double> acc(m);
+        std::vector<int64_t> stamp(m, -1);
+        std::vector<int32_t> touched;
+        touched.reserve(4096);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t c = 0; c < nchunk; ++c) {
+            const int64_t r0 = n * c / nchunk, r1 = n * (c + 1) / nchunk;
+            auto& oc = ccol[c];
+            auto& ov = cval[c];
+            for (int64_t i = r0; i < r1; ++i) {
+                touched.clear();
+                for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                    const int32_t j = A.ci[k];
+                    const double a = A.v[k];
+                    for (int64_t t = Y.rp[j]; t < Y.rp[j + 1]; ++t) {
+                        const int32_t K = Y.ci[t];
+                        if (stamp[K] != i) {
+                            stamp[K] = i;
+                            acc[K] = 0.0;
+                            touched.push_back(K);
+                        }
+                        acc[K] += a * Y.v[t];
+                    }
+                }
+                std::sort(touched.begin(), touched.end());
+                for (int32_t K : touched) {
+                    oc.push_back(K);
+                    ov.push_back(acc[K]);
+                }
+                cnt[i + 1] = (int64_t)touched.size();
+            }
+        }
+    }
+    C.rp.assign(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) C.rp[i + 1] = C.rp[i] + cnt[i + 1];
+    C.ci.resize(C.rp[n]);
+    C.v.resize(C.rp[n]);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const int64_t r0 = n * c / nchunk;
+        std::copy(ccol[c].begin(), ccol[c].end(), C.ci.begin() + C.rp[r0]);
+        std::copy(cval[c].begin(), cval[c].end(), C.v.begin() + C.rp[r0]);
+        std::vector<int32_t>().swap(ccol[c]);
+        std::vector<double>().swap(cval[c]);
+    }
+    return C;
+}
+
+void mirror_drop(Csr& C) {
+    const int64_t n = C.nrows;
+    std::vector<double> nv(C.nnz());
+    std::vector<int64_t> cnt(n + 1, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t r = 0; r < n; ++r) {
+        int64_t keep = 0;
+        for (int64_t k = C.rp[r]; k < C.rp[r + 1]; ++k) {
+            const int32_t c = C.ci[k];
+            double val = C.v[k];
+            if (c < r) {  // C4: lower entry takes the upper one's value
+                double u;
+                val = lookup(C, c, (int32_t)r, u) ? u : 0.0;
+            }
+            nv[k] = val;
+            keep += (val != 0.0);  // C5
+        }
+        cnt[r + 1] = keep;
+    }
+    std::vector<int64_t> rp(n + 1, 0);
+    for (int64_t r = 0; r < n; ++r) rp[r + 1] = rp[r] + cnt[r + 1];
+    std::vector<int32_t> ci(rp[n]);
+    std::vector<double> v(rp[n]);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t r = 0; r < n; ++r) {
+        int64_t o = rp[r];
+        for (int64_t k = C.rp[r]; k < C.rp[r + 1]; ++k)
+            if (nv[k] != 0.0) {
+                ci[o] = C.ci[k];
+                v[o] = nv[k];
+                ++o;
+            }
+    }
+    C.rp.swap(rp);
+    C.ci.swap(ci);
+    C.v.swap(v);
+}
+
+// ------------------------------------------------------------------ matching
+// Locally-dominant pointer rounds.  Eq. 3.2 key |c_ij| per stored off-diagonal,
+// always evaluated with (lo, hi) = (min, max) orientation (C2) so both endpoints
+// see bit-identical keys.  Each free vertex points at its best free neighbour
+// under (|c| desc, lo asc, hi asc) — for a fixed vertex this is "largest key,
+// then smallest neighbour index".  Mutual pointers are matched; only vertices
+// whose pointer target was just matched are re-examined (total work O(nnz)).
+void ld_matching(const Csr& A, const std::vector<double>& w, std::vector<int32_t>& mate) {
+    const int64_t n = A.nrows;
+    const std::vector<double> d = diagonal(A);
+    std::vector<double> key(A.nnz());
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const int64_t j = A.ci[k];
+            if (j == i) {
+                key[k] = -1.0;
+                continue;
+            }
+            const int64_t lo = std::min(i, j), hi = std::max(i, j);
+            const double a = A.v[k];  // == a_{lo,hi}: A is exactly symmetric
+            const double den = (d[lo] * w[lo]) * w[lo] + (d[hi] * w[hi]) * w[hi];
+            if (den == 0.0) {
+                key[k] = -1.0;
+                continue;
+            }
+            const double c = 1.0 - (((2.0 * a) * w[lo]) * w[hi]) / den;
+            key[k] = (c == 0.0) ? -1.0 : std::fabs(c);
+        }
+    mate.assign(n, -1);
+    std::vector<int32_t> ptr(n, -1);
+    auto best = [&](int64_t v) -> int32_t {
+        int32_t b = -1;
+        double bk = -1.0;
+        for (int64_t k = A.rp[v]; k < A.rp[v + 1]; ++k) {
+            const double kk = key[k];
+            if (kk < 0.0) continue;
+            const int32_t u = A.ci[k];
+            if (mate[u] >= 0) continue;
+            if (kk > bk || (kk == bk && u < b)) {
+                bk = kk;
+                b = u;
+            }
+        }
+        return b;
+    };
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t v = 0; v < n; ++v) ptr[v] = best(v);
+
+    std::vector<int32_t> stamp(n, -1), stamp2(n, -1);
+    std::vector<int32_t> cand(n);
+    for (int64_t v = 0; v < n; ++v) cand[v] = (int32_t)v;
+    const int nt = omp_get_max_threads();
+    for (int32_t round = 0; !cand.empty(); ++round) {
+        // 1. mutual pointers among the candidates
+        std::vector<std::vector<int32_t>> part(nt);
+#pragma omp parallel
+        {
+            auto& mine = part[omp_get_thread_num()];
+#pragma omp for schedule(static)
+            for (int64_t q = 0; q < (int64_t)cand.size(); ++q) {
+                const int32_t v = cand[q];
+                if (mate[v] >= 0) continue;
+                const int32_t t = ptr[v];
+                if (t > v && mate[t] < 0 && ptr[t] == v) mine.push_back(v);
+            }
+        }
+        std::vector<int32_t> heads = concat(part);
+        if (heads.empty()) break;
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < (int64_t)heads.size(); ++q) {
+            const int32_t v = heads[q], t = ptr[v];
+            mate[v] = t;
+            mate[t] = v;
+        }
+        // 2. free vertices that pointed at a newly matched vertex
+        for (auto& p : part) p.clear();
+#pragma omp parallel
+        {
+            auto& mine = part[omp_get_thread_num()];
+#pragma omp for schedule(dynamic, 256)
+            for (int64_t q = 0; q < (int64_t)heads.size(); ++q) {
+                const int32_t ends[2] = {heads[q], mate[heads[q]]};
+                for (int32_t e : ends)
+                    for (int64_t k = A.rp[e]; k < A.rp[e + 1]; ++k) {
+                        const int32_t u = A.ci[k];
+                        if (mate[u] >= 0 || (ptr[u] != ends[0] && ptr[u] != ends[1])) continue;
+                        const int32_t old = stamp[u];
+                        if (old != round && __sync_bool_compare_and_swap(&stamp[u], old, round))
+                            mine.push_back(u);
+                    }
+            }
+        }
+        std::vector<int32_t> W = concat(part);
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (int64_t q = 0; q < (int64_t)W.size(); ++q) ptr[W[q]] = best(W[q]);
+        // 3. next candidates: W and their new targets
+        for (auto& p : part) p.clear();
+#pragma omp parallel
+        {
+            auto& mine = part[omp_get_thread_num()];
+#pragma omp for schedule(static)
+            for (int64_t q = 0; q < (int64_t)W.size(); ++q) {
+                const int32_t u = W[q];
+                const int32_t pair[2] = {u, ptr[u]};
+                for (int32_t x : pair) {
+                    if (x < 0) continue;
+                    int32_t old = stamp2[x];
+                    if (old != round && __sync_bool_compare_and_swap(&stamp2[x], old, round))
+                        mine.push_back(x);
+                }
+            }
+        }
+        cand = concat(part);
+    }
+}
+
+// ------------------------------------------------------------------ checks
+int validate(const Csr& A, const std::vector<double>& w, std::string& err) {
+    if (A.nrows != A.ncols || A.nrows <= 0) {
+        err = "matrix must be square and non-empty";
+        return SETUP_ERR_ARG;
+    }
+    int bad = 0;
+    int64_t badrow = -1;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(max : bad)
+    for (int64_t i = 0; i < A.nrows; ++i) {
+        bool has_d = false;
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const int32_t c = A.ci[k];
+            if (c < 0 || c >= A.ncols || (k > A.rp[i] && c <= A.ci[k - 1])) {
+                bad = std::max(bad, 3);
+                badrow = i;
+                break;
+            }
+            double t;
+            if (!lookup(A, c, (int32_t)i, t) || t != A.v[k]) {
+                bad = std::max(bad, 2);
+                badrow = i;
+                break;
+            }
+            if (c == i) {
+                has_d = true;
+                if (!(A.v[k] > 0.0)) {
+                    bad = std::max(bad, 1);
+                    badrow = i;
+                }
+            }
+        }
+        if (!has_d) {
+            bad = std::max(bad, 1);
+            badrow = i;
+        }
+    }
+    if (bad == 3) {
+        err = "column indices must be in range and strictly ascending (row " +
+              std::to_string(badrow) + ")";
+        return SETUP_ERR_ARG;
+    }
+    if (bad == 2) {
+        err = "matrix is not exactly symmetric (row " + std::to_string(badrow) + ")";
+        return SETUP_ERR_ARG;
+    }
+    if (bad == 1) {
+        err = "non-positive or missing diagonal (row " + std::to_string(badrow) + ")";
+        return SETUP_ERR_NOT_SPD;
+    }
+    bool anyw = false;
+    for (double x : w)
+        if (x != 0.0) {
+            anyw = true;
+            break;
+        }
+    if (!anyw) {
+        err = "weight vector w is identically zero";
+        return SETUP_ERR_NOT_SPD;
+    }
+    return SETUP_OK;
+}
+
+// ------------------------------------------------------------------ build
+namespace {
+
+struct Sweep {
+    std::vector<int32_t> agg;
+    std::vector<double> pval;  // NaN: no stored entry
+    int64_t nc = 0;
+};
+
+// Aggregates from the matching: pairs and singletons numbered by ascending
+// minimum member (R5); pairwise values of Eq. 3.3 with the
+// parenthesisation of O2.4.
+Sweep aggregate_and_values(const std::vector<int32_t>& mate, const std::vector<double>& w) {
+    const int64_t n = (int64_t)mate.size();
+    Sweep s;
+    s.agg.resize(n);
+    s.pval.resize(n);
+    std::vector<int32_t> id(n);
+    int64_t nc = 0;
+    for (int64_t v = 0; v < n; ++v) {
+        const bool head = mate[v] < 0 || mate[v] > v;
+        id[v] = (int32_t)nc;
+        nc += head;
+    }
+    s.nc = nc;
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < n; ++v) {
+        const int64_t j = mate[v];
+        if (j < 0) {
+            s.agg[v] = id[v];
+            s.pval[v] = (w[v] == 0.0) ? 1.0 : w[v] / std::fabs(w[v]);
+            continue;
+        }
+        const int64_t lo = std::min<int64_t>(v, j), hi = std::max<int64_t>(v, j);
+        s.agg[v] = id[lo];
+        const double nrm = std::sqrt((w[lo] * w[lo]) + (w[hi] * w[hi]));
+        if (nrm == 0.0) {
+            s.pval[v] = (v == lo) ? 1.0 : nan;
+        } else {
+            const double p = w[v] / nrm;
+            s.pval[v] = (p == 0.0) ? nan : p;
+        }
+    }
+    return s;
+}
+
+Csr one_per_row(const std::vector<int32_t>& agg, const std::vector<double>& pval, int64_t nc) {
+    Csr P;
+    const int64_t n = (int64_t)agg.size();
+    P.nrows = n;
+    P.ncols = nc;
+    P.rp.assign(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) P.rp[i + 1] = P.rp[i] + (std::isnan(pval[i]) ? 0 : 1);
+    P.ci.resize(P.rp[n]);
+    P.v.resize(P.rp[n]);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+        if (!std::isnan(pval[i])) {
+            P.ci[P.rp[i]] = agg[i];
+            P.v[P.rp[i]] = pval[i];
+        }
+    return P;
+}
+
+Csr galerkin(const Csr& P, const Csr& A) {
+    Csr T = spgemm_canonical(A, P);
+    Csr Pt = transpose(P);
+    Csr C = spgemm_canonical(Pt, T);
+    mirror_drop(C);
+    return C;
+}
+
+std::vector<double> l1_inv(const Csr& A) {
+    std::vector<double> m(A.nrows);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < A.nrows; ++i) {
+        double s = 0.0;
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) s += std::fabs(A.v[k]);
+        m[i] = 1.0 / s;
+    }
+    return m;
+}
+
+// Dense Cholesky and explicit inverse of the coarsest matrix (reading R2).
+bool dense_inverse(const Csr& A, std::vector<double>& inv) {
+    const int64_t n = A.nrows;
+    std::vector<double> L(n * n, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) L[i * n + A.ci[k]] = A.v[k];
+    for (int64_t j = 0; j < n; ++j) {
+        double dj = L[j * n + j];
+        for (int64_t k = 0; k < j; ++k) dj -= L[j * n + k] * L[j * n + k];
+        if (!(dj > 0.0)) return false;
+        const double ljj = std::sqrt(dj);
+        L[j * n + j] = ljj;
+#pragma omp parallel for schedule(static) if (n > 256)
+        for (int64_t i = j + 1; i < n; ++i) {
+            double s = L[i * n + j];
+            for (int64_t k = 0; k < j; ++k) s -= L[i * n + k] * L[j * n + k];
+            L[i * n + j] = s / ljj;
+        }
+    }
+    inv.assign(n * n, 0.0);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t c = 0; c < n; ++c) {
+        std::vector<double> y(n);
+        for (int64_t i = 0; i < n; ++i) {
+            double s = (i == c) ? 1.0 : 0.0;
+            for (int64_t k = 0; k < i; ++k) s -= L[i * n + k] * y[k];
+            y[i] = s / L[i * n + i];
+        }
+        for (int64_t i = n - 1; i >= 0; --i) {
+            double s = y[i];
+            for (int64_t k = i + 1; k < n; ++k) s -= L[k * n + i] * y[k];
+            y[i] = s / L[i * n + i];
+        }
+        for (int64_t i = 0; i < n; ++i) inv[i * n + c] = y[i];
+    }
+    // symmetrise (A^{-1} is symmetric; the two triangular solves are not exactly)
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = i + 1; j < n; ++j) {
+            const double a = 0.5 * (inv[i * n + j] + inv[j * n + i]);
+            inv[i * n + j] = a;
+            inv[j * n + i] = a;
+        }
+    return true;
+}
+
+}  // namespace
+
+int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
+          std::string& err) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (cfg.threads > 0) omp_set_num_threads(cfg.threads);
+    if (cfg.sweeps_per_level < 1 || cfg.max_coarse_size < 1 || cfg.max_levels < 1 ||
+        cfg.pre_sweeps < 1 || cfg.post_sweeps < 1 || !(cfg.prol_omega_scale > 0.0)) {
+        err = "invalid configuration";
+        return SETUP_ERR_ARG;
+    }
+    int st = validate(A0, w0, err);
+    if (st != SETUP_OK) return st;
+    out.lv.clear();
+    out.lv.emplace_back();
+    out.lv[0].A = std::move(A0);
+    out.lv[0].w = std::move(w0);
+    for (int l = 0;; ++l) {
+        Level& L = out.lv[l];
+        const Csr& A = L.A;
+        L.m = l1_inv(A);  // O7
+        const int64_t n = A.nrows;
+        if (n <= cfg.max_coarse_size || l == cfg.max_levels - 1) break;  // O1
+        // O2: m pairwise sweeps; O3: composite map and values
+        std::vector<int32_t> comp_agg(n);
+        std::vector<double> comp_val(n, 1.0);
+        for (int64_t i = 0; i < n; ++i) comp_agg[i] = (int32_t)i;
+        Csr As_store;
+        const Csr* As = &A;
+        std::vector<double> ws = L.w;
+        int64_t ns = n;
+        int done = 0;
+        for (int s = 0; s < cfg.sweeps_per_level; ++s) {
+            std::vector<int32_t> mate;
+            ld_matching(*As, ws, mate);
+            Sweep sw = aggregate_and_values(mate, ws);
+            if (sw.nc == ns) break;  // no size reduction
+            Csr Ps = one_per_row(sw.agg, sw.pval, sw.nc);
+            Csr An = galerkin(Ps, *As);
+            std::vector<double> wn = restrict_vec(Ps, ws);
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < n; ++i) {
+                const int32_t a = comp_agg[i];
+                comp_val[i] = comp_val[i] * sw.pval[a];
+                comp_agg[i] = sw.agg[a];
+            }
+            As_store = std::move(An);
+            As = &As_store;
+            ws.swap(wn);
+            ns = sw.nc;
+            ++done;
+        }
+        As_store = Csr();
+        if (done == 0 || (double)n / (double)ns < cfg.min_coarsening_ratio) break;  // O1
+        const int64_t nc = ns;
+        Csr P = one_per_row(comp_agg, comp_val, nc);
+        Csr Pb;
+        if (cfg.smooth_prolongator) {
+            // O4: omega = scale / max_i (sum_j |a_ij|)/a_ii
+            const std::vector<double> d = diagonal(A);
+            double mx = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : mx)
+            for (int64_t i = 0; i < n; ++i) {
+                double s = 0.0;
+                for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) s += std::fabs(A.v[k]);
+                mx = std::max(mx, s / d[i]);
+            }
+            L.omega = cfg.prol_omega_scale / mx;
+            // O5: P-bar[i,G] = P[i,G] - (omega/a_ii) * (A P)[i,G]
+            Csr T = spgemm_canonical(A, P);
+            std::vector<int64_t> cnt(n + 1, 0);
+            std::vector<double> nv(T.nnz());
+#pragma omp parallel for schedule(dynamic, 4096)
+            for (int64_t i = 0; i < n; ++i) {
+                const double f = L.omega / d[i];
+                int64_t keep = 0;
+                for (int64_t k = T.rp[i]; k < T.rp[i + 1]; ++k) {
+                    const bool own = (P.rp[i + 1] > P.rp[i]) && T.ci[k] == P.ci[P.rp[i]];
+                    const double p = own ? P.v[P.rp[i]] : 0.0;
+                    nv[k] = p - f * T.v[k];
+                    keep += (nv[k] != 0.0);
+                }
+                cnt[i + 1] = keep;
+            }
+            Pb.nrows = n;
+            Pb.ncols = nc;
+            Pb.rp.assign(n + 1, 0);
+            for (int64_t i = 0; i < n; ++i) Pb.rp[i + 1] = Pb.rp[i] + cnt[i + 1];
+            Pb.ci.resize(Pb.rp[n]);
+            Pb.v.resize(Pb.rp[n]);
+#pragma omp parallel for schedule(dynamic, 4096)
+            for (int64_t i = 0; i < n; ++i) {
+                int64_t o = Pb.rp[i];
+                for (int64_t k = T.rp[i]; k < T.rp[i + 1]; ++k)
+                    if (nv[k] != 0.0) {
+                        Pb.ci[o] = T.ci[k];
+                        Pb.v[o] = nv[k];
+                        ++o;
+                    }
+            }
+        } else {
+            L.omega = 0.0;
+            Pb = P;
+        }
+        // O6: A_{l+1} = P-bar^T A P-bar (mirrored), w_{l+1} = P^T w (R6)
+        Level next;
+        next.A = galerkin(Pb, A);
+        next.w = restrict_vec(P, L.w);
+        L.R = transpose(Pb);
+        L.P = std::move(Pb);
+        L.agg = std::move(comp_agg);
+        L.sweeps = done;
+        out.lv.push_back(std::move(next));
+    }
+    if (!dense_inverse(out.lv.back().A, out.coarse_inv)) {  // O8
+        err = "coarsest-level Cholesky failed (matrix not s.p.d.)";
+        return SETUP_ERR_NOT_SPD;
+    }
+    out.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return SETUP_OK;
+}
+
+}  // namespace amgsetup

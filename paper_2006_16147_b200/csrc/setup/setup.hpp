@@ -1,0 +1,65 @@
+// setup.hpp — host-side hierarchy construction of the product library.
+//
+// Built once per matrix (setup on the host; the solve phase runs
+// on the GPU).  Independent of oracle/: different algorithms (parallel
+// locally-dominant pointer rounds instead of a sorted greedy scan, row-parallel
+// SpGEMM with per-thread accumulators) that follow the same canonical arithmetic
+// contract so that the aggregate maps are bit-identical.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace amgsetup {
+
+struct Csr {
+    int64_t nrows = 0, ncols = 0;
+    std::vector<int64_t> rp;   // nrows+1
+    std::vector<int32_t> ci;   // ascending within a row
+    std::vector<double> v;
+    int64_t nnz() const { return rp.empty() ? 0 : rp[nrows]; }
+};
+
+struct Config {
+    int sweeps_per_level = 3;
+    int smooth_prolongator = 1;
+    double prol_omega_scale = 4.0 / 3.0;
+    int64_t max_coarse_size = 200;
+    int max_levels = 20;
+    double min_coarsening_ratio = 1.2;
+    int pre_sweeps = 1, post_sweeps = 1;
+    int threads = 0;
+};
+
+struct Level {
+    Csr A;                    // A_l
+    Csr P;                    // smoothed prolongator P-bar_l (n_l x n_{l+1}), empty at coarsest
+    Csr R;                    // P-bar_l^T
+    std::vector<int32_t> agg; // composite aggregate map (n_l), empty at coarsest
+    std::vector<double> w;    // w_l
+    std::vector<double> m;    // l1-Jacobi inverse diagonal 1/(sum_j |a_ij|)
+    double omega = 0.0;
+    int sweeps = 0;
+};
+
+struct Hierarchy {
+    std::vector<Level> lv;
+    std::vector<double> coarse_inv;  // dense A_L^{-1}, row-major n_L x n_L
+    double setup_s = 0.0;
+};
+
+enum { SETUP_OK = 0, SETUP_ERR_ARG = 1, SETUP_ERR_NOT_SPD = 2 };
+
+// Validates A (square, sorted, exactly symmetric, positive diagonal) and w.
+int validate(const Csr& A, const std::vector<double>& w, std::string& err);
+// Full build.  A0 is moved in.
+int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
+          std::string& err);
+
+// Building blocks (exported for the setup self-tests).
+Csr spgemm_canonical(const Csr& A, const Csr& Y);
+Csr transpose(const Csr& X);
+void mirror_drop(Csr& C);
+void ld_matching(const Csr& A, const std::vector<double>& w, std::vector<int32_t>& mate);
+
+}  // namespace amgsetup

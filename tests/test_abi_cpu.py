@@ -1,0 +1,187 @@
+"""CPU-side checks of the product library (no GPU needed):
+
+  * libamg_b200.so loads and exports every function declared in include/amg_b200.h;
+  * its host setup (parallel locally-dominant matching, row-parallel canonical
+    SpGEMM — an implementation independent of oracle/) reproduces the oracle's
+    aggregate maps bit-exactly at every level, and (a stronger diagnostic) the
+    coarse operators A_l and smoothed prolongators P-bar_l bit for bit;
+  * argument validation and error codes.
+"""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs import config_problem, jump27, poisson7, uniform01
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def amg():
+    import paper_2006_16147_b200 as amg
+    return amg
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "amg_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+char\s*\*|int|void)\s+(amg_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol(amg):
+    names = declared_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(amg.lib, n), n
+    from paper_2006_16147_b200 import _abi
+    assert set(_abi.EXPORTED) <= set(names)
+
+
+def test_config_default_matches_header(amg):
+    c = amg.amg_config_default()
+    assert (c.sweeps_per_level, c.smooth_prolongator, c.max_coarse_size, c.max_levels) == (3, 1, 200, 20)
+    assert c.prol_omega_scale == 4.0 / 3.0 and c.min_coarsening_ratio == 1.2
+    assert (c.pre_sweeps, c.post_sweeps, c.use_graphs) == (1, 1, 1)
+
+
+class HostH:
+    """Wrapper of the amg_host_* inspection entry points."""
+
+    def __init__(self, amg, A, w=None, **cfg):
+        L = amg.lib
+        self.L = L
+        self.h = C.c_void_p()
+        c = amg.make_config(**cfg)
+        self._keep = [np.ascontiguousarray(A.rowptr, np.int64), np.ascontiguousarray(A.colind, np.int64),
+                      np.ascontiguousarray(A.values, np.float64)]
+        wp = None
+        if w is not None:
+            self._keep.append(np.ascontiguousarray(w, np.float64))
+            wp = C.c_void_p(self._keep[-1].ctypes.data)
+        L.amg_host_hierarchy_build.argtypes = [C.c_int64] + [C.c_void_p] * 4 + [C.c_void_p, C.c_void_p]
+        self.code = L.amg_host_hierarchy_build(A.n_global, *[C.c_void_p(a.ctypes.data) for a in self._keep[:3]],
+                                               wp, C.byref(c), C.byref(self.h))
+
+    def __del__(self):
+        if self.h:
+            self.L.amg_host_hierarchy_destroy(self.h)
+
+    @property
+    def nlevels(self):
+        n = C.c_int32()
+        self.L.amg_host_num_levels(self.h, C.byref(n))
+        return n.value
+
+    def sizes(self, l):
+        n, a, p = C.c_int64(), C.c_int64(), C.c_int64()
+        om = C.c_double()
+        self.L.amg_host_level_sizes(self.h, l, C.byref(n), C.byref(a), C.byref(p), C.byref(om))
+        return n.value, a.value, p.value, om.value
+
+    def agg(self, l):
+        n = self.sizes(l)[0]
+        out = np.zeros(n, np.int64)
+        assert self.L.amg_host_level_aggregates(self.h, l, C.c_void_p(out.ctypes.data)) == 0
+        return out
+
+    def matrix(self, l, which):
+        n, nnzA, nnzP, _ = self.sizes(l)
+        nnz = nnzA if which == 0 else nnzP
+        rp = np.zeros(n + 1, np.int64)
+        ci = np.zeros(max(nnz, 1), np.int64)
+        v = np.zeros(max(nnz, 1))
+        assert self.L.amg_host_level_matrix(self.h, l, which, C.c_void_p(rp.ctypes.data),
+                                            C.c_void_p(ci.ctypes.data), C.c_void_p(v.ctypes.data)) == 0
+        return rp, ci[:nnz], v[:nnz]
+
+
+def _compare(amg, A, w=None, **cfg):
+    hl = HostH(amg, A, w=w, **cfg)
+    assert hl.code == 0, amg.amg_last_error()
+    ho = O.OracleHierarchy(A, w=w, **cfg)
+    assert hl.nlevels == ho.nlevels
+    for l in range(ho.nlevels):
+        assert hl.sizes(l)[0] == ho.level_n(l)
+        rp, ci, v = hl.matrix(l, 0)
+        orp, oci, ov = ho.A(l).arrays()
+        assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+        assert np.array_equal(v.view(np.int64), ov.view(np.int64)), f"A_{l} values differ bitwise"
+        if l + 1 < ho.nlevels:
+            assert np.array_equal(hl.agg(l), ho.agg(l)), f"aggregates differ at level {l}"
+            assert hl.sizes(l)[3] == ho.omega(l)
+            rp, ci, v = hl.matrix(l, 1)
+            orp, oci, ov = ho.P(l).arrays()
+            assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+            assert np.array_equal(v.view(np.int64), ov.view(np.int64)), f"P_{l} values differ bitwise"
+    return hl, ho
+
+
+@pytest.mark.parametrize("case", ["c1", "aniso_32", "jump_16", "ragged", "unsmoothed_20", "random_w",
+                                  "omega_text", "m4_sweeps", "c4_like_24x24x48"])
+def test_host_setup_bit_exact_vs_oracle(amg, case):
+    w, cfg = None, {}
+    if case == "c1":
+        A = config_problem(1)[0]
+    elif case == "aniso_32":
+        A = poisson7(32, 32, 32, (1, 1, 0.01))
+        cfg = dict(pre_sweeps=2, post_sweeps=2)
+    elif case == "jump_16":
+        A = jump27(16)
+    elif case == "ragged":
+        A = poisson7(17, 13, 11)
+    elif case == "unsmoothed_20":
+        A = poisson7(20, 20, 20)
+        cfg = dict(smooth_prolongator=0)
+    elif case == "random_w":
+        A = poisson7(14, 12, 10)
+        w = 0.5 + uniform01(99, A.n_global)
+    elif case == "omega_text":
+        A = poisson7(16, 16, 16)
+        cfg = dict(prol_omega_scale=1.0)
+    elif case == "m4_sweeps":
+        A = poisson7(24, 24, 24)
+        cfg = dict(sweeps_per_level=4, max_coarse_size=20)
+    else:
+        A = poisson7(24, 24, 48)
+        cfg = dict(max_coarse_size=400)
+    _compare(amg, A, w=w, **cfg)
+
+
+@pytest.mark.slow
+def test_host_setup_reproduces_tableSM_80cube(amg):
+    """The library's own setup also reproduces Table SM:
+    80^3, unsmoothed 3 sweeps -> nl = 5, cr = 8 per level, coarsest 125."""
+    A = poisson7(80, 80, 80)
+    hl = HostH(amg, A, smooth_prolongator=0)
+    assert hl.code == 0
+    sizes = [hl.sizes(l)[0] for l in range(hl.nlevels)]
+    assert sizes == [512000, 64000, 8000, 1000, 125]
+
+
+@pytest.mark.slow
+def test_host_setup_bit_exact_c2(amg):
+    """Full config 2 (128^3): every level's aggregates, A_l and P-bar_l bit-exact."""
+    A = config_problem(2)[0]
+    _compare(amg, A)
+
+
+def test_host_setup_errors(amg):
+    A = poisson7(4, 4, 4)
+    A.values = A.values.copy()
+    A.values[1] = -2.0
+    assert HostH(amg, A).code == 1  # asymmetric
+    A = poisson7(4, 4, 4)
+    A.values = -A.values
+    assert HostH(amg, A).code == 2  # non-positive diagonal
+    A = poisson7(4, 4, 4)
+    assert HostH(amg, A, w=np.zeros(64)).code == 2  # w == 0
+    A = poisson7(4, 4, 4)
+    assert HostH(amg, A, pre_sweeps=0).code == 1
+    A = poisson7(4, 4, 4)
+    A.colind = A.colind.copy()
+    A.colind[0], A.colind[1] = A.colind[1], A.colind[0]  # unsorted row
+    assert HostH(amg, A).code == 1

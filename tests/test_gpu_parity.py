@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * aggregate maps bit-exact at every level;
+  * one preconditioner application on a seeded vector <= 1e-12 relative 2-norm;
+  * PCG iterations equal or +-1;
+  * x within 1e-8 relative, compared at EQUAL iteration counts (fixed-count mode,
+    rtol = 0, maxit = min of the two natural counts; SURVEY.md §4 protocol).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs import config_problem, jump27, poisson7, uniform01, uniform_pm1
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+VCYCLE_TOL = 1e-12
+X_TOL = 1e-8
+
+
+def _amg():
+    import paper_2006_16147_b200 as amg
+    return amg
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    amg = _amg()
+    c = amg.Context(device=0)
+    yield c
+    c.close()
+
+
+def _cfg(**kw):
+    return _amg().make_config(**kw) if kw else None
+
+
+# name -> (A builder, b builder, oracle kwargs, library config kwargs)
+def _case(name):
+    if name == "c1":
+        A, b, _ = config_problem(1)
+        return A, b, {}, {}
+    if name == "c2":
+        A, b, _ = config_problem(2)
+        return A, b, {}, {}
+    if name == "c3_64":  # config-3 analogue: anisotropic, 2/2 sweeps
+        A, b, _ = config_problem(3, grid=(64, 64, 64))
+        kw = dict(pre_sweeps=2, post_sweeps=2)
+        return A, b, kw, kw
+    if name == "c4_64x64x128":  # config-4 analogue, 2-slab weak-scaling shape, maxsize 200*2
+        A, b, _ = config_problem(4, grid=(64, 64, 128))
+        kw = dict(max_coarse_size=400)
+        return A, b, kw, kw
+    if name == "c5_32":  # config-5 analogue: 27-point jump coefficients
+        A = jump27(32)
+        b = uniform01(5, A.n_global)
+        return A, b, {}, {}
+    if name == "ragged_17x13x11":
+        A = poisson7(17, 13, 11)
+        b = uniform_pm1(7, A.n_global)
+        return A, b, {}, {}
+    if name == "unsmoothed_24":
+        A = poisson7(24, 24, 24)
+        b = np.ones(A.n_global)
+        kw = dict(smooth_prolongator=0)
+        return A, b, kw, kw
+    if name == "omega_text_32":  # reading R3 alternative: omega = 1/||D^-1 A||
+        A = poisson7(32, 32, 32)
+        b = np.ones(A.n_global)
+        kw = dict(prol_omega_scale=1.0)
+        return A, b, kw, kw
+    if name == "single_level":
+        A = poisson7(5, 4, 3)
+        b = uniform01(3, A.n_global)
+        return A, b, {}, {}
+    raise KeyError(name)
+
+
+CASES = ["c1", "c2", "c3_64", "c4_64x64x128", "c5_32", "ragged_17x13x11", "unsmoothed_24",
+         "omega_text_32", "single_level"]
+_cache = {}
+
+
+def _built(ctx, name):
+    if name not in _cache:
+        A, b, okw, lkw = _case(name)
+        ho = O.OracleHierarchy(A, **okw)
+        h = _amg().Hierarchy(ctx, A, cfg=_cfg(**lkw))
+        _cache.clear()
+        _cache[name] = (A, b, ho, h)
+    return _cache[name]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_hierarchy_and_aggregates_bit_exact(ctx, name):
+    A, b, ho, h = _built(ctx, name)
+    assert h.sizes() == ho.sizes()
+    for l in range(h.nlevels):
+        info = h.level_info(l)
+        assert info["nnzA"] == ho.nnz(l)
+    for l in range(h.nlevels - 1):
+        assert np.array_equal(h.level_aggregates(l), ho.agg(l)), f"level {l}"
+    rep = h.report()
+    assert rep["opc"] == pytest.approx(ho.opc, rel=1e-15)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_vcycle_parity(ctx, name):
+    A, b, ho, h = _built(ctx, name)
+    r = uniform_pm1(1000 + len(name), A.n_global)  # seeded parity vector (R17)
+    z = h.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    zo = ho.vcycle(r)
+    rel = np.linalg.norm(z - zo) / np.linalg.norm(zo)
+    assert rel <= VCYCLE_TOL, rel
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pcg_parity(ctx, name):
+    A, b, ho, h = _built(ctx, name)
+    bt = torch.tensor(b, device="cuda:0")
+    x, rep = h.solve(bt, rtol=1e-6, maxit=500)
+    xo, info = ho.pcg(b, rtol=1e-6, maxit=500)
+    assert rep["converged"] == 1 and info["status"] == O.OR_OK
+    assert abs(rep["iterations"] - info["iterations"]) <= 1, (rep["iterations"], info["iterations"])
+    assert rep["final_relres"] <= 1e-6
+    k = min(rep["iterations"], info["iterations"])
+    x, rep2 = h.solve(bt, rtol=0.0, maxit=k)
+    assert rep2["iterations"] == k
+    xo, _ = ho.pcg(b, rtol=0.0, maxit=k)
+    rel = np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo)
+    assert rel <= X_TOL, rel
+
+
+def test_pcg_edge_cases(ctx):
+    amg = _amg()
+    A = poisson7(12, 10, 9)
+    h = amg.Hierarchy(ctx, A)
+    n = A.n_global
+    # b = 0 -> x = 0 after 0 iterations
+    x, rep = h.solve(torch.zeros(n, dtype=torch.float64, device="cuda:0"))
+    assert rep["iterations"] == 0 and rep["converged"] == 1 and not x.any()
+    b = torch.tensor(uniform01(11, n), device="cuda:0")
+    # maxit = 0 -> not converged, x = 0
+    x, rep = h.solve(b, rtol=1e-6, maxit=0)
+    assert rep["iterations"] == 0 and rep["converged"] == 0 and not x.any()
+    # rtol = 0 runs exactly maxit iterations
+    x, rep = h.solve(b, rtol=0.0, maxit=7)
+    assert rep["iterations"] == 7 and rep["converged"] == 0
+    # determinism: bitwise identical repeats
+    x1, _ = h.solve(b, rtol=1e-8)
+    x2, _ = h.solve(b, rtol=1e-8)
+    assert torch.equal(x1, x2)
+    # host-buffer entry point == device entry point
+    xh, reph = h.solve_host(b.cpu().numpy(), rtol=1e-8)
+    assert np.array_equal(xh, x1.cpu().numpy())
+
+
+def test_eager_launches_equal_graph(ctx):
+    amg = _amg()
+    A = poisson7(20, 18, 16)
+    b = torch.tensor(uniform01(12, A.n_global), device="cuda:0")
+    hg = amg.Hierarchy(ctx, A)
+    he = amg.Hierarchy(ctx, A, cfg=amg.make_config(use_graphs=0))
+    xg, rg = hg.solve(b)
+    xe, re_ = he.solve(b)
+    assert rg["iterations"] == re_["iterations"]
+    assert torch.equal(xg, xe)
+    assert torch.equal(hg.precond_apply(b), he.precond_apply(b))
+
+
+def test_build_errors(ctx):
+    amg = _amg()
+    A = poisson7(4, 4, 4)
+    A.values = A.values.copy()
+    A.values[1] = -2.0  # breaks symmetry
+    with pytest.raises(amg.AmgError) as e:
+        amg.Hierarchy(ctx, A)
+    assert e.value.code == 1
+    A = poisson7(4, 4, 4)
+    A.values = -A.values  # negative diagonal
+    with pytest.raises(amg.AmgError) as e:
+        amg.Hierarchy(ctx, A)
+    assert e.value.code == 2
+
+
+def test_vcycle_properties_full_c4(ctx):
+    """BASELINE config 4 at its full per-GPU size (256^3), in the configuration
+    bench.py times: level-0 aggregates equal the closed-form 2x2x2 cubes (pin P4),
+    the device V-cycle is linear and symmetric, and PCG converges with a true
+    residual at the requested tolerance."""
+    amg = _amg()
+    A, b, meta = config_problem(4)
+    h = amg.Hierarchy(ctx, A)
+    nx = 256
+    i = np.arange(A.n_global)
+    x, y, z = i % nx, (i // nx) % nx, i // (nx * nx)
+    cube = x // 2 + (nx // 2) * (y // 2 + (nx // 2) * (z // 2))
+    assert np.array_equal(h.level_aggregates(0), cube)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    r = torch.rand(A.n_global, generator=g, dtype=torch.float64).cuda()
+    s = torch.rand(A.n_global, generator=g, dtype=torch.float64).cuda()
+    Br, Bs = h.precond_apply(r).clone(), h.precond_apply(s).clone()
+    lin = h.precond_apply(2.0 * r - 3.0 * s)
+    assert (torch.linalg.norm(lin - (2.0 * Br - 3.0 * Bs)) / torch.linalg.norm(lin)).item() <= 1e-12
+    sym = abs(torch.dot(Br, s) - torch.dot(r, Bs)).item()
+    assert sym <= 1e-12 * torch.linalg.norm(r).item() * torch.linalg.norm(s).item()
+    assert torch.dot(r, Br).item() > 0
+    bt = torch.tensor(b, device="cuda:0")
+    xs, rep = h.solve(bt, rtol=1e-6)
+    assert rep["converged"] == 1
+    Asp = torch.sparse_csr_tensor(torch.tensor(A.rowptr), torch.tensor(A.colind), torch.tensor(A.values),
+                                  size=(A.n_global, A.n_global)).cuda()
+    res = bt - (Asp @ xs.unsqueeze(1)).squeeze(1)
+    assert (torch.linalg.norm(res) / torch.linalg.norm(bt)).item() <= 1.5e-6
