@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,6 +41,7 @@ void set_err(const std::string& s) { g_err = s; }
     } while (0)
 
 enum { FMT_SELL = 0, FMT_CSRV = 1, FMT_DENSE = 2 };
+constexpr int kVWBlock = 256;  // CSR-vector "VW" value meaning one block per row
 
 struct DevMat {
     int fmt = FMT_SELL;
@@ -67,6 +69,7 @@ struct DevLevel {
     DevMat A, P, R;
     double* m = nullptr;
     double* b = nullptr;   // rhs of the level (unused at level 0: the caller's vector)
+    double* mb = nullptr;  // m o b, written by the restriction into this level (levels >= 1)
     double* r = nullptr;   // residual
     double* xa = nullptr;  // the level's x (output of its V-cycle)
     double* xb = nullptr;  // ping-pong partner
@@ -126,6 +129,7 @@ struct amg_hier_s {
             D.R.release();
             cudaFree(D.m);
             cudaFree(D.b);
+            cudaFree(D.mb);
             cudaFree(D.r);
             cudaFree(D.xa);
             cudaFree(D.xb);
@@ -194,6 +198,13 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
     } else {
         const CsrView v{M.rp, M.col, M.val, M.nrows};
         const int64_t need = (M.nrows * M.vw + kBlock - 1) / kBlock;
+        if (M.vw == kVWBlock) {
+            static const int cap = max_grid((const void*)k_csrb<G, E>, nsm);
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(M.nrows, cap));
+            k_csrb<G, E><<<grid, kBlock, 0, L.s>>>(v, g, e, rc);
+            L.end();
+            return;
+        }
         switch (M.vw) {
 #define VWCASE(W)                                                                 \
     case W: {                                                                     \
@@ -244,12 +255,18 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const double* b0, double* z0, cons
         const double n8 = 8.0 * (double)D.n;
         if (s1 == 1) {
             // x = m o b is never stored: r = b - A (m o b)
-            launch_mat(L, D.A, GMB{D.m, b}, EResid{b, D.r}, no_red(), "resid0", 3 * n8);
+            if (l == 0)
+                launch_mat(L, D.A, GMB{D.m, b}, EResid{b, D.r}, no_red(), "resid0", 3 * n8);
+            else
+                launch_mat(L, D.A, GVec{D.mb}, EResid{b, D.r}, no_red(), "resid0", 3 * n8);
         } else {
             // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
             double* xi = D.xa;
             double* xo = D.xb;
-            launch_mat(L, D.A, GMB{D.m, b}, ESweep0{b, D.m, xi}, no_red(), "sweep0", 3 * n8);
+            if (l == 0)
+                launch_mat(L, D.A, GMB{D.m, b}, ESweep0{b, D.m, xi}, no_red(), "sweep0", 3 * n8);
+            else
+                launch_mat(L, D.A, GVec{D.mb}, ESweep0{b, D.m, xi}, no_red(), "sweep0", 3 * n8);
             for (int s = 2; s < s1; ++s) {
                 launch_mat(L, D.A, GVec{xi}, ESweep<false>{xi, b, D.m, xo}, no_red(), "presweep", 4 * n8);
                 std::swap(xi, xo);
@@ -257,9 +274,13 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const double* b0, double* z0, cons
             launch_mat(L, D.A, GVec{xi}, EResid{b, D.r}, no_red(), "resid", 3 * n8);
             xpre[l] = xi;
         }
-        double* bc = (l + 1 < nlev) ? h->lv[l + 1].b : h->cb;
-        const int64_t nc = (l + 1 < nlev) ? h->lv[l + 1].n : h->nL;
-        launch_mat(L, D.R, GVec{D.r}, EStore{bc}, no_red(), "restrict", n8 + 8.0 * (double)nc);
+        if (l + 1 < nlev) {
+            DevLevel& C = h->lv[l + 1];
+            launch_mat(L, D.R, GVec{D.r}, EStoreMB{C.b, C.m, C.mb}, no_red(), "restrict",
+                       n8 + 24.0 * (double)C.n);
+        } else {
+            launch_mat(L, D.R, GVec{D.r}, EStore{h->cb}, no_red(), "restrict", n8 + 8.0 * (double)h->nL);
+        }
     }
     enqueue_coarse(h, L, h->cb, h->cx);  // z_L = A_L^{-1} b_L (reading R2)
     // ---- up: prolongation, post-smoothing
@@ -274,7 +295,10 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const double* b0, double* z0, cons
                                              // may run in place on xpre
         double* dst = (s2 % 2 == 1) ? tmp : fin;
         if (s1 == 1) {
-            launch_mat(L, D.P, GVec{e}, EProlong0{b, D.m, dst}, no_red(), "prolong0", 3 * n8 + 8.0 * nc);
+            if (l == 0)
+                launch_mat(L, D.P, GVec{e}, EProlong0{b, D.m, dst}, no_red(), "prolong0", 3 * n8 + 8.0 * nc);
+            else
+                launch_mat(L, D.P, GVec{e}, EProlongMB{D.mb, dst}, no_red(), "prolong0", 2 * n8 + 8.0 * nc);
         } else {
             launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[l], dst}, no_red(), "prolong", 2 * n8 + 8.0 * nc);
         }
@@ -353,7 +377,10 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D) {
     int64_t padded = 0;
     for (int64_t s = 0; s < nsl; ++s) padded += 32 * (int64_t)width[s];
     const double mean = n ? (double)nnz / (double)n : 0.0;
-    const bool sell = mean <= 48.0 && (double)padded <= 1.15 * (double)nnz + 64.0 &&
+    // SELL-32 (one thread per row, coalesced column-major slices) needs little padding and
+    // enough slices to fill the GPU (>= ~16 warps per SM); long rows are fine there because
+    // every lane streams its own row with many loads in flight.
+    const bool sell = (double)padded <= 1.10 * (double)nnz + 64.0 && nsl >= 148 * 16 &&
                       padded / 32 < (int64_t)UINT32_MAX;
     if (sell) {
         D.fmt = FMT_SELL;
@@ -386,7 +413,13 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D) {
         }
         D.fmt = FMT_CSRV;
         D.stored = nnz;
-        D.vw = mean <= 3 ? 2 : mean <= 12 ? 4 : mean <= 40 ? 8 : mean <= 160 ? 16 : 32;
+        // lanes per row: enough threads to fill 148 SMs x 2048 threads, 2..32 lanes per
+        // row inside a warp, or a whole block per row for few very long rows
+        const double want = 148.0 * 2048.0 / (double)std::max<int64_t>(n, 1);
+        int vw = 2;
+        while (vw < 32 && (vw < want || vw * 8 < mean) && vw * 2 <= std::max(2.0, mean)) vw *= 2;
+        if (mean >= 256.0 && (double)n * 32.0 < 148.0 * 2048.0 * 2.0) vw = kVWBlock;
+        D.vw = vw;
         std::vector<int32_t> rp(n + 1);
         for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)M.rp[i];
         int st;
@@ -617,6 +650,9 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     amg_config_t cfg;
     amg_config_default(&cfg);
     if (cfg_in) cfg = *cfg_in;
+    // AMG_EAGER=1 forces eager launches (ncu cannot profile kernels inside graphs
+    // that contain conditional nodes)
+    if (const char* ev = std::getenv("AMG_EAGER")) cfg.use_graphs = (ev[0] == '1') ? 0 : cfg.use_graphs;
     CK(cudaSetDevice(ctx->device));
 
     amgsetup::Hierarchy H;
@@ -649,6 +685,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         if ((st = upload_mat(S.R, D.R))) return fail(st);
         if ((st = dev_copy(&D.m, S.m.data(), S.m.size()))) return fail(st);
         if (l > 0 && (st = dev_alloc(&D.b, D.n))) return fail(st);
+        if (l > 0 && (st = dev_alloc(&D.mb, D.n))) return fail(st);
         if ((st = dev_alloc(&D.r, D.n))) return fail(st);
         if ((st = dev_alloc(&D.xa, D.n))) return fail(st);
         if ((st = dev_alloc(&D.xb, D.n))) return fail(st);

@@ -206,6 +206,29 @@ struct EStore {
         return 0.0;
     }
 };
+// y = s ; mb = m o y                         (restriction that also pre-multiplies the
+//                                             coarse rhs by the coarse l1 diagonal)
+struct EStoreMB {
+    static constexpr bool kDot = false;
+    double* __restrict__ y;
+    const double* __restrict__ m;
+    double* __restrict__ mb;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        y[i] = s;
+        mb[i] = m[i] * s;
+        return 0.0;
+    }
+};
+// x = mb + s                                (prolongation after one pre-sweep from 0, mb = m o b)
+struct EProlongMB {
+    static constexpr bool kDot = false;
+    const double* __restrict__ mb;
+    double* __restrict__ xo;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        xo[i] = mb[i] + s;
+        return 0.0;
+    }
+};
 // x = m b + s                               (prolongation after one pre-sweep from 0)
 struct EProlong0 {
     static constexpr bool kDot = false;
@@ -295,6 +318,32 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
 #pragma unroll
         for (int o = VW / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, VW);
         if (sub == 0 && row < A.n) d += e(row, acc);
+    }
+    if constexpr (E::kDot) grid_reduce(d, rc);
+}
+
+// ------------------------------------------------------- CSR block-per-row
+// For few, long rows (deep levels: hundreds to thousands of entries per row):
+// one 256-thread block per row, fixed-order block reduction.
+template <class G, class E>
+__global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc) {
+    __shared__ double part[kBlock / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double d = 0.0;
+    for (int64_t row = blockIdx.x; row < A.n; row += gridDim.x) {
+        const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
+        double acc = 0.0;
+#pragma unroll 4
+        for (int32_t k = k0 + threadIdx.x; k < k1; k += kBlock) acc += ld_stream(A.v + k) * g(ld_stream(A.ci + k));
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) part[wid] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < kBlock / 32; ++w) s += part[w];
+            d += e(row, s);
+        }
+        __syncthreads();
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
 }
