@@ -89,7 +89,8 @@ typedef struct {
 void amg_config_default(amg_config_t* cfg);
 
 /* Creates a context bound to CUDA device `device` and stream `cuda_stream`
- * (a cudaStream_t; NULL = the legacy default stream).  For nranks > 1,
+ * (a cudaStream_t; NULL = a non-blocking stream created and owned by the context —
+ * CUDA graphs cannot be captured on the legacy default stream).  For nranks > 1,
  * `nccl_unique_id` points to the 128-byte ncclUniqueId produced by rank 0 and
  * broadcast by the caller (e.g. through torch.distributed); it is ignored when
  * nranks == 1.  Returns AMG_ERR_ARG for rank/nranks out of range, AMG_ERR_CUDA /
@@ -135,7 +136,8 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev);
 /* Hierarchy inspection.
  * amg_level_info: global rows, global nnz of A_l and P-bar_l (0 at the coarsest),
  * this rank's row block of level l and the device storage format of A_l
- * (0 = SELL-32, 1 = CSR-vector, 2 = dense inverse (coarsest)). */
+ * (0 = SELL-32, 1 = CSR-vector, 2 = dense inverse (coarsest), 3 = SDIA-32: slices of 32
+ * rows aligned by column offset, no per-entry column index). */
 int amg_num_levels(amg_hier_t h, int32_t* nlevels);
 int amg_level_info(amg_hier_t h, int32_t lvl, int64_t* n_global, int64_t* nnzA_global,
                    int64_t* nnzP_global, int64_t* row_begin, int64_t* row_end, int32_t* format);
@@ -148,10 +150,14 @@ int amg_hierarchy_report(amg_hier_t h, amg_report_t* rep);
 /* Kernel timing probe: runs `napply` V-cycles with CUDA events around every kernel
  * on the context stream (eager launches) and writes, for up to `cap` kernels of
  * one V-cycle in launch order, the average device milliseconds (ms_out), the
- * algorithmic bytes of one launch per SURVEY.md §8d (bytes_out) and a static name
- * (names_out, may be NULL).  *count receives the number of kernels per V-cycle. */
+ * algorithmic bytes of one launch per SURVEY.md §8d (bytes_out: 12 B per stored
+ * entry + 4 B per row for every operator), the bytes the chosen device format
+ * actually has to move (stored_bytes_out; smaller than bytes_out for SDIA-32,
+ * which stores no per-entry column index) and a static name (names_out).  Any
+ * output pointer may be NULL.  *count receives the number of kernels per V-cycle. */
 int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out,
-                       double* bytes_out, const char** names_out, int32_t* count);
+                       double* bytes_out, double* stored_bytes_out, const char** names_out,
+                       int32_t* count);
 
 /* ---- Host-only view of the setup phase (no device needed) -----------------
  * Runs exactly the setup that amg_hierarchy_build runs (the same C++ code) on a

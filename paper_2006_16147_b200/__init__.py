@@ -160,9 +160,11 @@ class Hierarchy:
     def profile_vcycle(self, napply: int = 10, cap: int = 256):
         ms = np.zeros(cap)
         by = np.zeros(cap)
+        sb = np.zeros(cap)
         names = (C.c_char_p * cap)()
         cnt = C.c_int32()
-        check(lib.amg_profile_vcycle(self.h, napply, cap, _ptr(ms), _ptr(by), names, C.byref(cnt)),
+        check(lib.amg_profile_vcycle(self.h, napply, cap, _ptr(ms), _ptr(by), _ptr(sb), names, C.byref(cnt)),
               "amg_profile_vcycle")
         k = min(cnt.value, cap)
-        return [dict(name=names[i].decode(), ms=float(ms[i]), bytes=float(by[i])) for i in range(k)]
+        return [dict(name=names[i].decode(), ms=float(ms[i]), bytes=float(by[i]), stored_bytes=float(sb[i]))
+                for i in range(k)]

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libamg_b200.so")
 
 AMG_OK, AMG_ERR_ARG, AMG_ERR_NOT_SPD, AMG_ERR_CUDA, AMG_ERR_NCCL, AMG_ERR_OOM = 0, 1, 2, 3, 4, 5
 AMG_NOT_CONVERGED, AMG_ERR_BREAKDOWN = 6, 7
-FORMATS = {0: "sell32", 1: "csr_vector", 2: "dense_inverse"}
+FORMATS = {0: "sell32", 1: "csr_vector", 2: "dense_inverse", 3: "sdia32"}
 
 
 class amg_config_t(C.Structure):
@@ -58,7 +58,7 @@ _SIG = {
                                  C.POINTER(C.c_int32)]),
     "amg_level_aggregates": (C.c_int, [_vp, C.c_int32, _vp]),
     "amg_hierarchy_report": (C.c_int, [_vp, C.POINTER(amg_report_t)]),
-    "amg_profile_vcycle": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp,
+    "amg_profile_vcycle": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp,
                                      C.POINTER(C.c_int32)]),
     "amg_last_error": (C.c_char_p, []),
 }

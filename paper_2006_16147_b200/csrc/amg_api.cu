@@ -40,25 +40,37 @@ void set_err(const std::string& s) { g_err = s; }
         }                                                                        \
     } while (0)
 
-enum { FMT_SELL = 0, FMT_CSRV = 1, FMT_DENSE = 2 };
+enum { FMT_SELL = 0, FMT_CSRV = 1, FMT_DENSE = 2, FMT_SDIA = 3 };
 constexpr int kVWBlock = 256;  // CSR-vector "VW" value meaning one block per row
 
 struct DevMat {
     int fmt = FMT_SELL;
     int vw = 32;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
-    uint32_t* sptr = nullptr;  // SELL
+    uint32_t* sptr = nullptr;  // SELL / SDIA
+    int32_t* offs = nullptr;   // SDIA: one column offset per slice column
     int32_t* rp = nullptr;     // CSR
     int32_t* col = nullptr;
     double* val = nullptr;
     // algorithmic bytes of one pass over the operator: 12 nnz + 4 (n+1)
     double model_bytes() const { return 12.0 * (double)nnz + 4.0 * (double)(nrows + 1); }
+    // bytes the chosen device format actually stores for one pass
+    double stored_bytes() const {
+        const double nsl = (double)((nrows + 31) / 32);
+        switch (fmt) {
+            case FMT_SELL: return 12.0 * (double)stored + 4.0 * (nsl + 1);
+            case FMT_SDIA: return 8.0 * (double)stored + 4.0 * (double)stored / 32.0 + 4.0 * (nsl + 1);
+            default: return 12.0 * (double)nnz + 4.0 * (double)(nrows + 1);
+        }
+    }
     void release() {
         cudaFree(sptr);
+        cudaFree(offs);
         cudaFree(rp);
         cudaFree(col);
         cudaFree(val);
         sptr = nullptr;
+        offs = nullptr;
         rp = col = nullptr;
         val = nullptr;
     }
@@ -80,7 +92,8 @@ struct DevLevel {
 
 struct KernelRec {
     const char* name;
-    double bytes;
+    double bytes;         // algorithmic
+    double stored_bytes;  // what the device format actually moves (compulsory)
     cudaEvent_t e0, e1;
 };
 
@@ -173,9 +186,9 @@ int vec_grid(int64_t n, int nsm) {
 struct Launch {
     amg_hier_s* h;
     cudaStream_t s;
-    void begin(const char* name, double bytes) {
+    void begin(const char* name, double bytes, double stored = -1.0) {
         if (!h->prof) return;
-        KernelRec r{name, bytes, nullptr, nullptr};
+        KernelRec r{name, bytes, stored < 0.0 ? bytes : stored, nullptr, nullptr};
         cudaEventCreate(&r.e0);
         cudaEventCreate(&r.e1);
         cudaEventRecord(r.e0, s);
@@ -189,8 +202,13 @@ struct Launch {
 template <class G, class E>
 void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* name, double vec_bytes) {
     const int nsm = L.h->ctx->nsm;
-    L.begin(name, M.model_bytes() + vec_bytes);
-    if (M.fmt == FMT_SELL) {
+    L.begin(name, M.model_bytes() + vec_bytes, M.stored_bytes() + vec_bytes);
+    if (M.fmt == FMT_SDIA) {
+        static const int cap = max_grid((const void*)k_sdia<G, E>, nsm);
+        const int64_t need = (M.nrows + kBlock - 1) / kBlock;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
+        k_sdia<G, E><<<grid, kBlock, 0, L.s>>>(SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols}, g, e, rc);
+    } else if (M.fmt == FMT_SELL) {
         static const int cap = max_grid((const void*)k_sell<G, E>, nsm);
         const int64_t need = (M.nrows + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
@@ -377,6 +395,50 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D) {
     int64_t padded = 0;
     for (int64_t s = 0; s < nsl; ++s) padded += 32 * (int64_t)width[s];
     const double mean = n ? (double)nnz / (double)n : 0.0;
+    // SDIA-32 candidate: per slice, the sorted distinct offsets col - row
+    if (M.nrows == M.ncols && nsl >= 148 * 16 && mean <= 64.0) {
+        std::vector<uint32_t> dw(nsl, 0);
+        std::vector<std::vector<int32_t>> soffs(nsl);
+#pragma omp parallel for schedule(static)
+        for (int64_t s = 0; s < nsl; ++s) {
+            auto& o = soffs[s];
+            for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r)
+                for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t) o.push_back((int32_t)((int64_t)M.ci[t] - r));
+            std::sort(o.begin(), o.end());
+            o.erase(std::unique(o.begin(), o.end()), o.end());
+            dw[s] = (uint32_t)o.size();
+        }
+        int64_t dpad = 0;
+        for (int64_t s = 0; s < nsl; ++s) dpad += 32 * (int64_t)dw[s];
+        if ((double)dpad <= 1.02 * (double)padded + 64.0 && dpad / 32 < (int64_t)UINT32_MAX) {
+            D.fmt = FMT_SDIA;
+            D.stored = dpad;
+            std::vector<uint32_t> sptr(nsl + 1, 0);
+            for (int64_t s = 0; s < nsl; ++s) sptr[s + 1] = sptr[s] + dw[s];
+            std::vector<int32_t> offs(dpad / 32);
+            std::vector<double> val(dpad, 0.0);
+#pragma omp parallel for schedule(static)
+            for (int64_t s = 0; s < nsl; ++s) {
+                const auto& o = soffs[s];
+                std::copy(o.begin(), o.end(), offs.begin() + sptr[s]);
+                const int64_t base = (int64_t)sptr[s] * 32;
+                for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r) {
+                    const int64_t lane = r - s * 32;
+                    size_t k = 0;
+                    for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t) {
+                        const int32_t d = (int32_t)((int64_t)M.ci[t] - r);
+                        while (o[k] != d) ++k;  // both ascending
+                        val[base + (int64_t)k * 32 + lane] = M.v[t];
+                    }
+                }
+            }
+            int st;
+            if ((st = dev_copy(&D.sptr, sptr.data(), sptr.size()))) return st;
+            if ((st = dev_copy(&D.offs, offs.data(), offs.size()))) return st;
+            if ((st = dev_copy(&D.val, val.data(), val.size()))) return st;
+            return AMG_OK;
+        }
+    }
     // SELL-32 (one thread per row, coalesced column-major slices) needs little padding and
     // enough slices to fill the GPU (>= ~16 warps per SM); long rows are fine there because
     // every lane streams its own row with many loads in flight.
@@ -418,7 +480,9 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D) {
         const double want = 148.0 * 2048.0 / (double)std::max<int64_t>(n, 1);
         int vw = 2;
         while (vw < 32 && (vw < want || vw * 8 < mean) && vw * 2 <= std::max(2.0, mean)) vw *= 2;
-        if (mean >= 256.0 && (double)n * 32.0 < 148.0 * 2048.0 * 2.0) vw = kVWBlock;
+        static const double block_mean = std::getenv("AMG_BLOCK_MEAN") ? std::atof(std::getenv("AMG_BLOCK_MEAN")) : 256.0;
+        static const double block_rows = std::getenv("AMG_BLOCK_ROWS") ? std::atof(std::getenv("AMG_BLOCK_ROWS")) : 18944.0;
+        if (mean >= block_mean && (double)n < block_rows) vw = kVWBlock;
         D.vw = vw;
         std::vector<int32_t> rp(n + 1);
         for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)M.rp[i];
@@ -878,7 +942,7 @@ int amg_hierarchy_report(amg_hier_t h, amg_report_t* rep) {
 }
 
 int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out, double* bytes_out,
-                       const char** names_out, int32_t* count) {
+                       double* stored_bytes_out, const char** names_out, int32_t* count) {
     if (!h || napply < 1 || !count) {
         set_err("amg_profile_vcycle: bad argument");
         return AMG_ERR_ARG;
@@ -906,6 +970,7 @@ int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out
         }
         if (ms_out) ms_out[k] = tot / napply;
         if (bytes_out) bytes_out[k] = recs[k].bytes;
+        if (stored_bytes_out) stored_bytes_out[k] = recs[k].stored_bytes;
         if (names_out) names_out[k] = recs[k].name;
     }
     for (auto& r : recs) {

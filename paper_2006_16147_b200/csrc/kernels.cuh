@@ -290,6 +290,45 @@ __global__ void __launch_bounds__(kBlock) k_sell(SellView A, G g, E e, RedCtx rc
     if constexpr (E::kDot) grid_reduce(d, rc);
 }
 
+// ------------------------------------------------------------ SDIA-32 kernel
+// Sliced-diagonal layout for square stencil-like operators: inside a slice of
+// 32 rows the entries are aligned by their offset d = col - row (one int32 per
+// slice column, shared by the 32 lanes), so no per-entry column index is
+// stored.  Holes (a row without that offset) hold value 0; their column is
+// clamped into range.  Entry order inside a row stays ascending in column.
+struct SdiaView {
+    const uint32_t* __restrict__ sptr;  // nslices+1, offsets in units of 32 entries
+    const int32_t* __restrict__ offs;   // one offset per slice column (sptr units)
+    const double* __restrict__ val;
+    int64_t n;
+    int32_t ncols;
+};
+
+template <class G, class E>
+__global__ void __launch_bounds__(kBlock) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
+    const int64_t nslices = (A.n + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
+    double d = 0.0;
+    for (int64_t s = w0; s < nslices; s += nw) {
+        const uint32_t b0 = __ldg(A.sptr + s);
+        const uint32_t w = __ldg(A.sptr + s + 1) - b0;
+        const int64_t row = (s << 5) + lane;
+        const int32_t* o = A.offs + b0;
+        const double* v = A.val + (int64_t)b0 * 32 + lane;
+        const int32_t rmax = A.ncols - 1;
+        double acc = 0.0;
+#pragma unroll 8
+        for (uint32_t k = 0; k < w; ++k) {
+            const int32_t c = min(max((int32_t)row + __ldg(o + k), 0), rmax);
+            acc += ld_stream(v + 32 * k) * g(c);
+        }
+        if (row < A.n) d += e(row, acc);
+    }
+    if constexpr (E::kDot) grid_reduce(d, rc);
+}
+
 // ---------------------------------------------------------- CSR-vector kernel
 struct CsrView {
     const int32_t* __restrict__ rp;
