@@ -67,7 +67,12 @@ typedef struct {
                                      this are held whole on every rank (default 64 MiB) */
     int32_t setup_threads;        /* host OpenMP threads for setup; 0 = all available */
     int32_t use_graphs;           /* 1 (default): solve/apply run as CUDA graphs; 0: eager
-                                     launches (debug / per-kernel timing) */
+                                     launches (debug / per-kernel timing).  Multi-rank solves
+                                     always run eagerly with one status read per iteration. */
+    int32_t emulate_ranks;        /* single-rank contexts only: > 1 partitions the hierarchy into
+                                     this many equal row blocks held by ONE process on one GPU and
+                                     runs the multi-rank kernels with in-process halo copies
+                                     ("loopback"); the caller's vectors stay global.  Default 1. */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */
@@ -87,6 +92,9 @@ typedef struct {
 
 /* Fills *cfg with the defaults listed above. */
 void amg_config_default(amg_config_t* cfg);
+
+/* Writes a fresh 128-byte ncclUniqueId to out128 (call on rank 0, then broadcast). */
+int amg_nccl_unique_id(void* out128);
 
 /* Creates a context bound to CUDA device `device` and stream `cuda_stream`
  * (a cudaStream_t; NULL = a non-blocking stream created and owned by the context —
@@ -180,6 +188,21 @@ int amg_host_level_aggregates(amg_host_hier_t h, int32_t lvl, int64_t* agg_out);
  * int64 rowptr (n_l+1), int64 colind and fp64 values (nnz entries). */
 int amg_host_level_matrix(amg_host_hier_t h, int32_t lvl, int32_t which, int64_t* rowptr,
                           int64_t* colind, double* values);
+
+/* Partition plan of the host hierarchy over `nranks` ranks with level-0 row blocks
+ * row_bounds[0..nranks] (coarse rows owned by the rank of their
+ * aggregate's minimum member; levels whose operator bytes are <= replicate_below_bytes,
+ * and the coarsest, replicated).  Host only; inspected with amg_host_plan_level /
+ * amg_host_plan_array (used by the CPU multi-rank tests). */
+int amg_host_partition(amg_host_hier_t h, int32_t nranks, const int64_t* row_bounds,
+                       int64_t replicate_below_bytes);
+/* info16 = {replicated, n_global, own_begin, own_end, comp_begin, comp_end, win_begin,
+ * win_end, rst_begin, rst_end, n_recv, n_send, nnz(A_loc), nnz(P_loc), nnz(R_loc), 0} */
+int amg_host_plan_level(amg_host_hier_t h, int32_t rank, int32_t lvl, int64_t* info16);
+/* which: 0 recv_off (nranks+1, int64), 1 recv_ids, 2 send_off, 3 send_ids (global ids,
+ * int64), 4/5/6 A_loc rowptr/colind (int64, window frame)/values, 7/8/9 P_loc, 10/11/12
+ * R_loc, 13 l1 inverse diagonal over the window (fp64).  Caller-allocated. */
+int amg_host_plan_array(amg_host_hier_t h, int32_t rank, int32_t lvl, int32_t which, void* out);
 
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* amg_last_error(void);

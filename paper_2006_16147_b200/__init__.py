@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _abi
 from ._abi import (AMG_ERR_BREAKDOWN, AMG_NOT_CONVERGED, AMG_OK, AmgError, amg_config_default,  # noqa: F401
-                   amg_config_t, amg_last_error, amg_report_t, check, lib)
+                   amg_config_t, amg_last_error, amg_report_t, check, lib, nccl_unique_id)
 
 __all__ = ["Context", "Hierarchy", "amg_config_default", "AmgError", "lib"]
 

@@ -23,7 +23,7 @@ class amg_config_t(C.Structure):
                 ("max_levels", C.c_int32), ("min_coarsening_ratio", C.c_double),
                 ("pre_sweeps", C.c_int32), ("post_sweeps", C.c_int32),
                 ("replicate_below_bytes", C.c_int64), ("setup_threads", C.c_int32),
-                ("use_graphs", C.c_int32)]
+                ("use_graphs", C.c_int32), ("emulate_ranks", C.c_int32)]
 
 
 class amg_report_t(C.Structure):
@@ -61,6 +61,17 @@ _SIG = {
     "amg_profile_vcycle": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp,
                                      C.POINTER(C.c_int32)]),
     "amg_last_error": (C.c_char_p, []),
+    "amg_nccl_unique_id": (C.c_int, [_vp]),
+    "amg_host_hierarchy_build": (C.c_int, [C.c_int64, _vp, _vp, _vp, _vp, C.POINTER(amg_config_t),
+                                           C.POINTER(_vp)]),
+    "amg_host_hierarchy_destroy": (C.c_int, [_vp]),
+    "amg_host_num_levels": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
+    "amg_host_level_sizes": (C.c_int, [_vp, C.c_int32, _i64p, _i64p, _i64p, C.POINTER(C.c_double)]),
+    "amg_host_level_aggregates": (C.c_int, [_vp, C.c_int32, _vp]),
+    "amg_host_level_matrix": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp]),
+    "amg_host_partition": (C.c_int, [_vp, C.c_int32, _vp, C.c_int64]),
+    "amg_host_plan_level": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
+    "amg_host_plan_array": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp]),
 }
 for _name, (_res, _args) in _SIG.items():
     _f = getattr(lib, _name)
@@ -92,3 +103,9 @@ def amg_config_default() -> amg_config_t:
 
 def amg_last_error() -> str:
     return lib.amg_last_error().decode(errors="replace")
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib.amg_nccl_unique_id(buf), "amg_nccl_unique_id")
+    return buf.raw

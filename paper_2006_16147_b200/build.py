@@ -18,9 +18,15 @@ LIB = os.path.join(PKG, "libamg_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES_CXX = [os.path.join(CSRC, "setup", "setup.cpp")]
+
+def _nccl_dir():
+    import nvidia.nccl
+    return list(nvidia.nccl.__path__)[0]
+
+SOURCES_CXX = [os.path.join(CSRC, "setup", "setup.cpp"), os.path.join(CSRC, "setup", "partition.cpp")]
 SOURCES_CU = [os.path.join(CSRC, "amg_api.cu")]
 HEADERS = [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "setup", "setup.hpp"),
+           os.path.join(CSRC, "setup", "partition.hpp"),
            os.path.join(ROOT, "include", "amg_b200.h")]
 
 
@@ -48,14 +54,17 @@ def build_library(force: bool = False, verbose_ptxas: bool = False) -> str:
     for src in SOURCES_CU:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         if force or _stale(obj, [src] + HEADERS):
-            cmd = [NVCC] + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler",
+            cmd = [NVCC] + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-I", os.path.join(_nccl_dir(), "include"),
+                                   "-Xcompiler",
                                    "-fPIC,-fopenmp,-ffp-contract=off", "-c", src, "-o", obj]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
             _run(cmd)
         objs.append(obj)
     if force or _stale(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lgomp", "-Xlinker", "-z,defs"])
+        nlib = os.path.join(_nccl_dir(), "lib")
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
+             ["-lgomp", "-L", nlib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nlib}", "-Xlinker", "-z,defs"])
     return LIB
 
 

@@ -1,14 +1,28 @@
 // amg_api.cu — implementation of include/amg_b200.h.
 //
 // Host side: validates/copies the caller's CSR, runs the C++ setup
-// (csrc/setup), chooses a device format per operator, uploads, and drives the
-// solve phase.  Device side: kernels.cuh.  A PCG solve is ONE graph launch: a
-// prologue kernel followed by a CUDA-graph WHILE node whose body is
+// (csrc/setup), partitions the hierarchy over the ranks (csrc/setup/partition),
+// chooses a device format per operator, uploads, and drives the solve phase.
+// Device side: kernels.cuh.
+//
+// Single rank: a PCG solve is ONE graph launch — a prologue kernel followed by
+// a CUDA-graph WHILE node whose body is
 //   V-cycle(r -> z) [fused r^T z -> beta]   -> p = z + beta p
 //   q = A p [fused p^T q -> alpha]          -> x += alpha p, r -= alpha q [fused
 //   ||r||^2 -> convergence test -> cudaGraphSetConditional]
-// so the iteration count is decided on the device (no host round trip).
+// so the iteration count is decided on the device.
+//
+// Several ranks (north_star (4)): every rank owns a row block of
+// every distributed level and holds each level vector as a window of the global
+// vector; before each kernel that gathers a vector, its halo is exchanged
+// (pack -> NCCL send/recv over NVLink -> unpack).  Dot products reduce locally,
+// the per-rank totals are all-gathered and summed in rank order (identical and
+// deterministic on all ranks).  Deep levels are replicated after one gather.
+// The same per-rank code runs in "loopback" mode (cfg.emulate_ranks > 1): all
+// ranks live in one process on one GPU and the transport is a device copy,
+// which is how the multi-rank kernels are parity-tested on a single B200.
 #include <cuda_runtime.h>
+#include <nccl.h>
 #include <omp.h>
 
 #include <algorithm>
@@ -17,11 +31,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
 #include "../../include/amg_b200.h"
 #include "kernels.cuh"
+#include "setup/partition.hpp"
 #include "setup/setup.hpp"
 
 using namespace amgk;
@@ -40,6 +56,15 @@ void set_err(const std::string& s) { g_err = s; }
         }                                                                        \
     } while (0)
 
+#define NK(call)                                                         \
+    do {                                                                 \
+        ncclResult_t r_ = (call);                                        \
+        if (r_ != ncclSuccess) {                                         \
+            set_err(std::string(#call) + ": " + ncclGetErrorString(r_)); \
+            return AMG_ERR_NCCL;                                         \
+        }                                                                \
+    } while (0)
+
 enum { FMT_SELL = 0, FMT_CSRV = 1, FMT_DENSE = 2, FMT_SDIA = 3 };
 constexpr int kVWBlock = 256;  // CSR-vector "VW" value meaning one block per row
 
@@ -47,6 +72,7 @@ struct DevMat {
     int fmt = FMT_SELL;
     int vw = 32;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
+    int32_t shift = 0;         // SDIA: row -> window column frame
     uint32_t* sptr = nullptr;  // SELL / SDIA
     int32_t* offs = nullptr;   // SDIA: one column offset per slice column
     int32_t* rp = nullptr;     // CSR
@@ -76,18 +102,54 @@ struct DevMat {
     }
 };
 
+// Halo exchange plan of one level on one rank.
+struct Exch {
+    int64_t nsend = 0, nrecv = 0;
+    std::vector<int64_t> send_off, recv_off;  // np+1 (host)
+    int32_t* send_idx = nullptr;              // window positions to pack
+    int32_t* recv_idx = nullptr;              // window positions to unpack into
+    double* sbuf = nullptr;
+    double* rbuf = nullptr;
+    void release() {
+        cudaFree(send_idx);
+        cudaFree(recv_idx);
+        cudaFree(sbuf);
+        cudaFree(rbuf);
+        send_idx = recv_idx = nullptr;
+        sbuf = rbuf = nullptr;
+    }
+};
+
 struct DevLevel {
-    int64_t n = 0;
+    bool replicated = false;
+    bool coarsest = false;
+    int64_t n_global = 0;
+    int64_t own_begin = 0, own_n = 0;
+    int64_t comp_n = 0, win_n = 0;
+    int64_t ep_off = 0;    // comp_begin - win_begin
+    int64_t own_off = 0;   // own_begin - win_begin
+    int64_t rst_n = 0;     // rows of R computed here
+    int64_t rst_off = 0;   // rst_begin - next.win_begin
     DevMat A, P, R;
-    double* m = nullptr;
-    double* b = nullptr;   // rhs of the level (unused at level 0: the caller's vector)
-    double* mb = nullptr;  // m o b, written by the restriction into this level (levels >= 1)
-    double* r = nullptr;   // residual
-    double* xa = nullptr;  // the level's x (output of its V-cycle)
-    double* xb = nullptr;  // ping-pong partner
-    std::vector<int32_t> agg;
-    int sweeps = 0;
-    double omega = 0.0;
+    double* m = nullptr;   // window-sized vectors
+    double* b = nullptr;
+    double* mb = nullptr;
+    double* r = nullptr;
+    double* xa = nullptr;
+    double* xb = nullptr;
+    Exch ex;
+    void release() {
+        A.release();
+        P.release();
+        R.release();
+        cudaFree(m);
+        cudaFree(b);
+        cudaFree(mb);
+        cudaFree(r);
+        cudaFree(xa);
+        cudaFree(xb);
+        ex.release();
+    }
 };
 
 struct KernelRec {
@@ -97,6 +159,35 @@ struct KernelRec {
     cudaEvent_t e0, e1;
 };
 
+// Device state of one rank.
+struct RankState {
+    int rank = 0;
+    std::vector<DevLevel> lv;   // all levels; the last one is the (replicated) coarsest
+    double* cinv = nullptr;     // dense A_L^{-1}, row-major
+    int64_t nL = 0;
+    int64_t user_off = 0;       // offset of this rank's rows in the caller's vectors (loopback)
+    double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr;  // level-0 window vectors
+    PcgState* st = nullptr;
+    double* partials = nullptr;
+    unsigned int* ticket = nullptr;
+    double* dot_local = nullptr;  // this rank's dot total
+    double* dot_all = nullptr;    // all-gathered totals (np)
+    void release() {
+        for (auto& D : lv) D.release();
+        cudaFree(cinv);
+        cudaFree(pr);
+        cudaFree(pz);
+        cudaFree(pp);
+        cudaFree(pq);
+        cudaFree(st);
+        cudaFree(partials);
+        cudaFree(ticket);
+        cudaFree(dot_local);
+        cudaFree(dot_all);
+    }
+    const DevLevel& L0() const { return lv[0]; }
+};
+
 }  // namespace
 
 struct amg_ctx_s {
@@ -104,24 +195,22 @@ struct amg_ctx_s {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int nsm = 148;
+    ncclComm_t nccl = nullptr;
 };
 
 struct amg_hier_s {
     amg_ctx_s* ctx = nullptr;
     amg_config_t cfg{};
-    std::vector<DevLevel> lv;   // non-coarsest levels
-    DevMat A0;                  // level-0 operator when the hierarchy has one level
-    int64_t n0 = 0, nnz0 = 0, nL = 0;
-    int64_t nnzL = 0;
-    double* cinv = nullptr;     // dense A_L^{-1}, row-major
-    double* cb = nullptr;       // coarsest rhs
-    double* cx = nullptr;       // coarsest solution
-    double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr;  // PCG vectors
+    int np = 1;                 // ranks of the partition
+    bool loopback = false;      // all ranks in this process (emulate_ranks)
+    std::vector<RankState> ranks;  // local ranks (1, or np in loopback mode)
+    std::vector<std::vector<int32_t>> agg;  // host aggregate maps (owned rows; all rows in loopback)
+    std::vector<int64_t> lvl_n, lvl_nnzA, lvl_nnzP;  // global level statistics
+    std::vector<int32_t> lvl_fmt;
+    std::vector<int64_t> lvl_own_begin, lvl_own_end;  // this rank's owned rows per level
+    int64_t n0_local = 0;       // rows of the caller's vectors
     double *hb = nullptr, *hx = nullptr;  // staging for amg_solve_host
-    PcgState* st = nullptr;
     PcgState* st_host = nullptr;
-    double* partials = nullptr;
-    unsigned int* ticket = nullptr;
     double setup_s = 0, opc = 0, avg_cr = 0, bytes_v = 0, bytes_it = 0;
     cudaGraphExec_t solve_exec = nullptr;
     const double* solve_b = nullptr;
@@ -132,35 +221,15 @@ struct amg_hier_s {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<KernelRec>* prof = nullptr;
 
-    const DevMat& Afine() const { return lv.empty() ? A0 : lv[0].A; }
+    bool multi() const { return np > 1; }
+    int nlev() const { return (int)ranks[0].lv.size(); }
     ~amg_hier_s() {
         if (solve_exec) cudaGraphExecDestroy(solve_exec);
         if (apply_exec) cudaGraphExecDestroy(apply_exec);
-        for (auto& D : lv) {
-            D.A.release();
-            D.P.release();
-            D.R.release();
-            cudaFree(D.m);
-            cudaFree(D.b);
-            cudaFree(D.mb);
-            cudaFree(D.r);
-            cudaFree(D.xa);
-            cudaFree(D.xb);
-        }
-        A0.release();
-        cudaFree(cinv);
-        cudaFree(cb);
-        cudaFree(cx);
-        cudaFree(pr);
-        cudaFree(pz);
-        cudaFree(pp);
-        cudaFree(pq);
+        for (auto& R : ranks) R.release();
         cudaFree(hb);
         cudaFree(hx);
-        cudaFree(st);
         cudaFreeHost(st_host);
-        cudaFree(partials);
-        cudaFree(ticket);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
     }
@@ -207,7 +276,8 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         static const int cap = max_grid((const void*)k_sdia<G, E>, nsm);
         const int64_t need = (M.nrows + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        k_sdia<G, E><<<grid, kBlock, 0, L.s>>>(SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols}, g, e, rc);
+        k_sdia<G, E><<<grid, kBlock, 0, L.s>>>(SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift},
+                                                g, e, rc);
     } else if (M.fmt == FMT_SELL) {
         static const int cap = max_grid((const void*)k_sell<G, E>, nsm);
         const int64_t need = (M.nrows + kBlock - 1) / kBlock;
@@ -245,120 +315,264 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
 }
 
 RedCtx no_red() { return RedCtx{nullptr, nullptr, nullptr, nullptr, 0ull, FIN_NONE}; }
-RedCtx red(amg_hier_s* h, int kind, unsigned long long cond) {
-    return RedCtx{h->partials, h->ticket, nullptr, h->st, cond, kind};
+
+// Dot epilogue context: fused finisher on one rank; local total (deferred) on many.
+RedCtx dot_red(amg_hier_s* h, RankState& R, int kind, unsigned long long cond) {
+    if (!h->multi()) return RedCtx{R.partials, R.ticket, nullptr, R.st, cond, kind};
+    return RedCtx{R.partials, R.ticket, R.dot_local, nullptr, 0ull, FIN_NONE};
 }
 
-// z0 = A_L^{-1} b0 on the coarsest level.
-void enqueue_coarse(amg_hier_s* h, Launch& L, const double* b, double* z) {
-    L.begin("coarse_gemv", 8.0 * (double)h->nL * (double)h->nL + 16.0 * (double)h->nL);
-    k_dense_gemv<<<vec_grid(h->nL * 32, h->ctx->nsm), kBlock, 0, L.s>>>(h->cinv, b, z, h->nL);
-    L.end();
+// ------------------------------------------------------------- communication
+// Multi-rank: gather every rank's dot total to every rank, then finish in rank order.
+void dot_finish(amg_hier_s* h, Launch& L, int kind) {
+    if (!h->multi()) return;
+    if (h->loopback) {
+        for (auto& Rd : h->ranks)
+            for (auto& Rs : h->ranks)
+                cudaMemcpyAsync(Rd.dot_all + Rs.rank, Rs.dot_local, sizeof(double), cudaMemcpyDeviceToDevice, L.s);
+    } else {
+        RankState& R = h->ranks[0];
+        ncclAllGather(R.dot_local, R.dot_all, 1, ncclDouble, h->ctx->nccl, L.s);
+    }
+    for (auto& R : h->ranks) {
+        RedCtx rc{nullptr, nullptr, nullptr, R.st, 0ull, kind};
+        k_finish<<<1, 32, 0, L.s>>>(R.dot_all, h->np, rc);
+    }
 }
 
-// One V-cycle z0 = B b0 (Eq. 3.1) enqueued on
-// L.s.  If `rz` is given, the last level-0 post-sweep also reduces b0^T z0.
-void enqueue_vcycle(amg_hier_s* h, Launch& L, const double* b0, double* z0, const RedCtx* rz) {
-    const int nlev = (int)h->lv.size();
+using VecOf = std::function<double*(RankState&)>;
+
+// Halo exchange of a level-l vector (window base pointer given per rank).
+void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) {
+    if (!h->multi()) return;
+    const int nsm = h->ctx->nsm;
+    bool any = false;
+    for (auto& R : h->ranks) any |= (R.lv[l].ex.nsend > 0 || R.lv[l].ex.nrecv > 0);
+    if (!any && h->loopback) return;
+    for (auto& R : h->ranks) {
+        const Exch& E = R.lv[l].ex;
+        if (E.nsend) k_pack<<<vec_grid(E.nsend, nsm), kBlock, 0, L.s>>>(vec(R), E.send_idx, E.sbuf, E.nsend);
+    }
+    if (h->loopback) {
+        for (auto& Rd : h->ranks) {
+            const Exch& Ed = Rd.lv[l].ex;
+            for (auto& Rs : h->ranks) {
+                const int64_t cnt = Ed.recv_off[Rs.rank + 1] - Ed.recv_off[Rs.rank];
+                if (!cnt) continue;
+                const Exch& Es = Rs.lv[l].ex;
+                cudaMemcpyAsync(Ed.rbuf + Ed.recv_off[Rs.rank], Es.sbuf + Es.send_off[Rd.rank], cnt * sizeof(double),
+                                cudaMemcpyDeviceToDevice, L.s);
+            }
+        }
+    } else {
+        RankState& R = h->ranks[0];
+        const Exch& E = R.lv[l].ex;
+        ncclGroupStart();
+        for (int q = 0; q < h->np; ++q) {
+            const int64_t ns = E.send_off[q + 1] - E.send_off[q];
+            const int64_t nr = E.recv_off[q + 1] - E.recv_off[q];
+            if (ns) ncclSend(E.sbuf + E.send_off[q], ns, ncclDouble, q, h->ctx->nccl, L.s);
+            if (nr) ncclRecv(E.rbuf + E.recv_off[q], nr, ncclDouble, q, h->ctx->nccl, L.s);
+        }
+        ncclGroupEnd();
+    }
+    for (auto& R : h->ranks) {
+        const Exch& E = R.lv[l].ex;
+        if (E.nrecv) k_unpack<<<vec_grid(E.nrecv, nsm), kBlock, 0, L.s>>>(vec(R), E.recv_idx, E.rbuf, E.nrecv);
+    }
+}
+
+// ------------------------------------------------------------- V-cycle
+// z0 = B b0 (Eq. 3.1).  b0/z0 give each rank's
+// level-0 WINDOW base pointers.  With `rz`, the last level-0 post-sweep also
+// reduces b0^T z0 (kind FIN_RZ).
+void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, bool rz) {
+    const int nl = h->nlev();
     const int s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
-    if (nlev == 0) {  // single-level hierarchy: B = A^{-1}
-        enqueue_coarse(h, L, b0, z0);
+    const int nsm = h->ctx->nsm;
+    const int nr = (int)h->ranks.size();
+    auto ri_of = [&](RankState& R) { return (int)(&R - h->ranks.data()); };
+    if (nl == 1) {  // single-level hierarchy: B = A^{-1} (replicated, np == 1)
+        for (auto& R : h->ranks) {
+            L.begin("coarse_gemv", 8.0 * (double)R.nL * (double)R.nL + 16.0 * (double)R.nL);
+            k_dense_gemv<<<vec_grid(R.nL * 32, nsm), kBlock, 0, L.s>>>(R.cinv, b0(R), z0(R), R.nL);
+            L.end();
+            if (rz) {
+                L.begin("dot_rz", 16.0 * R.nL);
+                k_dot<<<vec_grid(R.nL, nsm), kBlock, 0, L.s>>>(b0(R), z0(R), R.nL, dot_red(h, R, FIN_RZ, 0));
+                L.end();
+            }
+        }
+        if (rz) dot_finish(h, L, FIN_RZ);
         return;
     }
-    std::vector<double*> xpre(nlev, nullptr);  // pre-smoothed x of each level (s1 >= 2)
+    std::vector<std::vector<double*>> xpre(nr, std::vector<double*>(nl, nullptr));
     // ---- down: pre-smoothing, residual, restriction
-    for (int l = 0; l < nlev; ++l) {
-        DevLevel& D = h->lv[l];
-        const double* b = (l == 0) ? b0 : D.b;
-        const double n8 = 8.0 * (double)D.n;
-        if (s1 == 1) {
-            // x = m o b is never stored: r = b - A (m o b)
-            if (l == 0)
-                launch_mat(L, D.A, GMB{D.m, b}, EResid{b, D.r}, no_red(), "resid0", 3 * n8);
-            else
-                launch_mat(L, D.A, GVec{D.mb}, EResid{b, D.r}, no_red(), "resid0", 3 * n8);
-        } else {
-            // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
-            double* xi = D.xa;
-            double* xo = D.xb;
-            if (l == 0)
-                launch_mat(L, D.A, GMB{D.m, b}, ESweep0{b, D.m, xi}, no_red(), "sweep0", 3 * n8);
-            else
-                launch_mat(L, D.A, GVec{D.mb}, ESweep0{b, D.m, xi}, no_red(), "sweep0", 3 * n8);
-            for (int s = 2; s < s1; ++s) {
-                launch_mat(L, D.A, GVec{xi}, ESweep<false>{xi, b, D.m, xo}, no_red(), "presweep", 4 * n8);
-                std::swap(xi, xo);
+    for (int l = 0; l + 1 < nl; ++l) {
+        const bool dist = !h->ranks[0].lv[l].replicated;
+        auto bvec = [&](RankState& R) -> double* { return l == 0 ? b0(R) : R.lv[l].b; };
+        if (dist) {
+            if (l == 0) exchange(h, L, 0, [&](RankState& R) { return b0(R); });
+            else exchange(h, L, l, [&](RankState& R) { return R.lv[l].mb; });
+        }
+        for (int ri = 0; ri < nr; ++ri) {
+            RankState& R = h->ranks[ri];
+            DevLevel& D = R.lv[l];
+            const double* b = bvec(R);
+            const double* be = b + D.ep_off;
+            const double n8 = 8.0 * (double)D.comp_n;
+            if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b)
+                if (l == 0)
+                    launch_mat(L, D.A, GMB{D.m, b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
+                else
+                    launch_mat(L, D.A, GVec{D.mb}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
+            } else {  // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
+                if (l == 0)
+                    launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.m + D.ep_off, D.xa + D.ep_off}, no_red(), "sweep0",
+                               3 * n8);
+                else
+                    launch_mat(L, D.A, GVec{D.mb}, ESweep0{be, D.m + D.ep_off, D.xa + D.ep_off}, no_red(), "sweep0",
+                               3 * n8);
+                xpre[ri][l] = D.xa;
             }
-            launch_mat(L, D.A, GVec{xi}, EResid{b, D.r}, no_red(), "resid", 3 * n8);
-            xpre[l] = xi;
         }
-        if (l + 1 < nlev) {
-            DevLevel& C = h->lv[l + 1];
-            launch_mat(L, D.R, GVec{D.r}, EStoreMB{C.b, C.m, C.mb}, no_red(), "restrict",
-                       n8 + 24.0 * (double)C.n);
-        } else {
-            launch_mat(L, D.R, GVec{D.r}, EStore{h->cb}, no_red(), "restrict", n8 + 8.0 * (double)h->nL);
+        if (s1 >= 2) {
+            for (int s = 2; s < s1; ++s) {
+                if (dist) exchange(h, L, l, [&](RankState& R) { return xpre[ri_of(R)][l]; });
+                for (int ri = 0; ri < nr; ++ri) {
+                    RankState& R = h->ranks[ri];
+                    DevLevel& D = R.lv[l];
+                    double* xi = xpre[ri][l];
+                    double* xo = (xi == D.xa) ? D.xb : D.xa;
+                    launch_mat(L, D.A, GVec{xi},
+                               ESweep<false>{xi + D.ep_off, bvec(R) + D.ep_off, D.m + D.ep_off, xo + D.ep_off},
+                               no_red(), "presweep", 4 * 8.0 * (double)D.comp_n);
+                    xpre[ri][l] = xo;
+                }
+            }
+            if (dist) exchange(h, L, l, [&](RankState& R) { return xpre[ri_of(R)][l]; });
+            for (int ri = 0; ri < nr; ++ri) {
+                RankState& R = h->ranks[ri];
+                DevLevel& D = R.lv[l];
+                launch_mat(L, D.A, GVec{xpre[ri][l]}, EResid{bvec(R) + D.ep_off, D.r + D.ep_off}, no_red(), "resid",
+                           3 * 8.0 * (double)D.comp_n);
+            }
+        }
+        if (dist) exchange(h, L, l, [&](RankState& R) { return R.lv[l].r; });
+        for (auto& R : h->ranks) {
+            DevLevel& D = R.lv[l];
+            DevLevel& C = R.lv[l + 1];
+            if (!C.coarsest)
+                launch_mat(L, D.R, GVec{D.r}, EStoreMB{C.b + D.rst_off, C.m + D.rst_off, C.mb + D.rst_off}, no_red(),
+                           "restrict", 8.0 * (double)D.comp_n + 24.0 * (double)D.rst_n);
+            else
+                launch_mat(L, D.R, GVec{D.r}, EStore{C.b + D.rst_off}, no_red(), "restrict",
+                           8.0 * (double)D.comp_n + 8.0 * (double)D.rst_n);
+        }
+        if (h->ranks[0].lv[l + 1].replicated && dist) {  // first replicated level: gather the rhs
+            exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].b; });
+            if (!h->ranks[0].lv[l + 1].coarsest) exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].mb; });
         }
     }
-    enqueue_coarse(h, L, h->cb, h->cx);  // z_L = A_L^{-1} b_L (reading R2)
+    // ---- coarsest: z_L = A_L^{-1} b_L (reading R2), replicated on every rank
+    for (auto& R : h->ranks) {
+        DevLevel& C = R.lv[nl - 1];
+        L.begin("coarse_gemv", 8.0 * (double)R.nL * (double)R.nL + 16.0 * (double)R.nL);
+        k_dense_gemv<<<vec_grid(R.nL * 32, nsm), kBlock, 0, L.s>>>(R.cinv, C.b, C.xa, R.nL);
+        L.end();
+    }
     // ---- up: prolongation, post-smoothing
-    for (int l = nlev - 1; l >= 0; --l) {
-        DevLevel& D = h->lv[l];
-        const double* b = (l == 0) ? b0 : D.b;
-        const double* e = (l + 1 < nlev) ? h->lv[l + 1].xa : h->cx;
-        const int64_t nc = (l + 1 < nlev) ? h->lv[l + 1].n : h->nL;
-        const double n8 = 8.0 * (double)D.n;
-        double* fin = (l == 0) ? z0 : D.xa;  // the level's result (read by level l-1)
-        double* tmp = D.xb;                  // the prolongation update is row-local, so it
-                                             // may run in place on xpre
-        double* dst = (s2 % 2 == 1) ? tmp : fin;
-        if (s1 == 1) {
-            if (l == 0)
-                launch_mat(L, D.P, GVec{e}, EProlong0{b, D.m, dst}, no_red(), "prolong0", 3 * n8 + 8.0 * nc);
-            else
-                launch_mat(L, D.P, GVec{e}, EProlongMB{D.mb, dst}, no_red(), "prolong0", 2 * n8 + 8.0 * nc);
-        } else {
-            launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[l], dst}, no_red(), "prolong", 2 * n8 + 8.0 * nc);
+    for (int l = nl - 2; l >= 0; --l) {
+        const bool dist = !h->ranks[0].lv[l].replicated;
+        if (!h->ranks[0].lv[l + 1].replicated) exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].xa; });
+        std::vector<double*> cur(nr), fin(nr), tmp(nr);
+        for (int ri = 0; ri < nr; ++ri) {
+            RankState& R = h->ranks[ri];
+            DevLevel& D = R.lv[l];
+            const double* b = (l == 0) ? b0(R) : D.b;
+            const double* e = R.lv[l + 1].xa;
+            const double nc8 = 8.0 * (double)R.lv[l + 1].comp_n;
+            fin[ri] = (l == 0) ? z0(R) : D.xa;  // the level's result (read by level l-1)
+            tmp[ri] = D.xb;                     // the prolongation update is row-local: may run in place
+            double* dst = (s2 % 2 == 1) ? tmp[ri] : fin[ri];
+            const double n8 = 8.0 * (double)D.comp_n;
+            if (s1 == 1) {
+                if (l == 0)
+                    launch_mat(L, D.P, GVec{e}, EProlong0{b + D.ep_off, D.m + D.ep_off, dst + D.ep_off}, no_red(),
+                               "prolong0", 3 * n8 + nc8);
+                else
+                    launch_mat(L, D.P, GVec{e}, EProlongMB{D.mb + D.ep_off, dst + D.ep_off}, no_red(), "prolong0",
+                               2 * n8 + nc8);
+            } else {
+                launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[ri][l] + D.ep_off, dst + D.ep_off}, no_red(), "prolong",
+                           2 * n8 + nc8);
+            }
+            cur[ri] = dst;
         }
-        double* xi = dst;
         for (int s = 0; s < s2; ++s) {
-            double* xo = (xi == tmp) ? fin : tmp;
-            if (l == 0 && s == s2 - 1 && rz)
-                launch_mat(L, D.A, GVec{xi}, ESweep<true>{xi, b, D.m, xo}, *rz, "postsweep_dot", 4 * n8);
-            else
-                launch_mat(L, D.A, GVec{xi}, ESweep<false>{xi, b, D.m, xo}, no_red(), "postsweep", 4 * n8);
-            xi = xo;
+            const bool last = (s == s2 - 1);
+            if (dist) exchange(h, L, l, [&](RankState& R) { return cur[ri_of(R)]; });
+            for (int ri = 0; ri < nr; ++ri) {
+                RankState& R = h->ranks[ri];
+                DevLevel& D = R.lv[l];
+                const double* b = (l == 0) ? b0(R) : D.b;
+                double* xi = cur[ri];
+                double* xo = (xi == tmp[ri]) ? fin[ri] : tmp[ri];
+                const double n8 = 8.0 * (double)D.comp_n;
+                if (l == 0 && last && rz)
+                    launch_mat(L, D.A, GVec{xi},
+                               ESweep<true>{xi + D.ep_off, b + D.ep_off, D.m + D.ep_off, xo + D.ep_off},
+                               dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 4 * n8);
+                else
+                    launch_mat(L, D.A, GVec{xi},
+                               ESweep<false>{xi + D.ep_off, b + D.ep_off, D.m + D.ep_off, xo + D.ep_off}, no_red(),
+                               "postsweep", 4 * n8);
+                cur[ri] = xo;
+            }
         }
     }
+    if (rz) dot_finish(h, L, FIN_RZ);
 }
 
 // PCG loop body, rotated so that the convergence test is the last node:
 //   z = V(r), rho' = r^T z, beta ; p = z + beta p ; q = A p, alpha ; x, r update, test.
-void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x, unsigned long long cond) {
-    const int64_t n = h->n0;
+void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long long cond) {
     const int nsm = h->ctx->nsm;
-    RedCtx rz = red(h, FIN_RZ, 0);
-    if (!h->lv.empty()) {
-        enqueue_vcycle(h, L, h->pr, h->pz, &rz);
-    } else {
-        enqueue_coarse(h, L, h->pr, h->pz);
-        L.begin("dot_rz", 16.0 * n);
-        k_dot<<<vec_grid(n, nsm), kBlock, 0, L.s>>>(h->pr, h->pz, n, rz);
+    enqueue_vcycle(h, L, [](RankState& R) { return R.pr; }, [](RankState& R) { return R.pz; }, true);
+    for (auto& R : h->ranks) {
+        const DevLevel& D = R.L0();
+        L.begin("pupdate", 24.0 * D.own_n);
+        k_pupdate<<<vec_grid(D.own_n, nsm), kBlock, 0, L.s>>>(R.pz + D.own_off, R.pp + D.own_off, D.own_n, R.st);
         L.end();
     }
-    L.begin("pupdate", 24.0 * n);
-    k_pupdate<<<vec_grid(n, nsm), kBlock, 0, L.s>>>(h->pz, h->pp, n, h->st);
-    L.end();
-    launch_mat(L, h->Afine(), GVec{h->pp}, ESpmvDot{h->pp, h->pq}, red(h, FIN_PQ, 0), "spmv_dot", 16.0 * n);
-    L.begin("axpy_rr", 48.0 * n);
-    k_axpy_rr<<<vec_grid(n, nsm), kBlock, 0, L.s>>>(x, h->pr, h->pp, h->pq, n, red(h, FIN_RR, cond));
-    L.end();
+    exchange(h, L, 0, [](RankState& R) { return R.pp; });
+    for (auto& R : h->ranks) {
+        const DevLevel& D = R.L0();
+        launch_mat(L, D.A, GVec{R.pp}, ESpmvDot{R.pp + D.own_off, R.pq + D.own_off}, dot_red(h, R, FIN_PQ, 0),
+                   "spmv_dot", 16.0 * D.own_n);
+    }
+    dot_finish(h, L, FIN_PQ);
+    for (auto& R : h->ranks) {
+        const DevLevel& D = R.L0();
+        L.begin("axpy_rr", 48.0 * D.own_n);
+        k_axpy_rr<<<vec_grid(D.own_n, nsm), kBlock, 0, L.s>>>(x_user + R.user_off, R.pr + D.own_off,
+                                                               R.pp + D.own_off, R.pq + D.own_off, D.own_n, R.st,
+                                                               dot_red(h, R, FIN_RR, cond));
+        L.end();
+    }
+    dot_finish(h, L, FIN_RR);
 }
 
-void enqueue_pcg_init(amg_hier_s* h, Launch& L, const double* b, double* x, unsigned long long cond) {
-    L.begin("pcg_init", 24.0 * h->n0);
-    k_pcg_init<<<vec_grid(h->n0, h->ctx->nsm), kBlock, 0, L.s>>>(b, h->pr, x, h->n0, red(h, FIN_BNORM, cond));
-    L.end();
+void enqueue_pcg_init(amg_hier_s* h, Launch& L, const double* b_user, double* x_user, unsigned long long cond) {
+    for (auto& R : h->ranks) {
+        const DevLevel& D = R.L0();
+        L.begin("pcg_init", 24.0 * D.own_n);
+        k_pcg_init<<<vec_grid(D.own_n, h->ctx->nsm), kBlock, 0, L.s>>>(b_user + R.user_off, R.pr + D.own_off,
+                                                                        x_user + R.user_off, D.own_n,
+                                                                        dot_red(h, R, FIN_BNORM, cond));
+        L.end();
+    }
+    dot_finish(h, L, FIN_BNORM);
 }
 
 // ------------------------------------------------------------- upload
@@ -377,13 +591,16 @@ int dev_alloc(T** dst, size_t count) {
 }
 
 // Per-operator storage choice (north_star (1): "CSR/sliced-ELL storage chosen per
-// level"): SELL-32 when rows are short and padding is small, CSR-vector with
-// VW lanes per row otherwise.
-int upload_mat(const amgsetup::Csr& M, DevMat& D) {
+// level"): SDIA-32 for stencil-like square operators whose slices share few column
+// offsets, SELL-32 for short rows with little padding, CSR-vector (VW lanes per
+// row, or one block per row) otherwise.  `shift` maps local rows to the column
+// window frame (comp_begin - win_begin); `square` marks A_l.
+int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift) {
     const int64_t n = M.nrows, nnz = M.nnz();
     D.nrows = n;
     D.ncols = M.ncols;
     D.nnz = nnz;
+    D.shift = (int32_t)shift;
     const int64_t nsl = (n + 31) / 32;
     std::vector<uint32_t> width(nsl, 0);
 #pragma omp parallel for schedule(static)
@@ -395,15 +612,15 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D) {
     int64_t padded = 0;
     for (int64_t s = 0; s < nsl; ++s) padded += 32 * (int64_t)width[s];
     const double mean = n ? (double)nnz / (double)n : 0.0;
-    // SDIA-32 candidate: per slice, the sorted distinct offsets col - row
-    if (M.nrows == M.ncols && nsl >= 148 * 16 && mean <= 64.0) {
+    // SDIA-32 candidate: per slice, the sorted distinct offsets col - (row + shift)
+    if (square && nsl >= 148 * 16 && mean <= 64.0) {
         std::vector<uint32_t> dw(nsl, 0);
         std::vector<std::vector<int32_t>> soffs(nsl);
 #pragma omp parallel for schedule(static)
         for (int64_t s = 0; s < nsl; ++s) {
             auto& o = soffs[s];
             for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r)
-                for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t) o.push_back((int32_t)((int64_t)M.ci[t] - r));
+                for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t) o.push_back((int32_t)((int64_t)M.ci[t] - (r + shift)));
             std::sort(o.begin(), o.end());
             o.erase(std::unique(o.begin(), o.end()), o.end());
             dw[s] = (uint32_t)o.size();
@@ -426,7 +643,7 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D) {
                     const int64_t lane = r - s * 32;
                     size_t k = 0;
                     for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t) {
-                        const int32_t d = (int32_t)((int64_t)M.ci[t] - r);
+                        const int32_t d = (int32_t)((int64_t)M.ci[t] - (r + shift));
                         while (o[k] != d) ++k;  // both ascending
                         val[base + (int64_t)k * 32 + lane] = M.v[t];
                     }
@@ -440,8 +657,7 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D) {
         }
     }
     // SELL-32 (one thread per row, coalesced column-major slices) needs little padding and
-    // enough slices to fill the GPU (>= ~16 warps per SM); long rows are fine there because
-    // every lane streams its own row with many loads in flight.
+    // enough slices to fill the GPU (>= ~16 warps per SM)
     const bool sell = (double)padded <= 1.10 * (double)nnz + 64.0 && nsl >= 148 * 16 &&
                       padded / 32 < (int64_t)UINT32_MAX;
     if (sell) {
@@ -457,44 +673,107 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D) {
             for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r) {
                 const int64_t lane = r - s * 32;
                 int64_t k = 0;
+                int32_t last = 0;
                 for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t, ++k) {
-                    col[base + k * 32 + lane] = M.ci[t];
+                    col[base + k * 32 + lane] = last = M.ci[t];
                     val[base + k * 32 + lane] = M.v[t];
                 }
-                for (; k < width[s]; ++k) col[base + k * 32 + lane] = (int32_t)std::min<int64_t>(r, M.ncols - 1);
+                for (; k < width[s]; ++k) col[base + k * 32 + lane] = last;
             }
         }
         int st;
         if ((st = dev_copy(&D.sptr, sptr.data(), sptr.size()))) return st;
         if ((st = dev_copy(&D.col, col.data(), col.size()))) return st;
         if ((st = dev_copy(&D.val, val.data(), val.size()))) return st;
-    } else {
-        if (nnz >= (int64_t)INT32_MAX) {
-            set_err("operator too large for 32-bit CSR row pointers on one rank");
-            return AMG_ERR_ARG;
+        return AMG_OK;
+    }
+    if (nnz >= (int64_t)INT32_MAX) {
+        set_err("operator too large for 32-bit CSR row pointers on one rank");
+        return AMG_ERR_ARG;
+    }
+    D.fmt = FMT_CSRV;
+    D.stored = nnz;
+    // lanes per row: enough threads to fill 148 SMs x 2048 threads, 2..32 lanes per
+    // row inside a warp, or a whole block per row for few very long rows
+    const double want = 148.0 * 2048.0 / (double)std::max<int64_t>(n, 1);
+    int vw = 2;
+    while (vw < 32 && (vw < want || vw * 8 < mean) && vw * 2 <= std::max(2.0, mean)) vw *= 2;
+    if (mean >= 256.0 && (double)n < 18944.0) vw = kVWBlock;
+    D.vw = vw;
+    std::vector<int32_t> rp(n + 1);
+    for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)M.rp[i];
+    int st;
+    if ((st = dev_copy(&D.rp, rp.data(), rp.size()))) return st;
+    if ((st = dev_copy(&D.col, M.ci.data(), M.ci.size()))) return st;
+    if ((st = dev_copy(&D.val, M.v.data(), M.v.size()))) return st;
+    return AMG_OK;
+}
+
+// Uploads one rank's plan.  coarse_inv: the dense A_L^{-1}.
+int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<double>& coarse_inv, RankState& R) {
+    const int nl = (int)P.lv.size();
+    R.rank = P.rank;
+    R.lv.resize(nl);
+    int st;
+    for (int l = 0; l < nl; ++l) {
+        const amgsetup::RankLevel& S = P.lv[l];
+        DevLevel& D = R.lv[l];
+        D.replicated = S.replicated;
+        D.coarsest = (l == nl - 1);
+        D.n_global = S.n_global;
+        D.own_begin = S.own_begin;
+        D.own_n = S.own_end - S.own_begin;
+        D.comp_n = S.comp_end - S.comp_begin;
+        D.win_n = S.win_end - S.win_begin;
+        D.ep_off = S.comp_begin - S.win_begin;
+        D.own_off = S.own_begin - S.win_begin;
+        const size_t wn = (size_t)D.win_n;
+        if (!D.coarsest) {
+            D.rst_n = S.rst_end - S.rst_begin;
+            D.rst_off = S.rst_begin - P.lv[l + 1].win_begin;
+            if ((st = upload_mat(S.A, D.A, true, D.ep_off))) return st;
+            if ((st = upload_mat(S.P, D.P, false, 0))) return st;
+            if ((st = upload_mat(S.R, D.R, false, 0))) return st;
+            if ((st = dev_copy(&D.m, S.m.data(), S.m.size()))) return st;
+            if ((st = dev_alloc(&D.mb, wn))) return st;
+            if ((st = dev_alloc(&D.r, wn))) return st;
+            if ((st = dev_alloc(&D.xb, wn))) return st;
         }
-        D.fmt = FMT_CSRV;
-        D.stored = nnz;
-        // lanes per row: enough threads to fill 148 SMs x 2048 threads, 2..32 lanes per
-        // row inside a warp, or a whole block per row for few very long rows
-        const double want = 148.0 * 2048.0 / (double)std::max<int64_t>(n, 1);
-        int vw = 2;
-        while (vw < 32 && (vw < want || vw * 8 < mean) && vw * 2 <= std::max(2.0, mean)) vw *= 2;
-        static const double block_mean = std::getenv("AMG_BLOCK_MEAN") ? std::atof(std::getenv("AMG_BLOCK_MEAN")) : 256.0;
-        static const double block_rows = std::getenv("AMG_BLOCK_ROWS") ? std::atof(std::getenv("AMG_BLOCK_ROWS")) : 18944.0;
-        if (mean >= block_mean && (double)n < block_rows) vw = kVWBlock;
-        D.vw = vw;
-        std::vector<int32_t> rp(n + 1);
-        for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)M.rp[i];
-        int st;
-        if ((st = dev_copy(&D.rp, rp.data(), rp.size()))) return st;
-        if ((st = dev_copy(&D.col, M.ci.data(), M.ci.size()))) return st;
-        if ((st = dev_copy(&D.val, M.v.data(), M.v.size()))) return st;
+        if ((st = dev_alloc(&D.b, wn))) return st;
+        if ((st = dev_alloc(&D.xa, wn))) return st;
+        // halo plan: window positions
+        Exch& E = D.ex;
+        E.send_off = S.send_off;
+        E.recv_off = S.recv_off;
+        E.nsend = (int64_t)S.send_ids.size();
+        E.nrecv = (int64_t)S.recv_ids.size();
+        std::vector<int32_t> si(E.nsend), ri(E.nrecv);
+        for (int64_t k = 0; k < E.nsend; ++k) si[k] = (int32_t)(S.send_ids[k] - S.win_begin);
+        for (int64_t k = 0; k < E.nrecv; ++k) ri[k] = (int32_t)(S.recv_ids[k] - S.win_begin);
+        if ((st = dev_copy(&E.send_idx, si.data(), si.size()))) return st;
+        if ((st = dev_copy(&E.recv_idx, ri.data(), ri.size()))) return st;
+        if ((st = dev_alloc(&E.sbuf, E.nsend))) return st;
+        if ((st = dev_alloc(&E.rbuf, E.nrecv))) return st;
+    }
+    R.nL = P.lv[nl - 1].n_global;
+    if ((st = dev_copy(&R.cinv, coarse_inv.data(), coarse_inv.size()))) return st;
+    const size_t w0 = (size_t)R.lv[0].win_n;
+    if ((st = dev_alloc(&R.pr, w0))) return st;
+    if ((st = dev_alloc(&R.pz, w0))) return st;
+    if ((st = dev_alloc(&R.pp, w0))) return st;
+    if ((st = dev_alloc(&R.pq, w0))) return st;
+    if ((st = dev_alloc(&R.st, 1))) return st;
+    if ((st = dev_alloc(&R.partials, kMaxPartials))) return st;
+    if ((st = dev_alloc(&R.ticket, 1))) return st;
+    if ((st = dev_alloc(&R.dot_local, 1))) return st;
+    if ((st = dev_alloc(&R.dot_all, (size_t)h->np))) return st;
+    if (nl == 1) {  // single-level: level 0 is the coarsest; give it an operator for q = A p
+        if ((st = upload_mat(P.lv[0].A, R.lv[0].A, true, 0))) return st;
     }
     return AMG_OK;
 }
 
-// SURVEY.md §8d byte model.
+// SURVEY.md §8d byte model (global hierarchy).
 void byte_model(amg_hier_s* h, const amgsetup::Hierarchy& H) {
     const double s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
     double bv = 0.0;
@@ -510,6 +789,25 @@ void byte_model(amg_hier_s* h, const amgsetup::Hierarchy& H) {
     h->bytes_v = bv;
     const double n0 = (double)H.lv[0].A.nrows;
     h->bytes_it = bv + 12.0 * (double)H.lv[0].A.nnz() + 4.0 * (n0 + 1) + 88.0 * n0;
+}
+
+void hier_stats(amg_hier_s* h, const amgsetup::Hierarchy& H) {
+    const size_t nl = H.lv.size();
+    double s = 0.0;
+    for (auto& L : H.lv) s += (double)L.A.nnz();
+    h->opc = s / (double)H.lv[0].A.nnz();
+    double cr = 0.0;
+    for (size_t l = 0; l + 1 < nl; ++l) cr += (double)H.lv[l].A.nrows / (double)H.lv[l + 1].A.nrows;
+    h->avg_cr = nl > 1 ? cr / (double)(nl - 1) : 1.0;
+    h->lvl_n.resize(nl);
+    h->lvl_nnzA.resize(nl);
+    h->lvl_nnzP.resize(nl);
+    for (size_t l = 0; l < nl; ++l) {
+        h->lvl_n[l] = H.lv[l].A.nrows;
+        h->lvl_nnzA[l] = H.lv[l].A.nnz();
+        h->lvl_nnzP[l] = H.lv[l].P.nnz();
+    }
+    byte_model(h, H);
 }
 
 int ensure_solve_graph(amg_hier_s* h, const double* b, double* x) {
@@ -549,6 +847,26 @@ int ensure_solve_graph(amg_hier_s* h, const double* b, double* x) {
     return AMG_OK;
 }
 
+// V-cycle on the caller's vectors: level-0 window staging for multi-rank.
+void enqueue_apply(amg_hier_s* h, Launch& L, const double* r_user, double* z_user) {
+    if (!h->multi()) {
+        enqueue_vcycle(h, L, [&](RankState&) { return const_cast<double*>(r_user); },
+                       [&](RankState&) { return z_user; }, false);
+        return;
+    }
+    for (auto& R : h->ranks) {
+        const DevLevel& D = R.L0();
+        cudaMemcpyAsync(R.pr + D.own_off, r_user + R.user_off, sizeof(double) * D.own_n, cudaMemcpyDeviceToDevice,
+                        L.s);
+    }
+    enqueue_vcycle(h, L, [](RankState& R) { return R.pr; }, [](RankState& R) { return R.pz; }, false);
+    for (auto& R : h->ranks) {
+        const DevLevel& D = R.L0();
+        cudaMemcpyAsync(z_user + R.user_off, R.pz + D.own_off, sizeof(double) * D.own_n, cudaMemcpyDeviceToDevice,
+                        L.s);
+    }
+}
+
 int ensure_apply_graph(amg_hier_s* h, const double* r, double* z) {
     if (h->apply_exec && h->apply_r == r && h->apply_z == z) return AMG_OK;
     if (h->apply_exec) {
@@ -559,7 +877,7 @@ int ensure_apply_graph(amg_hier_s* h, const double* r, double* z) {
     Launch L{h, s};
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    enqueue_vcycle(h, L, r, z, nullptr);
+    enqueue_apply(h, L, r, z);
     CK(cudaStreamEndCapture(s, &g));
     CK(cudaGraphInstantiate(&h->apply_exec, g, 0));
     CK(cudaGraphDestroy(g));
@@ -569,7 +887,7 @@ int ensure_apply_graph(amg_hier_s* h, const double* r, double* z) {
 }
 
 void fill_report(amg_hier_s* h, amg_report_t* rep) {
-    rep->nlevels = (int32_t)h->lv.size() + 1;
+    rep->nlevels = (int32_t)h->lvl_n.size();
     rep->setup_s = h->setup_s;
     rep->opc = h->opc;
     rep->avg_cr = h->avg_cr;
@@ -578,8 +896,8 @@ void fill_report(amg_hier_s* h, amg_report_t* rep) {
 }
 
 // Copies the caller's CSR into the setup's form and runs the host setup.
-int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values,
-               const double* w, const amg_config_t& cfg, amgsetup::Hierarchy& H) {
+int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values, const double* w,
+               const amg_config_t& cfg, amgsetup::Hierarchy& H) {
     if (!rowptr || !colind || !values || n <= 0) {
         set_err("null argument or empty matrix");
         return AMG_ERR_ARG;
@@ -636,6 +954,151 @@ int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const do
     return AMG_OK;
 }
 
+// ---------------------------------------------------- plan (de)serialisation
+struct Blob {
+    std::vector<char> b;
+    size_t pos = 0;
+    template <class T>
+    void put(const T& v) {
+        const char* p = (const char*)&v;
+        b.insert(b.end(), p, p + sizeof(T));
+    }
+    template <class T>
+    void putv(const std::vector<T>& v) {
+        put<int64_t>((int64_t)v.size());
+        const char* p = (const char*)v.data();
+        b.insert(b.end(), p, p + v.size() * sizeof(T));
+    }
+    template <class T>
+    T get() {
+        T v;
+        std::memcpy(&v, b.data() + pos, sizeof(T));
+        pos += sizeof(T);
+        return v;
+    }
+    template <class T>
+    void getv(std::vector<T>& v) {
+        const int64_t n = get<int64_t>();
+        v.resize(n);
+        std::memcpy(v.data(), b.data() + pos, n * sizeof(T));
+        pos += n * sizeof(T);
+    }
+    void put_csr(const amgsetup::Csr& M) {
+        put(M.nrows);
+        put(M.ncols);
+        putv(M.rp);
+        putv(M.ci);
+        putv(M.v);
+    }
+    void get_csr(amgsetup::Csr& M) {
+        M.nrows = get<int64_t>();
+        M.ncols = get<int64_t>();
+        getv(M.rp);
+        getv(M.ci);
+        getv(M.v);
+    }
+};
+
+void serialize(const amgsetup::RankPlan& P, const std::vector<double>& cinv, const std::vector<int32_t>* agg_own,
+               int nl, Blob& B) {
+    B.put<int32_t>(P.rank);
+    B.put<int32_t>(P.nranks);
+    B.put<int32_t>((int32_t)P.lv.size());
+    for (const auto& L : P.lv) {
+        B.put<int32_t>(L.replicated ? 1 : 0);
+        B.put(L.n_global);
+        B.put(L.own_begin);
+        B.put(L.own_end);
+        B.put(L.comp_begin);
+        B.put(L.comp_end);
+        B.put(L.win_begin);
+        B.put(L.win_end);
+        B.put(L.rst_begin);
+        B.put(L.rst_end);
+        B.putv(L.recv_off);
+        B.putv(L.recv_ids);
+        B.putv(L.send_off);
+        B.putv(L.send_ids);
+        B.put_csr(L.A);
+        B.put_csr(L.P);
+        B.put_csr(L.R);
+        B.putv(L.m);
+    }
+    B.putv(cinv);
+    for (int l = 0; l + 1 < nl; ++l) B.putv(agg_own[l]);
+}
+
+void deserialize(Blob& B, amgsetup::RankPlan& P, std::vector<double>& cinv, std::vector<std::vector<int32_t>>& agg) {
+    P.rank = B.get<int32_t>();
+    P.nranks = B.get<int32_t>();
+    const int nl = B.get<int32_t>();
+    P.lv.resize(nl);
+    for (auto& L : P.lv) {
+        L.replicated = B.get<int32_t>() != 0;
+        L.n_global = B.get<int64_t>();
+        L.own_begin = B.get<int64_t>();
+        L.own_end = B.get<int64_t>();
+        L.comp_begin = B.get<int64_t>();
+        L.comp_end = B.get<int64_t>();
+        L.win_begin = B.get<int64_t>();
+        L.win_end = B.get<int64_t>();
+        L.rst_begin = B.get<int64_t>();
+        L.rst_end = B.get<int64_t>();
+        B.getv(L.recv_off);
+        B.getv(L.recv_ids);
+        B.getv(L.send_off);
+        B.getv(L.send_ids);
+        B.get_csr(L.A);
+        B.get_csr(L.P);
+        B.get_csr(L.R);
+        B.getv(L.m);
+    }
+    B.getv(cinv);
+    agg.assign(nl > 0 ? nl - 1 : 0, {});
+    for (int l = 0; l + 1 < nl; ++l) B.getv(agg[l]);
+}
+
+// NCCL point-to-point of a host byte buffer through a device staging buffer.
+int nccl_send_bytes(amg_ctx_s* c, const std::vector<char>& buf, int peer) {
+    int64_t n = (int64_t)buf.size();
+    char* d = nullptr;
+    CK(cudaMalloc(&d, std::max<int64_t>(n, 8) + 8));
+    CK(cudaMemcpy(d, &n, 8, cudaMemcpyHostToDevice));
+    if (n) CK(cudaMemcpy(d + 8, buf.data(), n, cudaMemcpyHostToDevice));
+    NK(ncclSend(d, 8, ncclChar, peer, c->nccl, c->stream));
+    if (n) NK(ncclSend(d + 8, n, ncclChar, peer, c->nccl, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d);
+    return AMG_OK;
+}
+
+int nccl_recv_bytes(amg_ctx_s* c, std::vector<char>& buf, int peer) {
+    int64_t* dn = nullptr;
+    CK(cudaMalloc(&dn, 8));
+    NK(ncclRecv(dn, 8, ncclChar, peer, c->nccl, c->stream));
+    int64_t n = 0;
+    CK(cudaMemcpyAsync(&n, dn, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dn);
+    buf.resize(n);
+    if (n) {
+        char* d = nullptr;
+        CK(cudaMalloc(&d, n));
+        NK(ncclRecv(d, n, ncclChar, peer, c->nccl, c->stream));
+        CK(cudaMemcpyAsync(buf.data(), d, n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        cudaFree(d);
+    }
+    return AMG_OK;
+}
+
+template <class T>
+void blob_put_array(Blob& B, const T* p, int64_t n) {
+    B.put<int64_t>(n);
+    const char* c = (const char*)p;
+    B.b.insert(B.b.end(), c, c + n * sizeof(T));
+}
+
 }  // namespace
 
 // ===================================================================== ABI
@@ -656,17 +1119,22 @@ void amg_config_default(amg_config_t* c) {
     c->replicate_below_bytes = 64ll << 20;
     c->setup_threads = 0;
     c->use_graphs = 1;
+    c->emulate_ranks = 1;
+}
+
+int amg_nccl_unique_id(void* out128) {
+    if (!out128) return AMG_ERR_ARG;
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, 128);
+    return AMG_OK;
 }
 
 int amg_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id, void* cuda_stream,
                    amg_ctx_t* out) {
-    (void)nccl_unique_id;
-    if (!out || nranks < 1 || rank < 0 || rank >= nranks) {
-        set_err("amg_ctx_create: bad rank/nranks or null out");
-        return AMG_ERR_ARG;
-    }
-    if (nranks > 1) {
-        set_err("amg_ctx_create: multi-rank contexts are not built in this version");
+    if (!out || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_unique_id)) {
+        set_err("amg_ctx_create: bad rank/nranks, null out, or missing NCCL unique id");
         return AMG_ERR_ARG;
     }
     *out = nullptr;
@@ -687,30 +1155,39 @@ int amg_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
         }
         c->own_stream = true;
     }
+    if (nranks > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_unique_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+        if (r != ncclSuccess) {
+            if (c->own_stream) cudaStreamDestroy(c->stream);
+            delete c;
+            set_err(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+            return AMG_ERR_NCCL;
+        }
+    }
     *out = c;
     return AMG_OK;
 }
 
 int amg_ctx_destroy(amg_ctx_t c) {
     if (!c) return AMG_OK;
+    if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return AMG_OK;
 }
 
-int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int64_t row_end,
-                        const int64_t* rowptr, const int64_t* colind, const double* values, const double* w,
-                        const amg_config_t* cfg_in, amg_hier_t* out) {
+int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int64_t row_end, const int64_t* rowptr,
+                        const int64_t* colind, const double* values, const double* w, const amg_config_t* cfg_in,
+                        amg_hier_t* out) {
     auto t0 = std::chrono::steady_clock::now();
-    if (!ctx || !out || !rowptr || !colind || !values || n_global <= 0) {
-        set_err("amg_hierarchy_build: null argument or empty matrix");
+    if (!ctx || !out || !rowptr || !colind || !values || n_global <= 0 || row_begin < 0 || row_end < row_begin ||
+        row_end > n_global) {
+        set_err("amg_hierarchy_build: null argument, empty matrix or bad row block");
         return AMG_ERR_ARG;
     }
     *out = nullptr;
-    if (row_begin != 0 || row_end != n_global) {
-        set_err("amg_hierarchy_build: a single-rank context must own all rows");
-        return AMG_ERR_ARG;
-    }
     amg_config_t cfg;
     amg_config_default(&cfg);
     if (cfg_in) cfg = *cfg_in;
@@ -718,72 +1195,162 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     // that contain conditional nodes)
     if (const char* ev = std::getenv("AMG_EAGER")) cfg.use_graphs = (ev[0] == '1') ? 0 : cfg.use_graphs;
     CK(cudaSetDevice(ctx->device));
-
-    amgsetup::Hierarchy H;
-    {
-        const int hs = host_setup(n_global, rowptr, colind, values, w, cfg, H);
-        if (hs != AMG_OK) {
-            set_err("amg_hierarchy_build: " + g_err);
-            return hs;
-        }
+    const int nr = ctx->nranks;
+    if (nr == 1 && (row_begin != 0 || row_end != n_global)) {
+        set_err("amg_hierarchy_build: a single-rank context must own all rows");
+        return AMG_ERR_ARG;
     }
-    // ---- upload
+    if (nr > 1 && cfg.emulate_ranks > 1) {
+        set_err("amg_hierarchy_build: emulate_ranks is for single-rank contexts");
+        return AMG_ERR_ARG;
+    }
+    const int np = nr > 1 ? nr : std::max(1, cfg.emulate_ranks);
     auto* h = new amg_hier_s();
     h->ctx = ctx;
     h->cfg = cfg;
-    const size_t nl = H.lv.size();
-    h->n0 = H.lv[0].A.nrows;
-    h->nnz0 = H.lv[0].A.nnz();
-    int st = AMG_OK;
+    h->np = np;
+    h->loopback = (nr == 1 && np > 1);
     auto fail = [&](int code) {
         delete h;
         return code;
     };
-    h->lv.resize(nl - 1);
-    for (size_t l = 0; l + 1 < nl; ++l) {
-        DevLevel& D = h->lv[l];
-        const amgsetup::Level& S = H.lv[l];
-        D.n = S.A.nrows;
-        if ((st = upload_mat(S.A, D.A))) return fail(st);
-        if ((st = upload_mat(S.P, D.P))) return fail(st);
-        if ((st = upload_mat(S.R, D.R))) return fail(st);
-        if ((st = dev_copy(&D.m, S.m.data(), S.m.size()))) return fail(st);
-        if (l > 0 && (st = dev_alloc(&D.b, D.n))) return fail(st);
-        if (l > 0 && (st = dev_alloc(&D.mb, D.n))) return fail(st);
-        if ((st = dev_alloc(&D.r, D.n))) return fail(st);
-        if ((st = dev_alloc(&D.xa, D.n))) return fail(st);
-        if ((st = dev_alloc(&D.xb, D.n))) return fail(st);
-        D.agg = S.agg;
-        D.sweeps = S.sweeps;
-        D.omega = S.omega;
+    if (h->multi()) h->cfg.use_graphs = 0;  // multi-rank solves run eagerly (host loop)
+    int st = AMG_OK;
+    if (nr == 1) {
+        amgsetup::Hierarchy H;
+        if ((st = host_setup(n_global, rowptr, colind, values, w, cfg, H))) {
+            set_err("amg_hierarchy_build: " + g_err);
+            return fail(st);
+        }
+        std::vector<int64_t> bounds(np + 1);
+        for (int g = 0; g <= np; ++g) bounds[g] = n_global * g / np;
+        std::vector<amgsetup::RankPlan> plans;
+        std::string err;
+        if (!amgsetup::partition(H, bounds, cfg.replicate_below_bytes, plans, err)) {
+            set_err("amg_hierarchy_build: " + err);
+            return fail(AMG_ERR_ARG);
+        }
+        hier_stats(h, H);
+        h->ranks.resize(np);
+        for (int g = 0; g < np; ++g)
+            if ((st = upload_rank(h, plans[g], H.coarse_inv, h->ranks[g]))) return fail(st);
+        for (int g = 0; g < np; ++g) h->ranks[g].user_off = h->loopback ? plans[g].lv[0].own_begin : 0;
+        for (size_t l = 0; l + 1 < H.lv.size(); ++l) h->agg.push_back(H.lv[l].agg);
+        h->lvl_own_begin.assign(H.lv.size(), 0);
+        h->lvl_own_end = h->lvl_n;
+        h->n0_local = n_global;
+        for (size_t l = 0; l < H.lv.size(); ++l)
+            h->lvl_fmt.push_back(l + 1 < H.lv.size() ? h->ranks[0].lv[l].A.fmt : FMT_DENSE);
+    } else {
+        // ---- NCCL: gather the matrix on rank 0, build there, send each rank its plan
+        const int me = ctx->rank;
+        const int64_t nloc = row_end - row_begin;
+        Blob mine;
+        mine.put(row_begin);
+        mine.put(row_end);
+        blob_put_array(mine, rowptr, nloc + 1);
+        blob_put_array(mine, colind, rowptr[nloc]);
+        blob_put_array(mine, values, rowptr[nloc]);
+        std::vector<double> wl(nloc, 1.0);
+        if (w) std::copy(w, w + nloc, wl.begin());
+        mine.putv(wl);
+        Blob myplan;
+        if (me == 0) {
+            std::vector<Blob> parts(nr);
+            parts[0] = mine;
+            for (int q = 1; q < nr; ++q)
+                if ((st = nccl_recv_bytes(ctx, parts[q].b, q))) return fail(st);
+            std::vector<int64_t> gr(n_global + 1, 0), gc;
+            std::vector<double> gv, gw(n_global, 1.0);
+            std::vector<int64_t> bounds(nr + 1, 0);
+            for (int q = 0; q < nr; ++q) {
+                Blob& B = parts[q];
+                const int64_t rb = B.get<int64_t>(), re = B.get<int64_t>();
+                std::vector<int64_t> rp, ci;
+                std::vector<double> v, ww;
+                B.getv(rp);
+                B.getv(ci);
+                B.getv(v);
+                B.getv(ww);
+                if (q > 0 && rb != bounds[q]) {
+                    set_err("amg_hierarchy_build: row blocks must be contiguous and in rank order");
+                    return fail(AMG_ERR_ARG);
+                }
+                bounds[q] = rb;
+                bounds[q + 1] = re;
+                const int64_t off = (int64_t)gc.size();
+                for (int64_t i = 0; i < re - rb; ++i) gr[rb + i + 1] = off + rp[i + 1];
+                gc.insert(gc.end(), ci.begin(), ci.end());
+                gv.insert(gv.end(), v.begin(), v.end());
+                std::copy(ww.begin(), ww.end(), gw.begin() + rb);
+            }
+            if (bounds[0] != 0 || bounds[nr] != n_global) {
+                set_err("amg_hierarchy_build: row blocks do not cover [0, n_global)");
+                return fail(AMG_ERR_ARG);
+            }
+            amgsetup::Hierarchy H;
+            if ((st = host_setup(n_global, gr.data(), gc.data(), gv.data(), gw.data(), cfg, H))) {
+                set_err("amg_hierarchy_build: " + g_err);
+                return fail(st);
+            }
+            std::vector<amgsetup::RankPlan> plans;
+            std::string err;
+            if (!amgsetup::partition(H, bounds, cfg.replicate_below_bytes, plans, err)) {
+                set_err("amg_hierarchy_build: " + err);
+                return fail(AMG_ERR_ARG);
+            }
+            hier_stats(h, H);
+            Blob stats;
+            stats.putv(h->lvl_n);
+            stats.putv(h->lvl_nnzA);
+            stats.putv(h->lvl_nnzP);
+            stats.put(h->opc);
+            stats.put(h->avg_cr);
+            stats.put(h->bytes_v);
+            stats.put(h->bytes_it);
+            const int nl = (int)H.lv.size();
+            for (int q = nr - 1; q >= 0; --q) {
+                std::vector<std::vector<int32_t>> agg_own(nl > 0 ? nl - 1 : 0);
+                for (int l = 0; l + 1 < nl; ++l)
+                    agg_own[l].assign(H.lv[l].agg.begin() + plans[q].lv[l].own_begin,
+                                      H.lv[l].agg.begin() + plans[q].lv[l].own_end);
+                Blob B;
+                B.b = stats.b;
+                serialize(plans[q], H.coarse_inv, agg_own.data(), nl, B);
+                if (q == 0) myplan = std::move(B);
+                else if ((st = nccl_send_bytes(ctx, B.b, q))) return fail(st);
+            }
+        } else {
+            if ((st = nccl_send_bytes(ctx, mine.b, 0))) return fail(st);
+            if ((st = nccl_recv_bytes(ctx, myplan.b, 0))) return fail(st);
+        }
+        myplan.getv(h->lvl_n);
+        myplan.getv(h->lvl_nnzA);
+        myplan.getv(h->lvl_nnzP);
+        h->opc = myplan.get<double>();
+        h->avg_cr = myplan.get<double>();
+        h->bytes_v = myplan.get<double>();
+        h->bytes_it = myplan.get<double>();
+        amgsetup::RankPlan P;
+        std::vector<double> cinv;
+        deserialize(myplan, P, cinv, h->agg);
+        h->ranks.resize(1);
+        if ((st = upload_rank(h, P, cinv, h->ranks[0]))) return fail(st);
+        h->ranks[0].user_off = 0;
+        for (auto& L : P.lv) {
+            h->lvl_own_begin.push_back(L.own_begin);
+            h->lvl_own_end.push_back(L.own_end);
+        }
+        h->n0_local = P.lv[0].own_end - P.lv[0].own_begin;
+        for (size_t l = 0; l < P.lv.size(); ++l)
+            h->lvl_fmt.push_back(l + 1 < P.lv.size() ? h->ranks[0].lv[l].A.fmt : FMT_DENSE);
     }
-    if (nl == 1 && (st = upload_mat(H.lv[0].A, h->A0))) return fail(st);
-    h->nL = H.lv.back().A.nrows;
-    h->nnzL = H.lv.back().A.nnz();
-    if ((st = dev_copy(&h->cinv, H.coarse_inv.data(), H.coarse_inv.size()))) return fail(st);
-    if ((st = dev_alloc(&h->cb, h->nL))) return fail(st);
-    if ((st = dev_alloc(&h->cx, h->nL))) return fail(st);
-    if ((st = dev_alloc(&h->pr, h->n0))) return fail(st);
-    if ((st = dev_alloc(&h->pz, h->n0))) return fail(st);
-    if ((st = dev_alloc(&h->pp, h->n0))) return fail(st);
-    if ((st = dev_alloc(&h->pq, h->n0))) return fail(st);
-    if ((st = dev_alloc(&h->st, 1))) return fail(st);
-    if ((st = dev_alloc(&h->partials, kMaxPartials))) return fail(st);
-    if ((st = dev_alloc(&h->ticket, 1))) return fail(st);
     if (cudaMallocHost((void**)&h->st_host, sizeof(PcgState)) != cudaSuccess) {
         set_err("cudaMallocHost failed");
         return fail(AMG_ERR_OOM);
     }
     cudaEventCreate(&h->ev0);
     cudaEventCreate(&h->ev1);
-    // ---- statistics and the §8d byte model
-    double s = 0.0;
-    for (auto& L : H.lv) s += (double)L.A.nnz();
-    h->opc = s / (double)H.lv[0].A.nnz();
-    double cr = 0.0;
-    for (size_t l = 0; l + 1 < nl; ++l) cr += (double)H.lv[l].A.nrows / (double)H.lv[l + 1].A.nrows;
-    h->avg_cr = nl > 1 ? cr / (double)(nl - 1) : 1.0;
-    byte_model(h, H);
     CK(cudaDeviceSynchronize());
     h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h;
@@ -809,20 +1376,20 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
     init.rtol = rtol;
     init.maxit = maxit;
     *h->st_host = init;
-    CK(cudaMemcpyAsync(h->st, h->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+    for (auto& R : h->ranks) CK(cudaMemcpyAsync(R.st, h->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord(h->ev0, s));
-    if (h->cfg.use_graphs) {
+    if (h->cfg.use_graphs && !h->multi()) {
         int e = ensure_solve_graph(h, b_dev, x_dev);
         if (e) return e;
         CK(cudaGraphLaunch(h->solve_exec, s));
         CK(cudaEventRecord(h->ev1, s));
-        CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h->st_host, h->ranks[0].st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     } else {
         Launch L{h, s};
         enqueue_pcg_init(h, L, b_dev, x_dev, 0);
         for (;;) {
-            CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(h->st_host, h->ranks[0].st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             if (h->st_host->status != ST_RUNNING) break;
             enqueue_pcg_body(h, L, x_dev, 0);
@@ -859,13 +1426,13 @@ int amg_solve_host(amg_hier_t h, const double* b_host, double* x_host, double rt
     }
     CK(cudaSetDevice(h->ctx->device));
     int st;
-    if (!h->hb && (st = dev_alloc(&h->hb, h->n0))) return st;
-    if (!h->hx && (st = dev_alloc(&h->hx, h->n0))) return st;
+    if (!h->hb && (st = dev_alloc(&h->hb, h->n0_local))) return st;
+    if (!h->hx && (st = dev_alloc(&h->hx, h->n0_local))) return st;
     cudaStream_t s = h->ctx->stream;
-    CK(cudaMemcpyAsync(h->hb, b_host, sizeof(double) * h->n0, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(h->hb, b_host, sizeof(double) * h->n0_local, cudaMemcpyHostToDevice, s));
     const int code = amg_solve(h, h->hb, h->hx, rtol, maxit, rep);
     if (code != AMG_OK && code != AMG_NOT_CONVERGED && code != AMG_ERR_BREAKDOWN) return code;
-    CK(cudaMemcpyAsync(x_host, h->hx, sizeof(double) * h->n0, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(x_host, h->hx, sizeof(double) * h->n0_local, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return code;
 }
@@ -877,13 +1444,13 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
     }
     CK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
-    if (h->cfg.use_graphs) {
+    if (h->cfg.use_graphs && !h->multi()) {
         int e = ensure_apply_graph(h, r_dev, z_dev);
         if (e) return e;
         CK(cudaGraphLaunch(h->apply_exec, s));
     } else {
         Launch L{h, s};
-        enqueue_vcycle(h, L, r_dev, z_dev, nullptr);
+        enqueue_apply(h, L, r_dev, z_dev);
     }
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
@@ -892,44 +1459,31 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
 
 int amg_num_levels(amg_hier_t h, int32_t* nl) {
     if (!h || !nl) return AMG_ERR_ARG;
-    *nl = (int32_t)h->lv.size() + 1;
+    *nl = (int32_t)h->lvl_n.size();
     return AMG_OK;
 }
 
 int amg_level_info(amg_hier_t h, int32_t l, int64_t* n_global, int64_t* nnzA, int64_t* nnzP, int64_t* rb,
                    int64_t* re, int32_t* format) {
-    if (!h || l < 0 || l > (int32_t)h->lv.size()) {
+    if (!h || l < 0 || l >= (int32_t)h->lvl_n.size()) {
         set_err("amg_level_info: bad level");
         return AMG_ERR_ARG;
     }
-    int64_t n, a, p;
-    int32_t f;
-    if (l < (int32_t)h->lv.size()) {
-        n = h->lv[l].n;
-        a = h->lv[l].A.nnz;
-        p = h->lv[l].P.nnz;
-        f = h->lv[l].A.fmt;
-    } else {
-        n = h->nL;
-        a = h->nnzL;
-        p = 0;
-        f = FMT_DENSE;
-    }
-    if (n_global) *n_global = n;
-    if (nnzA) *nnzA = a;
-    if (nnzP) *nnzP = p;
-    if (rb) *rb = 0;
-    if (re) *re = n;
-    if (format) *format = f;
+    if (n_global) *n_global = h->lvl_n[l];
+    if (nnzA) *nnzA = h->lvl_nnzA[l];
+    if (nnzP) *nnzP = h->lvl_nnzP[l];
+    if (rb) *rb = h->lvl_own_begin[l];
+    if (re) *re = h->lvl_own_end[l];
+    if (format) *format = h->lvl_fmt[l];
     return AMG_OK;
 }
 
 int amg_level_aggregates(amg_hier_t h, int32_t l, int64_t* agg) {
-    if (!h || !agg || l < 0 || l >= (int32_t)h->lv.size()) {
+    if (!h || !agg || l < 0 || l >= (int32_t)h->agg.size()) {
         set_err("amg_level_aggregates: bad level");
         return AMG_ERR_ARG;
     }
-    const auto& a = h->lv[l].agg;
+    const auto& a = h->agg[l];
     for (size_t i = 0; i < a.size(); ++i) agg[i] = a[i];
     return AMG_OK;
 }
@@ -949,13 +1503,15 @@ int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out
     }
     CK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
-    CK(cudaMemsetAsync(h->pr, 0, sizeof(double) * h->n0, s));
+    for (auto& R : h->ranks) CK(cudaMemsetAsync(R.pr, 0, sizeof(double) * R.lv[0].win_n, s));
     std::vector<KernelRec> recs;
     Launch L{h, s};
-    enqueue_vcycle(h, L, h->pr, h->pz, nullptr);  // warm-up
+    auto b0 = [](RankState& R) { return R.pr; };
+    auto z0 = [](RankState& R) { return R.pz; };
+    enqueue_vcycle(h, L, b0, z0, false);  // warm-up
     CK(cudaStreamSynchronize(s));
     h->prof = &recs;
-    for (int a = 0; a < napply; ++a) enqueue_vcycle(h, L, h->pr, h->pz, nullptr);
+    for (int a = 0; a < napply; ++a) enqueue_vcycle(h, L, b0, z0, false);
     h->prof = nullptr;
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
@@ -980,8 +1536,10 @@ int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out
     return AMG_OK;
 }
 
+// ---------------------------------------------------------- host-only view
 struct amg_host_hier_s {
     amgsetup::Hierarchy H;
+    std::vector<amgsetup::RankPlan> plans;
 };
 
 int amg_host_hierarchy_build(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values,
@@ -1051,6 +1609,68 @@ int amg_host_level_matrix(amg_host_hier_t h, int32_t l, int32_t which, int64_t* 
     for (int64_t k = 0; k < M.nnz(); ++k) {
         colind[k] = M.ci[k];
         values[k] = M.v[k];
+    }
+    return AMG_OK;
+}
+
+int amg_host_partition(amg_host_hier_t h, int32_t nranks, const int64_t* row_bounds, int64_t replicate_below_bytes) {
+    if (!h || nranks < 1 || !row_bounds) {
+        set_err("amg_host_partition: bad argument");
+        return AMG_ERR_ARG;
+    }
+    std::vector<int64_t> b(row_bounds, row_bounds + nranks + 1);
+    std::string err;
+    if (!amgsetup::partition(h->H, b, replicate_below_bytes, h->plans, err)) {
+        set_err("amg_host_partition: " + err);
+        return AMG_ERR_ARG;
+    }
+    return AMG_OK;
+}
+
+int amg_host_plan_level(amg_host_hier_t h, int32_t rank, int32_t l, int64_t* info16) {
+    if (!h || rank < 0 || rank >= (int32_t)h->plans.size() || l < 0 || l >= (int32_t)h->plans[rank].lv.size() ||
+        !info16) {
+        set_err("amg_host_plan_level: bad argument");
+        return AMG_ERR_ARG;
+    }
+    const auto& L = h->plans[rank].lv[l];
+    const int64_t v[16] = {L.replicated ? 1 : 0, L.n_global, L.own_begin, L.own_end, L.comp_begin, L.comp_end,
+                           L.win_begin, L.win_end, L.rst_begin, L.rst_end, (int64_t)L.recv_ids.size(),
+                           (int64_t)L.send_ids.size(), L.A.nnz(), L.P.nnz(), L.R.nnz(), 0};
+    std::memcpy(info16, v, sizeof(v));
+    return AMG_OK;
+}
+
+int amg_host_plan_array(amg_host_hier_t h, int32_t rank, int32_t l, int32_t which, void* out) {
+    if (!h || rank < 0 || rank >= (int32_t)h->plans.size() || l < 0 || l >= (int32_t)h->plans[rank].lv.size() ||
+        !out) {
+        set_err("amg_host_plan_array: bad argument");
+        return AMG_ERR_ARG;
+    }
+    const auto& L = h->plans[rank].lv[l];
+    auto cp64 = [&](const std::vector<int64_t>& v) { std::memcpy(out, v.data(), v.size() * sizeof(int64_t)); };
+    auto csr = [&](const amgsetup::Csr& M, int part) {
+        if (part == 0) {
+            cp64(M.rp);
+        } else if (part == 1) {
+            int64_t* o = (int64_t*)out;
+            for (size_t k = 0; k < M.ci.size(); ++k) o[k] = M.ci[k];
+        } else {
+            std::memcpy(out, M.v.data(), M.v.size() * sizeof(double));
+        }
+    };
+    switch (which) {
+        case 0: cp64(L.recv_off); break;
+        case 1: cp64(L.recv_ids); break;
+        case 2: cp64(L.send_off); break;
+        case 3: cp64(L.send_ids); break;
+        case 4: case 5: case 6: csr(L.A, which - 4); break;
+        case 7: case 8: case 9: csr(L.P, which - 7); break;
+        case 10: case 11: case 12: csr(L.R, which - 10); break;
+        case 13: std::memcpy(out, L.m.data(), L.m.size() * sizeof(double)); break;
+        default:
+            set_err("amg_host_plan_array: bad selector");
+            return AMG_ERR_ARG;
     }
     return AMG_OK;
 }

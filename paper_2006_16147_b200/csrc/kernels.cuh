@@ -42,6 +42,8 @@ struct PcgState {
 };
 
 enum FinishKind : int32_t { FIN_NONE = 0, FIN_BNORM = 1, FIN_RZ = 2, FIN_PQ = 3, FIN_RR = 4 };
+// Multi-rank: a dot kernel only writes its local total (rc.out, kind FIN_NONE);
+// the per-rank totals are all-gathered and k_finish sums them in rank order.
 
 struct RedCtx {
     double* partials;     // >= gridDim.x doubles
@@ -302,6 +304,7 @@ struct SdiaView {
     const double* __restrict__ val;
     int64_t n;
     int32_t ncols;
+    int32_t shift;  // row -> column frame: col = row + shift + offset (multi-rank windows)
 };
 
 template <class G, class E>
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(kBlock) k_sdia(SdiaView A, G g, E e, RedCtx rc
         double acc = 0.0;
 #pragma unroll 8
         for (uint32_t k = 0; k < w; ++k) {
-            const int32_t c = min(max((int32_t)row + __ldg(o + k), 0), rmax);
+            const int32_t c = min(max((int32_t)row + A.shift + __ldg(o + k), 0), rmax);
             acc += ld_stream(v + 32 * k) * g(c);
         }
         if (row < A.n) d += e(row, acc);
@@ -422,8 +425,8 @@ __global__ void __launch_bounds__(kBlock) k_pupdate(const double* __restrict__ z
 // x += alpha p ; r -= alpha q ; ||r||^2 -> FIN_RR
 __global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ x, double* __restrict__ r,
                                                     const double* __restrict__ p, const double* __restrict__ q,
-                                                    int64_t n, RedCtx rc) {
-    const double alpha = rc.st->alpha;
+                                                    int64_t n, const PcgState* __restrict__ st, RedCtx rc) {
+    const double alpha = st->alpha;
     double d = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         x[i] = x[i] + alpha * p[i];
@@ -432,6 +435,27 @@ __global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ x, doub
         d += ri * ri;
     }
     grid_reduce(d, rc);
+}
+
+// Multi-rank dot finisher: sum the all-gathered per-rank totals in rank order.
+__global__ void k_finish(const double* __restrict__ totals, int np, RedCtx rc) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int g = 0; g < np; ++g) s += totals[g];
+        finish(rc, s);
+    }
+}
+
+// Halo pack / unpack: buf[k] = v[idx[k]] ; v[idx[k]] = buf[k]
+__global__ void __launch_bounds__(kBlock) k_pack(const double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                 double* __restrict__ buf, int64_t n) {
+    for (int64_t k = (int64_t)blockIdx.x * kBlock + threadIdx.x; k < n; k += (int64_t)gridDim.x * kBlock)
+        buf[k] = v[idx[k]];
+}
+__global__ void __launch_bounds__(kBlock) k_unpack(double* __restrict__ v, const int32_t* __restrict__ idx,
+                                                   const double* __restrict__ buf, int64_t n) {
+    for (int64_t k = (int64_t)blockIdx.x * kBlock + threadIdx.x; k < n; k += (int64_t)gridDim.x * kBlock)
+        v[idx[k]] = buf[k];
 }
 
 // Coarsest level: z = A_L^{-1} b, dense row-major inverse, one warp per row.

@@ -1,0 +1,88 @@
+"""Multi-rank CUDA path on one GPU ("loopback", cfg.emulate_ranks = np).
+
+The hierarchy is partitioned into np row blocks exactly as across np GPUs; every
+rank's kernels run on its own window of each level, halos are packed, copied
+device-to-device (instead of NCCL send/recv) and unpacked, dot products are
+reduced per rank, all-gathered and summed in rank order, and the deep levels are
+replicated after a gather.  Same parity bars as the single-rank path against the
+CPU oracle.  (Ranks that wait on each other are never launched as concurrent
+kernels on one GPU: the loopback transport is stream-ordered copies.)
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs import config_problem, jump27, poisson7, uniform01, uniform_pm1
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2006_16147_b200 as amg
+    c = amg.Context(device=0)
+    yield c
+    c.close()
+
+
+def _case(name):
+    if name == "c4_slabs":
+        A, b, _ = config_problem(4, grid=(32, 32, 64))
+        return A, b, {}
+    if name == "aniso22":
+        A, b, _ = config_problem(3, grid=(32, 32, 32))
+        return A, b, dict(pre_sweeps=2, post_sweeps=2)
+    if name == "jump27":
+        A = jump27(16)
+        return A, uniform01(5, A.n_global), {}
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("rep_bytes", [0, 1 << 22])
+@pytest.mark.parametrize("np_", [2, 3, 4])
+@pytest.mark.parametrize("name", ["c4_slabs", "aniso22", "jump27"])
+def test_loopback_multirank_parity(ctx, name, np_, rep_bytes):
+    import paper_2006_16147_b200 as amg
+    A, b, kw = _case(name)
+    ho = O.OracleHierarchy(A, **kw)
+    h = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=np_, replicate_below_bytes=rep_bytes, **kw))
+    assert h.sizes() == ho.sizes()
+    for l in range(h.nlevels - 1):
+        assert np.array_equal(h.level_aggregates(l), ho.agg(l))
+    r = uniform_pm1(2024, A.n_global)
+    z = h.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    zo = ho.vcycle(r)
+    assert np.linalg.norm(z - zo) / np.linalg.norm(zo) <= 1e-12
+    bt = torch.tensor(b, device="cuda:0")
+    x, rep = h.solve(bt)
+    xo, info = ho.pcg(b)
+    assert rep["converged"] == 1
+    assert abs(rep["iterations"] - info["iterations"]) <= 1
+    k = min(rep["iterations"], info["iterations"])
+    x, _ = h.solve(bt, rtol=0.0, maxit=k)
+    xo, _ = ho.pcg(b, rtol=0.0, maxit=k)
+    assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-8
+
+
+def test_loopback_matches_single_rank_and_is_deterministic(ctx):
+    import paper_2006_16147_b200 as amg
+    A, b, _ = config_problem(4, grid=(32, 32, 96))
+    bt = torch.tensor(b, device="cuda:0")
+    h1 = amg.Hierarchy(ctx, A)
+    h3 = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=3, replicate_below_bytes=0))
+    x1, r1 = h1.solve(bt)
+    x3, r3 = h3.solve(bt)
+    assert r1["iterations"] == r3["iterations"]
+    assert (torch.linalg.norm(x1 - x3) / torch.linalg.norm(x1)).item() <= 1e-10
+    x3b, _ = h3.solve(bt)
+    assert torch.equal(x3, x3b)
+    xh, _ = h3.solve_host(b)
+    assert np.array_equal(xh, x3.cpu().numpy())
+
+
+def test_too_small_for_ranks_is_an_error(ctx):
+    import paper_2006_16147_b200 as amg
+    A = poisson7(5, 4, 3)  # single-level hierarchy
+    with pytest.raises(amg.AmgError):
+        amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=2))
