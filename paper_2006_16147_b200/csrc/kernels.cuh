@@ -272,7 +272,7 @@ struct SellView {
 };
 
 template <class G, class E>
-__global__ void __launch_bounds__(kBlock) k_sell(SellView A, G g, E e, RedCtx rc) {
+__global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx rc) {
     const int64_t nslices = (A.n + 31) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -308,7 +308,7 @@ struct SdiaView {
 };
 
 template <class G, class E>
-__global__ void __launch_bounds__(kBlock) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
+__global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
     const int64_t nslices = (A.n + 31) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
