@@ -428,11 +428,9 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
                     launch_mat(L, D.A, GVec{D.mb}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
             } else {  // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
                 if (l == 0)
-                    launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.m + D.ep_off, D.xa + D.ep_off}, no_red(), "sweep0",
-                               3 * n8);
+                    launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
                 else
-                    launch_mat(L, D.A, GVec{D.mb}, ESweep0{be, D.m + D.ep_off, D.xa + D.ep_off}, no_red(), "sweep0",
-                               3 * n8);
+                    launch_mat(L, D.A, GVec{D.mb}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
                 xpre[ri][l] = D.xa;
             }
         }
@@ -444,9 +442,8 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
                     DevLevel& D = R.lv[l];
                     double* xi = xpre[ri][l];
                     double* xo = (xi == D.xa) ? D.xb : D.xa;
-                    launch_mat(L, D.A, GVec{xi},
-                               ESweep<false>{xi + D.ep_off, bvec(R) + D.ep_off, D.m + D.ep_off, xo + D.ep_off},
-                               no_red(), "presweep", 4 * 8.0 * (double)D.comp_n);
+                    launch_mat(L, D.A, GVec{xi}, ESweep<false>{xi + D.ep_off, bvec(R) + D.ep_off, xo + D.ep_off},
+                               no_red(), "presweep", 3 * 8.0 * (double)D.comp_n);
                     xpre[ri][l] = xo;
                 }
             }
@@ -496,13 +493,8 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
             tmp[ri] = D.xb;                     // the prolongation update is row-local: may run in place
             double* dst = (s2 % 2 == 1) ? tmp[ri] : fin[ri];
             const double n8 = 8.0 * (double)D.comp_n;
-            if (s1 == 1) {
-                if (l == 0)
-                    launch_mat(L, D.P, GVec{e}, EProlong0{b + D.ep_off, D.m + D.ep_off, dst + D.ep_off}, no_red(),
-                               "prolong0", 3 * n8 + nc8);
-                else
-                    launch_mat(L, D.P, GVec{e}, EProlongMB{D.mb + D.ep_off, dst + D.ep_off}, no_red(), "prolong0",
-                               2 * n8 + nc8);
+            if (s1 == 1) {  // u = P-bar e only; the first post-sweep adds m o b (EPost1)
+                launch_mat(L, D.P, GVec{e}, EStore{dst + D.ep_off}, no_red(), "prolong", n8 + nc8);
             } else {
                 launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[ri][l] + D.ep_off, dst + D.ep_off}, no_red(), "prolong",
                            2 * n8 + nc8);
@@ -519,14 +511,51 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
                 double* xi = cur[ri];
                 double* xo = (xi == tmp[ri]) ? fin[ri] : tmp[ri];
                 const double n8 = 8.0 * (double)D.comp_n;
-                if (l == 0 && last && rz)
-                    launch_mat(L, D.A, GVec{xi},
-                               ESweep<true>{xi + D.ep_off, b + D.ep_off, D.m + D.ep_off, xo + D.ep_off},
-                               dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 4 * n8);
-                else
-                    launch_mat(L, D.A, GVec{xi},
-                               ESweep<false>{xi + D.ep_off, b + D.ep_off, D.m + D.ep_off, xo + D.ep_off}, no_red(),
-                               "postsweep", 4 * n8);
+                const bool dot = (l == 0 && last && rz);
+                // short rows: m_i recomputed from the streamed row; long rows: read m
+                const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
+                const double mb8 = abs ? 0.0 : n8;
+                double* m = D.m + D.ep_off;
+                if (s == 0 && s1 == 1) {
+                    const double* bo = (l == 0) ? b + D.ep_off : D.mb + D.ep_off;
+                    const double* rr = D.r + D.ep_off;
+                    double* uu = xi + D.ep_off;
+                    double* xx = xo + D.ep_off;
+                    if (dot && abs)
+                        launch_mat(L, D.A, GVec{xi}, EPost1<true, false, true>{uu, rr, bo, xx},
+                                   dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 4 * n8);
+                    else if (dot)
+                        launch_mat(L, D.A, GVec{xi}, EPost1<true, false, false>{uu, rr, bo, xx, m},
+                                   dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 5 * n8);
+                    else if (l == 0 && abs)
+                        launch_mat(L, D.A, GVec{xi}, EPost1<false, false, true>{uu, rr, bo, xx}, no_red(),
+                                   "postsweep", 4 * n8);
+                    else if (l == 0)
+                        launch_mat(L, D.A, GVec{xi}, EPost1<false, false, false>{uu, rr, bo, xx, m}, no_red(),
+                                   "postsweep", 5 * n8);
+                    else if (abs)
+                        launch_mat(L, D.A, GVec{xi}, EPost1<false, true, true>{uu, rr, bo, xx}, no_red(),
+                                   "postsweep", 4 * n8);
+                    else
+                        launch_mat(L, D.A, GVec{xi}, EPost1<false, true, false>{uu, rr, bo, xx, m}, no_red(),
+                                   "postsweep", 5 * n8);
+                } else if (dot) {
+                    if (abs)
+                        launch_mat(L, D.A, GVec{xi}, ESweep<true, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off},
+                                   dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 3 * n8);
+                    else
+                        launch_mat(L, D.A, GVec{xi},
+                                   ESweep<true, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m},
+                                   dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 3 * n8 + mb8);
+                } else {
+                    if (abs)
+                        launch_mat(L, D.A, GVec{xi}, ESweep<false, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off},
+                                   no_red(), "postsweep", 3 * n8);
+                    else
+                        launch_mat(L, D.A, GVec{xi},
+                                   ESweep<false, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m}, no_red(),
+                                   "postsweep", 3 * n8 + mb8);
+                }
                 cur[ri] = xo;
             }
         }

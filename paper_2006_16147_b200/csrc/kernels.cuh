@@ -162,9 +162,19 @@ struct GMB {   // (m o b)_j : the first l1-Jacobi sweep from x = 0 (R9)
 };
 
 // ------------------------------------------------------------- epilogues
+// An epilogue with `kAbs = true` also receives asum = sum_k |a_ik| of the row it
+// streams, i.e. the l1-Jacobi diagonal 1/m_i (nb = 1), so m_i is
+// recomputed in registers instead of being read from HBM.
+template <class E>
+__device__ __forceinline__ double apply_epi(const E& e, int64_t i, double s, double asum) {
+    if constexpr (E::kAbs) return e(i, s, asum);
+    else return e(i, s);
+}
+
 // r = b - s                                (residual; s = A x or A (m o b))
 struct EResid {
     static constexpr bool kDot = false;
+    static constexpr bool kAbs = false;
     const double* __restrict__ b;
     double* __restrict__ r;
     __device__ __forceinline__ double operator()(int64_t i, double s) const {
@@ -173,28 +183,57 @@ struct EResid {
     }
 };
 // x' = x + m (b - s)                        (l1-Jacobi sweep, out of place)
-template <bool DOT>
+// ABS = true: m_i = 1/asum from the streamed row (short rows); false: m_i read
+// from `m` (long rows, where the extra per-entry |a| chain costs more than 8 B/row).
+template <bool DOT, bool ABS = true>
 struct ESweep {
     static constexpr bool kDot = DOT;
+    static constexpr bool kAbs = ABS;
     const double* __restrict__ x;
     const double* __restrict__ b;
-    const double* __restrict__ m;
     double* __restrict__ xo;
-    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+    const double* __restrict__ m = nullptr;
+    __device__ __forceinline__ double f(int64_t i, double s, double mi) const {
         const double bi = b[i];
-        const double v = x[i] + m[i] * (bi - s);
+        const double v = x[i] + mi * (bi - s);
         xo[i] = v;
         return DOT ? bi * v : 0.0;  // r^T z at the end of the level-0 V-cycle
     }
+    __device__ __forceinline__ double operator()(int64_t i, double s, double asum) const { return f(i, s, 1.0 / asum); }
+    __device__ __forceinline__ double operator()(int64_t i, double s) const { return f(i, s, m[i]); }
+};
+// First post-sweep after ONE pre-sweep from zero.  With x1 = m b, r = b - A x1 (kept
+// from the down phase) and the prolongation u = P-bar e, the sweep on x = x1 + u is
+//   x' = x1 + u + m (b - A x1 - A u) = m b + u + m (r - A u)        (Eq. 3.1, exact)
+// so u is gathered instead of x and neither the prolongation nor this sweep reads m.
+// MB: the rhs is given premultiplied (mb = m o b, levels >= 1) instead of b.
+template <bool DOT, bool MB, bool ABS = true>
+struct EPost1 {
+    static constexpr bool kDot = DOT;
+    static constexpr bool kAbs = ABS;
+    const double* __restrict__ u;
+    const double* __restrict__ r;
+    const double* __restrict__ bmb;  // b (level 0) or m o b (MB)
+    double* __restrict__ xo;
+    const double* __restrict__ m = nullptr;
+    __device__ __forceinline__ double f(int64_t i, double s, double mi) const {
+        const double bi = bmb[i];
+        const double x1 = MB ? bi : mi * bi;
+        const double v = x1 + u[i] + mi * (r[i] - s);
+        xo[i] = v;
+        return DOT ? bi * v : 0.0;  // DOT only at level 0 (b = r of PCG)
+    }
+    __device__ __forceinline__ double operator()(int64_t i, double s, double asum) const { return f(i, s, 1.0 / asum); }
+    __device__ __forceinline__ double operator()(int64_t i, double s) const { return f(i, s, m[i]); }
 };
 // x' = m b + m (b - s)  with s = A (m o b)  (two sweeps from x = 0, s1 >= 2)
 struct ESweep0 {
     static constexpr bool kDot = false;
+    static constexpr bool kAbs = true;
     const double* __restrict__ b;
-    const double* __restrict__ m;
     double* __restrict__ xo;
-    __device__ __forceinline__ double operator()(int64_t i, double s) const {
-        const double mi = m[i], bi = b[i];
+    __device__ __forceinline__ double operator()(int64_t i, double s, double asum) const {
+        const double mi = 1.0 / asum, bi = b[i];
         xo[i] = mi * bi + mi * (bi - s);
         return 0.0;
     }
@@ -202,6 +241,7 @@ struct ESweep0 {
 // y = s                                     (restriction b_{l+1} = P-bar^T r)
 struct EStore {
     static constexpr bool kDot = false;
+    static constexpr bool kAbs = false;
     double* __restrict__ y;
     __device__ __forceinline__ double operator()(int64_t i, double s) const {
         y[i] = s;
@@ -212,6 +252,7 @@ struct EStore {
 //                                             coarse rhs by the coarse l1 diagonal)
 struct EStoreMB {
     static constexpr bool kDot = false;
+    static constexpr bool kAbs = false;
     double* __restrict__ y;
     const double* __restrict__ m;
     double* __restrict__ mb;
@@ -224,6 +265,7 @@ struct EStoreMB {
 // x = mb + s                                (prolongation after one pre-sweep from 0, mb = m o b)
 struct EProlongMB {
     static constexpr bool kDot = false;
+    static constexpr bool kAbs = false;
     const double* __restrict__ mb;
     double* __restrict__ xo;
     __device__ __forceinline__ double operator()(int64_t i, double s) const {
@@ -234,6 +276,7 @@ struct EProlongMB {
 // x = m b + s                               (prolongation after one pre-sweep from 0)
 struct EProlong0 {
     static constexpr bool kDot = false;
+    static constexpr bool kAbs = false;
     const double* __restrict__ b;
     const double* __restrict__ m;
     double* __restrict__ xo;
@@ -245,6 +288,7 @@ struct EProlong0 {
 // x' = x + s                                (prolongation, general)
 struct EProlongAdd {
     static constexpr bool kDot = false;
+    static constexpr bool kAbs = false;
     const double* x;
     double* xo;
     __device__ __forceinline__ double operator()(int64_t i, double s) const {
@@ -255,6 +299,7 @@ struct EProlongAdd {
 // q = s, returns p_i q_i                    (PCG: q = A p fused with p^T q)
 struct ESpmvDot {
     static constexpr bool kDot = true;
+    static constexpr bool kAbs = false;
     const double* __restrict__ p;
     double* __restrict__ q;
     __device__ __forceinline__ double operator()(int64_t i, double s) const {
@@ -283,11 +328,15 @@ __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
         const int32_t* c = A.col + (int64_t)b0 * 32 + lane;
         const double* v = A.val + (int64_t)b0 * 32 + lane;
-        double acc = 0.0;
+        double acc = 0.0, asum = 0.0;
 #pragma unroll 8
-        for (uint32_t k = 0; k < w; ++k) acc += ld_stream(v + 32 * k) * g(ld_stream(c + 32 * k));
+        for (uint32_t k = 0; k < w; ++k) {
+            const double a = ld_stream(v + 32 * k);
+            acc += a * g(ld_stream(c + 32 * k));
+            if constexpr (E::kAbs) asum += fabs(a);
+        }
         const int64_t row = (s << 5) + lane;
-        if (row < A.n) d += e(row, acc);
+        if (row < A.n) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
 }
@@ -321,13 +370,15 @@ __global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx
         const int32_t* o = A.offs + b0;
         const double* v = A.val + (int64_t)b0 * 32 + lane;
         const int32_t rmax = A.ncols - 1;
-        double acc = 0.0;
+        double acc = 0.0, asum = 0.0;
 #pragma unroll 8
         for (uint32_t k = 0; k < w; ++k) {
             const int32_t c = min(max((int32_t)row + A.shift + __ldg(o + k), 0), rmax);
-            acc += ld_stream(v + 32 * k) * g(c);
+            const double a = ld_stream(v + 32 * k);
+            acc += a * g(c);
+            if constexpr (E::kAbs) asum += fabs(a);
         }
-        if (row < A.n) d += e(row, acc);
+        if (row < A.n) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
 }
@@ -351,15 +402,22 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
     const int64_t iters = (A.n + ng - 1) / ng;
     for (int64_t it = 0; it < iters; ++it) {
         const int64_t row = g0 + it * ng;
-        double acc = 0.0;
+        double acc = 0.0, asum = 0.0;
         if (row < A.n) {
             const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
 #pragma unroll 4
-            for (int32_t k = k0 + sub; k < k1; k += VW) acc += ld_stream(A.v + k) * g(ld_stream(A.ci + k));
+            for (int32_t k = k0 + sub; k < k1; k += VW) {
+                const double a = ld_stream(A.v + k);
+                acc += a * g(ld_stream(A.ci + k));
+                if constexpr (E::kAbs) asum += fabs(a);
+            }
         }
 #pragma unroll
-        for (int o = VW / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, VW);
-        if (sub == 0 && row < A.n) d += e(row, acc);
+        for (int o = VW / 2; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o, VW);
+            if constexpr (E::kAbs) asum += __shfl_xor_sync(0xffffffffu, asum, o, VW);
+        }
+        if (sub == 0 && row < A.n) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
 }
@@ -369,21 +427,34 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
 // one 256-thread block per row, fixed-order block reduction.
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc) {
-    __shared__ double part[kBlock / 32];
+    __shared__ double part[kBlock / 32], apart[kBlock / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double d = 0.0;
     for (int64_t row = blockIdx.x; row < A.n; row += gridDim.x) {
         const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
-        double acc = 0.0;
+        double acc = 0.0, asum = 0.0;
 #pragma unroll 4
-        for (int32_t k = k0 + threadIdx.x; k < k1; k += kBlock) acc += ld_stream(A.v + k) * g(ld_stream(A.ci + k));
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) part[wid] = acc;
+        for (int32_t k = k0 + threadIdx.x; k < k1; k += kBlock) {
+            const double a = ld_stream(A.v + k);
+            acc += a * g(ld_stream(A.ci + k));
+            if constexpr (E::kAbs) asum += fabs(a);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if constexpr (E::kAbs) asum += __shfl_xor_sync(0xffffffffu, asum, o);
+        }
+        if (lane == 0) {
+            part[wid] = acc;
+            apart[wid] = asum;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int w = 0; w < kBlock / 32; ++w) s += part[w];
-            d += e(row, s);
+            double s = 0.0, as = 0.0;
+            for (int w = 0; w < kBlock / 32; ++w) {
+                s += part[w];
+                as += apart[w];
+            }
+            d += apply_epi(e, row, s, as);
         }
         __syncthreads();
     }
