@@ -251,6 +251,26 @@ int vec_grid(int64_t n, int nsm) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)nsm * 8));
 }
 
+// Kernel launch with programmatic stream serialization (PDL, see kernels.cuh).
+bool pdl_enabled() {
+    static const bool on = !(std::getenv("AMG_PDL") && std::getenv("AMG_PDL")[0] == '0');
+    return on;
+}
+template <class... KArgs, class... Args>
+void launch_k(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // Optional per-launch CUDA-event timing (amg_profile_vcycle).
 struct Launch {
     amg_hier_s* h;
@@ -276,20 +296,20 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         static const int cap = max_grid((const void*)k_sdia<G, E>, nsm);
         const int64_t need = (M.nrows + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        k_sdia<G, E><<<grid, kBlock, 0, L.s>>>(SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift},
+        launch_k(k_sdia<G, E>, grid, kBlock, L.s, SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift},
                                                 g, e, rc);
     } else if (M.fmt == FMT_SELL) {
         static const int cap = max_grid((const void*)k_sell<G, E>, nsm);
         const int64_t need = (M.nrows + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        k_sell<G, E><<<grid, kBlock, 0, L.s>>>(SellView{M.sptr, M.col, M.val, M.nrows}, g, e, rc);
+        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows}, g, e, rc);
     } else {
         const CsrView v{M.rp, M.col, M.val, M.nrows};
         const int64_t need = (M.nrows * M.vw + kBlock - 1) / kBlock;
         if (M.vw == kVWBlock) {
             static const int cap = max_grid((const void*)k_csrb<G, E>, nsm);
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(M.nrows, cap));
-            k_csrb<G, E><<<grid, kBlock, 0, L.s>>>(v, g, e, rc);
+            launch_k(k_csrb<G, E>, grid, kBlock, L.s, v, g, e, rc);
             L.end();
             return;
         }
@@ -298,7 +318,7 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
     case W: {                                                                     \
         static const int cap = max_grid((const void*)k_csrv<W, G, E>, nsm);       \
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap)); \
-        k_csrv<W, G, E><<<grid, kBlock, 0, L.s>>>(v, g, e, rc);                   \
+        launch_k(k_csrv<W, G, E>, grid, kBlock, L.s, v, g, e, rc);                   \
         break;                                                                    \
     }
             VWCASE(2)
@@ -336,7 +356,7 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind) {
     }
     for (auto& R : h->ranks) {
         RedCtx rc{nullptr, nullptr, nullptr, R.st, 0ull, kind};
-        k_finish<<<1, 32, 0, L.s>>>(R.dot_all, h->np, rc);
+        launch_k(k_finish, 1, 32, L.s, R.dot_all, h->np, rc);
     }
 }
 
@@ -351,7 +371,7 @@ void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) {
     if (!any && h->loopback) return;
     for (auto& R : h->ranks) {
         const Exch& E = R.lv[l].ex;
-        if (E.nsend) k_pack<<<vec_grid(E.nsend, nsm), kBlock, 0, L.s>>>(vec(R), E.send_idx, E.sbuf, E.nsend);
+        if (E.nsend) launch_k(k_pack, vec_grid(E.nsend, nsm), kBlock, L.s, vec(R), E.send_idx, E.sbuf, E.nsend);
     }
     if (h->loopback) {
         for (auto& Rd : h->ranks) {
@@ -378,7 +398,7 @@ void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) {
     }
     for (auto& R : h->ranks) {
         const Exch& E = R.lv[l].ex;
-        if (E.nrecv) k_unpack<<<vec_grid(E.nrecv, nsm), kBlock, 0, L.s>>>(vec(R), E.recv_idx, E.rbuf, E.nrecv);
+        if (E.nrecv) launch_k(k_unpack, vec_grid(E.nrecv, nsm), kBlock, L.s, vec(R), E.recv_idx, E.rbuf, E.nrecv);
     }
 }
 
@@ -395,11 +415,11 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
     if (nl == 1) {  // single-level hierarchy: B = A^{-1} (replicated, np == 1)
         for (auto& R : h->ranks) {
             L.begin("coarse_gemv", 8.0 * (double)R.nL * (double)R.nL + 16.0 * (double)R.nL);
-            k_dense_gemv<<<vec_grid(R.nL * 32, nsm), kBlock, 0, L.s>>>(R.cinv, b0(R), z0(R), R.nL);
+            launch_k(k_dense_gemv, vec_grid(R.nL * 32, nsm), kBlock, L.s, R.cinv, b0(R), z0(R), R.nL);
             L.end();
             if (rz) {
                 L.begin("dot_rz", 16.0 * R.nL);
-                k_dot<<<vec_grid(R.nL, nsm), kBlock, 0, L.s>>>(b0(R), z0(R), R.nL, dot_red(h, R, FIN_RZ, 0));
+                launch_k(k_dot, vec_grid(R.nL, nsm), kBlock, L.s, b0(R), z0(R), R.nL, dot_red(h, R, FIN_RZ, 0));
                 L.end();
             }
         }
@@ -475,7 +495,7 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
     for (auto& R : h->ranks) {
         DevLevel& C = R.lv[nl - 1];
         L.begin("coarse_gemv", 8.0 * (double)R.nL * (double)R.nL + 16.0 * (double)R.nL);
-        k_dense_gemv<<<vec_grid(R.nL * 32, nsm), kBlock, 0, L.s>>>(R.cinv, C.b, C.xa, R.nL);
+        launch_k(k_dense_gemv, vec_grid(R.nL * 32, nsm), kBlock, L.s, R.cinv, C.b, C.xa, R.nL);
         L.end();
     }
     // ---- up: prolongation, post-smoothing
@@ -571,7 +591,7 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
         L.begin("pupdate", 24.0 * D.own_n);
-        k_pupdate<<<vec_grid(D.own_n, nsm), kBlock, 0, L.s>>>(R.pz + D.own_off, R.pp + D.own_off, D.own_n, R.st);
+        launch_k(k_pupdate, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off, D.own_n, R.st);
         L.end();
     }
     exchange(h, L, 0, [](RankState& R) { return R.pp; });
@@ -584,7 +604,7 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
         L.begin("axpy_rr", 48.0 * D.own_n);
-        k_axpy_rr<<<vec_grid(D.own_n, nsm), kBlock, 0, L.s>>>(x_user + R.user_off, R.pr + D.own_off,
+        launch_k(k_axpy_rr, vec_grid(D.own_n, nsm), kBlock, L.s, x_user + R.user_off, R.pr + D.own_off,
                                                                R.pp + D.own_off, R.pq + D.own_off, D.own_n, R.st,
                                                                dot_red(h, R, FIN_RR, cond));
         L.end();
@@ -596,7 +616,7 @@ void enqueue_pcg_init(amg_hier_s* h, Launch& L, const double* b_user, double* x_
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
         L.begin("pcg_init", 24.0 * D.own_n);
-        k_pcg_init<<<vec_grid(D.own_n, h->ctx->nsm), kBlock, 0, L.s>>>(b_user + R.user_off, R.pr + D.own_off,
+        launch_k(k_pcg_init, vec_grid(D.own_n, h->ctx->nsm), kBlock, L.s, b_user + R.user_off, R.pr + D.own_off,
                                                                         x_user + R.user_off, D.own_n,
                                                                         dot_red(h, R, FIN_BNORM, cond));
         L.end();

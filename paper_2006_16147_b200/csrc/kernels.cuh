@@ -138,6 +138,17 @@ __device__ __forceinline__ void grid_reduce(double v, const RedCtx& rc) {
     }
 }
 
+// ------------------------------------------------- programmatic dependent launch
+// Every kernel is launched with programmatic stream serialization: it lets its
+// dependents begin launching at once (their blocks take SM slots only as ours
+// retire) and waits for its own prerequisites to complete and flush before it
+// touches memory.  This overlaps launch latency and block ramp-up with the tail
+// of the previous kernel — the deep levels are latency-bound.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- loads
 __device__ __forceinline__ double ld_stream(const double* p) {
     double r;
@@ -318,6 +329,7 @@ struct SellView {
 
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx rc) {
+    pdl_begin();
     const int64_t nslices = (A.n + 31) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -358,6 +370,7 @@ struct SdiaView {
 
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
+    pdl_begin();
     const int64_t nslices = (A.n + 31) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -393,6 +406,7 @@ struct CsrView {
 
 template <int VW, class G, class E>
 __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc) {
+    pdl_begin();
     const int64_t gid = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     const int sub = threadIdx.x % VW;
     const int64_t g0 = gid / VW;
@@ -427,6 +441,7 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
 // one 256-thread block per row, fixed-order block reduction.
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc) {
+    pdl_begin();
     __shared__ double part[kBlock / 32], apart[kBlock / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double d = 0.0;
@@ -465,6 +480,7 @@ __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc)
 // PCG prologue: r = b, x = 0, ||b||^2 -> FIN_BNORM
 __global__ void __launch_bounds__(kBlock) k_pcg_init(const double* __restrict__ b, double* __restrict__ r,
                                                      double* __restrict__ x, int64_t n, RedCtx rc) {
+    pdl_begin();
     double d = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         const double bi = b[i];
@@ -478,6 +494,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_init(const double* __restrict__ 
 // a^T b -> finisher (single-level hierarchies: r^T z)
 __global__ void __launch_bounds__(kBlock) k_dot(const double* __restrict__ a, const double* __restrict__ b,
                                                 int64_t n, RedCtx rc) {
+    pdl_begin();
     double d = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
         d += a[i] * b[i];
@@ -487,6 +504,7 @@ __global__ void __launch_bounds__(kBlock) k_dot(const double* __restrict__ a, co
 // p = z (first iteration) or p = z + beta p
 __global__ void __launch_bounds__(kBlock) k_pupdate(const double* __restrict__ z, double* __restrict__ p, int64_t n,
                                                     const PcgState* __restrict__ st) {
+    pdl_begin();
     const bool first = st->iter == 0;
     const double beta = st->beta;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
@@ -497,6 +515,7 @@ __global__ void __launch_bounds__(kBlock) k_pupdate(const double* __restrict__ z
 __global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ x, double* __restrict__ r,
                                                     const double* __restrict__ p, const double* __restrict__ q,
                                                     int64_t n, const PcgState* __restrict__ st, RedCtx rc) {
+    pdl_begin();
     const double alpha = st->alpha;
     double d = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
@@ -510,6 +529,7 @@ __global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ x, doub
 
 // Multi-rank dot finisher: sum the all-gathered per-rank totals in rank order.
 __global__ void k_finish(const double* __restrict__ totals, int np, RedCtx rc) {
+    pdl_begin();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
         for (int g = 0; g < np; ++g) s += totals[g];
@@ -520,11 +540,13 @@ __global__ void k_finish(const double* __restrict__ totals, int np, RedCtx rc) {
 // Halo pack / unpack: buf[k] = v[idx[k]] ; v[idx[k]] = buf[k]
 __global__ void __launch_bounds__(kBlock) k_pack(const double* __restrict__ v, const int32_t* __restrict__ idx,
                                                  double* __restrict__ buf, int64_t n) {
+    pdl_begin();
     for (int64_t k = (int64_t)blockIdx.x * kBlock + threadIdx.x; k < n; k += (int64_t)gridDim.x * kBlock)
         buf[k] = v[idx[k]];
 }
 __global__ void __launch_bounds__(kBlock) k_unpack(double* __restrict__ v, const int32_t* __restrict__ idx,
                                                    const double* __restrict__ buf, int64_t n) {
+    pdl_begin();
     for (int64_t k = (int64_t)blockIdx.x * kBlock + threadIdx.x; k < n; k += (int64_t)gridDim.x * kBlock)
         v[idx[k]] = buf[k];
 }
@@ -532,6 +554,7 @@ __global__ void __launch_bounds__(kBlock) k_unpack(double* __restrict__ v, const
 // Coarsest level: z = A_L^{-1} b, dense row-major inverse, one warp per row.
 __global__ void __launch_bounds__(kBlock) k_dense_gemv(const double* __restrict__ Ainv, const double* __restrict__ b,
                                                        double* __restrict__ z, int64_t n) {
+    pdl_begin();
     const int64_t warp = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
