@@ -214,3 +214,33 @@ def test_vcycle_properties_full_c4(ctx):
                                   size=(A.n_global, A.n_global)).cuda()
     res = bt - (Asp @ xs.unsqueeze(1)).squeeze(1)
     assert (torch.linalg.norm(res) / torch.linalg.norm(bt)).item() <= 1.5e-6
+
+
+def test_full_c3_anisotropic_properties(ctx):
+    """BASELINE config 3 at full size (256^3, (1,1,1e-2), 2/2 sweeps) as bench.py
+    --config 3 runs it: level-0 aggregates are the closed-form 4x2x1 bricks (pin P16),
+    the device V-cycle is linear and symmetric, PCG converges with the true residual
+    at the requested tolerance."""
+    amg = _amg()
+    A, b, meta = config_problem(3)
+    h = amg.Hierarchy(ctx, A, cfg=amg.make_config(pre_sweeps=2, post_sweeps=2))
+    nx = 256
+    i = np.arange(A.n_global)
+    x, y, z = i % nx, (i // nx) % nx, i // (nx * nx)
+    brick = x // 4 + (nx // 4) * (y // 2 + (nx // 2) * z)
+    assert np.array_equal(h.level_aggregates(0), brick)
+    g = torch.Generator(device="cpu").manual_seed(6)
+    r = torch.rand(A.n_global, generator=g, dtype=torch.float64).cuda()
+    s = torch.rand(A.n_global, generator=g, dtype=torch.float64).cuda()
+    Br, Bs = h.precond_apply(r).clone(), h.precond_apply(s).clone()
+    lin = h.precond_apply(0.5 * r + 2.0 * s)
+    assert (torch.linalg.norm(lin - (0.5 * Br + 2.0 * Bs)) / torch.linalg.norm(lin)).item() <= 1e-12
+    sym = abs(torch.dot(Br, s) - torch.dot(r, Bs)).item()
+    assert sym <= 1e-12 * torch.linalg.norm(r).item() * torch.linalg.norm(s).item()
+    bt = torch.tensor(b, device="cuda:0")
+    xs, rep = h.solve(bt, rtol=1e-6)
+    assert rep["converged"] == 1
+    Asp = torch.sparse_csr_tensor(torch.tensor(A.rowptr), torch.tensor(A.colind), torch.tensor(A.values),
+                                  size=(A.n_global, A.n_global)).cuda()
+    res = bt - (Asp @ xs.unsqueeze(1)).squeeze(1)
+    assert (torch.linalg.norm(res) / torch.linalg.norm(bt)).item() <= 1.5e-6
