@@ -75,6 +75,7 @@ struct DevMat {
     int32_t shift = 0;         // SDIA: row -> window column frame
     uint32_t* sptr = nullptr;  // SELL / SDIA
     int32_t* offs = nullptr;   // SDIA: one column offset per slice column
+    int32_t* anchor = nullptr; // SDIA of a rectangular operator: per-row base column
     int32_t* rp = nullptr;     // CSR
     int32_t* col = nullptr;
     double* val = nullptr;
@@ -85,18 +86,22 @@ struct DevMat {
         const double nsl = (double)((nrows + 31) / 32);
         switch (fmt) {
             case FMT_SELL: return 12.0 * (double)stored + 4.0 * (nsl + 1);
-            case FMT_SDIA: return 8.0 * (double)stored + 4.0 * (double)stored / 32.0 + 4.0 * (nsl + 1);
+            case FMT_SDIA:
+                return 8.0 * (double)stored + 4.0 * (double)stored / 32.0 + 4.0 * (nsl + 1) +
+                       (anchor ? 4.0 * (double)nrows : 0.0);
             default: return 12.0 * (double)nnz + 4.0 * (double)(nrows + 1);
         }
     }
     void release() {
         cudaFree(sptr);
         cudaFree(offs);
+        cudaFree(anchor);
         cudaFree(rp);
         cudaFree(col);
         cudaFree(val);
         sptr = nullptr;
         offs = nullptr;
+        anchor = nullptr;
         rp = col = nullptr;
         val = nullptr;
     }
@@ -296,8 +301,8 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         static const int cap = max_grid((const void*)k_sdia<G, E>, nsm);
         const int64_t need = (M.nrows + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        launch_k(k_sdia<G, E>, grid, kBlock, L.s, SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift},
-                                                g, e, rc);
+        launch_k(k_sdia<G, E>, grid, kBlock, L.s,
+                 SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor}, g, e, rc);
     } else if (M.fmt == FMT_SELL) {
         static const int cap = max_grid((const void*)k_sell<G, E>, nsm);
         const int64_t need = (M.nrows + kBlock - 1) / kBlock;
@@ -661,24 +666,39 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift) {
     int64_t padded = 0;
     for (int64_t s = 0; s < nsl; ++s) padded += 32 * (int64_t)width[s];
     const double mean = n ? (double)nnz / (double)n : 0.0;
-    // SDIA-32 candidate: per slice, the sorted distinct offsets col - (row + shift)
-    if (square && nsl >= 148 * 16 && mean <= 64.0) {
+    // SDIA-32 candidate: per slice, the sorted distinct offsets col - base(row), with
+    // base = row + shift for A_l and base = the row's first column (stored per row,
+    // "anchor") for the rectangular P-bar_l / R_l
+    if (nsl >= 148 * 16 && mean <= 64.0) {
+        std::vector<int32_t> anc;
+        if (!square) {
+            anc.resize(n);
+            for (int64_t r = 0; r < n; ++r) anc[r] = M.rp[r + 1] > M.rp[r] ? M.ci[M.rp[r]] : 0;
+        }
+        auto base = [&](int64_t r) -> int64_t { return square ? r + shift : (int64_t)anc[r]; };
         std::vector<uint32_t> dw(nsl, 0);
         std::vector<std::vector<int32_t>> soffs(nsl);
 #pragma omp parallel for schedule(static)
         for (int64_t s = 0; s < nsl; ++s) {
             auto& o = soffs[s];
             for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r)
-                for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t) o.push_back((int32_t)((int64_t)M.ci[t] - (r + shift)));
+                for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t) o.push_back((int32_t)((int64_t)M.ci[t] - base(r)));
             std::sort(o.begin(), o.end());
             o.erase(std::unique(o.begin(), o.end()), o.end());
             dw[s] = (uint32_t)o.size();
         }
         int64_t dpad = 0;
         for (int64_t s = 0; s < nsl; ++s) dpad += 32 * (int64_t)dw[s];
-        if ((double)dpad <= 1.02 * (double)padded + 64.0 && dpad / 32 < (int64_t)UINT32_MAX) {
+        const double sdia_bytes = 8.0 * (double)dpad + 4.0 * (double)dpad / 32.0 + (square ? 0.0 : 4.0 * (double)n);
+        const double sell_bytes = 12.0 * (double)padded;
+        const bool ok = square ? (double)dpad <= 1.02 * (double)padded + 64.0 : sdia_bytes <= 0.9 * sell_bytes;
+        if (ok && dpad / 32 < (int64_t)UINT32_MAX) {
             D.fmt = FMT_SDIA;
             D.stored = dpad;
+            if (!square) {
+                int st;
+                if ((st = dev_copy(&D.anchor, anc.data(), anc.size()))) return st;
+            }
             std::vector<uint32_t> sptr(nsl + 1, 0);
             for (int64_t s = 0; s < nsl; ++s) sptr[s + 1] = sptr[s] + dw[s];
             std::vector<int32_t> offs(dpad / 32);
@@ -687,14 +707,14 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift) {
             for (int64_t s = 0; s < nsl; ++s) {
                 const auto& o = soffs[s];
                 std::copy(o.begin(), o.end(), offs.begin() + sptr[s]);
-                const int64_t base = (int64_t)sptr[s] * 32;
+                const int64_t vbase = (int64_t)sptr[s] * 32;
                 for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r) {
                     const int64_t lane = r - s * 32;
                     size_t k = 0;
                     for (int64_t t = M.rp[r]; t < M.rp[r + 1]; ++t) {
-                        const int32_t d = (int32_t)((int64_t)M.ci[t] - (r + shift));
+                        const int32_t d = (int32_t)((int64_t)M.ci[t] - base(r));
                         while (o[k] != d) ++k;  // both ascending
-                        val[base + (int64_t)k * 32 + lane] = M.v[t];
+                        val[vbase + (int64_t)k * 32 + lane] = M.v[t];
                     }
                 }
             }

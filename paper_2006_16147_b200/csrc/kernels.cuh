@@ -366,6 +366,7 @@ struct SdiaView {
     int64_t n;
     int32_t ncols;
     int32_t shift;  // row -> column frame: col = row + shift + offset (multi-rank windows)
+    const int32_t* __restrict__ anchor;  // rectangular operators: col = anchor[row] + offset
 };
 
 template <class G, class E>
@@ -380,13 +381,15 @@ __global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx
         const uint32_t b0 = __ldg(A.sptr + s);
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
         const int64_t row = (s << 5) + lane;
+        const int32_t base =
+            A.anchor ? (row < A.n ? __ldg(A.anchor + row) : 0) : (int32_t)row + A.shift;
         const int32_t* o = A.offs + b0;
         const double* v = A.val + (int64_t)b0 * 32 + lane;
         const int32_t rmax = A.ncols - 1;
         double acc = 0.0, asum = 0.0;
 #pragma unroll 8
         for (uint32_t k = 0; k < w; ++k) {
-            const int32_t c = min(max((int32_t)row + A.shift + __ldg(o + k), 0), rmax);
+            const int32_t c = min(max(base + __ldg(o + k), 0), rmax);
             const double a = ld_stream(v + 32 * k);
             acc += a * g(c);
             if constexpr (E::kAbs) asum += fabs(a);
