@@ -595,8 +595,9 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
     enqueue_vcycle(h, L, [](RankState& R) { return R.pr; }, [](RankState& R) { return R.pz; }, true);
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
-        L.begin("pupdate", 24.0 * D.own_n);
-        launch_k(k_pupdate, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off, D.own_n, R.st);
+        L.begin("pupdate", 40.0 * D.own_n);
+        launch_k(k_pupdate, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off,
+                 x_user + R.user_off, D.own_n, R.st);
         L.end();
     }
     exchange(h, L, 0, [](RankState& R) { return R.pp; });
@@ -608,13 +609,22 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
     dot_finish(h, L, FIN_PQ);
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
-        L.begin("axpy_rr", 48.0 * D.own_n);
-        launch_k(k_axpy_rr, vec_grid(D.own_n, nsm), kBlock, L.s, x_user + R.user_off, R.pr + D.own_off,
-                                                               R.pp + D.own_off, R.pq + D.own_off, D.own_n, R.st,
-                                                               dot_red(h, R, FIN_RR, cond));
+        L.begin("axpy_rr", 24.0 * D.own_n);
+        launch_k(k_axpy_rr, vec_grid(D.own_n, nsm), kBlock, L.s, R.pr + D.own_off, R.pq + D.own_off, D.own_n, R.st,
+                 dot_red(h, R, FIN_RR, cond));
         L.end();
     }
     dot_finish(h, L, FIN_RR);
+}
+
+void enqueue_pcg_final(amg_hier_s* h, Launch& L, double* x_user) {
+    for (auto& R : h->ranks) {
+        const DevLevel& D = R.L0();
+        L.begin("xfinal", 24.0 * D.own_n);
+        launch_k(k_xfinal, vec_grid(D.own_n, h->ctx->nsm), kBlock, L.s, x_user + R.user_off, R.pp + D.own_off,
+                 D.own_n, R.st);
+        L.end();
+    }
 }
 
 void enqueue_pcg_init(amg_hier_s* h, Launch& L, const double* b_user, double* x_user, unsigned long long cond) {
@@ -909,6 +919,10 @@ int ensure_solve_graph(amg_hier_s* h, const double* b, double* x) {
     CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     enqueue_pcg_body(h, L, x, (unsigned long long)cond);
     CK(cudaStreamEndCapture(s, &body));
+    // after the loop: the deferred last x update
+    CK(cudaStreamBeginCaptureToGraph(s, g, &wnode, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+    enqueue_pcg_final(h, L, x);
+    CK(cudaStreamEndCapture(s, &g));
     CK(cudaGraphInstantiate(&h->solve_exec, g, 0));
     CK(cudaGraphDestroy(g));
     h->solve_b = b;
@@ -1463,6 +1477,7 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
             if (h->st_host->status != ST_RUNNING) break;
             enqueue_pcg_body(h, L, x_dev, 0);
         }
+        enqueue_pcg_final(h, L, x_dev);
         CK(cudaEventRecord(h->ev1, s));
         CK(cudaStreamSynchronize(s));
     }

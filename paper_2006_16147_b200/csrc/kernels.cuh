@@ -504,30 +504,48 @@ __global__ void __launch_bounds__(kBlock) k_dot(const double* __restrict__ a, co
     grid_reduce(d, rc);
 }
 
-// p = z (first iteration) or p = z + beta p
-__global__ void __launch_bounds__(kBlock) k_pupdate(const double* __restrict__ z, double* __restrict__ p, int64_t n,
+// p = z (first iteration) or p = z + beta p.  The previous iteration's
+// x += alpha p is applied here, where the old p is read anyway (deferred from
+// k_axpy_rr; the last one is applied by k_xfinal after the loop).
+__global__ void __launch_bounds__(kBlock) k_pupdate(const double* __restrict__ z, double* __restrict__ p,
+                                                    double* __restrict__ x, int64_t n,
                                                     const PcgState* __restrict__ st) {
     pdl_begin();
     const bool first = st->iter == 0;
-    const double beta = st->beta;
-    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
-        p[i] = first ? z[i] : z[i] + beta * p[i];
+    const double beta = st->beta, alpha = st->alpha;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        if (first) {
+            p[i] = z[i];
+        } else {
+            const double pi = p[i];
+            x[i] = x[i] + alpha * pi;
+            p[i] = z[i] + beta * pi;
+        }
+    }
 }
 
-// x += alpha p ; r -= alpha q ; ||r||^2 -> FIN_RR
-__global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ x, double* __restrict__ r,
-                                                    const double* __restrict__ p, const double* __restrict__ q,
-                                                    int64_t n, const PcgState* __restrict__ st, RedCtx rc) {
+// r -= alpha q ; ||r||^2 -> FIN_RR
+__global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ r, const double* __restrict__ q, int64_t n,
+                                                    const PcgState* __restrict__ st, RedCtx rc) {
     pdl_begin();
     const double alpha = st->alpha;
     double d = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
-        x[i] = x[i] + alpha * p[i];
         const double ri = r[i] - alpha * q[i];
         r[i] = ri;
         d += ri * ri;
     }
     grid_reduce(d, rc);
+}
+
+// After the loop: the pending x += alpha p of the last iteration.
+__global__ void __launch_bounds__(kBlock) k_xfinal(double* __restrict__ x, const double* __restrict__ p, int64_t n,
+                                                   const PcgState* __restrict__ st) {
+    pdl_begin();
+    if (st->iter == 0) return;
+    const double alpha = st->alpha;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        x[i] = x[i] + alpha * p[i];
 }
 
 // Multi-rank dot finisher: sum the all-gathered per-rank totals in rank order.
