@@ -51,9 +51,17 @@ struct ohier {
     int32_t nl;
     olevel* lv;
     int32_t pre, post;
+    /* coarsest solver: 0 = dense Cholesky (reading R2); 1 = CG preconditioned by
+     * l1-Jacobi, stopped at ||r||/||b|| < coarse_rtol or after coarse_maxit
+     * iterations */
+    int32_t coarse_cg;
+    double coarse_rtol;
+    int32_t coarse_maxit;
 };
 
 /* ------------------------------------------------------------------ helpers */
+static double dot(int64_t n, const double* a, const double* b);
+
 static void* xmalloc(size_t n) {
     void* p = malloc(n ? n : 1);
     if (!p) abort();
@@ -701,13 +709,63 @@ double or_avg_cr(const ohier* h) {
 }
 
 /* ------------------------------------------------------------------ V-cycle */
+/* Coarsest iterative solve: CG from x0 = 0
+ * preconditioned by the l1-Jacobi diagonal of A_L, stopped as soon as the
+ * relative residual is less than rtol, or after maxit iterations. */
+static void coarse_pcg(const ocsr* A, const double* m, int64_t n, double rtol, int32_t maxit, const double* b,
+                       double* x) {
+    double* r = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* z = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* p = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* q = (double*)xmalloc(sizeof(double) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        x[i] = 0.0;
+        r[i] = b[i];
+        z[i] = m[i] * r[i];
+        p[i] = z[i];
+    }
+    double bnorm = sqrt(dot(n, b, b));
+    double rho = dot(n, r, z);
+    if (bnorm > 0.0) {
+        for (int32_t k = 1; k <= maxit; ++k) {
+            or_spmv(A, p, q);
+            double pq = dot(n, p, q);
+            if (!(pq > 0.0)) break;
+            double alpha = rho / pq;
+            for (int64_t i = 0; i < n; ++i) {
+                x[i] = x[i] + alpha * p[i];
+                r[i] = r[i] - alpha * q[i];
+            }
+            if (sqrt(dot(n, r, r)) / bnorm < rtol) break;
+            for (int64_t i = 0; i < n; ++i) z[i] = m[i] * r[i];
+            double rho_new = dot(n, r, z);
+            double beta = rho_new / rho;
+            for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+            rho = rho_new;
+        }
+    }
+    free(r);
+    free(z);
+    free(p);
+    free(q);
+}
+
+void or_set_coarse_cg(ohier* h, int32_t on, double rtol, int32_t maxit) {
+    h->coarse_cg = on;
+    h->coarse_rtol = rtol;
+    h->coarse_maxit = maxit;
+}
+
 /* O10, Eq. 3.1: x = m.b; (s1-1) sweeps x += m.(b - A x);
  * e = V(l+1, P-bar^T (b - A x)); x += P-bar e; s2 sweeps; at l = L: A_L^{-1} b. */
 static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
     const olevel* L = &h->lv[l];
     int64_t n = L->n;
     if (l == h->nl - 1) {
-        cholesky_solve(n, L->L, b, x);
+        if (h->coarse_cg)
+            coarse_pcg(L->A, L->m, n, h->coarse_rtol, h->coarse_maxit, b, x);
+        else
+            cholesky_solve(n, L->L, b, x);
         return;
     }
     double* t = (double*)xmalloc(sizeof(double) * (size_t)n);
@@ -799,6 +857,75 @@ int32_t or_pcg(const ohier* h, const double* b, double* x, double rtol, int32_t 
         double beta = rho_new / rho;
         for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
         rho = rho_new;
+    }
+    or_spmv(A, x, q);
+    for (int64_t i = 0; i < n; ++i) q[i] = b[i] - q[i];
+    *true_relres = sqrt(dot(n, q, q)) / bnorm;
+done:
+    free(r);
+    free(z);
+    free(p);
+    free(q);
+    return st;
+}
+
+/* FCG(1): flexible CG with one-direction
+ * orthogonalisation, x0 = 0, for a (possibly nonlinear) preconditioner B:
+ *   z_k = B r_k; p_k = z_k - ((z_k^T q_{k-1}) / (p_{k-1}^T q_{k-1})) p_{k-1} (p_0 = z_0);
+ *   q_k = A p_k; alpha = (p_k^T r_k) / (p_k^T q_k); x += alpha p_k; r -= alpha q_k;
+ * stop when ||r_k||/||b|| <= rtol.  Returns as or_pcg. */
+int32_t or_fcg(const ohier* h, const double* b, double* x, double rtol, int32_t maxit, int32_t* iters,
+               double* relres, double* true_relres, double* hist) {
+    const ocsr* A = h->lv[0].A;
+    int64_t n = h->lv[0].n;
+    double* r = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* z = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* p = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* q = (double*)xmalloc(sizeof(double) * (size_t)n);
+    int32_t st = OR_NOT_CONVERGED;
+    for (int64_t i = 0; i < n; ++i) {
+        x[i] = 0.0;
+        r[i] = b[i];
+    }
+    double bnorm = sqrt(dot(n, b, b));
+    *iters = 0;
+    *relres = 0.0;
+    if (hist) hist[0] = 1.0;
+    if (bnorm == 0.0) {
+        *true_relres = 0.0;
+        st = OR_OK;
+        goto done;
+    }
+    *relres = 1.0;
+    double pq_prev = 0.0;
+    for (int32_t k = 1; k <= maxit; ++k) {
+        or_vcycle(h, r, z);
+        if (k == 1) {
+            memcpy(p, z, sizeof(double) * (size_t)n);
+        } else {
+            double beta = -dot(n, z, q) / pq_prev;
+            for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        }
+        or_spmv(A, p, q);
+        double pq = dot(n, p, q);
+        if (!(pq > 0.0)) {
+            st = OR_BREAKDOWN;
+            break;
+        }
+        double alpha = dot(n, p, r) / pq;
+        for (int64_t i = 0; i < n; ++i) {
+            x[i] = x[i] + alpha * p[i];
+            r[i] = r[i] - alpha * q[i];
+        }
+        pq_prev = pq;
+        double rel = sqrt(dot(n, r, r)) / bnorm;
+        *iters = k;
+        *relres = rel;
+        if (hist) hist[k] = rel;
+        if (rel <= rtol) {
+            st = OR_OK;
+            break;
+        }
     }
     or_spmv(A, x, q);
     for (int64_t i = 0; i < n; ++i) q[i] = b[i] - q[i];

@@ -74,6 +74,11 @@ double  or_avg_cr(const ohier* h);
 void    or_vcycle(const ohier* h, const double* r, double* z);
 int32_t or_pcg(const ohier* h, const double* b, double* x, double rtol, int32_t maxit,
                int32_t* iters, double* relres, double* true_relres, double* hist);
+/* SURVEY §8f NEXT-2 (the paper's GPU method VA3S5CS1): FCG(1) outer
+ * solver and the coarsest level solved by l1-Jacobi-preconditioned CG. */
+int32_t or_fcg(const ohier* h, const double* b, double* x, double rtol, int32_t maxit,
+               int32_t* iters, double* relres, double* true_relres, double* hist);
+void    or_set_coarse_cg(ohier* h, int32_t on, double rtol, int32_t maxit);
 
 #ifdef __cplusplus
 }

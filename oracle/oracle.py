@@ -74,6 +74,10 @@ def lib():
         "or_pcg": (C.c_int32, [_vp, _f64p, _f64p, C.c_double, C.c_int32,
                                C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                C.POINTER(C.c_double), _vp]),
+        "or_fcg": (C.c_int32, [_vp, _f64p, _f64p, C.c_double, C.c_int32,
+                               C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                               C.POINTER(C.c_double), _vp]),
+        "or_set_coarse_cg": (None, [_vp, C.c_int32, C.c_double, C.c_int32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -289,14 +293,21 @@ class OracleHierarchy:
         lib().or_vcycle(self.h, _cf(r), z)
         return z
 
-    def pcg(self, b, rtol=1e-6, maxit=500, history=False):
+    def set_coarse_cg(self, on=True, rtol=1e-4, maxit=30):
+        """Coarsest level by l1-Jacobi PCG instead of Cholesky."""
+        lib().or_set_coarse_cg(self.h, int(on), float(rtol), int(maxit))
+
+    def fcg(self, b, rtol=1e-6, maxit=500, history=False):
+        return self.pcg(b, rtol, maxit, history, _fn="or_fcg")
+
+    def pcg(self, b, rtol=1e-6, maxit=500, history=False, _fn="or_pcg"):
         x = np.zeros(self.n)
         it = C.c_int32(0)
         rr = C.c_double(0)
         tr = C.c_double(0)
         hist = np.zeros(maxit + 1) if history else None
-        st = lib().or_pcg(self.h, _cf(b), x, float(rtol), int(maxit), C.byref(it), C.byref(rr),
-                          C.byref(tr), hist.ctypes.data_as(C.c_void_p) if history else None)
+        st = getattr(lib(), _fn)(self.h, _cf(b), x, float(rtol), int(maxit), C.byref(it), C.byref(rr),
+                                 C.byref(tr), hist.ctypes.data_as(C.c_void_p) if history else None)
         out = dict(status=st, iterations=it.value, relres=rr.value, true_relres=tr.value)
         if history:
             out["history"] = hist[:it.value + 1]
