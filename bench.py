@@ -170,6 +170,22 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours
+def method_settings(args, meta, world):
+    """--method default: the north_star path (PCG, l1-Jacobi with the config's sweeps, direct
+    coarsest, maxsize 200*np).  --method va3s5cs1: the paper's own GPU method:
+    FCG(1), 4/4 l1-Jacobi sweeps, coarsest CG + l1-Jacobi to 1e-4 / 30 its,
+    maxsize 12*200*np."""
+    if args.method == "va3s5cs1":
+        return {"name": "va3s5cs1", "desc": "3 matching sweeps/level, smoothed P (omega=4/3/||D^-1A||), "
+                                            "FCG(1), coarsest l1-Jacobi CG (1e-4, 30 its)",
+                "cfg": dict(pre_sweeps=4, post_sweeps=4, max_coarse_size=12 * 200 * world, krylov=1,
+                            coarse_solver=1, coarse_rtol=1e-4, coarse_maxit=30)}
+    return {"name": "default", "desc": "3 matching sweeps/level, smoothed P (omega=4/3/||D^-1A||), PCG, "
+                                       "direct coarsest",
+            "cfg": dict(pre_sweeps=meta["sweeps"][0], post_sweeps=meta["sweeps"][1],
+                        max_coarse_size=meta["max_coarse_size"])}
+
+
 def run_ours(args):
     import torch
 
@@ -190,8 +206,8 @@ def run_ours(args):
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     ctx = amg.Context(device=local, rank=rank, nranks=world, nccl_uid=uid, stream=stream.cuda_stream)
-    cfg = amg.make_config(pre_sweeps=meta["sweeps"][0], post_sweeps=meta["sweeps"][1],
-                          max_coarse_size=meta["max_coarse_size"])
+    method = method_settings(args, meta, world)
+    cfg = amg.make_config(**method["cfg"])
     t0 = time.perf_counter()
     h = amg.Hierarchy(ctx, A, cfg=cfg)
     setup_s = time.perf_counter() - t0
@@ -281,9 +297,10 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config, meta["grid"]), "n_global": n_global,
                        "grid": list(meta["grid"]), "partition": f"z-slabs x{world}",
-                       "rtol": args.rtol, "sweeps": f"{meta['sweeps'][0]}/{meta['sweeps'][1]}",
-                       "hierarchy": "3 matching sweeps/level, smoothed P (omega=4/3/||D^-1A||), direct coarsest",
-                       "max_coarse_size": meta["max_coarse_size"], "rhs": meta["rhs"],
+                       "rtol": args.rtol, "method": method["name"],
+                       "sweeps": f"{method['cfg']['pre_sweeps']}/{method['cfg']['post_sweeps']}",
+                       "hierarchy": method["desc"],
+                       "max_coarse_size": method["cfg"]["max_coarse_size"], "rhs": meta["rhs"],
                        "l2_policy": "inputs larger than L2 (hierarchy >> 126 MB), no flush",
                        "parallelism": f"rowblock{world}"},
             "solve_s": ms_per_step * 1e-3, "device_solve_s": dev_solve_ms * 1e-3, "iterations": iters,
@@ -331,6 +348,7 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--maxit", type=int, default=500)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--method", choices=["default", "va3s5cs1"], default="default")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -73,6 +73,17 @@ typedef struct {
                                      this many equal row blocks held by ONE process on one GPU and
                                      runs the multi-rank kernels with in-process halo copies
                                      ("loopback"); the caller's vectors stay global.  Default 1. */
+    /* --- the paper's own GPU method VA3S5CS1 --- */
+    int32_t krylov;               /* outer solver of amg_solve: 0 = PCG (default, north_star;
+                                     reading R1), 1 = FCG(1) ("Flexible Conjugate
+                                     Gradient"), required when the preconditioner is nonlinear */
+    int32_t coarse_solver;        /* 0 = dense direct solve with the explicit inverse (default,
+                                     reading R2); 1 = CG preconditioned by the l1-Jacobi diagonal
+                                     of A_L, run as one thread-block-cluster
+                                     kernel; makes the V-cycle nonlinear (use krylov = 1) */
+    int32_t coarse_maxit;         /* coarse CG iteration cap (default 30) */
+    double  coarse_rtol;          /* coarse CG stops when ||r||/||b|| < this (default 1e-4,
+                                     PAPER.md:264) */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */

@@ -23,7 +23,9 @@ class amg_config_t(C.Structure):
                 ("max_levels", C.c_int32), ("min_coarsening_ratio", C.c_double),
                 ("pre_sweeps", C.c_int32), ("post_sweeps", C.c_int32),
                 ("replicate_below_bytes", C.c_int64), ("setup_threads", C.c_int32),
-                ("use_graphs", C.c_int32), ("emulate_ranks", C.c_int32)]
+                ("use_graphs", C.c_int32), ("emulate_ranks", C.c_int32),
+                ("krylov", C.c_int32), ("coarse_solver", C.c_int32), ("coarse_maxit", C.c_int32),
+                ("coarse_rtol", C.c_double)]
 
 
 class amg_report_t(C.Structure):

@@ -177,8 +177,20 @@ struct RankState {
     unsigned int* ticket = nullptr;
     double* dot_local = nullptr;  // this rank's dot total
     double* dot_all = nullptr;    // all-gathered totals (np)
+    // coarsest iterative solve (cfg.coarse_solver == 1): CSR of A_L, its l1 diagonal,
+    // the per-CTA row split and the cluster launch shape of k_coarse_cg
+    int32_t *cg_rp = nullptr, *cg_ci = nullptr, *cg_split = nullptr;
+    double *cg_v = nullptr, *cg_m = nullptr;
+    int64_t cg_nnz = 0;
+    int cg_ncta = 1, cg_smem_a = 0;
+    size_t cg_smem = 0;
     void release() {
         for (auto& D : lv) D.release();
+        cudaFree(cg_rp);
+        cudaFree(cg_ci);
+        cudaFree(cg_split);
+        cudaFree(cg_v);
+        cudaFree(cg_m);
         cudaFree(cinv);
         cudaFree(pr);
         cudaFree(pz);
@@ -407,11 +419,53 @@ void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) {
     }
 }
 
+// Coarsest-level solve z_L = B_L b_L: the explicit inverse (reading R2) or the
+// paper's l1-Jacobi-preconditioned CG as one cluster kernel.
+void launch_coarse(amg_hier_s* h, Launch& L, RankState& R, const double* b, double* x) {
+    const int nsm = h->ctx->nsm;
+    if (h->cfg.coarse_solver != 1) {
+        L.begin("coarse_gemv", 8.0 * (double)R.nL * (double)R.nL + 16.0 * (double)R.nL);
+        launch_k(k_dense_gemv, vec_grid(R.nL * 32, nsm), kBlock, L.s, R.cinv, b, x, R.nL);
+        L.end();
+        return;
+    }
+    // bytes of ONE pass over A_L (the iteration count is data dependent; latency-bound)
+    L.begin("coarse_cg", 12.0 * (double)R.cg_nnz + 4.0 * (double)(R.nL + 1) + 24.0 * (double)R.nL);
+    const CoarseCG A{R.cg_rp, R.cg_ci, R.cg_v, R.cg_m, R.cg_split, (int32_t)R.nL, R.cg_ncta, R.cg_smem_a,
+                     h->cfg.coarse_maxit, h->cfg.coarse_rtol};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)R.cg_ncta);
+    cfg.blockDim = dim3((unsigned)kCgBlock);
+    cfg.dynamicSmemBytes = R.cg_smem;
+    cfg.stream = L.s;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (R.cg_ncta > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)R.cg_ncta;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, k_coarse_cg, A, b, x);
+    L.end();
+}
+
 // ------------------------------------------------------------- V-cycle
 // z0 = B b0 (Eq. 3.1).  b0/z0 give each rank's
 // level-0 WINDOW base pointers.  With `rz`, the last level-0 post-sweep also
-// reduces b0^T z0 (kind FIN_RZ).
-void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, bool rz) {
+// reduces b0^T z0 (kind FIN_RZ), or, with a dot weight `dwv` (FCG), dwv^T z0
+// (kind FIN_ZQ).
+void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, bool rz,
+                    const VecOf* dwv = nullptr) {
+    const int dkind = dwv ? FIN_ZQ : FIN_RZ;
     const int nl = h->nlev();
     const int s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
     const int nsm = h->ctx->nsm;
@@ -419,16 +473,15 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
     auto ri_of = [&](RankState& R) { return (int)(&R - h->ranks.data()); };
     if (nl == 1) {  // single-level hierarchy: B = A^{-1} (replicated, np == 1)
         for (auto& R : h->ranks) {
-            L.begin("coarse_gemv", 8.0 * (double)R.nL * (double)R.nL + 16.0 * (double)R.nL);
-            launch_k(k_dense_gemv, vec_grid(R.nL * 32, nsm), kBlock, L.s, R.cinv, b0(R), z0(R), R.nL);
-            L.end();
+            launch_coarse(h, L, R, b0(R), z0(R));
             if (rz) {
                 L.begin("dot_rz", 16.0 * R.nL);
-                launch_k(k_dot, vec_grid(R.nL, nsm), kBlock, L.s, b0(R), z0(R), R.nL, dot_red(h, R, FIN_RZ, 0));
+                launch_k(k_dot, vec_grid(R.nL, nsm), kBlock, L.s, dwv ? (*dwv)(R) : b0(R), z0(R), R.nL,
+                         dot_red(h, R, dkind, 0));
                 L.end();
             }
         }
-        if (rz) dot_finish(h, L, FIN_RZ);
+        if (rz) dot_finish(h, L, dkind);
         return;
     }
     std::vector<std::vector<double*>> xpre(nr, std::vector<double*>(nl, nullptr));
@@ -499,9 +552,7 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
     // ---- coarsest: z_L = A_L^{-1} b_L (reading R2), replicated on every rank
     for (auto& R : h->ranks) {
         DevLevel& C = R.lv[nl - 1];
-        L.begin("coarse_gemv", 8.0 * (double)R.nL * (double)R.nL + 16.0 * (double)R.nL);
-        launch_k(k_dense_gemv, vec_grid(R.nL * 32, nsm), kBlock, L.s, R.cinv, C.b, C.xa, R.nL);
-        L.end();
+        launch_coarse(h, L, R, C.b, C.xa);
     }
     // ---- up: prolongation, post-smoothing
     for (int l = nl - 2; l >= 0; --l) {
@@ -537,6 +588,7 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
                 double* xo = (xi == tmp[ri]) ? fin[ri] : tmp[ri];
                 const double n8 = 8.0 * (double)D.comp_n;
                 const bool dot = (l == 0 && last && rz);
+                const double* dw = (dot && dwv) ? (*dwv)(R) + D.ep_off : nullptr;
                 // short rows: m_i recomputed from the streamed row; long rows: read m
                 const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
                 const double mb8 = abs ? 0.0 : n8;
@@ -547,11 +599,11 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
                     double* uu = xi + D.ep_off;
                     double* xx = xo + D.ep_off;
                     if (dot && abs)
-                        launch_mat(L, D.A, GVec{xi}, EPost1<true, false, true>{uu, rr, bo, xx},
-                                   dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 4 * n8);
+                        launch_mat(L, D.A, GVec{xi}, EPost1<true, false, true>{uu, rr, bo, xx, nullptr, dw},
+                                   dot_red(h, R, dkind, 0), "postsweep_dot", 4 * n8);
                     else if (dot)
-                        launch_mat(L, D.A, GVec{xi}, EPost1<true, false, false>{uu, rr, bo, xx, m},
-                                   dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 5 * n8);
+                        launch_mat(L, D.A, GVec{xi}, EPost1<true, false, false>{uu, rr, bo, xx, m, dw},
+                                   dot_red(h, R, dkind, 0), "postsweep_dot", 5 * n8);
                     else if (l == 0 && abs)
                         launch_mat(L, D.A, GVec{xi}, EPost1<false, false, true>{uu, rr, bo, xx}, no_red(),
                                    "postsweep", 4 * n8);
@@ -566,12 +618,13 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
                                    "postsweep", 5 * n8);
                 } else if (dot) {
                     if (abs)
-                        launch_mat(L, D.A, GVec{xi}, ESweep<true, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off},
-                                   dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 3 * n8);
+                        launch_mat(L, D.A, GVec{xi},
+                                   ESweep<true, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, nullptr, dw},
+                                   dot_red(h, R, dkind, 0), "postsweep_dot", 3 * n8);
                     else
                         launch_mat(L, D.A, GVec{xi},
-                                   ESweep<true, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m},
-                                   dot_red(h, R, FIN_RZ, 0), "postsweep_dot", 3 * n8 + mb8);
+                                   ESweep<true, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m, dw},
+                                   dot_red(h, R, dkind, 0), "postsweep_dot", 3 * n8 + mb8);
                 } else {
                     if (abs)
                         launch_mat(L, D.A, GVec{xi}, ESweep<false, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off},
@@ -585,28 +638,43 @@ void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, 
             }
         }
     }
-    if (rz) dot_finish(h, L, FIN_RZ);
+    if (rz) dot_finish(h, L, dkind);
 }
 
 // PCG loop body, rotated so that the convergence test is the last node:
 //   z = V(r), rho' = r^T z, beta ; p = z + beta p ; q = A p, alpha ; x, r update, test.
+//
+// FCG(1) (cfg.krylov == 1) uses the same rotation:
+//   z = V(r), beta = -(z^T q)/(p^T q)_prev ; p = z + beta p, p^T r ;
+//   q = A p, alpha = p^T r / p^T q ; x, r update, test.
 void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long long cond) {
     const int nsm = h->ctx->nsm;
-    enqueue_vcycle(h, L, [](RankState& R) { return R.pr; }, [](RankState& R) { return R.pz; }, true);
+    const bool fcg = h->cfg.krylov == 1;
+    const VecOf qv = [](RankState& R) { return R.pq; };
+    enqueue_vcycle(h, L, [](RankState& R) { return R.pr; }, [](RankState& R) { return R.pz; }, true,
+                   fcg ? &qv : nullptr);
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
-        L.begin("pupdate", 40.0 * D.own_n);
-        launch_k(k_pupdate, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off,
-                 x_user + R.user_off, D.own_n, R.st);
+        if (fcg) {
+            L.begin("pupdate_fcg", 48.0 * D.own_n);
+            launch_k(k_pupdate_fcg, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off,
+                     x_user + R.user_off, R.pr + D.own_off, D.own_n, R.st, dot_red(h, R, FIN_PR, 0));
+        } else {
+            L.begin("pupdate", 40.0 * D.own_n);
+            launch_k(k_pupdate, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off,
+                     x_user + R.user_off, D.own_n, R.st);
+        }
         L.end();
     }
+    if (fcg) dot_finish(h, L, FIN_PR);
     exchange(h, L, 0, [](RankState& R) { return R.pp; });
+    const int pqk = fcg ? FIN_PQF : FIN_PQ;
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
-        launch_mat(L, D.A, GVec{R.pp}, ESpmvDot{R.pp + D.own_off, R.pq + D.own_off}, dot_red(h, R, FIN_PQ, 0),
+        launch_mat(L, D.A, GVec{R.pp}, ESpmvDot{R.pp + D.own_off, R.pq + D.own_off}, dot_red(h, R, pqk, 0),
                    "spmv_dot", 16.0 * D.own_n);
     }
-    dot_finish(h, L, FIN_PQ);
+    dot_finish(h, L, pqk);
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
         L.begin("axpy_rr", 24.0 * D.own_n);
@@ -788,6 +856,83 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift) {
     return AMG_OK;
 }
 
+// Coarse CG (cfg.coarse_solver == 1): CSR of the replicated A_L, its l1 diagonal,
+// and the cluster shape of k_coarse_cg.  CTAs: enough that each holds <= ~16k
+// entries (the SpMV is spread over 16 warps per CTA), more if the CTA's rows of
+// A_L do not fit in shared memory, at most 16 (non-portable cluster size), and
+// no more than the device can co-schedule as one cluster.
+int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) {
+    const amgsetup::Csr& A = C.A;
+    const int64_t n = A.nrows, nnz = A.nnz();
+    if (n > 16384 || nnz >= (int64_t)INT32_MAX) {
+        set_err("coarse CG: the coarsest matrix is too large (n_L <= 16384 required)");
+        return AMG_ERR_ARG;
+    }
+    static bool attr_done = false;
+    if (!attr_done) {
+        CK(cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_done = true;
+    }
+    const size_t budget = 200 * 1024;
+    auto plan = [&](int ncta, std::vector<int32_t>& split, size_t& smem_base, size_t& smem_a) {
+        split.assign(ncta + 1, 0);
+        for (int c = 1; c < ncta; ++c) {
+            const int64_t target = nnz * c / ncta;
+            const int64_t r = std::lower_bound(A.rp.begin(), A.rp.end(), target) - A.rp.begin();
+            split[c] = (int32_t)std::max<int64_t>(split[c - 1] + 1, std::min<int64_t>(r, n - (ncta - c)));
+        }
+        split[ncta] = (int32_t)n;
+        int64_t own = 0, ann = 0;
+        for (int c = 0; c < ncta; ++c) {
+            own = std::max<int64_t>(own, split[c + 1] - split[c]);
+            ann = std::max<int64_t>(ann, A.rp[split[c + 1]] - A.rp[split[c]]);
+        }
+        smem_base = 8 * (size_t)n + 32 * (size_t)own;
+        smem_a = 12 * (size_t)ann;
+    };
+    int ncta = (int)std::min<int64_t>(16, std::max<int64_t>(1, (nnz + 16383) / 16384));
+    ncta = (int)std::min<int64_t>(ncta, n);
+    std::vector<int32_t> split;
+    size_t base = 0, sa = 0;
+    plan(ncta, split, base, sa);
+    while (base + sa > budget && ncta < 16 && ncta < n) plan(++ncta, split, base, sa);
+    for (;;) {  // the cluster must be co-schedulable
+        if (ncta == 1) break;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)ncta);
+        lc.blockDim = dim3((unsigned)kCgBlock);
+        lc.dynamicSmemBytes = base + (base + sa <= budget ? sa : 0);
+        cudaLaunchAttribute at;
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = (unsigned)ncta;
+        at.val.clusterDim.y = at.val.clusterDim.z = 1;
+        lc.attrs = &at;
+        lc.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_coarse_cg, &lc) == cudaSuccess && ncl > 0) break;
+        cudaGetLastError();
+        plan(--ncta, split, base, sa);
+    }
+    if (base > budget) {
+        set_err("coarse CG: the coarsest vectors do not fit in shared memory");
+        return AMG_ERR_ARG;
+    }
+    R.cg_ncta = ncta;
+    R.cg_smem_a = (base + sa <= budget) ? 1 : 0;
+    R.cg_smem = base + (R.cg_smem_a ? sa : 0);
+    R.cg_nnz = nnz;
+    std::vector<int32_t> rp(n + 1);
+    for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)A.rp[i];
+    int st;
+    if ((st = dev_copy(&R.cg_rp, rp.data(), rp.size()))) return st;
+    if ((st = dev_copy(&R.cg_ci, A.ci.data(), A.ci.size()))) return st;
+    if ((st = dev_copy(&R.cg_v, A.v.data(), A.v.size()))) return st;
+    if ((st = dev_copy(&R.cg_m, C.m.data(), C.m.size()))) return st;
+    if ((st = dev_copy(&R.cg_split, split.data(), split.size()))) return st;
+    return AMG_OK;
+}
+
 // Uploads one rank's plan.  coarse_inv: the dense A_L^{-1}.
 int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<double>& coarse_inv, RankState& R) {
     const int nl = (int)P.lv.size();
@@ -836,6 +981,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
     }
     R.nL = P.lv[nl - 1].n_global;
     if ((st = dev_copy(&R.cinv, coarse_inv.data(), coarse_inv.size()))) return st;
+    if (h->cfg.coarse_solver == 1 && (st = upload_coarse_cg(h, P.lv[nl - 1], R))) return st;
     const size_t w0 = (size_t)R.lv[0].win_n;
     if ((st = dev_alloc(&R.pr, w0))) return st;
     if ((st = dev_alloc(&R.pz, w0))) return st;
@@ -1203,6 +1349,10 @@ void amg_config_default(amg_config_t* c) {
     c->setup_threads = 0;
     c->use_graphs = 1;
     c->emulate_ranks = 1;
+    c->krylov = 0;
+    c->coarse_solver = 0;
+    c->coarse_maxit = 30;
+    c->coarse_rtol = 1e-4;
 }
 
 int amg_nccl_unique_id(void* out128) {
@@ -1277,6 +1427,11 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     // AMG_EAGER=1 forces eager launches (ncu cannot profile kernels inside graphs
     // that contain conditional nodes)
     if (const char* ev = std::getenv("AMG_EAGER")) cfg.use_graphs = (ev[0] == '1') ? 0 : cfg.use_graphs;
+    if ((cfg.krylov != 0 && cfg.krylov != 1) || (cfg.coarse_solver != 0 && cfg.coarse_solver != 1) ||
+        cfg.coarse_maxit < 1 || !(cfg.coarse_rtol >= 0.0)) {
+        set_err("amg_hierarchy_build: krylov / coarse_solver must be 0 or 1, coarse_maxit >= 1, coarse_rtol >= 0");
+        return AMG_ERR_ARG;
+    }
     CK(cudaSetDevice(ctx->device));
     const int nr = ctx->nranks;
     if (nr == 1 && (row_begin != 0 || row_end != n_global)) {

@@ -38,10 +38,16 @@ struct PcgState {
     double bnorm;   // ||b||_2
     double relres;  // ||r_k|| / ||b||
     double rtol;
+    double pr;      // FCG: p_k^T r_k
+    double pqprev;  // FCG: p_{k-1}^T q_{k-1}
     int32_t iter, maxit, status, pad;
 };
 
-enum FinishKind : int32_t { FIN_NONE = 0, FIN_BNORM = 1, FIN_RZ = 2, FIN_PQ = 3, FIN_RR = 4 };
+// FIN_ZQ / FIN_PR / FIN_PQF are the FCG(1) finishers:
+//   beta = -(z_k^T q_{k-1}) / (p_{k-1}^T q_{k-1}),  alpha = (p_k^T r_k) / (p_k^T q_k).
+enum FinishKind : int32_t {
+    FIN_NONE = 0, FIN_BNORM = 1, FIN_RZ = 2, FIN_PQ = 3, FIN_RR = 4, FIN_ZQ = 5, FIN_PR = 6, FIN_PQF = 7
+};
 // Multi-rank: a dot kernel only writes its local total (rc.out, kind FIN_NONE);
 // the per-rank totals are all-gathered and k_finish sums them in rank order.
 
@@ -87,6 +93,24 @@ __device__ __forceinline__ void finish(const RedCtx& rc, double total) {
             } else {
                 st->alpha = st->rho / total;
             }
+            break;
+        }
+        case FIN_ZQ: {  // FCG: beta = -(z^T q_prev) / (p_prev^T q_prev) (0 on the first iteration)
+            st->beta = (st->iter == 0) ? 0.0 : -total / st->pqprev;
+            break;
+        }
+        case FIN_PR: {  // FCG: p^T r of the new direction
+            st->pr = total;
+            break;
+        }
+        case FIN_PQF: {  // FCG: alpha = p^T r / p^T q ; breakdown if p^T q <= 0
+            if (!(total > 0.0)) {
+                st->status = ST_BREAKDOWN;
+                st->alpha = 0.0;
+            } else {
+                st->alpha = st->pr / total;
+            }
+            st->pqprev = total;
             break;
         }
         case FIN_RR: {  // convergence test on the recursive residual (reading R12)
@@ -204,11 +228,12 @@ struct ESweep {
     const double* __restrict__ b;
     double* __restrict__ xo;
     const double* __restrict__ m = nullptr;
+    const double* __restrict__ dw = nullptr;  // dot weight: nullptr = b (PCG r^T z), q (FCG z^T q)
     __device__ __forceinline__ double f(int64_t i, double s, double mi) const {
         const double bi = b[i];
         const double v = x[i] + mi * (bi - s);
         xo[i] = v;
-        return DOT ? bi * v : 0.0;  // r^T z at the end of the level-0 V-cycle
+        return DOT ? (dw ? dw[i] : bi) * v : 0.0;  // r^T z (or q^T z) at the end of the level-0 V-cycle
     }
     __device__ __forceinline__ double operator()(int64_t i, double s, double asum) const { return f(i, s, 1.0 / asum); }
     __device__ __forceinline__ double operator()(int64_t i, double s) const { return f(i, s, m[i]); }
@@ -227,12 +252,13 @@ struct EPost1 {
     const double* __restrict__ bmb;  // b (level 0) or m o b (MB)
     double* __restrict__ xo;
     const double* __restrict__ m = nullptr;
+    const double* __restrict__ dw = nullptr;  // dot weight: nullptr = b (PCG r^T z), q (FCG z^T q)
     __device__ __forceinline__ double f(int64_t i, double s, double mi) const {
         const double bi = bmb[i];
         const double x1 = MB ? bi : mi * bi;
         const double v = x1 + u[i] + mi * (r[i] - s);
         xo[i] = v;
-        return DOT ? bi * v : 0.0;  // DOT only at level 0 (b = r of PCG)
+        return DOT ? (dw ? dw[i] : bi) * v : 0.0;  // DOT only at level 0 (b = r of PCG)
     }
     __device__ __forceinline__ double operator()(int64_t i, double s, double asum) const { return f(i, s, 1.0 / asum); }
     __device__ __forceinline__ double operator()(int64_t i, double s) const { return f(i, s, m[i]); }
@@ -586,6 +612,198 @@ __global__ void __launch_bounds__(kBlock) k_dense_gemv(const double* __restrict_
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) z[row] = s;
     }
+}
+
+// FCG(1) direction update: p = z (first iteration) or
+// p = z + beta p with beta = -(z^T q_prev)/(p_prev^T q_prev); the deferred
+// x += alpha p_old is applied here as in k_pupdate, and p^T r -> FIN_PR.
+__global__ void __launch_bounds__(kBlock) k_pupdate_fcg(const double* __restrict__ z, double* __restrict__ p,
+                                                        double* __restrict__ x, const double* __restrict__ r,
+                                                        int64_t n, const PcgState* __restrict__ st, RedCtx rc) {
+    pdl_begin();
+    const bool first = st->iter == 0;
+    const double beta = st->beta, alpha = st->alpha;
+    double d = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        double pn;
+        if (first) {
+            pn = z[i];
+        } else {
+            const double pi = p[i];
+            x[i] = x[i] + alpha * pi;
+            pn = z[i] + beta * pi;
+        }
+        p[i] = pn;
+        d += pn * r[i];
+    }
+    grid_reduce(d, rc);
+}
+
+// ------------------------------------------------------- coarsest iterative solve
+// The paper's coarsest solver for the GPU runs: CG
+// preconditioned by the l1-Jacobi diagonal of A_L, x0 = 0, stopped as soon as
+// ||r||/||b|| < rtol or after maxit iterations (and on p^T A p <= 0).  A_L is
+// small (n_L <= a few thousand rows) and the loop is latency-bound, so the
+// whole solve is ONE kernel on ONE thread-block cluster: CTA c owns a contiguous
+// row block (balanced by nnz) and keeps its rows of A_L in shared memory when
+// they fit; every CTA holds the full direction vector p (its own slice is
+// published to the peers through distributed shared memory after each update);
+// dot products are reduced per CTA in a fixed tree and summed over the CTAs in
+// rank order, so every CTA computes bitwise-identical alpha, beta and stop
+// decisions.  Three cluster barriers per iteration.
+struct CoarseCG {
+    const int32_t* __restrict__ rp;    // CSR of A_L (n+1), int32
+    const int32_t* __restrict__ ci;
+    const double* __restrict__ v;
+    const double* __restrict__ m;      // l1-Jacobi inverse diagonal of A_L
+    const int32_t* __restrict__ split; // ncta+1 row boundaries
+    int32_t n;
+    int32_t ncta;
+    int32_t smem_a;                    // 1: the CTA's rows of A_L are staged in shared memory
+    int32_t maxit;
+    double rtol;
+};
+
+constexpr int kCgBlock = 512;
+
+__device__ __forceinline__ void cg_sync(int ncta) {
+    if (ncta > 1) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    } else {
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+// generic address of the same shared variable in cluster CTA `rank`
+template <class T>
+__device__ __forceinline__ T* peer_smem(T* p, uint32_t rank) {
+    uint64_t out;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"((uint64_t)p), "r"(rank));
+    return (T*)out;
+}
+
+// block sum of NV values, then the fixed rank-order sum over the cluster
+template <int NV>
+__device__ __forceinline__ void cg_allreduce(double (&v)[NV], double* wsum /*[NV][32]*/, double* slots /*[NV]*/,
+                                             int ncta) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        if (lane == 0) wsum[k * 32 + wid] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += wsum[threadIdx.x * 32 + w];
+        slots[threadIdx.x] = s;
+    }
+    cg_sync(ncta);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double s = 0.0;
+        for (int c = 0; c < ncta; ++c) s += (ncta > 1 ? peer_smem(slots, (uint32_t)c) : slots)[k];
+        v[k] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kCgBlock, 1) k_coarse_cg(CoarseCG A, const double* __restrict__ b,
+                                                           double* __restrict__ x) {
+    pdl_begin();
+    extern __shared__ __align__(16) unsigned char cg_smem[];
+    __shared__ double wsum[2 * 32];
+    __shared__ double slots[2][2];
+    const int ncta = A.ncta;
+    const uint32_t me = ncta > 1 ? cluster_rank() : 0u;
+    const int32_t r0 = A.split[me], r1 = A.split[me + 1], nown = r1 - r0;
+    const int n = A.n;
+    // shared layout: pfull[n] | r[nown] | x[nown] | q[nown] | m[nown] | (vals | cols)
+    double* pfull = (double*)cg_smem;
+    double* rs = pfull + n;
+    double* xs = rs + nown;
+    double* qs = xs + nown;
+    double* ms = qs + nown;
+    const int32_t k0 = A.rp[r0], nnz_own = A.rp[r1] - k0;
+    double* av = ms + nown;
+    int32_t* ac = (int32_t*)(av + (A.smem_a ? nnz_own : 0));
+    if (A.smem_a) {
+        for (int k = threadIdx.x; k < nnz_own; k += blockDim.x) {
+            av[k] = __ldg(A.v + k0 + k);
+            ac[k] = __ldg(A.ci + k0 + k);
+        }
+    }
+    const double* vals = A.smem_a ? av : A.v + k0;
+    const int32_t* cols = A.smem_a ? ac : A.ci + k0;
+    double* ps = pfull + r0;
+    // x = 0, r = b, z = m r, p = z; ||b||^2 and rho = r^T z
+    double red[2] = {0.0, 0.0};
+    for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+        const double bi = b[r0 + i], mi = A.m[r0 + i];
+        rs[i] = bi;
+        xs[i] = 0.0;
+        ms[i] = mi;
+        const double zi = mi * bi;
+        ps[i] = zi;
+        red[0] += bi * bi;
+        red[1] += bi * zi;
+    }
+    cg_allreduce<2>(red, wsum, slots[1], ncta);
+    const double bnorm = sqrt(red[0]);
+    double rho = red[1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    if (bnorm > 0.0) {
+        for (int it = 1; it <= A.maxit; ++it) {
+            // (A) publish / gather p
+            cg_sync(ncta);
+            if (ncta > 1) {
+                for (int c = 0; c < ncta; ++c) {
+                    if (c == (int)me) continue;
+                    const int32_t c0 = A.split[c], c1 = A.split[c + 1];
+                    const double* src = peer_smem(pfull, (uint32_t)c);
+                    for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) pfull[i] = src[i];
+                }
+                __syncthreads();
+            }
+            // q = A p on the own rows (warp per row), p^T q
+            double pq[1] = {0.0};
+            for (int i = wid; i < nown; i += nwarp) {
+                const int32_t a0 = A.rp[r0 + i] - k0, a1 = A.rp[r0 + i + 1] - k0;
+                double s = 0.0;
+                for (int k = a0 + lane; k < a1; k += 32) s += vals[k] * pfull[cols[k]];
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) {
+                    qs[i] = s;
+                    pq[0] += ps[i] * s;
+                }
+            }
+            cg_allreduce<1>(pq, wsum, slots[0], ncta);  // (B)
+            if (!(pq[0] > 0.0)) break;
+            const double alpha = rho / pq[0];
+            double rr[2] = {0.0, 0.0};
+            for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+                xs[i] = xs[i] + alpha * ps[i];
+                const double ri = rs[i] - alpha * qs[i];
+                rs[i] = ri;
+                rr[0] += ri * ri;
+                rr[1] += ri * (ms[i] * ri);
+            }
+            cg_allreduce<2>(rr, wsum, slots[1], ncta);  // (C)
+            if (sqrt(rr[0]) / bnorm < A.rtol) break;
+            const double beta = rr[1] / rho;
+            for (int i = threadIdx.x; i < nown; i += blockDim.x) ps[i] = ms[i] * rs[i] + beta * ps[i];
+            rho = rr[1];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nown; i += blockDim.x) x[r0 + i] = xs[i];
+    cg_sync(ncta);  // no CTA may exit while a peer can still read its shared memory
 }
 
 }  // namespace amgk

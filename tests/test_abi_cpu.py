@@ -46,6 +46,18 @@ def test_config_default_matches_header(amg):
     assert (c.sweeps_per_level, c.smooth_prolongator, c.max_coarse_size, c.max_levels) == (3, 1, 200, 20)
     assert c.prol_omega_scale == 4.0 / 3.0 and c.min_coarsening_ratio == 1.2
     assert (c.pre_sweeps, c.post_sweeps, c.use_graphs) == (1, 1, 1)
+    # the paper's GPU method is opt-in: PCG + direct coarsest by default (readings R1, R2)
+    assert (c.krylov, c.coarse_solver, c.coarse_maxit, c.coarse_rtol) == (0, 0, 30, 1e-4)
+
+
+def test_config_struct_layout_matches_header(amg):
+    # every field the header declares, in order, is in the ctypes mirror
+    import re
+    txt = open(os.path.join(ROOT, "include", "amg_b200.h")).read()
+    body = txt[txt.index("typedef struct {"):txt.index("} amg_config_t;")]
+    fields = re.findall(r"^\s*(?:int32_t|int64_t|double)\s+(\w+);", body, re.M)
+    from paper_2006_16147_b200 import _abi
+    assert fields == [f for f, _ in _abi.amg_config_t._fields_]
 
 
 class HostH:
