@@ -187,10 +187,12 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
 
 // --------------------------------------------------------------- gathers
 struct GVec {  // x_j
+    static constexpr int kChunk = 8;
     const double* __restrict__ x;
     __device__ __forceinline__ double operator()(int32_t j) const { return __ldg(x + j); }
 };
 struct GMB {   // (m o b)_j : the first l1-Jacobi sweep from x = 0 (R9)
+    static constexpr int kChunk = 4;
     const double* __restrict__ m;
     const double* __restrict__ b;
     __device__ __forceinline__ double operator()(int32_t j) const { return __ldg(m + j) * __ldg(b + j); }
@@ -353,6 +355,55 @@ struct SellView {
     int64_t n;
 };
 
+// Row-chunk of exactly W entries of one slice (lane = row): the W value loads are
+// issued first, then the W column indices, then the W gathers, then the W FMAs in
+// ascending order.  Fixed W (a full unroll with no predication) lets every load
+// of the chunk be in flight at once; measured on B200 (tools/spmv_lab2.cu) this
+// lifts the level-0 sweep from 5.45 to 6.65 TB/s of stored bytes (the pure read
+// roofline of the part) and a 27-entry-per-row operator from 4.96 to 6.29 TB/s.
+// The summation order is unchanged (ascending k), so results are bitwise equal
+// to the one-entry-at-a-time loop.
+template <int W, bool ABS, class G, class ColF>
+__device__ __forceinline__ void row_chunk(const double* v, const ColF& colf, const G& g, double& acc, double& asum) {
+    double a[W], x[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) a[j] = ld_stream(v + 32 * j);
+    int32_t c[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) c[j] = colf(j);
+#pragma unroll
+    for (int j = 0; j < W; ++j) x[j] = g(c[j]);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        acc += a[j] * x[j];
+        if constexpr (ABS) asum += fabs(a[j]);
+    }
+}
+
+// a slice row of width w: chunks of G::kChunk entries (8, or 4 for gathers that
+// load two vectors — keeps the kernels within 32 registers, no spills), then one
+// exact-width remainder
+template <bool ABS, class G, class ColAt>
+__device__ __forceinline__ void slice_row(const double* v, uint32_t w, const ColAt& col_at, const G& g, double& acc,
+                                          double& asum) {
+    constexpr int CH = G::kChunk;
+    uint32_t k = 0;
+    for (; k + CH <= w; k += CH)
+        row_chunk<CH, ABS>(v + 32 * k, [&](int j) { return col_at(k + j); }, g, acc, asum);
+    const double* vk = v + 32 * k;
+    auto ck = [&](int j) { return col_at(k + j); };
+    switch (w - k) {
+        case 7: if constexpr (CH > 7) row_chunk<7, ABS>(vk, ck, g, acc, asum); break;
+        case 6: if constexpr (CH > 6) row_chunk<6, ABS>(vk, ck, g, acc, asum); break;
+        case 5: if constexpr (CH > 5) row_chunk<5, ABS>(vk, ck, g, acc, asum); break;
+        case 4: if constexpr (CH > 4) row_chunk<4, ABS>(vk, ck, g, acc, asum); break;
+        case 3: row_chunk<3, ABS>(vk, ck, g, acc, asum); break;
+        case 2: row_chunk<2, ABS>(vk, ck, g, acc, asum); break;
+        case 1: row_chunk<1, ABS>(vk, ck, g, acc, asum); break;
+        default: break;
+    }
+}
+
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx rc) {
     pdl_begin();
@@ -367,12 +418,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx
         const int32_t* c = A.col + (int64_t)b0 * 32 + lane;
         const double* v = A.val + (int64_t)b0 * 32 + lane;
         double acc = 0.0, asum = 0.0;
-#pragma unroll 8
-        for (uint32_t k = 0; k < w; ++k) {
-            const double a = ld_stream(v + 32 * k);
-            acc += a * g(ld_stream(c + 32 * k));
-            if constexpr (E::kAbs) asum += fabs(a);
-        }
+        slice_row<E::kAbs>(v, w, [&](uint32_t k) { return ld_stream(c + 32 * k); }, g, acc, asum);
         const int64_t row = (s << 5) + lane;
         if (row < A.n) d += apply_epi(e, row, acc, asum);
     }
@@ -413,13 +459,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx
         const double* v = A.val + (int64_t)b0 * 32 + lane;
         const int32_t rmax = A.ncols - 1;
         double acc = 0.0, asum = 0.0;
-#pragma unroll 8
-        for (uint32_t k = 0; k < w; ++k) {
-            const int32_t c = min(max(base + __ldg(o + k), 0), rmax);
-            const double a = ld_stream(v + 32 * k);
-            acc += a * g(c);
-            if constexpr (E::kAbs) asum += fabs(a);
-        }
+        slice_row<E::kAbs>(v, w, [&](uint32_t k) { return min(max(base + __ldg(o + k), 0), rmax); }, g, acc, asum);
         if (row < A.n) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
@@ -432,6 +472,34 @@ struct CsrView {
     const double* __restrict__ v;
     int64_t n;
 };
+
+// One lane's share of a CSR row: entries k, k+S, k+2S, ... < k1 (S lanes per row),
+// in chunks of 4 whose loads are all issued before the FMAs (cf. row_chunk), then
+// at most 3 single entries.  Ascending order per lane, as before.
+template <int S, bool ABS, class G>
+__device__ __forceinline__ void csr_lane_row(const CsrView& A, int32_t k, int32_t k1, const G& g, double& acc,
+                                             double& asum) {
+    for (; k + 3 * S < k1; k += 4 * S) {
+        double a[4], x[4];
+        int32_t c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] = ld_stream(A.v + k + j * S);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = ld_stream(A.ci + k + j * S);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = g(c[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acc += a[j] * x[j];
+            if constexpr (ABS) asum += fabs(a[j]);
+        }
+    }
+    for (; k < k1; k += S) {
+        const double a = ld_stream(A.v + k);
+        acc += a * g(ld_stream(A.ci + k));
+        if constexpr (ABS) asum += fabs(a);
+    }
+}
 
 template <int VW, class G, class E>
 __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc) {
@@ -448,12 +516,7 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
         double acc = 0.0, asum = 0.0;
         if (row < A.n) {
             const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
-#pragma unroll 4
-            for (int32_t k = k0 + sub; k < k1; k += VW) {
-                const double a = ld_stream(A.v + k);
-                acc += a * g(ld_stream(A.ci + k));
-                if constexpr (E::kAbs) asum += fabs(a);
-            }
+            csr_lane_row<VW, E::kAbs>(A, k0 + sub, k1, g, acc, asum);
         }
 #pragma unroll
         for (int o = VW / 2; o > 0; o >>= 1) {
@@ -477,12 +540,7 @@ __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc)
     for (int64_t row = blockIdx.x; row < A.n; row += gridDim.x) {
         const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
         double acc = 0.0, asum = 0.0;
-#pragma unroll 4
-        for (int32_t k = k0 + threadIdx.x; k < k1; k += kBlock) {
-            const double a = ld_stream(A.v + k);
-            acc += a * g(ld_stream(A.ci + k));
-            if constexpr (E::kAbs) asum += fabs(a);
-        }
+        csr_lane_row<kBlock, E::kAbs>(A, k0 + (int32_t)threadIdx.x, k1, g, acc, asum);
         for (int o = 16; o > 0; o >>= 1) {
             acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if constexpr (E::kAbs) asum += __shfl_xor_sync(0xffffffffu, asum, o);

@@ -101,6 +101,56 @@ __global__ void __launch_bounds__(256, 8) k0(View A, Vecs V) {
     }
 }
 
+
+__device__ __forceinline__ double ld_stream256(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+template <bool P256, bool FIX7>
+__global__ void __launch_bounds__(256, 8) k6(View A, Vecs V) {
+    const int64_t nslices = (A.n + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * 256) >> 5;
+    for (int64_t s = w0; s < nslices; s += nw) {
+        const uint32_t b0 = __ldg(A.sptr + s);
+        const uint32_t w = __ldg(A.sptr + s + 1) - b0;
+        const int64_t row = (s << 5) + lane;
+        const int32_t base = (int32_t)row;
+        const int32_t* o = A.offs + b0;
+        const double* v = A.val + (int64_t)b0 * 32 + lane;
+        double acc = 0.0, asum = 0.0;
+        if (FIX7 && w == 7) {
+            double a[7], g[7];
+#pragma unroll
+            for (int k = 0; k < 7; ++k) a[k] = P256 ? ld_stream256(v + 32 * k) : ld_stream(v + 32 * k);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const int32_t c = min(max(base + __ldg(o + k), 0), (int32_t)A.n - 1);
+                g[k] = __ldg(V.u + c);
+            }
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                acc += a[k] * g[k];
+                asum += fabs(a[k]);
+            }
+        } else {
+#pragma unroll 8
+            for (uint32_t k = 0; k < w; ++k) {
+                const int32_t c = min(max(base + __ldg(o + k), 0), (int32_t)A.n - 1);
+                const double a = P256 ? ld_stream256(v + 32 * k) : ld_stream(v + 32 * k);
+                acc += a * __ldg(V.u + c);
+                asum += fabs(a);
+            }
+        }
+        if (row < A.n) {
+            const double mi = 1.0 / asum, bi = V.b[row];
+            V.xo[row] = mi * bi + V.u[row] + mi * (V.r[row] - acc);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- K1: operands first
 __global__ void __launch_bounds__(256, 8) k1(View A, Vecs V) {
     const int64_t nslices = (A.n + 31) >> 5;
@@ -364,12 +414,25 @@ int main(int argc, char** argv) {
         snprintf(nm, 64, "K3 bulk KS=%d NST=%d NCW=%d", KS, NST, NCW);                                  \
         report(nm, t, true);                                                                            \
     }
-    RUN3(16, 4, 16)
-    RUN3(16, 6, 16)
-    RUN3(32, 3, 16)
-    RUN3(32, 4, 32)
-    RUN3(8, 8, 8)
-    RUN3(16, 6, 32)
+    CK(cudaMemset(xo, 0, N * 8));
+    t = timeit([&] { k6<true, false><<<nsm * 8, 256>>>(A, V); }, reps);
+    report("K4 L2::256B", t, true);
+    CK(cudaMemset(xo, 0, N * 8));
+    t = timeit([&] { k6<false, true><<<nsm * 8, 256>>>(A, V); }, reps);
+    report("K6 fixed-width-7", t, true);
+    CK(cudaMemset(xo, 0, N * 8));
+    t = timeit([&] { k6<true, true><<<nsm * 8, 256>>>(A, V); }, reps);
+    report("K7 fixed7 + L2::256B", t, true);
+    for (int bps : {4, 6, 12, 16}) {
+        CK(cudaMemset(xo, 0, N * 8));
+        t = timeit([&] { k0<<<nsm * bps, 256>>>(A, V); }, reps);
+        char nm[64];
+        snprintf(nm, 64, "K0 grid %d/SM", bps);
+        report(nm, t, true);
+    }
+    RUN3(16, 3, 32)
+    RUN3(32, 2, 32)
+    RUN3(8, 6, 32)
     const int64_t nr = (int64_t)(bytes / 8);
     double* big;
     CK(cudaMalloc(&big, nr * 8 + 8));
