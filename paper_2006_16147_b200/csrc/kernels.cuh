@@ -380,13 +380,12 @@ __device__ __forceinline__ void row_chunk(const double* v, const ColF& colf, con
     }
 }
 
-// a slice row of width w: chunks of G::kChunk entries (8, or 4 for gathers that
-// load two vectors — keeps the kernels within 32 registers, no spills), then one
-// exact-width remainder
-template <bool ABS, class G, class ColAt>
+// a slice row of width w: chunks of CH entries (SELL: G::kChunk = 8, or 4 for
+// gathers that load two vectors, which keeps the kernels within 32 registers with
+// no spills; SDIA: 8), then one exact-width remainder
+template <int CH, bool ABS, class G, class ColAt>
 __device__ __forceinline__ void slice_row(const double* v, uint32_t w, const ColAt& col_at, const G& g, double& acc,
                                           double& asum) {
-    constexpr int CH = G::kChunk;
     uint32_t k = 0;
     for (; k + CH <= w; k += CH)
         row_chunk<CH, ABS>(v + 32 * k, [&](int j) { return col_at(k + j); }, g, acc, asum);
@@ -418,7 +417,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx
         const int32_t* c = A.col + (int64_t)b0 * 32 + lane;
         const double* v = A.val + (int64_t)b0 * 32 + lane;
         double acc = 0.0, asum = 0.0;
-        slice_row<E::kAbs>(v, w, [&](uint32_t k) { return ld_stream(c + 32 * k); }, g, acc, asum);
+        slice_row<G::kChunk, E::kAbs>(v, w, [&](uint32_t k) { return ld_stream(c + 32 * k); }, g, acc, asum);
         const int64_t row = (s << 5) + lane;
         if (row < A.n) d += apply_epi(e, row, acc, asum);
     }
@@ -459,7 +458,9 @@ __global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx
         const double* v = A.val + (int64_t)b0 * 32 + lane;
         const int32_t rmax = A.ncols - 1;
         double acc = 0.0, asum = 0.0;
-        slice_row<E::kAbs>(v, w, [&](uint32_t k) { return min(max(base + __ldg(o + k), 0), rmax); }, g, acc, asum);
+        // SDIA needs no registers for column indices: full chunks of 8 for every gather
+        slice_row<8, E::kAbs>(v, w, [&](uint32_t k) { return min(max(base + __ldg(o + k), 0), rmax); }, g, acc,
+                              asum);
         if (row < A.n) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
