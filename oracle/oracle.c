@@ -57,6 +57,9 @@ struct ohier {
     int32_t coarse_cg;
     double coarse_rtol;
     int32_t coarse_maxit;
+    /* cycle: 0 = V-cycle (Eq. 3.1); 1 = K-cycle */
+    int32_t cycle;
+    int64_t coarse_visits;  /* coarsest solves performed (instrumentation) */
 };
 
 /* ------------------------------------------------------------------ helpers */
@@ -756,12 +759,64 @@ void or_set_coarse_cg(ohier* h, int32_t on, double rtol, int32_t maxit) {
     h->coarse_maxit = maxit;
 }
 
+static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x);
+
+void or_set_cycle(ohier* h, int32_t cycle) { h->cycle = cycle; }
+int64_t or_coarse_visits(const ohier* h) { return h->coarse_visits; }
+
+/* K-cycle coarse correction ("at each level except the fine and the
+ * coarsest ones we apply two iterations of a Flexible Conjugate Gradient (FCG)
+ * method with the already defined AMG method starting on the current level as
+ * preconditioner"): two FCG(1) iterations on A_l x = b from x = 0, preconditioned
+ * by the cycle rooted at level l, no residual test:
+ *   z = B_l r; p = z; q = A p; alpha = p.r / p.q; x += alpha p; r -= alpha q;
+ *   z = B_l r; beta = -(z.q)/(p.q); p = z + beta p; q = A p; alpha = p.r / p.q;
+ *   x += alpha p.
+ * If p.q <= 0 the iteration stops and returns the current x. */
+static void kcycle_fcg2(const ohier* h, int32_t l, const double* b, double* x) {
+    const olevel* L = &h->lv[l];
+    int64_t n = L->n;
+    double* r = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* z = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* p = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* q = (double*)xmalloc(sizeof(double) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        x[i] = 0.0;
+        r[i] = b[i];
+    }
+    double pq = 0.0;
+    for (int32_t it = 0; it < 2; ++it) {
+        vcycle_rec(h, l, r, z);
+        if (it == 0) {
+            memcpy(p, z, sizeof(double) * (size_t)n);
+        } else {
+            double beta = -dot(n, z, q) / pq;
+            for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        }
+        or_spmv(L->A, p, q);
+        pq = dot(n, p, q);
+        if (!(pq > 0.0)) break;
+        double alpha = dot(n, p, r) / pq;
+        for (int64_t i = 0; i < n; ++i) {
+            x[i] = x[i] + alpha * p[i];
+            r[i] = r[i] - alpha * q[i];
+        }
+    }
+    free(r);
+    free(z);
+    free(p);
+    free(q);
+}
+
 /* O10, Eq. 3.1: x = m.b; (s1-1) sweeps x += m.(b - A x);
- * e = V(l+1, P-bar^T (b - A x)); x += P-bar e; s2 sweeps; at l = L: A_L^{-1} b. */
+ * e = V(l+1, P-bar^T (b - A x)); x += P-bar e; s2 sweeps; at l = L: A_L^{-1} b.
+ * With the K-cycle (h->cycle == 1) the coarse correction e of every level l whose
+ * coarse level l+1 is not the coarsest is kcycle_fcg2(l+1, P-bar^T (b - A x)). */
 static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
     const olevel* L = &h->lv[l];
     int64_t n = L->n;
     if (l == h->nl - 1) {
+        ((ohier*)h)->coarse_visits += 1;
         if (h->coarse_cg)
             coarse_pcg(L->A, L->m, n, h->coarse_rtol, h->coarse_maxit, b, x);
         else
@@ -782,7 +837,10 @@ static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
     double* bc = (double*)xmalloc(sizeof(double) * (size_t)nc);
     double* ec = (double*)xmalloc(sizeof(double) * (size_t)nc);
     or_spmv(L->R, t, bc); /* P-bar^T r, ascending fine index per coarse row */
-    vcycle_rec(h, l + 1, bc, ec);
+    if (h->cycle == 1 && l + 1 < h->nl - 1)
+        kcycle_fcg2(h, l + 1, bc, ec);
+    else
+        vcycle_rec(h, l + 1, bc, ec);
     or_spmv(L->P, ec, t);
     for (int64_t i = 0; i < n; ++i) x[i] = x[i] + t[i];
     for (int32_t s = 0; s < h->post; ++s) {

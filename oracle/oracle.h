@@ -79,6 +79,12 @@ int32_t or_pcg(const ohier* h, const double* b, double* x, double rtol, int32_t 
 int32_t or_fcg(const ohier* h, const double* b, double* x, double rtol, int32_t maxit,
                int32_t* iters, double* relres, double* true_relres, double* hist);
 void    or_set_coarse_cg(ohier* h, int32_t on, double rtol, int32_t maxit);
+/* cycle = 1 replaces the coarse correction of every level whose
+ * coarse level is not the coarsest by two FCG(1) iterations (K-cycle);
+ * or_vcycle / or_pcg / or_fcg then apply the K-cycle.  or_coarse_visits counts the
+ * coarsest solves performed since the hierarchy was built. */
+void    or_set_cycle(ohier* h, int32_t cycle);
+int64_t or_coarse_visits(const ohier* h);
 
 #ifdef __cplusplus
 }

@@ -78,6 +78,8 @@ def lib():
                                C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                C.POINTER(C.c_double), _vp]),
         "or_set_coarse_cg": (None, [_vp, C.c_int32, C.c_double, C.c_int32]),
+        "or_set_cycle": (None, [_vp, C.c_int32]),
+        "or_coarse_visits": (C.c_int64, [_vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -296,6 +298,14 @@ class OracleHierarchy:
     def set_coarse_cg(self, on=True, rtol=1e-4, maxit=30):
         """Coarsest level by l1-Jacobi PCG instead of Cholesky."""
         lib().or_set_coarse_cg(self.h, int(on), float(rtol), int(maxit))
+
+    def set_cycle(self, kind="V"):
+        """'V' (Eq. 3.1) or 'K' (K-cycle: two FCG(1) iterations per intermediate level)."""
+        lib().or_set_cycle(self.h, {"V": 0, "K": 1}[kind])
+
+    @property
+    def coarse_visits(self):
+        return lib().or_coarse_visits(self.h)
 
     def fcg(self, b, rtol=1e-6, maxit=500, history=False):
         return self.pcg(b, rtol, maxit, history, _fn="or_fcg")

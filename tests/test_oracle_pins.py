@@ -653,3 +653,94 @@ def test_va3s5cs1_fcg_converges_like_the_paper():
     assert info["true_relres"] <= 2e-6
     r = uniform_pm1(33, A.n_global)
     assert r @ h.vcycle(r) > 0
+
+
+# --------------------------------------------------------------- NEXT-4 pins (K-cycle)
+def test_kcycle_two_level_equals_vcycle():
+    """the K-cycle changes the coarse correction only at levels other than
+    the fine and the coarsest ones, so a two-level hierarchy gives the V-cycle exactly."""
+    A = poisson7(10, 9, 8)
+    h = O.OracleHierarchy(A, max_coarse_size=200)
+    assert h.nlevels == 2
+    r = uniform_pm1(40, A.n_global)
+    zv = h.vcycle(r)
+    h.set_cycle("K")
+    assert np.array_equal(h.vcycle(r), zv)
+
+
+def test_kcycle_three_levels_is_a_two_step_krylov_projection():
+    """Three levels (c1, 16^3): the level-1 correction of the K-cycle is two FCG(1)
+    steps on A_1 x = r_1 preconditioned by the (linear, s.p.d.) V-cycle B_1 rooted at
+    level 1, i.e. the A_1-orthogonal projection of A_1^{-1} r_1 onto
+    span{B_1 r_1, B_1 A_1 B_1 r_1} (CG optimality).  B_1 is built independently as the
+    V-cycle of the hierarchy grown from (A_1, w_1) and the projection is dense linear
+    algebra; the fine-level steps are Eq. 3.1 written out with numpy."""
+    A = poisson7(16, 16, 16)
+    h = O.OracleHierarchy(A)
+    assert h.sizes() == [4096, 512, 68]
+    A1 = h.A(1)
+    sub = O.OracleHierarchy(A1_inputs(A1), w=h.w(1))
+    assert sub.sizes() == [512, 68]
+    assert np.array_equal(sub.agg(0), h.agg(1))
+    n1 = 512
+    B1 = np.column_stack([sub.vcycle(e) for e in np.eye(n1)])
+    A1d = A1.to_scipy().toarray()
+    Ad = A.to_scipy()
+    P = h.P(0).to_scipy()
+    m = h.m(0)
+    r = uniform_pm1(41, A.n_global)
+    x1 = m * r                                    # pre-sweep from zero
+    rc = P.T @ (r - Ad @ x1)                      # restriction P-bar^T (b - A x)
+    V = np.column_stack([B1 @ rc, B1 @ (A1d @ (B1 @ rc))])
+    e = V @ np.linalg.solve(V.T @ A1d @ V, V.T @ rc)
+    x = x1 + P @ e                                # prolongation
+    x = x + m * (r - Ad @ x)                      # post-sweep
+    h.set_cycle("K")
+    z = h.vcycle(r)
+    assert np.linalg.norm(z - x) <= 1e-12 * np.linalg.norm(x)
+    assert np.linalg.norm(z - O.OracleHierarchy(A).vcycle(r)) > 1e-6 * np.linalg.norm(x)  # not the V-cycle
+
+
+def A1_inputs(A1):
+    """OracleCSR -> the generator's CSR record (rowptr/colind/values) for a fresh build."""
+    from inputs.problems import CSR
+    rp, ci, v = A1.arrays()
+    n = len(rp) - 1
+    return CSR(n_global=n, row_begin=0, row_end=n, rowptr=rp, colind=ci, values=v)
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16), (40, 40, 40)])
+def test_kcycle_coarsest_visits(dims):
+    """the K-cycle needs 2^(nl-2) coarsest-level visits per application
+    (two inner iterations at each of the nl-2 intermediate levels); the V-cycle one."""
+    A = poisson7(*dims)
+    h = O.OracleHierarchy(A, smooth_prolongator=0)
+    nl = h.nlevels
+    assert nl >= 3
+    r = uniform_pm1(42, A.n_global)
+    v0 = h.coarse_visits
+    h.vcycle(r)
+    assert h.coarse_visits - v0 == 1
+    h.set_cycle("K")
+    v0 = h.coarse_visits
+    h.vcycle(r)
+    assert h.coarse_visits - v0 == 2 ** (nl - 2)
+
+
+def test_kcycle_restores_convergence_of_unsmoothed_aggregation():
+    """with the piecewise-constant (unsmoothed) prolongator the V-cycle is
+    inadequate and the K-cycle is used instead (KA1: 3 matching sweeps, unsmoothed P).
+    The K-cycle preconditioner is positive on random vectors and FCG with it needs fewer
+    iterations than with the unsmoothed V-cycle."""
+    A = poisson7(48, 48, 48)
+    h = O.OracleHierarchy(A, smooth_prolongator=0)
+    b = np.ones(A.n_global)
+    _, iv = h.fcg(b, rtol=1e-6)
+    h.set_cycle("K")
+    _, ik = h.fcg(b, rtol=1e-6)
+    assert ik["status"] == O.OR_OK and iv["status"] == O.OR_OK
+    assert ik["iterations"] < iv["iterations"], (ik, iv)
+    assert ik["true_relres"] <= 2e-6
+    for s in range(5):
+        r = uniform_pm1(43 + s, A.n_global)
+        assert r @ h.vcycle(r) > 0
