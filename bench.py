@@ -174,12 +174,19 @@ def method_settings(args, meta, world):
     """--method default: the north_star path (PCG, l1-Jacobi with the config's sweeps, direct
     coarsest, maxsize 200*np).  --method va3s5cs1: the paper's own GPU method:
     FCG(1), 4/4 l1-Jacobi sweeps, coarsest CG + l1-Jacobi to 1e-4 / 30 its,
-    maxsize 12*200*np."""
+    maxsize 12*200*np.  --method ka1: the paper's KA1 hierarchy with the K-cycle
+    (PAPER.md:136, 277-312): unsmoothed 3-sweep matching, two inner FCG(1) iterations per
+    intermediate level, FCG(1) outer solver, l1-Jacobi sweeps of the config."""
     if args.method == "va3s5cs1":
         return {"name": "va3s5cs1", "desc": "3 matching sweeps/level, smoothed P (omega=4/3/||D^-1A||), "
                                             "FCG(1), coarsest l1-Jacobi CG (1e-4, 30 its)",
                 "cfg": dict(pre_sweeps=4, post_sweeps=4, max_coarse_size=12 * 200 * world, krylov=1,
                             coarse_solver=1, coarse_rtol=1e-4, coarse_maxit=30)}
+    if args.method == "ka1":
+        return {"name": "ka1", "desc": "3 matching sweeps/level, unsmoothed P, K-cycle (2 inner FCG(1) "
+                                       "iterations per intermediate level), FCG(1), direct coarsest",
+                "cfg": dict(pre_sweeps=meta["sweeps"][0], post_sweeps=meta["sweeps"][1],
+                            max_coarse_size=meta["max_coarse_size"], smooth_prolongator=0, cycle=1, krylov=1)}
     return {"name": "default", "desc": "3 matching sweeps/level, smoothed P (omega=4/3/||D^-1A||), PCG, "
                                        "direct coarsest",
             "cfg": dict(pre_sweeps=meta["sweeps"][0], post_sweeps=meta["sweeps"][1],
@@ -348,7 +355,7 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--maxit", type=int, default=500)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--method", choices=["default", "va3s5cs1"], default="default")
+    ap.add_argument("--method", choices=["default", "va3s5cs1", "ka1"], default="default")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -84,6 +84,11 @@ typedef struct {
     int32_t coarse_maxit;         /* coarse CG iteration cap (default 30) */
     double  coarse_rtol;          /* coarse CG stops when ||r||/||b|| < this (default 1e-4,
                                      PAPER.md:264) */
+    int32_t cycle;                /* 0 = V-cycle (default, Eq. 3.1); 1 = K-cycle: the coarse
+                                     correction of every level whose coarse level is not the
+                                     coarsest is two FCG(1) iterations preconditioned by the cycle
+                                     rooted there.  Nonlinear:
+                                     use krylov = 1.  Single-rank contexts only (AMG_ERR_ARG). */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */

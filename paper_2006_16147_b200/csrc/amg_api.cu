@@ -142,11 +142,16 @@ struct DevLevel {
     double* r = nullptr;
     double* xa = nullptr;
     double* xb = nullptr;
+    // K-cycle FCG vectors of this level (cfg.cycle == 1, levels 1..nl-2) and its
+    // device scalars {p^T r, p^T q, alpha, beta, stop}
+    double *kx = nullptr, *kr = nullptr, *kmb = nullptr, *kz = nullptr, *kp = nullptr, *kq = nullptr;
+    double* kst = nullptr;
     Exch ex;
     void release() {
         A.release();
         P.release();
         R.release();
+        for (double* v : {kx, kr, kmb, kz, kp, kq, kst}) cudaFree(v);
         cudaFree(m);
         cudaFree(b);
         cudaFree(mb);
@@ -351,12 +356,12 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
     L.end();
 }
 
-RedCtx no_red() { return RedCtx{nullptr, nullptr, nullptr, nullptr, 0ull, FIN_NONE}; }
+RedCtx no_red() { return RedCtx{nullptr, nullptr, nullptr, nullptr, 0ull, FIN_NONE, nullptr}; }
 
 // Dot epilogue context: fused finisher on one rank; local total (deferred) on many.
 RedCtx dot_red(amg_hier_s* h, RankState& R, int kind, unsigned long long cond) {
-    if (!h->multi()) return RedCtx{R.partials, R.ticket, nullptr, R.st, cond, kind};
-    return RedCtx{R.partials, R.ticket, R.dot_local, nullptr, 0ull, FIN_NONE};
+    if (!h->multi()) return RedCtx{R.partials, R.ticket, nullptr, R.st, cond, kind, nullptr};
+    return RedCtx{R.partials, R.ticket, R.dot_local, nullptr, 0ull, FIN_NONE, nullptr};
 }
 
 // ------------------------------------------------------------- communication
@@ -372,7 +377,7 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind) {
         ncclAllGather(R.dot_local, R.dot_all, 1, ncclDouble, h->ctx->nccl, L.s);
     }
     for (auto& R : h->ranks) {
-        RedCtx rc{nullptr, nullptr, nullptr, R.st, 0ull, kind};
+        RedCtx rc{nullptr, nullptr, nullptr, R.st, 0ull, kind, nullptr};
         launch_k(k_finish, 1, 32, L.s, R.dot_all, h->np, rc);
     }
 }
@@ -458,187 +463,232 @@ void launch_coarse(amg_hier_s* h, Launch& L, RankState& R, const double* b, doub
     L.end();
 }
 
-// ------------------------------------------------------------- V-cycle
-// z0 = B b0 (Eq. 3.1).  b0/z0 give each rank's
-// level-0 WINDOW base pointers.  With `rz`, the last level-0 post-sweep also
-// reduces b0^T z0 (kind FIN_RZ), or, with a dot weight `dwv` (FCG), dwv^T z0
-// (kind FIN_ZQ).
-void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, bool rz,
-                    const VecOf* dwv = nullptr) {
+// ------------------------------------------------------------- V-cycle / K-cycle
+void enqueue_fcg2(amg_hier_s* h, Launch& L, int l);
+
+// out = B_l b: the part of the cycle rooted at level l (Eq. 3.1;
+// SURVEY.md §8c O10).  bvec / outv give each rank's level-l WINDOW base pointers;
+// mbvec gives m o b for levels >= 1 (the restriction writes it) and is null at
+// level 0, where the first sweep gathers m_j b_j.  With `dot` (level 0 only), the
+// last post-sweep also reduces b^T out (kind FIN_RZ) or, with a dot weight `dwv`
+// (FCG), dwv^T out (kind FIN_ZQ).  The coarse correction is the cycle rooted at
+// level l+1, or, for the K-cycle (cfg.cycle == 1) when level l+1 is not the
+// coarsest, two FCG iterations at level l+1 (enqueue_fcg2).
+void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf* mbvec, const VecOf& outv,
+                   bool dot, const VecOf* dwv) {
     const int dkind = dwv ? FIN_ZQ : FIN_RZ;
     const int nl = h->nlev();
     const int s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
     const int nsm = h->ctx->nsm;
     const int nr = (int)h->ranks.size();
     auto ri_of = [&](RankState& R) { return (int)(&R - h->ranks.data()); };
-    if (nl == 1) {  // single-level hierarchy: B = A^{-1} (replicated, np == 1)
+    if (l == nl - 1) {  // coarsest: z_L = B_L b_L (reading R2 or the coarse CG), replicated on every rank
         for (auto& R : h->ranks) {
-            launch_coarse(h, L, R, b0(R), z0(R));
-            if (rz) {
+            launch_coarse(h, L, R, bvec(R), outv(R));
+            if (dot) {  // single-level hierarchy
                 L.begin("dot_rz", 16.0 * R.nL);
-                launch_k(k_dot, vec_grid(R.nL, nsm), kBlock, L.s, dwv ? (*dwv)(R) : b0(R), z0(R), R.nL,
+                launch_k(k_dot, vec_grid(R.nL, nsm), kBlock, L.s, dwv ? (*dwv)(R) : bvec(R), outv(R), R.nL,
                          dot_red(h, R, dkind, 0));
                 L.end();
             }
         }
-        if (rz) dot_finish(h, L, dkind);
+        if (dot) dot_finish(h, L, dkind);
         return;
     }
-    std::vector<std::vector<double*>> xpre(nr, std::vector<double*>(nl, nullptr));
+    std::vector<double*> xpre(nr, nullptr);
+    const bool dist = !h->ranks[0].lv[l].replicated;
     // ---- down: pre-smoothing, residual, restriction
-    for (int l = 0; l + 1 < nl; ++l) {
-        const bool dist = !h->ranks[0].lv[l].replicated;
-        auto bvec = [&](RankState& R) -> double* { return l == 0 ? b0(R) : R.lv[l].b; };
-        if (dist) {
-            if (l == 0) exchange(h, L, 0, [&](RankState& R) { return b0(R); });
-            else exchange(h, L, l, [&](RankState& R) { return R.lv[l].mb; });
+    if (dist) exchange(h, L, l, mbvec ? *mbvec : bvec);
+    for (int ri = 0; ri < nr; ++ri) {
+        RankState& R = h->ranks[ri];
+        DevLevel& D = R.lv[l];
+        const double* b = bvec(R);
+        const double* be = b + D.ep_off;
+        const double n8 = 8.0 * (double)D.comp_n;
+        if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b)
+            if (!mbvec)
+                launch_mat(L, D.A, GMB{D.m, b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
+            else
+                launch_mat(L, D.A, GVec{(*mbvec)(R)}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
+        } else {  // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
+            if (!mbvec)
+                launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
+            else
+                launch_mat(L, D.A, GVec{(*mbvec)(R)}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
+            xpre[ri] = D.xa;
         }
+    }
+    if (s1 >= 2) {
+        for (int s = 2; s < s1; ++s) {
+            if (dist) exchange(h, L, l, [&](RankState& R) { return xpre[ri_of(R)]; });
+            for (int ri = 0; ri < nr; ++ri) {
+                RankState& R = h->ranks[ri];
+                DevLevel& D = R.lv[l];
+                double* xi = xpre[ri];
+                double* xo = (xi == D.xa) ? D.xb : D.xa;
+                launch_mat(L, D.A, GVec{xi}, ESweep<false>{xi + D.ep_off, bvec(R) + D.ep_off, xo + D.ep_off},
+                           no_red(), "presweep", 3 * 8.0 * (double)D.comp_n);
+                xpre[ri] = xo;
+            }
+        }
+        if (dist) exchange(h, L, l, [&](RankState& R) { return xpre[ri_of(R)]; });
+        for (int ri = 0; ri < nr; ++ri) {
+            RankState& R = h->ranks[ri];
+            DevLevel& D = R.lv[l];
+            launch_mat(L, D.A, GVec{xpre[ri]}, EResid{bvec(R) + D.ep_off, D.r + D.ep_off}, no_red(), "resid",
+                       3 * 8.0 * (double)D.comp_n);
+        }
+    }
+    if (dist) exchange(h, L, l, [&](RankState& R) { return R.lv[l].r; });
+    for (auto& R : h->ranks) {
+        DevLevel& D = R.lv[l];
+        DevLevel& C = R.lv[l + 1];
+        if (!C.coarsest)
+            launch_mat(L, D.R, GVec{D.r}, EStoreMB{C.b + D.rst_off, C.m + D.rst_off, C.mb + D.rst_off}, no_red(),
+                       "restrict", 8.0 * (double)D.comp_n + 24.0 * (double)D.rst_n);
+        else
+            launch_mat(L, D.R, GVec{D.r}, EStore{C.b + D.rst_off}, no_red(), "restrict",
+                       8.0 * (double)D.comp_n + 8.0 * (double)D.rst_n);
+    }
+    if (h->ranks[0].lv[l + 1].replicated && dist) {  // first replicated level: gather the rhs
+        exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].b; });
+        if (!h->ranks[0].lv[l + 1].coarsest) exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].mb; });
+    }
+    // ---- coarse correction e_{l+1}
+    const bool kfcg = h->cfg.cycle == 1 && l + 1 < nl - 1;
+    const VecOf cb = [l](RankState& R) { return R.lv[l + 1].b; };
+    const VecOf cmb = [l](RankState& R) { return R.lv[l + 1].mb; };
+    const VecOf ev = kfcg ? VecOf([l](RankState& R) { return R.lv[l + 1].kx; })
+                          : VecOf([l](RankState& R) { return R.lv[l + 1].xa; });
+    if (kfcg) enqueue_fcg2(h, L, l + 1);
+    else enqueue_level(h, L, l + 1, cb, &cmb, ev, false, nullptr);
+    // ---- up: prolongation, post-smoothing
+    if (!h->ranks[0].lv[l + 1].replicated) exchange(h, L, l + 1, ev);
+    std::vector<double*> cur(nr), fin(nr), tmp(nr);
+    for (int ri = 0; ri < nr; ++ri) {
+        RankState& R = h->ranks[ri];
+        DevLevel& D = R.lv[l];
+        const double* e = ev(R);
+        const double nc8 = 8.0 * (double)R.lv[l + 1].comp_n;
+        fin[ri] = outv(R);  // the level's result (read by level l-1)
+        tmp[ri] = D.xb;     // the prolongation update is row-local: may run in place
+        double* dst = (s2 % 2 == 1) ? tmp[ri] : fin[ri];
+        const double n8 = 8.0 * (double)D.comp_n;
+        if (s1 == 1) {  // u = P-bar e only; the first post-sweep adds m o b (EPost1)
+            launch_mat(L, D.P, GVec{e}, EStore{dst + D.ep_off}, no_red(), "prolong", n8 + nc8);
+        } else {
+            launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off}, no_red(), "prolong",
+                       2 * n8 + nc8);
+        }
+        cur[ri] = dst;
+    }
+    for (int s = 0; s < s2; ++s) {
+        const bool last = (s == s2 - 1);
+        if (dist) exchange(h, L, l, [&](RankState& R) { return cur[ri_of(R)]; });
         for (int ri = 0; ri < nr; ++ri) {
             RankState& R = h->ranks[ri];
             DevLevel& D = R.lv[l];
             const double* b = bvec(R);
-            const double* be = b + D.ep_off;
+            double* xi = cur[ri];
+            double* xo = (xi == tmp[ri]) ? fin[ri] : tmp[ri];
             const double n8 = 8.0 * (double)D.comp_n;
-            if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b)
-                if (l == 0)
-                    launch_mat(L, D.A, GMB{D.m, b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
+            const bool dt = (dot && last);
+            const double* dw = (dt && dwv) ? (*dwv)(R) + D.ep_off : nullptr;
+            // short rows: m_i recomputed from the streamed row; long rows: read m
+            const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
+            const double mb8 = abs ? 0.0 : n8;
+            double* m = D.m + D.ep_off;
+            if (s == 0 && s1 == 1) {
+                const double* bo = !mbvec ? b + D.ep_off : (*mbvec)(R) + D.ep_off;
+                const double* rr = D.r + D.ep_off;
+                double* uu = xi + D.ep_off;
+                double* xx = xo + D.ep_off;
+                if (dt && abs)
+                    launch_mat(L, D.A, GVec{xi}, EPost1<true, false, true>{uu, rr, bo, xx, nullptr, dw},
+                               dot_red(h, R, dkind, 0), "postsweep_dot", 4 * n8);
+                else if (dt)
+                    launch_mat(L, D.A, GVec{xi}, EPost1<true, false, false>{uu, rr, bo, xx, m, dw},
+                               dot_red(h, R, dkind, 0), "postsweep_dot", 5 * n8);
+                else if (!mbvec && abs)
+                    launch_mat(L, D.A, GVec{xi}, EPost1<false, false, true>{uu, rr, bo, xx}, no_red(), "postsweep",
+                               4 * n8);
+                else if (!mbvec)
+                    launch_mat(L, D.A, GVec{xi}, EPost1<false, false, false>{uu, rr, bo, xx, m}, no_red(),
+                               "postsweep", 5 * n8);
+                else if (abs)
+                    launch_mat(L, D.A, GVec{xi}, EPost1<false, true, true>{uu, rr, bo, xx}, no_red(), "postsweep",
+                               4 * n8);
                 else
-                    launch_mat(L, D.A, GVec{D.mb}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
-            } else {  // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
-                if (l == 0)
-                    launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
+                    launch_mat(L, D.A, GVec{xi}, EPost1<false, true, false>{uu, rr, bo, xx, m}, no_red(),
+                               "postsweep", 5 * n8);
+            } else if (dt) {
+                if (abs)
+                    launch_mat(L, D.A, GVec{xi},
+                               ESweep<true, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, nullptr, dw},
+                               dot_red(h, R, dkind, 0), "postsweep_dot", 3 * n8);
                 else
-                    launch_mat(L, D.A, GVec{D.mb}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
-                xpre[ri][l] = D.xa;
-            }
-        }
-        if (s1 >= 2) {
-            for (int s = 2; s < s1; ++s) {
-                if (dist) exchange(h, L, l, [&](RankState& R) { return xpre[ri_of(R)][l]; });
-                for (int ri = 0; ri < nr; ++ri) {
-                    RankState& R = h->ranks[ri];
-                    DevLevel& D = R.lv[l];
-                    double* xi = xpre[ri][l];
-                    double* xo = (xi == D.xa) ? D.xb : D.xa;
-                    launch_mat(L, D.A, GVec{xi}, ESweep<false>{xi + D.ep_off, bvec(R) + D.ep_off, xo + D.ep_off},
-                               no_red(), "presweep", 3 * 8.0 * (double)D.comp_n);
-                    xpre[ri][l] = xo;
-                }
-            }
-            if (dist) exchange(h, L, l, [&](RankState& R) { return xpre[ri_of(R)][l]; });
-            for (int ri = 0; ri < nr; ++ri) {
-                RankState& R = h->ranks[ri];
-                DevLevel& D = R.lv[l];
-                launch_mat(L, D.A, GVec{xpre[ri][l]}, EResid{bvec(R) + D.ep_off, D.r + D.ep_off}, no_red(), "resid",
-                           3 * 8.0 * (double)D.comp_n);
-            }
-        }
-        if (dist) exchange(h, L, l, [&](RankState& R) { return R.lv[l].r; });
-        for (auto& R : h->ranks) {
-            DevLevel& D = R.lv[l];
-            DevLevel& C = R.lv[l + 1];
-            if (!C.coarsest)
-                launch_mat(L, D.R, GVec{D.r}, EStoreMB{C.b + D.rst_off, C.m + D.rst_off, C.mb + D.rst_off}, no_red(),
-                           "restrict", 8.0 * (double)D.comp_n + 24.0 * (double)D.rst_n);
-            else
-                launch_mat(L, D.R, GVec{D.r}, EStore{C.b + D.rst_off}, no_red(), "restrict",
-                           8.0 * (double)D.comp_n + 8.0 * (double)D.rst_n);
-        }
-        if (h->ranks[0].lv[l + 1].replicated && dist) {  // first replicated level: gather the rhs
-            exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].b; });
-            if (!h->ranks[0].lv[l + 1].coarsest) exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].mb; });
-        }
-    }
-    // ---- coarsest: z_L = A_L^{-1} b_L (reading R2), replicated on every rank
-    for (auto& R : h->ranks) {
-        DevLevel& C = R.lv[nl - 1];
-        launch_coarse(h, L, R, C.b, C.xa);
-    }
-    // ---- up: prolongation, post-smoothing
-    for (int l = nl - 2; l >= 0; --l) {
-        const bool dist = !h->ranks[0].lv[l].replicated;
-        if (!h->ranks[0].lv[l + 1].replicated) exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].xa; });
-        std::vector<double*> cur(nr), fin(nr), tmp(nr);
-        for (int ri = 0; ri < nr; ++ri) {
-            RankState& R = h->ranks[ri];
-            DevLevel& D = R.lv[l];
-            const double* b = (l == 0) ? b0(R) : D.b;
-            const double* e = R.lv[l + 1].xa;
-            const double nc8 = 8.0 * (double)R.lv[l + 1].comp_n;
-            fin[ri] = (l == 0) ? z0(R) : D.xa;  // the level's result (read by level l-1)
-            tmp[ri] = D.xb;                     // the prolongation update is row-local: may run in place
-            double* dst = (s2 % 2 == 1) ? tmp[ri] : fin[ri];
-            const double n8 = 8.0 * (double)D.comp_n;
-            if (s1 == 1) {  // u = P-bar e only; the first post-sweep adds m o b (EPost1)
-                launch_mat(L, D.P, GVec{e}, EStore{dst + D.ep_off}, no_red(), "prolong", n8 + nc8);
+                    launch_mat(L, D.A, GVec{xi}, ESweep<true, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m, dw},
+                               dot_red(h, R, dkind, 0), "postsweep_dot", 3 * n8 + mb8);
             } else {
-                launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[ri][l] + D.ep_off, dst + D.ep_off}, no_red(), "prolong",
-                           2 * n8 + nc8);
+                if (abs)
+                    launch_mat(L, D.A, GVec{xi}, ESweep<false, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off},
+                               no_red(), "postsweep", 3 * n8);
+                else
+                    launch_mat(L, D.A, GVec{xi}, ESweep<false, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m},
+                               no_red(), "postsweep", 3 * n8 + mb8);
             }
-            cur[ri] = dst;
-        }
-        for (int s = 0; s < s2; ++s) {
-            const bool last = (s == s2 - 1);
-            if (dist) exchange(h, L, l, [&](RankState& R) { return cur[ri_of(R)]; });
-            for (int ri = 0; ri < nr; ++ri) {
-                RankState& R = h->ranks[ri];
-                DevLevel& D = R.lv[l];
-                const double* b = (l == 0) ? b0(R) : D.b;
-                double* xi = cur[ri];
-                double* xo = (xi == tmp[ri]) ? fin[ri] : tmp[ri];
-                const double n8 = 8.0 * (double)D.comp_n;
-                const bool dot = (l == 0 && last && rz);
-                const double* dw = (dot && dwv) ? (*dwv)(R) + D.ep_off : nullptr;
-                // short rows: m_i recomputed from the streamed row; long rows: read m
-                const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
-                const double mb8 = abs ? 0.0 : n8;
-                double* m = D.m + D.ep_off;
-                if (s == 0 && s1 == 1) {
-                    const double* bo = (l == 0) ? b + D.ep_off : D.mb + D.ep_off;
-                    const double* rr = D.r + D.ep_off;
-                    double* uu = xi + D.ep_off;
-                    double* xx = xo + D.ep_off;
-                    if (dot && abs)
-                        launch_mat(L, D.A, GVec{xi}, EPost1<true, false, true>{uu, rr, bo, xx, nullptr, dw},
-                                   dot_red(h, R, dkind, 0), "postsweep_dot", 4 * n8);
-                    else if (dot)
-                        launch_mat(L, D.A, GVec{xi}, EPost1<true, false, false>{uu, rr, bo, xx, m, dw},
-                                   dot_red(h, R, dkind, 0), "postsweep_dot", 5 * n8);
-                    else if (l == 0 && abs)
-                        launch_mat(L, D.A, GVec{xi}, EPost1<false, false, true>{uu, rr, bo, xx}, no_red(),
-                                   "postsweep", 4 * n8);
-                    else if (l == 0)
-                        launch_mat(L, D.A, GVec{xi}, EPost1<false, false, false>{uu, rr, bo, xx, m}, no_red(),
-                                   "postsweep", 5 * n8);
-                    else if (abs)
-                        launch_mat(L, D.A, GVec{xi}, EPost1<false, true, true>{uu, rr, bo, xx}, no_red(),
-                                   "postsweep", 4 * n8);
-                    else
-                        launch_mat(L, D.A, GVec{xi}, EPost1<false, true, false>{uu, rr, bo, xx, m}, no_red(),
-                                   "postsweep", 5 * n8);
-                } else if (dot) {
-                    if (abs)
-                        launch_mat(L, D.A, GVec{xi},
-                                   ESweep<true, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, nullptr, dw},
-                                   dot_red(h, R, dkind, 0), "postsweep_dot", 3 * n8);
-                    else
-                        launch_mat(L, D.A, GVec{xi},
-                                   ESweep<true, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m, dw},
-                                   dot_red(h, R, dkind, 0), "postsweep_dot", 3 * n8 + mb8);
-                } else {
-                    if (abs)
-                        launch_mat(L, D.A, GVec{xi}, ESweep<false, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off},
-                                   no_red(), "postsweep", 3 * n8);
-                    else
-                        launch_mat(L, D.A, GVec{xi},
-                                   ESweep<false, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m}, no_red(),
-                                   "postsweep", 3 * n8 + mb8);
-                }
-                cur[ri] = xo;
-            }
+            cur[ri] = xo;
         }
     }
-    if (rz) dot_finish(h, L, dkind);
+    if (dot) dot_finish(h, L, dkind);
+}
+
+// K-cycle coarse correction at level l (oracle kcycle_fcg2): two
+// FCG(1) iterations on A_l x = b_l from x = 0, preconditioned by the cycle rooted
+// at level l, no residual test.  Single rank.  Scalars live in the level's
+// device-side K state {p^T r, p^T q, alpha, beta, stop}; every dot is fused into
+// the kernel that produces its operand and reduced deterministically.
+void enqueue_fcg2(amg_hier_s* h, Launch& L, int l) {
+    const int nsm = h->ctx->nsm;
+    RankState& R = h->ranks[0];
+    DevLevel& D = R.lv[l];
+    const int64_t n = D.comp_n;
+    const double n8 = 8.0 * (double)n;
+    auto kred = [&](int kind) { return RedCtx{R.partials, R.ticket, nullptr, nullptr, 0ull, kind, D.kst}; };
+    const VecOf bv = [l](RankState& R) { return R.lv[l].b; };
+    const VecOf mbv = [l](RankState& R) { return R.lv[l].mb; };
+    const VecOf kp = [l](RankState& R) { return R.lv[l].kp; };
+    const VecOf kr = [l](RankState& R) { return R.lv[l].kr; };
+    const VecOf kmb = [l](RankState& R) { return R.lv[l].kmb; };
+    const VecOf kz = [l](RankState& R) { return R.lv[l].kz; };
+    // iteration 1: p = z = B_l b ; p^T r (r = b)
+    enqueue_level(h, L, l, bv, &mbv, kp, false, nullptr);
+    L.begin("kfcg_dot_pr", 2 * n8);
+    launch_k(k_dot, vec_grid(n, nsm), kBlock, L.s, D.kp, D.b, n, kred(FIN_KPR0));
+    L.end();
+    launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(FIN_KALPHA), "kfcg_spmv", 2 * n8);
+    L.begin("kfcg_upd1", 7 * n8);
+    launch_k(k_kupd1, vec_grid(n, nsm), kBlock, L.s, D.kx, D.kr, D.kmb, D.kp, D.kq, D.b, D.m, n,
+             (const double*)D.kst);
+    L.end();
+    // iteration 2: z = B_l r ; beta = -(z^T q)/(p^T q) ; p = z + beta p, p^T r ; q = A p, alpha ; x += alpha p
+    enqueue_level(h, L, l, kr, &kmb, kz, false, nullptr);
+    L.begin("kfcg_dot_zq", 2 * n8);
+    launch_k(k_dot, vec_grid(n, nsm), kBlock, L.s, D.kz, D.kq, n, kred(FIN_KBETA));
+    L.end();
+    L.begin("kfcg_pupd", 4 * n8);
+    launch_k(k_kpupd, vec_grid(n, nsm), kBlock, L.s, D.kp, D.kz, D.kr, n, (const double*)D.kst, kred(FIN_KPR));
+    L.end();
+    launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(FIN_KALPHA), "kfcg_spmv", 2 * n8);
+    L.begin("kfcg_upd2", 3 * n8);
+    launch_k(k_kupd2, vec_grid(n, nsm), kBlock, L.s, D.kx, D.kp, n, (const double*)D.kst);
+    L.end();
+}
+
+// z0 = B b0 on the level-0 windows (the whole cycle).
+void enqueue_vcycle(amg_hier_s* h, Launch& L, const VecOf& b0, const VecOf& z0, bool rz,
+                    const VecOf* dwv = nullptr) {
+    enqueue_level(h, L, 0, b0, nullptr, z0, rz, dwv);
 }
 
 // PCG loop body, rotated so that the convergence test is the last node:
@@ -965,6 +1015,11 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
         }
         if ((st = dev_alloc(&D.b, wn))) return st;
         if ((st = dev_alloc(&D.xa, wn))) return st;
+        if (h->cfg.cycle == 1 && l >= 1 && l + 1 < nl) {
+            for (double** v : {&D.kx, &D.kr, &D.kmb, &D.kz, &D.kp, &D.kq})
+                if ((st = dev_alloc(v, wn))) return st;
+            if ((st = dev_alloc(&D.kst, 8))) return st;
+        }
         // halo plan: window positions
         Exch& E = D.ex;
         E.send_off = S.send_off;
@@ -998,19 +1053,25 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
     return AMG_OK;
 }
 
-// SURVEY.md §8d byte model (global hierarchy).
+// SURVEY.md §8d byte model (global hierarchy).  For the K-cycle every level-l part
+// runs 2^l times (l <= nl-2; the coarsest 2^(nl-2) times) and each of the 2^(l-1)
+// inner FCG solves at level l >= 1 adds two SpMVs and its vector updates
+// (176 B per row: p^T b, kupd1, z^T q, p-update, kupd2 and the SpMV p/q).
 void byte_model(amg_hier_s* h, const amgsetup::Hierarchy& H) {
     const double s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
+    const bool kc = h->cfg.cycle == 1;
     double bv = 0.0;
     const size_t nl = H.lv.size();
     for (size_t l = 0; l + 1 < nl; ++l) {
         const double n = (double)H.lv[l].A.nrows, nc = (double)H.lv[l + 1].A.nrows;
         const double MA = 12.0 * (double)H.lv[l].A.nnz() + 4.0 * (n + 1);
         const double MP = 12.0 * (double)H.lv[l].P.nnz() + 4.0 * (n + 1);
-        bv += (s1 + s2) * MA + 2 * MP + 8 * n * ((s1 + s2) + 2 + 3 * (s1 - 1) + 2 + 2 + 3 * s2) + 16 * nc;
+        const double visits = kc ? std::ldexp(1.0, (int)l) : 1.0;
+        bv += visits * ((s1 + s2) * MA + 2 * MP + 8 * n * ((s1 + s2) + 2 + 3 * (s1 - 1) + 2 + 2 + 3 * s2) + 16 * nc);
+        if (kc && l >= 1) bv += std::ldexp(1.0, (int)l - 1) * (2 * MA + 176.0 * n);
     }
     const double nL = (double)H.lv.back().A.nrows;
-    bv += 8 * nL * nL + 16 * nL;
+    bv += (kc && nl >= 2 ? std::ldexp(1.0, (int)nl - 2) : 1.0) * (8 * nL * nL + 16 * nL);
     h->bytes_v = bv;
     const double n0 = (double)H.lv[0].A.nrows;
     h->bytes_it = bv + 12.0 * (double)H.lv[0].A.nnz() + 4.0 * (n0 + 1) + 88.0 * n0;
@@ -1353,6 +1414,7 @@ void amg_config_default(amg_config_t* c) {
     c->coarse_solver = 0;
     c->coarse_maxit = 30;
     c->coarse_rtol = 1e-4;
+    c->cycle = 0;
 }
 
 int amg_nccl_unique_id(void* out128) {
@@ -1428,8 +1490,13 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     // that contain conditional nodes)
     if (const char* ev = std::getenv("AMG_EAGER")) cfg.use_graphs = (ev[0] == '1') ? 0 : cfg.use_graphs;
     if ((cfg.krylov != 0 && cfg.krylov != 1) || (cfg.coarse_solver != 0 && cfg.coarse_solver != 1) ||
-        cfg.coarse_maxit < 1 || !(cfg.coarse_rtol >= 0.0)) {
-        set_err("amg_hierarchy_build: krylov / coarse_solver must be 0 or 1, coarse_maxit >= 1, coarse_rtol >= 0");
+        cfg.coarse_maxit < 1 || !(cfg.coarse_rtol >= 0.0) || (cfg.cycle != 0 && cfg.cycle != 1)) {
+        set_err("amg_hierarchy_build: krylov / coarse_solver / cycle must be 0 or 1, coarse_maxit >= 1, "
+                "coarse_rtol >= 0");
+        return AMG_ERR_ARG;
+    }
+    if (cfg.cycle == 1 && (ctx->nranks > 1 || cfg.emulate_ranks > 1)) {
+        set_err("amg_hierarchy_build: the K-cycle is implemented for single-rank contexts only");
         return AMG_ERR_ARG;
     }
     CK(cudaSetDevice(ctx->device));

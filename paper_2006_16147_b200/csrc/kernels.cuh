@@ -45,8 +45,11 @@ struct PcgState {
 
 // FIN_ZQ / FIN_PR / FIN_PQF are the FCG(1) finishers:
 //   beta = -(z_k^T q_{k-1}) / (p_{k-1}^T q_{k-1}),  alpha = (p_k^T r_k) / (p_k^T q_k).
+// FIN_K* drive the two inner FCG(1) iterations of the K-cycle on a
+// per-level state k[] = {p^T r, p^T q, alpha, beta, stop}.
 enum FinishKind : int32_t {
-    FIN_NONE = 0, FIN_BNORM = 1, FIN_RZ = 2, FIN_PQ = 3, FIN_RR = 4, FIN_ZQ = 5, FIN_PR = 6, FIN_PQF = 7
+    FIN_NONE = 0, FIN_BNORM = 1, FIN_RZ = 2, FIN_PQ = 3, FIN_RR = 4, FIN_ZQ = 5, FIN_PR = 6, FIN_PQF = 7,
+    FIN_KPR0 = 8, FIN_KPR = 9, FIN_KALPHA = 10, FIN_KBETA = 11
 };
 // Multi-rank: a dot kernel only writes its local total (rc.out, kind FIN_NONE);
 // the per-rank totals are all-gathered and k_finish sums them in rank order.
@@ -58,10 +61,30 @@ struct RedCtx {
     PcgState* st;
     unsigned long long cond;  // cudaGraphConditionalHandle of the PCG WHILE node (0 = none)
     int32_t kind;
+    double* ks;               // K-cycle level state (FIN_K*), else nullptr
 };
 
 __device__ __forceinline__ void finish(const RedCtx& rc, double total) {
     if (rc.out) *rc.out = total;
+    if (rc.ks) {
+        double* k = rc.ks;
+        switch (rc.kind) {
+            case FIN_KPR0: k[4] = 0.0; k[0] = total; break;  // a new inner solve starts
+            case FIN_KPR: k[0] = total; break;
+            case FIN_KALPHA:  // alpha = p^T r / p^T q; p^T q <= 0 stops the inner solve (x kept)
+                if (k[4] != 0.0 || !(total > 0.0)) {
+                    k[2] = 0.0;
+                    k[4] = 1.0;
+                } else {
+                    k[2] = k[0] / total;
+                }
+                k[1] = total;
+                break;
+            case FIN_KBETA: k[3] = (k[4] != 0.0) ? 0.0 : -total / k[1]; break;
+            default: break;
+        }
+        return;
+    }
     PcgState* st = rc.st;
     if (!st) return;
     switch (rc.kind) {
@@ -696,6 +719,45 @@ __global__ void __launch_bounds__(kBlock) k_pupdate_fcg(const double* __restrict
         d += pn * r[i];
     }
     grid_reduce(d, rc);
+}
+
+// K-cycle inner FCG vector updates (k = {p^T r, p^T q, alpha, beta, stop})
+// x = alpha p ; r = b - alpha q ; mb = m o r
+__global__ void __launch_bounds__(kBlock) k_kupd1(double* __restrict__ x, double* __restrict__ r,
+                                                  double* __restrict__ mb, const double* __restrict__ p,
+                                                  const double* __restrict__ q, const double* __restrict__ b,
+                                                  const double* __restrict__ m, int64_t n,
+                                                  const double* __restrict__ k) {
+    pdl_begin();
+    const double alpha = k[2];
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        x[i] = alpha * p[i];
+        const double ri = b[i] - alpha * q[i];
+        r[i] = ri;
+        mb[i] = m[i] * ri;
+    }
+}
+// p = z + beta p ; p^T r -> finisher
+__global__ void __launch_bounds__(kBlock) k_kpupd(double* __restrict__ p, const double* __restrict__ z,
+                                                  const double* __restrict__ r, int64_t n,
+                                                  const double* __restrict__ k, RedCtx rc) {
+    pdl_begin();
+    const double beta = k[3];
+    double d = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        const double pn = z[i] + beta * p[i];
+        p[i] = pn;
+        d += pn * r[i];
+    }
+    grid_reduce(d, rc);
+}
+// x += alpha p
+__global__ void __launch_bounds__(kBlock) k_kupd2(double* __restrict__ x, const double* __restrict__ p, int64_t n,
+                                                  const double* __restrict__ k) {
+    pdl_begin();
+    const double alpha = k[2];
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        x[i] = x[i] + alpha * p[i];
 }
 
 // ------------------------------------------------------- coarsest iterative solve

@@ -48,6 +48,7 @@ def test_config_default_matches_header(amg):
     assert (c.pre_sweeps, c.post_sweeps, c.use_graphs) == (1, 1, 1)
     # the paper's GPU method is opt-in: PCG + direct coarsest by default (readings R1, R2)
     assert (c.krylov, c.coarse_solver, c.coarse_maxit, c.coarse_rtol) == (0, 0, 30, 1e-4)
+    assert c.cycle == 0  # V-cycle by default (the north_star path); K-cycle opt-in (NEXT-4)
 
 
 def test_config_struct_layout_matches_header(amg):
