@@ -12,12 +12,24 @@
 
 #include <omp.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <limits>
 
 namespace amgsetup {
+
+// AMG_SETUP_TIMING=1: per-phase wall times of the setup on stderr.
+void tmark(const char* what) {
+    static const bool on = std::getenv("AMG_SETUP_TIMING") && std::getenv("AMG_SETUP_TIMING")[0] == '1';
+    static auto last = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    if (on) std::fprintf(stderr, "[setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(now - last).count());
+    last = now;
+}
 
 namespace {
 
@@ -243,67 +255,81 @@ void ld_matching(const Csr& A, const std::vector<double>& w, std::vector<int32_t
     std::vector<int32_t> cand(n);
     for (int64_t v = 0; v < n; ++v) cand[v] = (int32_t)v;
     const int nt = omp_get_max_threads();
+    std::vector<int32_t> heads, W;
     for (int32_t round = 0; !cand.empty(); ++round) {
+        // With uniform keys (e.g. every level-0 edge of a constant-coefficient stencil
+        // has c = 7/6) the index tie-break makes the dominance chains long: most rounds
+        // only touch a handful of vertices.  Those rounds run on one thread (same
+        // result, no parallel-region overhead); large rounds run in parallel.
+        const bool par = cand.size() >= 16384;
         // 1. mutual pointers among the candidates
-        std::vector<std::vector<int32_t>> part(nt);
+        heads.clear();
+        if (par) {
+            std::vector<std::vector<int32_t>> part(nt);
 #pragma omp parallel
-        {
-            auto& mine = part[omp_get_thread_num()];
+            {
+                auto& mine = part[omp_get_thread_num()];
 #pragma omp for schedule(static)
-            for (int64_t q = 0; q < (int64_t)cand.size(); ++q) {
-                const int32_t v = cand[q];
+                for (int64_t q = 0; q < (int64_t)cand.size(); ++q) {
+                    const int32_t v = cand[q];
+                    if (mate[v] >= 0) continue;
+                    const int32_t t = ptr[v];
+                    if (t > v && mate[t] < 0 && ptr[t] == v) mine.push_back(v);
+                }
+            }
+            heads = concat(part);
+        } else {
+            for (const int32_t v : cand) {
                 if (mate[v] >= 0) continue;
                 const int32_t t = ptr[v];
-                if (t > v && mate[t] < 0 && ptr[t] == v) mine.push_back(v);
+                if (t > v && mate[t] < 0 && ptr[t] == v) heads.push_back(v);
             }
         }
-        std::vector<int32_t> heads = concat(part);
         if (heads.empty()) break;
-#pragma omp parallel for schedule(static)
-        for (int64_t q = 0; q < (int64_t)heads.size(); ++q) {
-            const int32_t v = heads[q], t = ptr[v];
+        for (const int32_t v : heads) {
+            const int32_t t = ptr[v];
             mate[v] = t;
             mate[t] = v;
         }
         // 2. free vertices that pointed at a newly matched vertex
-        for (auto& p : part) p.clear();
-#pragma omp parallel
-        {
-            auto& mine = part[omp_get_thread_num()];
-#pragma omp for schedule(dynamic, 256)
-            for (int64_t q = 0; q < (int64_t)heads.size(); ++q) {
-                const int32_t ends[2] = {heads[q], mate[heads[q]]};
-                for (int32_t e : ends)
-                    for (int64_t k = A.rp[e]; k < A.rp[e + 1]; ++k) {
-                        const int32_t u = A.ci[k];
-                        if (mate[u] >= 0 || (ptr[u] != ends[0] && ptr[u] != ends[1])) continue;
-                        const int32_t old = stamp[u];
-                        if (old != round && __sync_bool_compare_and_swap(&stamp[u], old, round))
-                            mine.push_back(u);
-                    }
-            }
-        }
-        std::vector<int32_t> W = concat(part);
-#pragma omp parallel for schedule(dynamic, 1024)
-        for (int64_t q = 0; q < (int64_t)W.size(); ++q) ptr[W[q]] = best(W[q]);
-        // 3. next candidates: W and their new targets
-        for (auto& p : part) p.clear();
-#pragma omp parallel
-        {
-            auto& mine = part[omp_get_thread_num()];
-#pragma omp for schedule(static)
-            for (int64_t q = 0; q < (int64_t)W.size(); ++q) {
-                const int32_t u = W[q];
-                const int32_t pair[2] = {u, ptr[u]};
-                for (int32_t x : pair) {
-                    if (x < 0) continue;
-                    int32_t old = stamp2[x];
-                    if (old != round && __sync_bool_compare_and_swap(&stamp2[x], old, round))
-                        mine.push_back(x);
+        auto collect_w = [&](int64_t q, std::vector<int32_t>& mine, bool atomic) {
+            const int32_t ends[2] = {heads[q], mate[heads[q]]};
+            for (int32_t e : ends)
+                for (int64_t k = A.rp[e]; k < A.rp[e + 1]; ++k) {
+                    const int32_t u = A.ci[k];
+                    if (mate[u] >= 0 || (ptr[u] != ends[0] && ptr[u] != ends[1])) continue;
+                    const int32_t old = stamp[u];
+                    if (old == round) continue;
+                    if (atomic ? __sync_bool_compare_and_swap(&stamp[u], old, round) : (stamp[u] = round, true))
+                        mine.push_back(u);
                 }
+        };
+        W.clear();
+        if (heads.size() >= 4096) {
+            std::vector<std::vector<int32_t>> part(nt);
+#pragma omp parallel
+            {
+                auto& mine = part[omp_get_thread_num()];
+#pragma omp for schedule(dynamic, 256)
+                for (int64_t q = 0; q < (int64_t)heads.size(); ++q) collect_w(q, mine, true);
+            }
+            W = concat(part);
+#pragma omp parallel for schedule(dynamic, 1024)
+            for (int64_t q = 0; q < (int64_t)W.size(); ++q) ptr[W[q]] = best(W[q]);
+        } else {
+            for (int64_t q = 0; q < (int64_t)heads.size(); ++q) collect_w(q, W, false);
+            for (const int32_t u : W) ptr[u] = best(u);
+        }
+        // 3. next candidates: W and their new targets
+        cand.clear();
+        for (const int32_t u : W) {
+            const int32_t pair[2] = {u, ptr[u]};
+            for (int32_t x : pair) {
+                if (x < 0 || stamp2[x] == round) continue;
+                stamp2[x] = round;
+                cand.push_back(x);
             }
         }
-        cand = concat(part);
     }
 }
 
@@ -533,11 +559,14 @@ int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
         int done = 0;
         for (int s = 0; s < cfg.sweeps_per_level; ++s) {
             std::vector<int32_t> mate;
+            tmark("(level start)");
             ld_matching(*As, ws, mate);
+            tmark("matching");
             Sweep sw = aggregate_and_values(mate, ws);
             if (sw.nc == ns) break;  // no size reduction
             Csr Ps = one_per_row(sw.agg, sw.pval, sw.nc);
             Csr An = galerkin(Ps, *As);
+            tmark("pairwise galerkin");
             std::vector<double> wn = restrict_vec(Ps, ws);
 #pragma omp parallel for schedule(static)
             for (int64_t i = 0; i < n; ++i) {
@@ -568,7 +597,9 @@ int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
             }
             L.omega = cfg.prol_omega_scale / mx;
             // O5: P-bar[i,G] = P[i,G] - (omega/a_ii) * (A P)[i,G]
+            tmark("composite P + omega");
             Csr T = spgemm_canonical(A, P);
+            tmark("A*P");
             std::vector<int64_t> cnt(n + 1, 0);
             std::vector<double> nv(T.nnz());
 #pragma omp parallel for schedule(dynamic, 4096)
@@ -605,14 +636,18 @@ int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
         }
         // O6: A_{l+1} = P-bar^T A P-bar (mirrored), w_{l+1} = P^T w (R6)
         Level next;
+        tmark("P-bar");
         next.A = galerkin(Pb, A);
+        tmark("galerkin P-bar^T A P-bar");
         next.w = restrict_vec(P, L.w);
         L.R = transpose(Pb);
+        tmark("w, R = P-bar^T");
         L.P = std::move(Pb);
         L.agg = std::move(comp_agg);
         L.sweeps = done;
         out.lv.push_back(std::move(next));
     }
+    tmark("(levels done)");
     if (!dense_inverse(out.lv.back().A, out.coarse_inv)) {  // O8
         err = "coarsest-level Cholesky failed (matrix not s.p.d.)";
         return SETUP_ERR_NOT_SPD;
