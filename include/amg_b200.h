@@ -89,6 +89,11 @@ typedef struct {
                                      coarsest is two FCG(1) iterations preconditioned by the cycle
                                      rooted there.  Nonlinear:
                                      use krylov = 1.  Single-rank contexts only (AMG_ERR_ARG). */
+    int32_t setup_device;         /* 0 = build the hierarchy on the host (C++/OpenMP, default);
+                                     1 = on the context's GPU (suitor
+                                     matching, expand-sort-compress canonical SpGEMM) with
+                                     bit-identical results.  Also honoured by
+                                     amg_host_hierarchy_build (current CUDA device). */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */

@@ -25,6 +25,8 @@ def _nccl_dir():
 
 SOURCES_CXX = [os.path.join(CSRC, "setup", "setup.cpp"), os.path.join(CSRC, "setup", "partition.cpp")]
 SOURCES_CU = [os.path.join(CSRC, "amg_api.cu")]
+# the GPU setup must follow the canonical arithmetic contract C1 (no FMA contraction)
+SOURCES_CU_NOFMA = [os.path.join(CSRC, "setup", "setup_gpu.cu")]
 HEADERS = [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "setup", "setup.hpp"),
            os.path.join(CSRC, "setup", "partition.hpp"),
            os.path.join(ROOT, "include", "amg_b200.h")]
@@ -51,12 +53,14 @@ def build_library(force: bool = False, verbose_ptxas: bool = False) -> str:
             _run(["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
                   "-Wall", "-c", src, "-o", obj])
         objs.append(obj)
-    for src in SOURCES_CU:
+    for src in SOURCES_CU + SOURCES_CU_NOFMA:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         if force or _stale(obj, [src] + HEADERS):
             cmd = [NVCC] + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-I", os.path.join(_nccl_dir(), "include"),
                                    "-Xcompiler",
                                    "-fPIC,-fopenmp,-ffp-contract=off", "-c", src, "-o", obj]
+            if src in SOURCES_CU_NOFMA:
+                cmd[1:1] = ["--fmad=false", "-prec-div=true", "-prec-sqrt=true"]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
             _run(cmd)

@@ -1235,6 +1235,7 @@ int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const do
     sc.pre_sweeps = cfg.pre_sweeps;
     sc.post_sweeps = cfg.post_sweeps;
     sc.threads = cfg.setup_threads;
+    sc.device = cfg.setup_device;
     std::string err;
     const int sst = amgsetup::build(std::move(A), std::move(wv), sc, H, err);
     if (sst != amgsetup::SETUP_OK) {
@@ -1415,6 +1416,7 @@ void amg_config_default(amg_config_t* c) {
     c->coarse_maxit = 30;
     c->coarse_rtol = 1e-4;
     c->cycle = 0;
+    c->setup_device = 0;
 }
 
 int amg_nccl_unique_id(void* out128) {

@@ -527,6 +527,8 @@ bool dense_inverse(const Csr& A, std::vector<double>& inv) {
 
 }  // namespace
 
+bool dense_inverse_host(const Csr& A, std::vector<double>& inv) { return dense_inverse(A, inv); }
+
 int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
           std::string& err) {
     auto t0 = std::chrono::steady_clock::now();
@@ -538,6 +540,12 @@ int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
     }
     int st = validate(A0, w0, err);
     if (st != SETUP_OK) return st;
+    tmark("(validate)");
+    if (cfg.device) {  // the same construction on the GPU (setup_gpu.cu)
+        st = build_gpu(std::move(A0), std::move(w0), cfg, out, err);
+        out.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return st;
+    }
     out.lv.clear();
     out.lv.emplace_back();
     out.lv[0].A = std::move(A0);

@@ -29,6 +29,7 @@ struct Config {
     double min_coarsening_ratio = 1.2;
     int pre_sweeps = 1, post_sweeps = 1;
     int threads = 0;
+    int device = 0;  // 1: build on the GPU (setup_gpu.cu, bit-identical results)
 };
 
 struct Level {
@@ -55,6 +56,11 @@ int validate(const Csr& A, const std::vector<double>& w, std::string& err);
 // Full build.  A0 is moved in.
 int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
           std::string& err);
+
+// The same build on the current CUDA device (setup_gpu.cu); A0 already validated.
+int build_gpu(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out, std::string& err);
+bool dense_inverse_host(const Csr& A, std::vector<double>& inv);
+void tmark(const char* what);
 
 // Building blocks (exported for the setup self-tests).
 Csr spgemm_canonical(const Csr& A, const Csr& Y);
