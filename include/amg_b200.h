@@ -89,11 +89,11 @@ typedef struct {
                                      coarsest is two FCG(1) iterations preconditioned by the cycle
                                      rooted there.  Nonlinear:
                                      use krylov = 1.  Single-rank contexts only (AMG_ERR_ARG). */
-    int32_t setup_device;         /* 0 = build the hierarchy on the host (C++/OpenMP, default);
-                                     1 = on the context's GPU (suitor
-                                     matching, expand-sort-compress canonical SpGEMM) with
-                                     bit-identical results.  Also honoured by
-                                     amg_host_hierarchy_build (current CUDA device). */
+    int32_t setup_device;         /* 1 = build the hierarchy on the context's GPU (default; SURVEY.md
+                                     §8f NEXT-1: suitor matching, expand-sort-compress canonical
+                                     SpGEMM), bit-identical to 0 = the host build (C++/OpenMP).
+                                     amg_host_hierarchy_build honours it (current CUDA device) when
+                                     a cfg is passed and builds on the host when cfg is NULL. */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */
@@ -188,7 +188,7 @@ int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out
                        double* bytes_out, double* stored_bytes_out, const char** names_out,
                        int32_t* count);
 
-/* ---- Host-only view of the setup phase (no device needed) -----------------
+/* ---- Host-only view of the setup phase (no device needed with setup_device = 0) ----
  * Runs exactly the setup that amg_hierarchy_build runs (the same C++ code) on a
  * whole matrix held by one process and keeps the host hierarchy, so the
  * aggregate maps, coarse operators and prolongators can be inspected, e.g. for

@@ -1416,7 +1416,7 @@ void amg_config_default(amg_config_t* c) {
     c->coarse_maxit = 30;
     c->coarse_rtol = 1e-4;
     c->cycle = 0;
-    c->setup_device = 0;
+    c->setup_device = 1;
 }
 
 int amg_nccl_unique_id(void* out128) {
@@ -1529,6 +1529,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
             set_err("amg_hierarchy_build: " + g_err);
             return fail(st);
         }
+        amgsetup::tmark("(hierarchy built)");
         std::vector<int64_t> bounds(np + 1);
         for (int g = 0; g <= np; ++g) bounds[g] = n_global * g / np;
         std::vector<amgsetup::RankPlan> plans;
@@ -1538,9 +1539,11 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
             return fail(AMG_ERR_ARG);
         }
         hier_stats(h, H);
+        amgsetup::tmark("partition");
         h->ranks.resize(np);
         for (int g = 0; g < np; ++g)
             if ((st = upload_rank(h, plans[g], H.coarse_inv, h->ranks[g]))) return fail(st);
+        amgsetup::tmark("device formats + upload");
         for (int g = 0; g < np; ++g) h->ranks[g].user_off = h->loopback ? plans[g].lv[0].own_begin : 0;
         for (size_t l = 0; l + 1 < H.lv.size(); ++l) h->agg.push_back(H.lv[l].agg);
         h->lvl_own_begin.assign(H.lv.size(), 0);
@@ -1860,6 +1863,7 @@ int amg_host_hierarchy_build(int64_t n, const int64_t* rowptr, const int64_t* co
     amg_config_t cfg;
     amg_config_default(&cfg);
     if (cfg_in) cfg = *cfg_in;
+    if (!cfg_in) cfg.setup_device = 0;  // the host-only view needs no device unless asked
     auto* h = new amg_host_hier_s();
     const int st = host_setup(n, rowptr, colind, values, w, cfg, h->H);
     if (st != AMG_OK) {

@@ -49,6 +49,7 @@ def test_config_default_matches_header(amg):
     # the paper's GPU method is opt-in: PCG + direct coarsest by default (readings R1, R2)
     assert (c.krylov, c.coarse_solver, c.coarse_maxit, c.coarse_rtol) == (0, 0, 30, 1e-4)
     assert c.cycle == 0  # V-cycle by default (the north_star path); K-cycle opt-in (NEXT-4)
+    assert c.setup_device == 1  # GPU setup (NEXT-1), bit-identical to the host build
 
 
 def test_config_struct_layout_matches_header(amg):
@@ -68,7 +69,7 @@ class HostH:
         L = amg.lib
         self.L = L
         self.h = C.c_void_p()
-        c = amg.make_config(**cfg)
+        c = amg.make_config(**dict({"setup_device": 0}, **cfg))  # host build unless asked (CPU box)
         self._keep = [np.ascontiguousarray(A.rowptr, np.int64), np.ascontiguousarray(A.colind, np.int64),
                       np.ascontiguousarray(A.values, np.float64)]
         wp = None

@@ -32,7 +32,7 @@ class Plan:
     def __init__(self, A, np_, bounds=None, rep_bytes=64 << 20, **cfg):
         amg = _amg()
         self.L = amg.lib
-        c = amg.make_config(**cfg)
+        c = amg.make_config(**dict({"setup_device": 0}, **cfg))  # host build (CPU box)
         self.keep = [np.ascontiguousarray(A.rowptr, np.int64), np.ascontiguousarray(A.colind, np.int64),
                      np.ascontiguousarray(A.values, np.float64)]
         self.h = C.c_void_p()
