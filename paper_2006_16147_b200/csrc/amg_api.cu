@@ -136,6 +136,10 @@ struct DevLevel {
     int64_t rst_n = 0;     // rows of R computed here
     int64_t rst_off = 0;   // rst_begin - next.win_begin
     DevMat A, P, R;
+    // A_l diag(m_l) (columns scaled by the l1 diagonal) for the residual of the first
+    // pre-sweep from zero, r = b - A (m o b) = b - (A diag(m)) b: the kernel gathers b
+    // alone, and no level needs m o b (s1 == 1 only)
+    DevMat Am;
     double* m = nullptr;   // window-sized vectors
     double* b = nullptr;
     double* mb = nullptr;
@@ -151,6 +155,7 @@ struct DevLevel {
         A.release();
         P.release();
         R.release();
+        Am.release();
         for (double* v : {kx, kr, kmb, kz, kp, kq, kst}) cudaFree(v);
         cudaFree(m);
         cudaFree(b);
@@ -177,6 +182,7 @@ struct RankState {
     int64_t nL = 0;
     int64_t user_off = 0;       // offset of this rank's rows in the caller's vectors (loopback)
     double *pr = nullptr, *pz = nullptr, *pp = nullptr, *pq = nullptr;  // level-0 window vectors
+    double* pp2 = nullptr;  // second p buffer (fused direction update, single rank)
     PcgState* st = nullptr;
     double* partials = nullptr;
     unsigned int* ticket = nullptr;
@@ -200,6 +206,7 @@ struct RankState {
         cudaFree(pr);
         cudaFree(pz);
         cudaFree(pp);
+        cudaFree(pp2);
         cudaFree(pq);
         cudaFree(st);
         cudaFree(partials);
@@ -497,6 +504,9 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     }
     std::vector<double*> xpre(nr, nullptr);
     const bool dist = !h->ranks[0].lv[l].replicated;
+    // s1 == 1: the residual streams A diag(m) and gathers b; m o b is never needed
+    const bool am = (s1 == 1);
+    if (am) mbvec = nullptr;
     // ---- down: pre-smoothing, residual, restriction
     if (dist) exchange(h, L, l, mbvec ? *mbvec : bvec);
     for (int ri = 0; ri < nr; ++ri) {
@@ -505,11 +515,8 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
         const double* b = bvec(R);
         const double* be = b + D.ep_off;
         const double n8 = 8.0 * (double)D.comp_n;
-        if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b)
-            if (!mbvec)
-                launch_mat(L, D.A, GMB{D.m, b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
-            else
-                launch_mat(L, D.A, GVec{(*mbvec)(R)}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
+        if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b) = b - (A diag(m)) b
+            launch_mat(L, D.Am, GVec{b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
         } else {  // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
             if (!mbvec)
                 launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
@@ -543,7 +550,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     for (auto& R : h->ranks) {
         DevLevel& D = R.lv[l];
         DevLevel& C = R.lv[l + 1];
-        if (!C.coarsest)
+        if (!C.coarsest && !am)
             launch_mat(L, D.R, GVec{D.r}, EStoreMB{C.b + D.rst_off, C.m + D.rst_off, C.mb + D.rst_off}, no_red(),
                        "restrict", 8.0 * (double)D.comp_n + 24.0 * (double)D.rst_n);
         else
@@ -552,7 +559,8 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     }
     if (h->ranks[0].lv[l + 1].replicated && dist) {  // first replicated level: gather the rhs
         exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].b; });
-        if (!h->ranks[0].lv[l + 1].coarsest) exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].mb; });
+        if (!h->ranks[0].lv[l + 1].coarsest && !am)
+            exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].mb; });
     }
     // ---- coarse correction e_{l+1}
     const bool kfcg = h->cfg.cycle == 1 && l + 1 < nl - 1;
@@ -703,28 +711,37 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
     const VecOf qv = [](RankState& R) { return R.pq; };
     enqueue_vcycle(h, L, [](RankState& R) { return R.pr; }, [](RankState& R) { return R.pz; }, true,
                    fcg ? &qv : nullptr);
-    for (auto& R : h->ranks) {
+    if (!fcg && !h->multi() && h->nlev() > 1) {
+        // p = z + beta p fused into q = A p (p double-buffered, selected on the device)
+        RankState& R = h->ranks[0];
         const DevLevel& D = R.L0();
-        if (fcg) {
-            L.begin("pupdate_fcg", 48.0 * D.own_n);
-            launch_k(k_pupdate_fcg, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off,
-                     x_user + R.user_off, R.pr + D.own_off, D.own_n, R.st, dot_red(h, R, FIN_PR, 0));
-        } else {
-            L.begin("pupdate", 40.0 * D.own_n);
-            launch_k(k_pupdate, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off,
-                     x_user + R.user_off, D.own_n, R.st);
+        launch_mat(L, D.A, GPz{R.pz, R.pp, R.pp2, R.st},
+                   ESpmvDotPz{R.pz, R.pp, R.pp2, R.pq, x_user + R.user_off, R.st}, dot_red(h, R, FIN_PQ, 0),
+                   "spmv_dot_pupd", 48.0 * D.own_n);
+    } else {  // multi-rank or FCG: separate direction update, halo of p, q = A p
+        for (auto& R : h->ranks) {
+            const DevLevel& D = R.L0();
+            if (fcg) {
+                L.begin("pupdate_fcg", 48.0 * D.own_n);
+                launch_k(k_pupdate_fcg, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off,
+                         x_user + R.user_off, R.pr + D.own_off, D.own_n, R.st, dot_red(h, R, FIN_PR, 0));
+            } else {
+                L.begin("pupdate", 40.0 * D.own_n);
+                launch_k(k_pupdate, vec_grid(D.own_n, nsm), kBlock, L.s, R.pz + D.own_off, R.pp + D.own_off,
+                         x_user + R.user_off, D.own_n, R.st);
+            }
+            L.end();
         }
-        L.end();
+        if (fcg) dot_finish(h, L, FIN_PR);
+        exchange(h, L, 0, [](RankState& R) { return R.pp; });
+        const int pqk = fcg ? FIN_PQF : FIN_PQ;
+        for (auto& R : h->ranks) {
+            const DevLevel& D = R.L0();
+            launch_mat(L, D.A, GVec{R.pp}, ESpmvDot{R.pp + D.own_off, R.pq + D.own_off}, dot_red(h, R, pqk, 0),
+                       "spmv_dot", 16.0 * D.own_n);
+        }
+        dot_finish(h, L, pqk);
     }
-    if (fcg) dot_finish(h, L, FIN_PR);
-    exchange(h, L, 0, [](RankState& R) { return R.pp; });
-    const int pqk = fcg ? FIN_PQF : FIN_PQ;
-    for (auto& R : h->ranks) {
-        const DevLevel& D = R.L0();
-        launch_mat(L, D.A, GVec{R.pp}, ESpmvDot{R.pp + D.own_off, R.pq + D.own_off}, dot_red(h, R, pqk, 0),
-                   "spmv_dot", 16.0 * D.own_n);
-    }
-    dot_finish(h, L, pqk);
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
         L.begin("axpy_rr", 24.0 * D.own_n);
@@ -739,8 +756,10 @@ void enqueue_pcg_final(amg_hier_s* h, Launch& L, double* x_user) {
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
         L.begin("xfinal", 24.0 * D.own_n);
-        launch_k(k_xfinal, vec_grid(D.own_n, h->ctx->nsm), kBlock, L.s, x_user + R.user_off, R.pp + D.own_off,
-                 D.own_n, R.st);
+        const bool fused = h->cfg.krylov != 1 && !h->multi() && h->nlev() > 1;
+        launch_k(k_xfinal, vec_grid(D.own_n, h->ctx->nsm), kBlock, L.s, x_user + R.user_off,
+                 (const double*)(R.pp + D.own_off), fused ? (const double*)R.pp2 : (const double*)nullptr,
+                 D.own_n, (const PcgState*)R.st);
         L.end();
     }
 }
@@ -1006,6 +1025,13 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
             D.rst_n = S.rst_end - S.rst_begin;
             D.rst_off = S.rst_begin - P.lv[l + 1].win_begin;
             if ((st = upload_mat(S.A, D.A, true, D.ep_off))) return st;
+            if (h->cfg.pre_sweeps == 1) {
+                amgsetup::Csr As = S.A;
+#pragma omp parallel for schedule(static)
+                for (int64_t i = 0; i < As.nrows; ++i)
+                    for (int64_t k = As.rp[i]; k < As.rp[i + 1]; ++k) As.v[k] = As.v[k] * S.m[As.ci[k]];
+                if ((st = upload_mat(As, D.Am, true, D.ep_off))) return st;
+            }
             if ((st = upload_mat(S.P, D.P, false, 0))) return st;
             if ((st = upload_mat(S.R, D.R, false, 0))) return st;
             if ((st = dev_copy(&D.m, S.m.data(), S.m.size()))) return st;
@@ -1041,6 +1067,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
     if ((st = dev_alloc(&R.pr, w0))) return st;
     if ((st = dev_alloc(&R.pz, w0))) return st;
     if ((st = dev_alloc(&R.pp, w0))) return st;
+    if (!h->multi() && (st = dev_alloc(&R.pp2, w0))) return st;
     if ((st = dev_alloc(&R.pq, w0))) return st;
     if ((st = dev_alloc(&R.st, 1))) return st;
     if ((st = dev_alloc(&R.partials, kMaxPartials))) return st;

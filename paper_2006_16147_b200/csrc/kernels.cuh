@@ -221,6 +221,34 @@ struct GMB {   // (m o b)_j : the first l1-Jacobi sweep from x = 0 (R9)
     __device__ __forceinline__ double operator()(int32_t j) const { return __ldg(m + j) * __ldg(b + j); }
 };
 
+// Functors whose operands depend on device-side PCG state (the p double buffer)
+// resolve them once per thread at kernel start; every other functor is unchanged.
+template <class T>
+__device__ __forceinline__ void bind(T&) {}
+
+// p_j = z_j + beta p_old_j (PCG direction update fused into q = A p; first
+// iteration p = z).  p lives in two buffers that alternate every iteration:
+// p_old = P[iter & 1], p_new = P[(iter + 1) & 1].
+struct GPz {
+    static constexpr int kChunk = 4;
+    const double* __restrict__ z;
+    const double* p0;
+    const double* p1;
+    const PcgState* st;
+    const double* pold = nullptr;
+    double beta = 0.0;
+    bool first = true;
+    __device__ __forceinline__ double operator()(int32_t j) const {
+        return first ? __ldg(z + j) : __ldg(z + j) + beta * __ldg(pold + j);
+    }
+};
+__device__ __forceinline__ void bind(GPz& g) {
+    const int32_t it = g.st->iter;
+    g.first = (it == 0);
+    g.beta = g.st->beta;
+    g.pold = (it & 1) ? g.p1 : g.p0;
+}
+
 // ------------------------------------------------------------- epilogues
 // An epilogue with `kAbs = true` also receives asum = sum_k |a_ik| of the row it
 // streams, i.e. the l1-Jacobi diagonal 1/m_i (nb = 1), so m_i is
@@ -358,6 +386,44 @@ struct EProlongAdd {
         return 0.0;
     }
 };
+// q = s with p = z + beta p_old formed on the fly (GPz): writes p_new and q,
+// applies the deferred x += alpha_prev p_old, returns p_i q_i
+struct ESpmvDotPz {
+    static constexpr bool kDot = true;
+    static constexpr bool kAbs = false;
+    const double* __restrict__ z;
+    double* p0;
+    double* p1;
+    double* __restrict__ q;
+    double* __restrict__ x;
+    const PcgState* st;
+    const double* pold = nullptr;
+    double* pnew = nullptr;
+    double beta = 0.0, alpha = 0.0;
+    bool first = true;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        double pi;
+        if (first) {
+            pi = z[i];
+        } else {
+            const double po = pold[i];
+            x[i] = x[i] + alpha * po;
+            pi = z[i] + beta * po;
+        }
+        pnew[i] = pi;
+        q[i] = s;
+        return pi * s;
+    }
+};
+__device__ __forceinline__ void bind(ESpmvDotPz& e) {
+    const int32_t it = e.st->iter;
+    e.first = (it == 0);
+    e.beta = e.st->beta;
+    e.alpha = e.st->alpha;
+    e.pold = (it & 1) ? e.p1 : e.p0;
+    e.pnew = (it & 1) ? e.p0 : e.p1;
+}
+
 // q = s, returns p_i q_i                    (PCG: q = A p fused with p^T q)
 struct ESpmvDot {
     static constexpr bool kDot = true;
@@ -429,6 +495,8 @@ __device__ __forceinline__ void slice_row(const double* v, uint32_t w, const Col
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx rc) {
     pdl_begin();
+    bind(g);
+    bind(e);
     const int64_t nslices = (A.n + 31) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -466,6 +534,8 @@ struct SdiaView {
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
     pdl_begin();
+    bind(g);
+    bind(e);
     const int64_t nslices = (A.n + 31) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -528,6 +598,8 @@ __device__ __forceinline__ void csr_lane_row(const CsrView& A, int32_t k, int32_
 template <int VW, class G, class E>
 __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc) {
     pdl_begin();
+    bind(g);
+    bind(e);
     const int64_t gid = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     const int sub = threadIdx.x % VW;
     const int64_t g0 = gid / VW;
@@ -558,6 +630,8 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc) {
     pdl_begin();
+    bind(g);
+    bind(e);
     __shared__ double part[kBlock / 32], apart[kBlock / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double d = 0.0;
@@ -646,12 +720,14 @@ __global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ r, cons
     grid_reduce(d, rc);
 }
 
-// After the loop: the pending x += alpha p of the last iteration.
-__global__ void __launch_bounds__(kBlock) k_xfinal(double* __restrict__ x, const double* __restrict__ p, int64_t n,
-                                                   const PcgState* __restrict__ st) {
+// After the loop: the pending x += alpha p of the last iteration (p1 != nullptr:
+// p double-buffered, the last direction is P[iter & 1]).
+__global__ void __launch_bounds__(kBlock) k_xfinal(double* __restrict__ x, const double* p0, const double* p1,
+                                                   int64_t n, const PcgState* __restrict__ st) {
     pdl_begin();
     if (st->iter == 0) return;
     const double alpha = st->alpha;
+    const double* __restrict__ p = (p1 && (st->iter & 1)) ? p1 : p0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
         x[i] = x[i] + alpha * p[i];
 }

@@ -10,10 +10,13 @@
 //    atomicMax on a packed (key rank, ~index) word); displaced suitors re-propose.
 //    Under the strict edge order (|c| desc, lo asc, hi asc) its result is the
 //    unique greedy = locally-dominant matching (reading R5);
-//  * SpGEMM: expand-sort-compress.  Products are generated in the canonical
-//    arrival order of C3 (row i of X, j ascending, K ascending), stably radix-
-//    sorted by (i, K), and each output entry is summed sequentially over its run,
-//    starting from +0.0 — the accumulation order of C3 exactly;
+//  * SpGEMM: expand-sort-compress for wide outputs.  Products are generated in
+//    the canonical arrival order of C3 (row i of X, j ascending, K ascending),
+//    stably radix-sorted by (i, K), and each output entry is summed sequentially
+//    over its run, starting from +0.0 — the accumulation order of C3 exactly.
+//    Narrow outputs (<= 16384 columns: the deep, dense-ish levels) use one block
+//    per row with a shared-memory dense accumulator and a barrier between the
+//    row's X entries, which gives every acc[K] the same arrival order;
 //  * transpose: stable radix sort by column (row order kept inside a column).
 // The coarsest dense inverse is computed on the host from the copied-back A_L
 // (n_L <= a few thousand).
@@ -343,6 +346,61 @@ __global__ void k_runsum(const uint64_t* key, const double* val, const int64_t* 
     }
 }
 
+// ---- SpGEMM with a dense per-row accumulator (narrow outputs, ncols <= kDenseMax):
+// one block per output row; for each entry j of row i of X in ascending order the
+// block's threads add x_ij*y_jK into acc[K] for the (distinct) K of row j of Y, with
+// a barrier between entries — so every acc[K] receives its products in exactly the
+// arrival order of C3.  Touched columns are emitted in ascending order with a block
+// scan.  VALUES = false: count only.
+constexpr int kDenseMax = 16384;
+constexpr int DB = 256;
+
+template <bool VALUES>
+__global__ void __launch_bounds__(DB) k_spgemm_dense(const int64_t* xrp, const int32_t* xci, const double* xv,
+                                                     int64_t nrows, const int64_t* yrp, const int32_t* yci,
+                                                     const double* yv, int32_t ncols, int64_t* cnt,
+                                                     const int64_t* crp, int32_t* cci, double* cv) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    double* acc = (double*)sm;
+    unsigned char* flag = (unsigned char*)(acc + (VALUES ? ncols : 0));
+    typedef cub::BlockScan<int, DB> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int total;
+    for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
+        for (int c = threadIdx.x; c < ncols; c += DB) {
+            if (VALUES) acc[c] = 0.0;
+            flag[c] = 0;
+        }
+        __syncthreads();
+        for (int64_t e = xrp[i]; e < xrp[i + 1]; ++e) {
+            const int32_t j = xci[e];
+            const double x = xv[e];
+            for (int64_t t = yrp[j] + threadIdx.x; t < yrp[j + 1]; t += DB) {
+                const int32_t K = yci[t];
+                if (VALUES) acc[K] = __dadd_rn(acc[K], __dmul_rn(x, yv[t]));
+                flag[K] = 1;
+            }
+            __syncthreads();
+        }
+        int64_t out = VALUES ? crp[i] : 0;
+        for (int c0 = 0; c0 < ncols; c0 += DB) {
+            const int c = c0 + threadIdx.x;
+            const int f = (c < ncols) ? flag[c] : 0;
+            int pos, agg;
+            Scan(tmp).ExclusiveSum(f, pos, agg);
+            if (VALUES && f) {
+                cci[out + pos] = c;
+                cv[out + pos] = acc[c];
+            }
+            out += agg;
+            __syncthreads();
+        }
+        if (!VALUES && threadIdx.x == 0) cnt[i] = out;
+        __syncthreads();
+    }
+    (void)total;
+}
+
 // ---- transpose (stable)
 __global__ void k_colkey(const int32_t* ci, int64_t nnz, uint32_t* ck, int64_t* idx) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
@@ -468,8 +526,39 @@ void rp_from_counts(const unsigned long long* cnt, int64_t n, Buf<int64_t>& rp, 
     incl_scan((const int64_t*)cnt, rp.p + 1, n, s);
 }
 
-// C = X Y in the canonical order of C3
+// C = X Y in the canonical order of C3: a dense per-row accumulator in shared
+// memory for narrow outputs, expand-sort-compress otherwise
+DCsr spgemm_dense(const DCsr& X, const DCsr& Y, cudaStream_t s) {
+    DCsr C;
+    C.nrows = X.nrows;
+    C.ncols = Y.ncols;
+    const int nc = (int)Y.ncols;
+    const size_t sm_cnt = (size_t)nc, sm_val = (size_t)nc * 9;
+    static bool attr = false;
+    if (!attr) {
+        GCK(cudaFuncSetAttribute(k_spgemm_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseMax * 9));
+        GCK(cudaFuncSetAttribute(k_spgemm_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseMax * 9));
+        attr = true;
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(X.nrows, 148 * 8));
+    Buf<int64_t> cnt(X.nrows + 1, s);
+    GCK(cudaMemsetAsync(cnt.p + X.nrows, 0, 8, s));
+    k_spgemm_dense<false><<<grid, DB, sm_cnt, s>>>(X.rp.p, X.ci.p, X.v.p, X.nrows, Y.rp.p, Y.ci.p, Y.v.p, nc, cnt.p,
+                                                   nullptr, nullptr, nullptr);
+    GCK(cudaGetLastError());
+    C.rp.alloc(X.nrows + 1, s);
+    excl_scan(cnt.p, C.rp.p, X.nrows + 1, s);
+    C.nnz = dev_get(C.rp.p + X.nrows, s);
+    C.ci.alloc(C.nnz, s);
+    C.v.alloc(C.nnz, s);
+    k_spgemm_dense<true><<<grid, DB, sm_val, s>>>(X.rp.p, X.ci.p, X.v.p, X.nrows, Y.rp.p, Y.ci.p, Y.v.p, nc, nullptr,
+                                                  C.rp.p, C.ci.p, C.v.p);
+    GCK(cudaGetLastError());
+    return C;
+}
+
 DCsr spgemm(const DCsr& X, const DCsr& Y, cudaStream_t s) {
+    if (Y.ncols <= kDenseMax && Y.ncols > 0) return spgemm_dense(X, Y, s);
     DCsr C;
     C.nrows = X.nrows;
     C.ncols = Y.ncols;
