@@ -516,7 +516,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
         const double* be = b + D.ep_off;
         const double n8 = 8.0 * (double)D.comp_n;
         if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b) = b - (A diag(m)) b
-            launch_mat(L, D.Am, GVec{b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 3 * n8);
+            launch_mat(L, D.Am, GVec{b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 2 * n8);
         } else {  // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
             if (!mbvec)
                 launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
@@ -1561,18 +1561,45 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         for (int g = 0; g <= np; ++g) bounds[g] = n_global * g / np;
         std::vector<amgsetup::RankPlan> plans;
         std::string err;
-        if (!amgsetup::partition(H, bounds, cfg.replicate_below_bytes, plans, err)) {
+        hier_stats(h, H);
+        const size_t nlv = H.lv.size();
+        for (size_t l = 0; l + 1 < nlv; ++l) h->agg.push_back(H.lv[l].agg);
+        if (np == 1) {
+            // one rank: the plan is the whole hierarchy (level 0 .. L-1 owned, the coarsest
+            // replicated, no halo) — move the operators instead of slicing copies
+            plans.resize(1);
+            amgsetup::RankPlan& P = plans[0];
+            P.rank = 0;
+            P.nranks = 1;
+            P.lv.resize(nlv);
+            for (size_t l = 0; l < nlv; ++l) {
+                amgsetup::RankLevel& Lv = P.lv[l];
+                amgsetup::Level& S = H.lv[l];
+                Lv.replicated = (l + 1 == nlv);
+                Lv.n_global = S.A.nrows;
+                Lv.own_begin = Lv.comp_begin = Lv.win_begin = 0;
+                Lv.own_end = Lv.comp_end = Lv.win_end = S.A.nrows;
+                if (l + 1 < nlv) {
+                    Lv.rst_begin = 0;
+                    Lv.rst_end = H.lv[l + 1].A.nrows;
+                }
+                Lv.recv_off.assign(2, 0);
+                Lv.send_off.assign(2, 0);
+                Lv.A = std::move(S.A);
+                Lv.P = std::move(S.P);
+                Lv.R = std::move(S.R);
+                Lv.m = std::move(S.m);
+            }
+        } else if (!amgsetup::partition(H, bounds, cfg.replicate_below_bytes, plans, err)) {
             set_err("amg_hierarchy_build: " + err);
             return fail(AMG_ERR_ARG);
         }
-        hier_stats(h, H);
         amgsetup::tmark("partition");
         h->ranks.resize(np);
         for (int g = 0; g < np; ++g)
             if ((st = upload_rank(h, plans[g], H.coarse_inv, h->ranks[g]))) return fail(st);
         amgsetup::tmark("device formats + upload");
         for (int g = 0; g < np; ++g) h->ranks[g].user_off = h->loopback ? plans[g].lv[0].own_begin : 0;
-        for (size_t l = 0; l + 1 < H.lv.size(); ++l) h->agg.push_back(H.lv[l].agg);
         h->lvl_own_begin.assign(H.lv.size(), 0);
         h->lvl_own_end = h->lvl_n;
         h->n0_local = n_global;
