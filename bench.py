@@ -214,7 +214,8 @@ def run_ours(args):
         uid = obj[0]
     ctx = amg.Context(device=local, rank=rank, nranks=world, nccl_uid=uid, stream=stream.cuda_stream)
     method = method_settings(args, meta, world)
-    cfg = amg.make_config(**method["cfg"])
+    extra = {} if args.tail_rows is None else {"tail_rows": args.tail_rows}
+    cfg = amg.make_config(**method["cfg"], **extra)
     t0 = time.perf_counter()
     h = amg.Hierarchy(ctx, A, cfg=cfg)
     setup_s = time.perf_counter() - t0
@@ -333,7 +334,10 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": n_global / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * bh.shape[0] * world,
                     "d2h_bytes_per_step": 8 * bh.shape[0] * world, "s_per_step": e2e_s},
-            "gpu_launches": args.steps * (1 + iters * (per_v + 3)),
+            # per solve: prologue + per iteration (cycle kernels + q = A p [+ p-update] + r-update)
+            # + the deferred final x update; single-rank PCG fuses the p-update into q = A p
+            "gpu_launches": args.steps * (2 + iters * (per_v + (2 if (method["cfg"].get("krylov", 0) == 0
+                                                                    and world == 1) else 3))),
             "clocks": ck,
         }
         print(json.dumps(line), flush=True)
@@ -356,6 +360,7 @@ def main():
     ap.add_argument("--maxit", type=int, default=500)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--method", choices=["default", "va3s5cs1", "ka1"], default="default")
+    ap.add_argument("--tail-rows", type=int, default=None, help="override cfg.tail_rows (0 = no persistent tail)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -94,6 +94,12 @@ typedef struct {
                                      SpGEMM), bit-identical to 0 = the host build (C++/OpenMP).
                                      amg_host_hierarchy_build honours it (current CUDA device) when
                                      a cfg is passed and builds on the host when cfg is NULL. */
+    int64_t tail_rows;            /* single-process contexts with a direct coarsest solve: the cycle
+                                     rooted at the first level l >= 1 with n_l <= tail_rows runs as
+                                     ONE cooperative persistent kernel (grid barriers between its
+                                     operations) instead of ~4 launches per level and visit.
+                                     Default 0 = off: measured slower than the launched graph on
+                                     B200 (grid barriers cost more than PDL launch overlap). */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */

@@ -25,7 +25,8 @@ class amg_config_t(C.Structure):
                 ("replicate_below_bytes", C.c_int64), ("setup_threads", C.c_int32),
                 ("use_graphs", C.c_int32), ("emulate_ranks", C.c_int32),
                 ("krylov", C.c_int32), ("coarse_solver", C.c_int32), ("coarse_maxit", C.c_int32),
-                ("coarse_rtol", C.c_double), ("cycle", C.c_int32), ("setup_device", C.c_int32)]
+                ("coarse_rtol", C.c_double), ("cycle", C.c_int32), ("setup_device", C.c_int32),
+                ("tail_rows", C.c_int64)]
 
 
 class amg_report_t(C.Structure):

@@ -249,10 +249,19 @@ struct amg_hier_s {
     double* apply_z = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<KernelRec>* prof = nullptr;
+    // persistent deep-level tail (single rank): first tail level, the compiled
+    // program (device), its cooperative grid and reduction scratch
+    int tail_level = -1;
+    TailOp* tail_prog = nullptr;
+    int tail_nops = 0, tail_grid = 0;
+    double* tail_partials = nullptr;
+    double tail_bytes = 0.0;
 
     bool multi() const { return np > 1; }
     int nlev() const { return (int)ranks[0].lv.size(); }
     ~amg_hier_s() {
+        cudaFree(tail_prog);
+        cudaFree(tail_partials);
         if (solve_exec) cudaGraphExecDestroy(solve_exec);
         if (apply_exec) cudaGraphExecDestroy(apply_exec);
         for (auto& R : ranks) R.release();
@@ -470,6 +479,215 @@ void launch_coarse(amg_hier_s* h, Launch& L, RankState& R, const double* b, doub
     L.end();
 }
 
+template <class T>
+int dev_copy(T** dst, const T* src, size_t count);
+template <class T>
+int dev_alloc(T** dst, size_t count);
+
+// ------------------------------------------------------------- persistent tail
+// The cycle rooted at the first tail level as a flat program for k_tail (single
+// rank): the same operations, in the same order and on the same vectors, as
+// enqueue_level / enqueue_fcg2 would launch for those levels.
+struct TailEmitter {
+    amg_hier_s* h;
+    std::vector<TailOp> ops;
+    double bytes = 0.0;
+    static TailOp op(int kind, int epi) {
+        TailOp o;
+        std::memset(&o, 0, sizeof(o));
+        o.kind = kind;
+        o.epi = epi;
+        o.fin = FIN_NONE;
+        return o;
+    }
+    void spmv(const DevMat& M, int epi, const double* g, double* y, int64_t nvec) {
+        TailOp o = op(TK_SPMV, epi);
+        o.rp = M.rp;
+        o.ci = M.col;
+        o.v = M.val;
+        o.n = M.nrows;
+        o.g = g;
+        o.y = y;
+        // lanes per row: enough groups to cover the grid, whole blocks for few long rows
+        const double mean = (double)M.nnz / (double)std::max<int64_t>(M.nrows, 1);
+        const double threads = (double)h->tail_grid * kBlock;
+        int vw = 4;
+        while (vw < 32 && (vw * (double)M.nrows < threads || vw * 8 < mean) && vw * 2 <= std::max(4.0, mean)) vw *= 2;
+        if (mean >= 256.0 && (double)M.nrows * 32 < threads) vw = kBlock;
+        o.vw = vw;
+        ops.push_back(o);
+        bytes += M.model_bytes() + 8.0 * (double)nvec * (double)M.nrows;
+    }
+    void level(int l, const double* b, const double* mb, double* out) {
+        RankState& R = h->ranks[0];
+        const int nl = h->nlev();
+        const int s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
+        DevLevel& D = R.lv[l];
+        if (l == nl - 1) {
+            TailOp o = op(TK_GEMV, 0);
+            o.v = R.cinv;
+            o.n = R.nL;
+            o.g = b;
+            o.y = out;
+            ops.push_back(o);
+            bytes += 8.0 * (double)R.nL * (double)R.nL + 16.0 * (double)R.nL;
+            return;
+        }
+        const bool am = (s1 == 1);
+        const double* xpre = nullptr;
+        if (am) {
+            spmv(D.Am, TE_RESID, b, D.r, 2);
+            ops.back().b = b;
+        } else {
+            spmv(D.A, TE_SWEEP0, mb, D.xa, 3);
+            ops.back().b = b;
+            ops.back().abs = 1;
+            xpre = D.xa;
+            for (int sw = 2; sw < s1; ++sw) {
+                double* xo = (xpre == D.xa) ? D.xb : D.xa;
+                spmv(D.A, TE_SWEEP, xpre, xo, 3);
+                ops.back().x = xpre;
+                ops.back().b = b;
+                ops.back().abs = 1;
+                xpre = xo;
+            }
+            spmv(D.A, TE_RESID, xpre, D.r, 3);
+            ops.back().b = b;
+        }
+        DevLevel& C = R.lv[l + 1];
+        if (!C.coarsest && !am) {
+            spmv(D.R, TE_STOREMB, D.r, C.b, 3);
+            ops.back().y2 = C.mb;
+            ops.back().m = C.m;
+        } else {
+            spmv(D.R, TE_STORE, D.r, C.b, 2);
+        }
+        const double* e;
+        if (h->cfg.cycle == 1 && l + 1 < nl - 1) {
+            fcg2(l + 1);
+            e = C.kx;
+        } else {
+            level(l + 1, C.b, C.mb, C.xa);
+            e = C.xa;
+        }
+        double* tmp = D.xb;
+        double* dst = (s2 % 2 == 1) ? tmp : out;
+        if (am) {
+            spmv(D.P, TE_STORE, e, dst, 2);
+        } else {
+            spmv(D.P, TE_PROLADD, e, dst, 3);
+            ops.back().x = xpre;
+        }
+        const double* cur = dst;
+        const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
+        for (int sw = 0; sw < s2; ++sw) {
+            double* xo = (cur == tmp) ? out : tmp;
+            if (sw == 0 && am) {
+                spmv(D.A, TE_POST1, cur, xo, 4);
+                ops.back().x = cur;
+                ops.back().r = D.r;
+                ops.back().b = b;
+                ops.back().mb = 0;
+            } else {
+                spmv(D.A, TE_SWEEP, cur, xo, 3);
+                ops.back().x = cur;
+                ops.back().b = b;
+            }
+            ops.back().abs = abs ? 1 : 0;
+            ops.back().m = D.m;
+            cur = xo;
+        }
+    }
+    void dot(const double* a, const double* b, int64_t n, double* ks, int fin) {
+        TailOp o = op(TK_DOT, 0);
+        o.b = a;
+        o.r = b;
+        o.n = n;
+        o.ks = ks;
+        o.fin = fin;
+        ops.push_back(o);
+        bytes += 16.0 * (double)n;
+    }
+    void fcg2(int l) {
+        RankState& R = h->ranks[0];
+        DevLevel& D = R.lv[l];
+        const int64_t n = D.comp_n;
+        if (h->cfg.pre_sweeps != 1) {  // the inner applications need m o r (SWEEP0 gathers it)
+            set_err("tail: K-cycle tail needs pre_sweeps == 1");
+        }
+        level(l, D.b, D.mb, D.kp);
+        dot(D.kp, D.b, n, D.kst, FIN_KPR0);
+        spmv(D.A, TE_SPMVDOT, D.kp, D.kq, 2);
+        ops.back().x = D.kp;
+        ops.back().ks = D.kst;
+        ops.back().fin = FIN_KALPHA;
+        TailOp u1 = op(TK_KUPD1, 0);
+        u1.n = n;
+        u1.y = D.kx;
+        u1.x = D.kp;
+        u1.y2 = D.kr;
+        u1.b = D.b;
+        u1.r = D.kq;
+        u1.ks = D.kst;
+        ops.push_back(u1);
+        bytes += 40.0 * (double)n;
+        level(l, D.kr, nullptr, D.kz);
+        dot(D.kz, D.kq, n, D.kst, FIN_KBETA);
+        TailOp pu = op(TK_KPUPD, 0);
+        pu.n = n;
+        pu.y = D.kp;
+        pu.b = D.kz;
+        pu.r = D.kr;
+        pu.ks = D.kst;
+        pu.fin = FIN_KPR;
+        ops.push_back(pu);
+        bytes += 32.0 * (double)n;
+        spmv(D.A, TE_SPMVDOT, D.kp, D.kq, 2);
+        ops.back().x = D.kp;
+        ops.back().ks = D.kst;
+        ops.back().fin = FIN_KALPHA;
+        TailOp u2 = op(TK_KUPD2, 0);
+        u2.n = n;
+        u2.y = D.kx;
+        u2.x = D.kp;
+        u2.ks = D.kst;
+        ops.push_back(u2);
+        bytes += 24.0 * (double)n;
+    }
+};
+
+int build_tail(amg_hier_s* h) {
+    const int lt = h->tail_level;
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tail, kBlock, 0));
+    h->tail_grid = std::max(1, std::min(nb, 6)) * h->ctx->nsm;
+    TailEmitter E{h, {}, 0.0};
+    RankState& R = h->ranks[0];
+    if (h->cfg.cycle == 1) E.fcg2(lt);
+    else E.level(lt, R.lv[lt].b, R.lv[lt].mb, R.lv[lt].xa);
+    int st;
+    if ((st = dev_copy(&h->tail_prog, E.ops.data(), E.ops.size()))) return st;
+    h->tail_nops = (int)E.ops.size();
+    h->tail_bytes = E.bytes;
+    if ((st = dev_alloc(&h->tail_partials, (size_t)h->tail_grid))) return st;
+    return AMG_OK;
+}
+
+void launch_tail(amg_hier_s* h, Launch& L) {
+    L.begin("tail", h->tail_bytes);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)h->tail_grid);
+    cfg.blockDim = dim3((unsigned)kBlock);
+    cfg.stream = L.s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_tail, (const TailOp*)h->tail_prog, (int32_t)h->tail_nops, h->tail_partials);
+    L.end();
+}
+
 // ------------------------------------------------------------- V-cycle / K-cycle
 void enqueue_fcg2(amg_hier_s* h, Launch& L, int l);
 
@@ -568,7 +786,8 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     const VecOf cmb = [l](RankState& R) { return R.lv[l + 1].mb; };
     const VecOf ev = kfcg ? VecOf([l](RankState& R) { return R.lv[l + 1].kx; })
                           : VecOf([l](RankState& R) { return R.lv[l + 1].xa; });
-    if (kfcg) enqueue_fcg2(h, L, l + 1);
+    if (h->tail_nops > 0 && l + 1 == h->tail_level) launch_tail(h, L);
+    else if (kfcg) enqueue_fcg2(h, L, l + 1);
     else enqueue_level(h, L, l + 1, cb, &cmb, ev, false, nullptr);
     // ---- up: prolongation, post-smoothing
     if (!h->ranks[0].lv[l + 1].replicated) exchange(h, L, l + 1, ev);
@@ -796,7 +1015,7 @@ int dev_alloc(T** dst, size_t count) {
 // offsets, SELL-32 for short rows with little padding, CSR-vector (VW lanes per
 // row, or one block per row) otherwise.  `shift` maps local rows to the column
 // window frame (comp_begin - win_begin); `square` marks A_l.
-int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift) {
+int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bool force_csr = false) {
     const int64_t n = M.nrows, nnz = M.nnz();
     D.nrows = n;
     D.ncols = M.ncols;
@@ -816,7 +1035,7 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift) {
     // SDIA-32 candidate: per slice, the sorted distinct offsets col - base(row), with
     // base = row + shift for A_l and base = the row's first column (stored per row,
     // "anchor") for the rectangular P-bar_l / R_l
-    if (nsl >= 148 * 16 && mean <= 64.0) {
+    if (!force_csr && nsl >= 148 * 16 && mean <= 64.0) {
         std::vector<int32_t> anc;
         if (!square) {
             anc.resize(n);
@@ -874,7 +1093,7 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift) {
     }
     // SELL-32 (one thread per row, coalesced column-major slices) needs little padding and
     // enough slices to fill the GPU (>= ~16 warps per SM)
-    const bool sell = (double)padded <= 1.10 * (double)nnz + 64.0 && nsl >= 148 * 16 &&
+    const bool sell = !force_csr && (double)padded <= 1.10 * (double)nnz + 64.0 && nsl >= 148 * 16 &&
                       padded / 32 < (int64_t)UINT32_MAX;
     if (sell) {
         D.fmt = FMT_SELL;
@@ -1024,16 +1243,17 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
         if (!D.coarsest) {
             D.rst_n = S.rst_end - S.rst_begin;
             D.rst_off = S.rst_begin - P.lv[l + 1].win_begin;
-            if ((st = upload_mat(S.A, D.A, true, D.ep_off))) return st;
+            const bool tcsr = h->tail_level >= 0 && l >= h->tail_level;  // tail levels: CSR for k_tail
+            if ((st = upload_mat(S.A, D.A, true, D.ep_off, tcsr))) return st;
             if (h->cfg.pre_sweeps == 1) {
                 amgsetup::Csr As = S.A;
 #pragma omp parallel for schedule(static)
                 for (int64_t i = 0; i < As.nrows; ++i)
                     for (int64_t k = As.rp[i]; k < As.rp[i + 1]; ++k) As.v[k] = As.v[k] * S.m[As.ci[k]];
-                if ((st = upload_mat(As, D.Am, true, D.ep_off))) return st;
+                if ((st = upload_mat(As, D.Am, true, D.ep_off, tcsr))) return st;
             }
-            if ((st = upload_mat(S.P, D.P, false, 0))) return st;
-            if ((st = upload_mat(S.R, D.R, false, 0))) return st;
+            if ((st = upload_mat(S.P, D.P, false, 0, tcsr))) return st;
+            if ((st = upload_mat(S.R, D.R, false, 0, tcsr))) return st;
             if ((st = dev_copy(&D.m, S.m.data(), S.m.size()))) return st;
             if ((st = dev_alloc(&D.mb, wn))) return st;
             if ((st = dev_alloc(&D.r, wn))) return st;
@@ -1444,6 +1664,7 @@ void amg_config_default(amg_config_t* c) {
     c->coarse_rtol = 1e-4;
     c->cycle = 0;
     c->setup_device = 1;
+    c->tail_rows = 0;
 }
 
 int amg_nccl_unique_id(void* out128) {
@@ -1564,6 +1785,16 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         hier_stats(h, H);
         const size_t nlv = H.lv.size();
         for (size_t l = 0; l + 1 < nlv; ++l) h->agg.push_back(H.lv[l].agg);
+        // persistent tail: the deep levels (n_l <= tail_rows, at least one non-coarsest)
+        // run as one cooperative kernel; single process, direct coarsest solve
+        if (np == 1 && cfg.tail_rows > 0 && cfg.coarse_solver == 0 && nlv >= 3 &&
+            (cfg.cycle == 0 || cfg.pre_sweeps == 1)) {
+            for (size_t l = 1; l + 1 < nlv; ++l)
+                if (H.lv[l].A.nrows <= cfg.tail_rows) {
+                    h->tail_level = (int)l;
+                    break;
+                }
+        }
         if (np == 1) {
             // one rank: the plan is the whole hierarchy (level 0 .. L-1 owned, the coarsest
             // replicated, no halo) — move the operators instead of slicing copies
@@ -1598,6 +1829,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         h->ranks.resize(np);
         for (int g = 0; g < np; ++g)
             if ((st = upload_rank(h, plans[g], H.coarse_inv, h->ranks[g]))) return fail(st);
+        if (h->tail_level > 0 && (st = build_tail(h))) return fail(st);
         amgsetup::tmark("device formats + upload");
         for (int g = 0; g < np; ++g) h->ranks[g].user_off = h->loopback ? plans[g].lv[0].own_begin : 0;
         h->lvl_own_begin.assign(H.lv.size(), 0);

@@ -22,8 +22,11 @@
 // alpha / beta / the convergence test on the device (and sets the CUDA-graph
 // WHILE condition), so no host round trip happens inside a solve.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+namespace cg = cooperative_groups;
 
 namespace amgk {
 
@@ -1001,6 +1004,205 @@ __global__ void __launch_bounds__(kCgBlock, 1) k_coarse_cg(CoarseCG A, const dou
     __syncthreads();
     for (int i = threadIdx.x; i < nown; i += blockDim.x) x[r0 + i] = xs[i];
     cg_sync(ncta);  // no CTA may exit while a peer can still read its shared memory
+}
+
+
+// ------------------------------------------------------- persistent deep-level tail
+// The deep levels of a cycle (n_l <= a few ten thousand rows) are latency-bound:
+// each of their ~4 kernels per level costs a launch and a ramp for a few us of
+// work, and the K-cycle visits them 2^l times.  The whole cycle rooted at the
+// first such level (V: one application; K: the level's two-iteration FCG solve)
+// is compiled on the host into a flat program of operations and executed by ONE
+// cooperative persistent kernel, with a grid barrier between operations.  Every
+// operation is a warp-per-row CSR row reduction with an epilogue, a dense GEMV
+// (coarsest), a dot product (fixed-order block partials -> one finisher) or a
+// vector update.  Dots are deterministic; the program runs the same operations
+// in the same order as the launched path (only the CSR row-sum lane split differs).
+enum TailKind : int32_t { TK_SPMV = 0, TK_GEMV = 1, TK_DOT = 2, TK_KUPD1 = 3, TK_KPUPD = 4, TK_KUPD2 = 5 };
+enum TailEpi : int32_t { TE_RESID = 0, TE_STORE = 1, TE_STOREMB = 2, TE_SWEEP0 = 3, TE_SWEEP = 4, TE_PROLADD = 5,
+                         TE_POST1 = 6, TE_SPMVDOT = 7 };
+// gather with a plain (coherent) load: inside k_tail the gathered vectors are
+// written by earlier operations of the same launch, so the read-only path
+// (ld.global.nc / __ldg) must not be used for them
+struct GVecC {
+    static constexpr int kChunk = 8;
+    const double* x;
+    __device__ __forceinline__ double operator()(int32_t j) const { return x[j]; }
+};
+
+struct TailOp {
+    int32_t kind, epi;
+    int32_t mb, abs;      // TE_POST1: rhs given as m o b; m from the streamed row
+    int32_t fin;          // finisher kind (FIN_K*) of a reduction, FIN_NONE otherwise
+    int32_t vw;           // TK_SPMV: lanes per row (4, 8, 16, 32, or 256 = one block per row)
+    const int32_t* rp;    // CSR (TK_SPMV) / dense row-major matrix in v (TK_GEMV)
+    const int32_t* ci;
+    const double* v;
+    int64_t n;            // rows (vector length)
+    const double* g;      // gathered vector
+    const double* b;      // rhs / first operand
+    const double* r;      // residual / second operand
+    const double* x;      // current iterate / u
+    double* y;            // output
+    double* y2;           // second output (m o y)
+    const double* m;      // l1 inverse diagonal
+    double* ks;           // K-cycle level state
+};
+
+__device__ __forceinline__ double tail_epi(const TailOp& o, int64_t i, double s, double asum) {
+    switch (o.epi) {
+        case TE_RESID: o.y[i] = o.b[i] - s; return 0.0;
+        case TE_STORE: o.y[i] = s; return 0.0;
+        case TE_STOREMB: o.y[i] = s; o.y2[i] = o.m[i] * s; return 0.0;
+        case TE_SWEEP0: {
+            const double mi = 1.0 / asum, bi = o.b[i];
+            o.y[i] = mi * bi + mi * (bi - s);
+            return 0.0;
+        }
+        case TE_SWEEP: {
+            const double mi = o.abs ? 1.0 / asum : o.m[i];
+            o.y[i] = o.x[i] + mi * (o.b[i] - s);
+            return 0.0;
+        }
+        case TE_PROLADD: o.y[i] = o.x[i] + s; return 0.0;
+        case TE_POST1: {
+            const double mi = o.abs ? 1.0 / asum : o.m[i];
+            const double bi = o.b[i];
+            const double x1 = o.mb ? bi : mi * bi;
+            o.y[i] = x1 + o.x[i] + mi * (o.r[i] - s);
+            return 0.0;
+        }
+        case TE_SPMVDOT: o.y[i] = s; return o.x[i] * s;
+        default: return 0.0;
+    }
+}
+
+__device__ __forceinline__ void tail_finish(const TailOp& o, double total) {
+    RedCtx rc{nullptr, nullptr, nullptr, nullptr, 0ull, o.fin, o.ks};
+    finish(rc, total);
+}
+
+// rows of one TK_SPMV operation, VW lanes per row (VW = 256: a whole block per row)
+template <int VW>
+__device__ __forceinline__ double tail_spmv(const TailOp& o, double* wpart) {
+    const CsrView A{o.rp, o.ci, o.v, o.n};
+    double d = 0.0;
+    if constexpr (VW == kBlock) {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int64_t row = blockIdx.x; row < o.n; row += gridDim.x) {
+            const int32_t k0 = __ldg(o.rp + row), k1 = __ldg(o.rp + row + 1);
+            double acc = 0.0, asum = 0.0;
+            if (o.abs) csr_lane_row<kBlock, true>(A, k0 + (int32_t)threadIdx.x, k1, GVecC{o.g}, acc, asum);
+            else csr_lane_row<kBlock, false>(A, k0 + (int32_t)threadIdx.x, k1, GVecC{o.g}, acc, asum);
+            for (int off = 16; off > 0; off >>= 1) {
+                acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                asum += __shfl_xor_sync(0xffffffffu, asum, off);
+            }
+            if (lane == 0) {
+                wpart[wid] = acc;
+                wpart[kBlock / 32 + wid] = asum;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double sa = 0.0, sb = 0.0;
+                for (int w = 0; w < kBlock / 32; ++w) {
+                    sa += wpart[w];
+                    sb += wpart[kBlock / 32 + w];
+                }
+                d += tail_epi(o, row, sa, sb);
+            }
+            __syncthreads();
+        }
+    } else {
+        const int sub = threadIdx.x % VW;
+        const int64_t g0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) / VW;
+        const int64_t ng = ((int64_t)gridDim.x * kBlock) / VW;
+        const int64_t iters = (o.n + ng - 1) / ng;
+        for (int64_t it = 0; it < iters; ++it) {
+            const int64_t row = g0 + it * ng;
+            double acc = 0.0, asum = 0.0;
+            if (row < o.n) {
+                const int32_t k0 = __ldg(o.rp + row), k1 = __ldg(o.rp + row + 1);
+                if (o.abs) csr_lane_row<VW, true>(A, k0 + sub, k1, GVecC{o.g}, acc, asum);
+                else csr_lane_row<VW, false>(A, k0 + sub, k1, GVecC{o.g}, acc, asum);
+            }
+#pragma unroll
+            for (int off = VW / 2; off > 0; off >>= 1) {
+                acc += __shfl_xor_sync(0xffffffffu, acc, off, VW);
+                asum += __shfl_xor_sync(0xffffffffu, asum, off, VW);
+            }
+            if (sub == 0 && row < o.n) d += tail_epi(o, row, acc, asum);
+        }
+    }
+    return d;
+}
+
+__global__ void __launch_bounds__(kBlock, 6) k_tail(const TailOp* __restrict__ prog, int32_t nops, double* partials) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double wsum[kBlock / 32];
+    __shared__ double wpart[2 * (kBlock / 32)];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
+    const int64_t gt = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * kBlock;
+    for (int32_t k = 0; k < nops; ++k) {
+        const TailOp& o = prog[k];
+        double d = 0.0;
+        if (o.kind == TK_SPMV) {
+            switch (o.vw) {
+                case 4: d = tail_spmv<4>(o, wpart); break;
+                case 8: d = tail_spmv<8>(o, wpart); break;
+                case 16: d = tail_spmv<16>(o, wpart); break;
+                case kBlock: d = tail_spmv<kBlock>(o, wpart); break;
+                default: d = tail_spmv<32>(o, wpart); break;
+            }
+        } else if (o.kind == TK_GEMV) {
+            for (int64_t row = gw; row < o.n; row += nw) {
+                const double* a = o.v + row * o.n;
+                double sacc = 0.0;
+                for (int64_t c = lane; c < o.n; c += 32) sacc += __ldg(a + c) * o.g[c];
+                for (int off = 16; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
+                if (lane == 0) o.y[row] = sacc;
+            }
+        } else if (o.kind == TK_DOT) {
+            for (int64_t i = gt; i < o.n; i += nt) d += o.b[i] * o.r[i];
+        } else if (o.kind == TK_KUPD1) {  // y = alpha p (x = p) ; y2 = b - alpha q (r = q)
+            const double alpha = o.ks[2];
+            for (int64_t i = gt; i < o.n; i += nt) {
+                o.y[i] = alpha * o.x[i];
+                o.y2[i] = o.b[i] - alpha * o.r[i];
+            }
+        } else if (o.kind == TK_KPUPD) {  // p = z + beta p ; p^T r
+            const double beta = o.ks[3];
+            for (int64_t i = gt; i < o.n; i += nt) {
+                const double pn = o.b[i] + beta * o.y[i];
+                o.y[i] = pn;
+                d += pn * o.r[i];
+            }
+        } else if (o.kind == TK_KUPD2) {  // x += alpha p
+            const double alpha = o.ks[2];
+            for (int64_t i = gt; i < o.n; i += nt) o.y[i] = o.y[i] + alpha * o.x[i];
+        }
+        if (o.fin != FIN_NONE) {  // deterministic reduction: warp tree, block partial, fixed-order total
+            for (int off = 16; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+            if (lane == 0) wsum[wid] = d;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double sb = 0.0;
+                for (int w = 0; w < kBlock / 32; ++w) sb += wsum[w];
+                partials[blockIdx.x] = sb;
+            }
+            grid.sync();
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                double tot = 0.0;
+                for (unsigned int bb = 0; bb < gridDim.x; ++bb) tot += ((volatile double*)partials)[bb];
+                tail_finish(o, tot);
+                __threadfence();
+            }
+        }
+        grid.sync();
+    }
 }
 
 }  // namespace amgk

@@ -50,6 +50,7 @@ def test_config_default_matches_header(amg):
     assert (c.krylov, c.coarse_solver, c.coarse_maxit, c.coarse_rtol) == (0, 0, 30, 1e-4)
     assert c.cycle == 0  # V-cycle by default (the north_star path); K-cycle opt-in (NEXT-4)
     assert c.setup_device == 1  # GPU setup (NEXT-1), bit-identical to the host build
+    assert c.tail_rows == 0  # persistent cooperative tail: experimental, off by default (slower)
 
 
 def test_config_struct_layout_matches_header(amg):
