@@ -45,6 +45,8 @@ typedef struct {
     double omega;
     int32_t sweeps;   /* pairwise sweeps actually performed */
     double* L;        /* coarsest: dense Cholesky factor (row-major, lower) */
+    ocsr* Wd;         /* INVK smoother: D^{-1} W, W = truncated L^{-1} (lower, unit diagonal) */
+    ocsr* Z;          /* INVK smoother: W^T */
 } olevel;
 
 struct ohier {
@@ -59,6 +61,8 @@ struct ohier {
     int32_t coarse_maxit;
     /* cycle: 0 = V-cycle (Eq. 3.1); 1 = K-cycle */
     int32_t cycle;
+    /* smoother: 0 = l1-Jacobi; 1 = INVK */
+    int32_t smoother;
     int64_t coarse_visits;  /* coarsest solves performed (instrumentation) */
 };
 
@@ -545,6 +549,8 @@ static void level_free(olevel* L) {
     free(L->w);
     free(L->m);
     free(L->L);
+    or_csr_free(L->Wd);
+    or_csr_free(L->Z);
 }
 
 /* Build the hierarchy, O1-O9. */
@@ -762,6 +768,204 @@ void or_set_coarse_cg(ohier* h, int32_t on, double rtol, int32_t maxit) {
 static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x);
 
 void or_set_cycle(ohier* h, int32_t cycle) { h->cycle = cycle; }
+
+/* ------------------------------------------------------------------ INVK
+ * "inversion and sparsification of an incomplete factorization
+ * ... in the form M = L D L^T ... M^{-1} = L^{-T} D^{-1} L^{-1} = Z D^{-1} Z^T ...
+ * positional dropping", Table 1 caption: "the incomplete LU factorization with 0
+ * levels of fill-in, and admitting a single level of fill-in in the inversion".
+ * Readings (I1-I3): ILU(0) of an s.p.d. matrix in LDL^T form is IC(0) on
+ * the pattern of A; the inverse W = L^{-1} keeps the entries of level <= fill where
+ * the diagonal and the pattern of L have level 0 and an entry first created through
+ * l_ik w_kj has level lev(w_kj) + 1; the kept entries satisfy the truncated recurrence.
+ * One block (the whole level) per process: with one process HINVK = INVK. */
+
+/* IC(0): strict lower L (pattern of tril(A)) and pivots d.  Returns 0 on a non-positive pivot. */
+static int ic0(const ocsr* A, ocsr** Lout, double* d) {
+    int64_t n = A->nrows;
+    int64_t* rp = (int64_t*)xcalloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t c = 0;
+        for (int64_t k = A->rp[i]; k < A->rp[i + 1]; ++k) c += (A->ci[k] < i);
+        rp[i + 1] = rp[i] + c;
+    }
+    ocsr* L = (ocsr*)xcalloc(1, sizeof(ocsr));
+    L->nrows = L->ncols = n;
+    L->rp = rp;
+    L->ci = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)rp[n]);
+    L->v = (double*)xmalloc(sizeof(double) * (size_t)rp[n]);
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t o = rp[i];
+        double aii = 0.0;
+        for (int64_t k = A->rp[i]; k < A->rp[i + 1]; ++k) {
+            if (A->ci[k] < i) {
+                L->ci[o] = A->ci[k];
+                L->v[o] = A->v[k];
+                ++o;
+            } else if (A->ci[k] == i) {
+                aii = A->v[k];
+            }
+        }
+        /* l_ij = (a_ij - sum_{k < j} (l_ik d_k) l_jk) / d_j, j ascending, k ascending */
+        for (int64_t t = rp[i]; t < rp[i + 1]; ++t) {
+            int64_t j = L->ci[t];
+            double sv = L->v[t];
+            int64_t q = L->rp[j];
+            for (int64_t u = rp[i]; u < t; ++u) {
+                int64_t k = L->ci[u];
+                while (q < L->rp[j + 1] && L->ci[q] < k) ++q;
+                if (q < L->rp[j + 1] && L->ci[q] == k) sv = sv - (L->v[u] * d[k]) * L->v[q];
+            }
+            L->v[t] = sv / d[j];
+        }
+        double di = aii;
+        for (int64_t t = rp[i]; t < rp[i + 1]; ++t) di = di - (L->v[t] * L->v[t]) * d[L->ci[t]];
+        if (!(di > 0.0)) {
+            or_csr_free(L);
+            return 0;
+        }
+        d[i] = di;
+    }
+    *Lout = L;
+    return 1;
+}
+
+/* W = L^{-1} truncated to fill level <= fill, row by row:
+ *   w_i = e_i - sum_{k in row i of L, ascending} l_ik w_k   (rows w_k already truncated),
+ * each w_ij accumulated in arrival order (k ascending, then the columns of row k
+ * ascending) and negated; lev(i,j) = 0 for j = i and the pattern of L, otherwise
+ * min over the contributing k of lev(k,j) + 1.  W has a unit diagonal (last in row). */
+static ocsr* invk_inverse(const ocsr* L, int32_t fill) {
+    int64_t n = L->nrows;
+    double* acc = (double*)xcalloc((size_t)n, sizeof(double));
+    int32_t* lev = (int32_t*)xmalloc(sizeof(int32_t) * (size_t)n);
+    int64_t* mark = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)n);
+    int64_t* cols = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)n);
+    for (int64_t j = 0; j < n; ++j) mark[j] = -1;
+    int64_t cap = 16 * n + 16, nnz = 0;
+    int64_t* rp = (int64_t*)xcalloc((size_t)n + 1, sizeof(int64_t));
+    int64_t* ci = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)cap);
+    double* v = (double*)xmalloc(sizeof(double) * (size_t)cap);
+    int32_t* lv = (int32_t*)xmalloc(sizeof(int32_t) * (size_t)cap);
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t nc = 0;
+        for (int64_t t = L->rp[i]; t < L->rp[i + 1]; ++t) {
+            int64_t j = L->ci[t];
+            mark[j] = i;
+            acc[j] = 0.0;
+            lev[j] = 0;
+            cols[nc++] = j;
+        }
+        for (int64_t t = L->rp[i]; t < L->rp[i + 1]; ++t) {
+            int64_t k = L->ci[t];
+            double lik = L->v[t];
+            for (int64_t q = rp[k]; q < rp[k + 1]; ++q) {
+                int64_t j = ci[q];
+                int32_t cl = lv[q] + 1;
+                if (mark[j] != i) {
+                    mark[j] = i;
+                    acc[j] = 0.0;
+                    lev[j] = cl;
+                    cols[nc++] = j;
+                } else if (cl < lev[j]) {
+                    lev[j] = cl;
+                }
+                acc[j] = acc[j] + lik * v[q];
+            }
+        }
+        /* keep level <= fill, ascending columns, then the unit diagonal */
+        for (int64_t a = 1; a < nc; ++a) { /* insertion sort (rows are short) */
+            int64_t x = cols[a], b = a - 1;
+            while (b >= 0 && cols[b] > x) {
+                cols[b + 1] = cols[b];
+                --b;
+            }
+            cols[b + 1] = x;
+        }
+        if (nnz + nc + 1 > cap) {
+            cap = 2 * (nnz + nc + 1);
+            ci = (int64_t*)realloc(ci, sizeof(int64_t) * (size_t)cap);
+            v = (double*)realloc(v, sizeof(double) * (size_t)cap);
+            lv = (int32_t*)realloc(lv, sizeof(int32_t) * (size_t)cap);
+            if (!ci || !v || !lv) abort();
+        }
+        for (int64_t a = 0; a < nc; ++a) {
+            int64_t j = cols[a];
+            if (lev[j] <= fill) {
+                ci[nnz] = j;
+                v[nnz] = -acc[j];
+                lv[nnz] = lev[j];
+                ++nnz;
+            }
+        }
+        ci[nnz] = i;
+        v[nnz] = 1.0;
+        lv[nnz] = 0;
+        ++nnz;
+        rp[i + 1] = nnz;
+    }
+    ocsr* W = (ocsr*)xcalloc(1, sizeof(ocsr));
+    W->nrows = W->ncols = n;
+    W->rp = rp;
+    W->ci = ci;
+    W->v = v;
+    free(lv);
+    free(acc);
+    free(lev);
+    free(mark);
+    free(cols);
+    return W;
+}
+
+/* INVK factors of level l: Wd = D^{-1} W (row i scaled by 1/d_i) and Z = W^T, so
+ * that M^{-1} r = W^T D^{-1} W r = Z (Wd r).  Returns 0 on an IC(0) breakdown. */
+static int invk_level(olevel* Lv, int32_t fill) {
+    int64_t n = Lv->n;
+    double* d = (double*)xmalloc(sizeof(double) * (size_t)n);
+    ocsr* L = NULL;
+    if (!ic0(Lv->A, &L, d)) {
+        free(d);
+        return 0;
+    }
+    ocsr* W = invk_inverse(L, fill);
+    or_csr_free(L);
+    Lv->Z = or_transpose(W);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = W->rp[i]; k < W->rp[i + 1]; ++k) W->v[k] = W->v[k] / d[i];
+    Lv->Wd = W;
+    free(d);
+    return 1;
+}
+
+int32_t or_set_smoother(ohier* h, int32_t kind, int32_t fill) {
+    h->smoother = kind;
+    if (kind != 1) return OR_OK;
+    for (int32_t l = 0; l + 1 < h->nl; ++l) {
+        olevel* Lv = &h->lv[l];
+        or_csr_free(Lv->Wd);
+        or_csr_free(Lv->Z);
+        Lv->Wd = Lv->Z = NULL;
+        if (!invk_level(Lv, fill)) return OR_ERR_NOT_SPD;
+    }
+    return OR_OK;
+}
+
+const ocsr* or_level_invk(const ohier* h, int32_t l, int32_t which) {
+    return which == 0 ? h->lv[l].Wd : h->lv[l].Z;
+}
+
+/* one smoothing step x = x + M^{-1}(b - A x) (or x = M^{-1} b from zero) with the
+ * level's smoother: l1-Jacobi m o (.) or INVK Z (Wd (.)) */
+static void smooth_apply(const ohier* h, const olevel* Lv, const double* res, double* out, double* tmp) {
+    int64_t n = Lv->n;
+    if (h->smoother == 1) {
+        or_spmv(Lv->Wd, res, tmp);
+        or_spmv(Lv->Z, tmp, out);
+    } else {
+        for (int64_t i = 0; i < n; ++i) out[i] = Lv->m[i] * res[i];
+    }
+}
+
 int64_t or_coarse_visits(const ohier* h) { return h->coarse_visits; }
 
 /* K-cycle coarse correction ("at each level except the fine and the
@@ -825,10 +1029,14 @@ static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
     }
     double* t = (double*)xmalloc(sizeof(double) * (size_t)n);
     double* xn = (double*)xmalloc(sizeof(double) * (size_t)n);
-    for (int64_t i = 0; i < n; ++i) x[i] = L->m[i] * b[i];
+    double* u = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* tmp = (double*)xmalloc(sizeof(double) * (size_t)n);
+    smooth_apply(h, L, b, x, tmp); /* first pre-sweep from x = 0: x = M^{-1} b */
     for (int32_t s = 1; s < h->pre; ++s) {
         or_spmv(L->A, x, t);
-        for (int64_t i = 0; i < n; ++i) xn[i] = x[i] + L->m[i] * (b[i] - t[i]);
+        for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
+        smooth_apply(h, L, t, u, tmp);
+        for (int64_t i = 0; i < n; ++i) xn[i] = x[i] + u[i];
         memcpy(x, xn, sizeof(double) * (size_t)n);
     }
     or_spmv(L->A, x, t);
@@ -843,13 +1051,17 @@ static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
         vcycle_rec(h, l + 1, bc, ec);
     or_spmv(L->P, ec, t);
     for (int64_t i = 0; i < n; ++i) x[i] = x[i] + t[i];
-    for (int32_t s = 0; s < h->post; ++s) {
+    for (int32_t s = 0; s < h->post; ++s) { /* post-smoothing with M^T = M */
         or_spmv(L->A, x, t);
-        for (int64_t i = 0; i < n; ++i) xn[i] = x[i] + L->m[i] * (b[i] - t[i]);
+        for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
+        smooth_apply(h, L, t, u, tmp);
+        for (int64_t i = 0; i < n; ++i) xn[i] = x[i] + u[i];
         memcpy(x, xn, sizeof(double) * (size_t)n);
     }
     free(t);
     free(xn);
+    free(u);
+    free(tmp);
     free(bc);
     free(ec);
 }

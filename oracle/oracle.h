@@ -84,6 +84,13 @@ void    or_set_coarse_cg(ohier* h, int32_t on, double rtol, int32_t maxit);
  * or_vcycle / or_pcg / or_fcg then apply the K-cycle.  or_coarse_visits counts the
  * coarsest solves performed since the hierarchy was built. */
 void    or_set_cycle(ohier* h, int32_t cycle);
+/* smoother kind 1 = INVK: IC(0) = ILU(0) in
+ * LDL^T form, W = L^{-1} truncated to `fill` levels of positional fill, smoothing
+ * step x += W^T D^{-1} W (b - A x) on every non-coarsest level; 0 = l1-Jacobi.
+ * Returns OR_ERR_NOT_SPD on a non-positive IC(0) pivot.  or_level_invk returns
+ * D^{-1} W (which = 0) or Z = W^T (which = 1) of level l. */
+int32_t or_set_smoother(ohier* h, int32_t kind, int32_t fill);
+const ocsr* or_level_invk(const ohier* h, int32_t l, int32_t which);
 int64_t or_coarse_visits(const ohier* h);
 
 #ifdef __cplusplus

@@ -79,6 +79,8 @@ def lib():
                                C.POINTER(C.c_double), _vp]),
         "or_set_coarse_cg": (None, [_vp, C.c_int32, C.c_double, C.c_int32]),
         "or_set_cycle": (None, [_vp, C.c_int32]),
+        "or_set_smoother": (C.c_int32, [_vp, C.c_int32, C.c_int32]),
+        "or_level_invk": (_vp, [_vp, C.c_int32, C.c_int32]),
         "or_coarse_visits": (C.c_int64, [_vp]),
     }
     for name, (res, args) in sig.items():
@@ -302,6 +304,16 @@ class OracleHierarchy:
     def set_cycle(self, kind="V"):
         """'V' (Eq. 3.1) or 'K' (K-cycle: two FCG(1) iterations per intermediate level)."""
         lib().or_set_cycle(self.h, {"V": 0, "K": 1}[kind])
+
+    def set_smoother(self, kind="l1jacobi", fill=1):
+        """'l1jacobi' or 'invk' (`fill` levels in the inversion)."""
+        st = lib().or_set_smoother(self.h, {"l1jacobi": 0, "invk": 1}[kind], int(fill))
+        if st != OR_OK:
+            raise RuntimeError(f"or_set_smoother failed with status {st}")
+
+    def invk(self, l, which):
+        """which = 0: D^{-1} W; 1: Z = W^T (INVK factors of level l, borrowed)."""
+        return OracleCSR(lib().or_level_invk(self.h, l, which), owned=False)
 
     @property
     def coarse_visits(self):

@@ -744,3 +744,108 @@ def test_kcycle_restores_convergence_of_unsmoothed_aggregation():
     for s in range(5):
         r = uniform_pm1(43 + s, A.n_global)
         assert r @ h.vcycle(r) > 0
+
+
+# --------------------------------------------------------------- NEXT-3 pins (INVK)
+def _dense(M):
+    return M.to_scipy().toarray()
+
+
+def _invk_parts(h, l=0):
+    """Dense W (unit lower), D (pivots) and Z from the oracle's INVK factors of level l."""
+    Wd = _dense(h.invk(l, 0))
+    Z = _dense(h.invk(l, 1))
+    W = Z.T
+    d = 1.0 / np.diag(Wd)  # Wd = D^{-1} W with a unit diagonal in W
+    return W, d, Z, Wd
+
+
+def test_invk_ic0_reproduces_A_on_its_pattern():
+    """IC(0) (= ILU(0) of an s.p.d. matrix in LDL^T form): L D L^T equals A on
+    the pattern of A (the defining property of the zero-fill factorisation)."""
+    A = poisson7(6, 5, 4)
+    h = O.OracleHierarchy(A, max_coarse_size=20)
+    h.set_smoother("invk", fill=10 ** 6)  # unbounded fill: W = L^{-1} exactly
+    W, d, _, _ = _invk_parts(h)
+    L = np.linalg.inv(W)
+    assert np.allclose(np.diag(L), 1.0, atol=1e-12)
+    M = L @ np.diag(d) @ L.T
+    Ad = A.to_scipy().toarray()
+    pat = Ad != 0
+    assert np.abs(M[pat] - Ad[pat]).max() <= 1e-12 * np.abs(Ad).max()
+    assert np.abs(M[~pat]).max() > 1e-6  # IC(0) fill is dropped, so M != A off the pattern
+
+
+def test_invk_tridiagonal_is_exact_and_one_sweep_solves():
+    """1-D Poisson: IC(0) is the exact Cholesky factorisation (no fill to drop), and with
+    unbounded fill in the inversion M^{-1} = A^{-1} (unbounded-fill INVK = exact
+    (LDL^T)^{-1}); fill 1 keeps exactly the first two sub-diagonals of L^{-1}."""
+    n = 12
+    A = poisson7(n, 1, 1, k=(1.0, 0.0, 0.0))
+    Ad = A.to_scipy().toarray()
+    h = O.OracleHierarchy(A, max_coarse_size=4)
+    h.set_smoother("invk", fill=10 ** 6)
+    W, d, Z, Wd = _invk_parts(h)
+    Minv = Z @ Wd
+    assert np.abs(Minv @ Ad - np.eye(n)).max() <= 1e-12
+    Lex = np.linalg.cholesky(Ad)
+    Linv = np.linalg.inv(Lex / np.diag(Lex))       # exact unit-lower L^{-1}
+    h.set_smoother("invk", fill=1)
+    W1, _, _, _ = _invk_parts(h)
+    band = np.tril(np.triu(np.ones((n, n)), -2))   # diagonal and two sub-diagonals
+    assert np.abs(W1 - Linv * band).max() <= 1e-13
+    assert np.count_nonzero(W1) == n + (n - 1) + (n - 2)
+
+
+@pytest.mark.parametrize("fill", [0, 1, 2])
+def test_invk_truncated_inverse_satisfies_its_equations(fill):
+    """Positional sparsification: on its kept pattern S the truncated
+    inverse satisfies (L W)_ij = delta_ij for every (i, j) in S; the pattern grows with the
+    fill level; level 0 is the pattern of L (plus the diagonal)."""
+    A = poisson7(5, 4, 4)
+    Ad = A.to_scipy().toarray()
+    h = O.OracleHierarchy(A, max_coarse_size=10)
+    h.set_smoother("invk", fill=10 ** 6)
+    Wx, dx, _, _ = _invk_parts(h)
+    L = np.linalg.inv(Wx)                          # the IC(0) factor itself
+    h.set_smoother("invk", fill=fill)
+    W, d, _, _ = _invk_parts(h)
+    assert np.allclose(d, dx, rtol=0, atol=0)
+    S = W != 0
+    LW = L @ W
+    assert np.abs((LW - np.eye(len(d)))[S]).max() <= 1e-12
+    if fill == 0:
+        assert np.array_equal(S, (np.tril(Ad) != 0))
+
+
+def test_invk_smoother_is_A_convergent_and_cycle_is_spd():
+    """the smoothers used are A-convergent, ||I - M^{-1} A||_A < 1; the
+    V-cycle with INVK smoothing stays symmetric positive definite (PCG applies)."""
+    A = poisson7(16, 16, 16)
+    Ad = A.to_scipy().toarray()
+    h = O.OracleHierarchy(A)
+    h.set_smoother("invk", fill=1)
+    _, _, Z, Wd = _invk_parts(h)
+    Minv = Z @ Wd
+    lam = np.linalg.eigvals(Minv @ Ad).real
+    assert lam.min() > 0 and lam.max() < 2  # spectrum of I - M^{-1}A inside (-1, 1)
+    B = np.column_stack([h.vcycle(e) for e in np.eye(A.n_global)[:, :64].T])
+    Ad64 = np.eye(A.n_global)[:, :64]
+    sym = Ad64.T @ B
+    assert np.abs(sym - sym.T).max() <= 1e-12 * np.abs(sym).max()
+    for s in range(3):
+        r = uniform_pm1(60 + s, A.n_global)
+        assert r @ h.vcycle(r) > 0
+
+
+def test_invk_va3s3cs1_converges_faster_than_one_l1_jacobi_sweep():
+    """VA3S3CS1 (one INVK sweep) needs no more FCG iterations than the
+    l1-Jacobi V-cycle with the same sweep count (INVK is the stronger smoother, Table 1)."""
+    A = poisson7(40, 40, 40)
+    b = np.ones(A.n_global)
+    h = O.OracleHierarchy(A)
+    _, ij = h.pcg(b, rtol=1e-6)
+    h.set_smoother("invk", fill=1)
+    _, ii = h.fcg(b, rtol=1e-6)
+    assert ii["status"] == O.OR_OK and ii["iterations"] < ij["iterations"], (ii, ij)
+    assert ii["true_relres"] <= 2e-6
