@@ -182,6 +182,11 @@ def method_settings(args, meta, world):
                                             "FCG(1), coarsest l1-Jacobi CG (1e-4, 30 its)",
                 "cfg": dict(pre_sweeps=4, post_sweeps=4, max_coarse_size=12 * 200 * world, krylov=1,
                             coarse_solver=1, coarse_rtol=1e-4, coarse_maxit=30)}
+    if args.method == "invk":
+        return {"name": "invk", "desc": "3 matching sweeps/level, smoothed P (omega=4/3/||D^-1A||), INVK smoother "
+                                        "(IC(0) + 1 level of fill in the inversion), PCG, direct coarsest",
+                "cfg": dict(pre_sweeps=meta["sweeps"][0], post_sweeps=meta["sweeps"][1],
+                            max_coarse_size=meta["max_coarse_size"], smoother=1, invk_fill=1)}
     if args.method == "ka1":
         return {"name": "ka1", "desc": "3 matching sweeps/level, unsmoothed P, K-cycle (2 inner FCG(1) "
                                        "iterations per intermediate level), FCG(1), direct coarsest",
@@ -359,7 +364,7 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--maxit", type=int, default=500)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--method", choices=["default", "va3s5cs1", "ka1"], default="default")
+    ap.add_argument("--method", choices=["default", "va3s5cs1", "ka1", "invk"], default="default")
     ap.add_argument("--tail-rows", type=int, default=None, help="override cfg.tail_rows (0 = no persistent tail)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -100,6 +100,13 @@ typedef struct {
                                      operations) instead of ~4 launches per level and visit.
                                      Default 0 = off: measured slower than the launched graph on
                                      B200 (grid barriers cost more than PDL launch overlap). */
+    int32_t smoother;             /* 0 = l1-Jacobi (default); 1 = INVK (
+                                     SURVEY.md §8f NEXT-3): IC(0) = ILU(0) in LDL^T form, W = L^{-1}
+                                     with `invk_fill` levels of positional fill, a smoothing step is
+                                     x += W^T D^{-1} W (b - A x) (two extra SpMVs).  Single-rank
+                                     contexts only.  With one process HINVK = INVK. */
+    int32_t invk_fill;            /* fill levels admitted in the inversion (default 1, Table 1
+                                     caption PAPER.md:207) */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */

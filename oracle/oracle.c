@@ -945,7 +945,12 @@ int32_t or_set_smoother(ohier* h, int32_t kind, int32_t fill) {
         or_csr_free(Lv->Wd);
         or_csr_free(Lv->Z);
         Lv->Wd = Lv->Z = NULL;
-        if (!invk_level(Lv, fill)) return OR_ERR_NOT_SPD;
+        /* reading I4: fill is admitted on stencil-like levels (<= 27 entries per row);
+         * denser coarse levels keep the pattern of L (fill 0), otherwise the level-1
+         * pattern of an already dense row fills in the whole triangle */
+        int64_t nnz = Lv->A->rp[Lv->n];
+        int32_t f = ((double)nnz <= 27.0 * (double)Lv->n) ? fill : 0;
+        if (!invk_level(Lv, f)) return OR_ERR_NOT_SPD;
     }
     return OR_OK;
 }

@@ -140,6 +140,8 @@ struct DevLevel {
     // pre-sweep from zero, r = b - A (m o b) = b - (A diag(m)) b: the kernel gathers b
     // alone, and no level needs m o b (s1 == 1 only)
     DevMat Am;
+    // INVK smoother (cfg.smoother == 1): D^{-1} W and Z = W^T
+    DevMat Wd, Z;
     double* m = nullptr;   // window-sized vectors
     double* b = nullptr;
     double* mb = nullptr;
@@ -156,6 +158,8 @@ struct DevLevel {
         P.release();
         R.release();
         Am.release();
+        Wd.release();
+        Z.release();
         for (double* v : {kx, kr, kmb, kz, kp, kq, kst}) cudaFree(v);
         cudaFree(m);
         cudaFree(b);
@@ -690,6 +694,51 @@ void launch_tail(amg_hier_s* h, Launch& L) {
 
 // ------------------------------------------------------------- V-cycle / K-cycle
 void enqueue_fcg2(amg_hier_s* h, Launch& L, int l);
+void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf* mbvec, const VecOf& outv,
+                   bool dot, const VecOf* dwv);
+
+// Level l of the cycle with the INVK smoother (cfg.smoother == 1; single rank):
+// M^{-1} r = Z (Wd r), Wd = D^{-1} W, Z = W^T.  The iterate lives
+// in `out` throughout (every update is row-local), Wd r in the level's mb buffer
+// (m o b is not used with INVK), residuals in r:
+//   out = Z (Wd b); [s1-1 times: r' = b - A out; out += Z (Wd r')]; r = b - A out;
+//   b_{l+1} = R r; e = cycle(l+1); out += P-bar e; s2 times: r' = b - A out;
+//   out += Z (Wd r')   (the last one at level 0 also reduces the PCG/FCG dot).
+void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf& outv, bool dot,
+                        const VecOf* dwv) {
+    const int dkind = dwv ? FIN_ZQ : FIN_RZ;
+    const int nl = h->nlev();
+    const int s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
+    RankState& R = h->ranks[0];
+    DevLevel& D = R.lv[l];
+    DevLevel& C = R.lv[l + 1];
+    const double* b = bvec(R);
+    double* x = outv(R);
+    const double n8 = 8.0 * (double)D.comp_n;
+    launch_mat(L, D.Wd, GVec{b}, EStore{D.mb}, no_red(), "invk_w", 2 * n8);
+    launch_mat(L, D.Z, GVec{D.mb}, EStore{x}, no_red(), "invk_z", 2 * n8);
+    auto sweep = [&](bool dt) {
+        launch_mat(L, D.A, GVec{x}, EResid{b, D.r}, no_red(), "invk_resid", 3 * n8);
+        launch_mat(L, D.Wd, GVec{D.r}, EStore{D.mb}, no_red(), "invk_w", 2 * n8);
+        if (dt)
+            launch_mat(L, D.Z, GVec{D.mb}, EAddDot<true>{x, x, dwv ? (*dwv)(R) : b}, dot_red(h, R, dkind, 0),
+                       "invk_z_dot", 4 * n8);
+        else
+            launch_mat(L, D.Z, GVec{D.mb}, EAddDot<false>{x, x}, no_red(), "invk_z", 3 * n8);
+    };
+    for (int sw = 1; sw < s1; ++sw) sweep(false);
+    launch_mat(L, D.A, GVec{x}, EResid{b, D.r}, no_red(), "resid", 3 * n8);
+    launch_mat(L, D.R, GVec{D.r}, EStore{C.b}, no_red(), "restrict", n8 + 8.0 * (double)C.comp_n);
+    const bool kfcg = h->cfg.cycle == 1 && l + 1 < nl - 1;
+    const VecOf cb = [l](RankState& R) { return R.lv[l + 1].b; };
+    const VecOf ev = kfcg ? VecOf([l](RankState& R) { return R.lv[l + 1].kx; })
+                          : VecOf([l](RankState& R) { return R.lv[l + 1].xa; });
+    if (kfcg) enqueue_fcg2(h, L, l + 1);
+    else enqueue_level(h, L, l + 1, cb, nullptr, ev, false, nullptr);
+    launch_mat(L, D.P, GVec{ev(R)}, EProlongAdd{x, x}, no_red(), "prolong", 2 * n8 + 8.0 * (double)C.comp_n);
+    for (int sw = 0; sw < s2; ++sw) sweep(dot && sw == s2 - 1);
+    if (dot) dot_finish(h, L, dkind);
+}
 
 // out = B_l b: the part of the cycle rooted at level l (Eq. 3.1;
 // SURVEY.md §8c O10).  bvec / outv give each rank's level-l WINDOW base pointers;
@@ -707,6 +756,10 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     const int nsm = h->ctx->nsm;
     const int nr = (int)h->ranks.size();
     auto ri_of = [&](RankState& R) { return (int)(&R - h->ranks.data()); };
+    if (h->cfg.smoother == 1 && l < nl - 1) {
+        enqueue_level_invk(h, L, l, bvec, outv, dot, dwv);
+        return;
+    }
     if (l == nl - 1) {  // coarsest: z_L = B_L b_L (reading R2 or the coarse CG), replicated on every rank
         for (auto& R : h->ranks) {
             launch_coarse(h, L, R, bvec(R), outv(R));
@@ -1245,7 +1298,10 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
             D.rst_off = S.rst_begin - P.lv[l + 1].win_begin;
             const bool tcsr = h->tail_level >= 0 && l >= h->tail_level;  // tail levels: CSR for k_tail
             if ((st = upload_mat(S.A, D.A, true, D.ep_off, tcsr))) return st;
-            if (h->cfg.pre_sweeps == 1) {
+            if (h->cfg.smoother == 1) {
+                if ((st = upload_mat(S.Wd, D.Wd, true, D.ep_off))) return st;
+                if ((st = upload_mat(S.Z, D.Z, true, D.ep_off))) return st;
+            } else if (h->cfg.pre_sweeps == 1) {
                 amgsetup::Csr As = S.A;
 #pragma omp parallel for schedule(static)
                 for (int64_t i = 0; i < As.nrows; ++i)
@@ -1315,6 +1371,9 @@ void byte_model(amg_hier_s* h, const amgsetup::Hierarchy& H) {
         const double MP = 12.0 * (double)H.lv[l].P.nnz() + 4.0 * (n + 1);
         const double visits = kc ? std::ldexp(1.0, (int)l) : 1.0;
         bv += visits * ((s1 + s2) * MA + 2 * MP + 8 * n * ((s1 + s2) + 2 + 3 * (s1 - 1) + 2 + 2 + 3 * s2) + 16 * nc);
+        if (h->cfg.smoother == 1)  // INVK: every smoothing step also streams Wd and Z (+ t write/read)
+            bv += visits * (s1 + s2) *
+                  (12.0 * (double)(H.lv[l].Wd.nnz() + H.lv[l].Z.nnz()) + 8.0 * (n + 1) + 16.0 * n);
         if (kc && l >= 1) bv += std::ldexp(1.0, (int)l - 1) * (2 * MA + 176.0 * n);
     }
     const double nL = (double)H.lv.back().A.nrows;
@@ -1665,6 +1724,8 @@ void amg_config_default(amg_config_t* c) {
     c->cycle = 0;
     c->setup_device = 1;
     c->tail_rows = 0;
+    c->smoother = 0;
+    c->invk_fill = 1;
 }
 
 int amg_nccl_unique_id(void* out128) {
@@ -1745,6 +1806,14 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
                 "coarse_rtol >= 0");
         return AMG_ERR_ARG;
     }
+    if ((cfg.smoother != 0 && cfg.smoother != 1) || cfg.invk_fill < 0) {
+        set_err("amg_hierarchy_build: smoother must be 0 (l1-Jacobi) or 1 (INVK), invk_fill >= 0");
+        return AMG_ERR_ARG;
+    }
+    if (cfg.smoother == 1 && (ctx->nranks > 1 || cfg.emulate_ranks > 1)) {
+        set_err("amg_hierarchy_build: the INVK smoother is implemented for single-rank contexts only");
+        return AMG_ERR_ARG;
+    }
     if (cfg.cycle == 1 && (ctx->nranks > 1 || cfg.emulate_ranks > 1)) {
         set_err("amg_hierarchy_build: the K-cycle is implemented for single-rank contexts only");
         return AMG_ERR_ARG;
@@ -1777,6 +1846,18 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
             set_err("amg_hierarchy_build: " + g_err);
             return fail(st);
         }
+        if (cfg.smoother == 1) {  // INVK factors of every non-coarsest level (host)
+            for (size_t l = 0; l + 1 < H.lv.size(); ++l) {
+                // reading I4: positional fill only on stencil-like levels (<= 27 entries/row)
+                const amgsetup::Csr& Al = H.lv[l].A;
+                const int f = ((double)Al.nnz() <= 27.0 * (double)Al.nrows) ? cfg.invk_fill : 0;
+                if (!amgsetup::invk_factors(Al, f, H.lv[l].Wd, H.lv[l].Z)) {
+                    set_err("amg_hierarchy_build: INVK: non-positive IC(0) pivot");
+                    return fail(AMG_ERR_NOT_SPD);
+                }
+            }
+            amgsetup::tmark("INVK factors");
+        }
         amgsetup::tmark("(hierarchy built)");
         std::vector<int64_t> bounds(np + 1);
         for (int g = 0; g <= np; ++g) bounds[g] = n_global * g / np;
@@ -1787,7 +1868,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         for (size_t l = 0; l + 1 < nlv; ++l) h->agg.push_back(H.lv[l].agg);
         // persistent tail: the deep levels (n_l <= tail_rows, at least one non-coarsest)
         // run as one cooperative kernel; single process, direct coarsest solve
-        if (np == 1 && cfg.tail_rows > 0 && cfg.coarse_solver == 0 && nlv >= 3 &&
+        if (np == 1 && cfg.tail_rows > 0 && cfg.coarse_solver == 0 && cfg.smoother == 0 && nlv >= 3 &&
             (cfg.cycle == 0 || cfg.pre_sweeps == 1)) {
             for (size_t l = 1; l + 1 < nlv; ++l)
                 if (H.lv[l].A.nrows <= cfg.tail_rows) {
@@ -1820,6 +1901,8 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
                 Lv.P = std::move(S.P);
                 Lv.R = std::move(S.R);
                 Lv.m = std::move(S.m);
+                Lv.Wd = std::move(S.Wd);
+                Lv.Z = std::move(S.Z);
             }
         } else if (!amgsetup::partition(H, bounds, cfg.replicate_below_bytes, plans, err)) {
             set_err("amg_hierarchy_build: " + err);

@@ -427,6 +427,22 @@ __device__ __forceinline__ void bind(ESpmvDotPz& e) {
     e.pnew = (it & 1) ? e.p0 : e.p1;
 }
 
+// x' = x + s, returns dw_i x'_i (DOT)       (INVK: x' = x + Z (D^-1 W r); the level-0
+//                                            last post-sweep also reduces r^T z or q^T z)
+template <bool DOT>
+struct EAddDot {
+    static constexpr bool kDot = DOT;
+    static constexpr bool kAbs = false;
+    const double* x;
+    double* xo;
+    const double* __restrict__ dw = nullptr;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        const double v = x[i] + s;
+        xo[i] = v;
+        return DOT ? dw[i] * v : 0.0;
+    }
+};
+
 // q = s, returns p_i q_i                    (PCG: q = A p fused with p^T q)
 struct ESpmvDot {
     static constexpr bool kDot = true;

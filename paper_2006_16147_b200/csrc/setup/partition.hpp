@@ -37,6 +37,7 @@ struct RankLevel {
     Csr P;  // rows [comp_begin, comp_end), columns in the level-(l+1) window frame
     Csr R;  // rows [rst_begin, rst_end) of level l+1, columns in the level-l window frame
     std::vector<double> m;  // l1-Jacobi inverse diagonal over the whole window
+    Csr Wd, Z;              // INVK factors (single rank only)
 };
 
 struct RankPlan {

@@ -529,6 +529,112 @@ bool dense_inverse(const Csr& A, std::vector<double>& inv) {
 
 bool dense_inverse_host(const Csr& A, std::vector<double>& inv) { return dense_inverse(A, inv); }
 
+// ------------------------------------------------------------------ INVK
+// IC(0) with a scatter map of the current row (position of each column of row i in
+// L), then the truncated inverse by the row recurrence w_i = e_i - sum_k l_ik w_k with
+// a dense accumulator and per-column fill levels; summation orders as the readings
+// I1-I3 state (k ascending; within a row of W, ascending columns).
+bool invk_factors(const Csr& A, int fill, Csr& Wd, Csr& Z) {
+    const int64_t n = A.nrows;
+    Csr L;
+    L.nrows = L.ncols = n;
+    L.rp.assign(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t c = 0;
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) c += (A.ci[k] < i);
+        L.rp[i + 1] = L.rp[i] + c;
+    }
+    L.ci.resize(L.rp[n]);
+    L.v.resize(L.rp[n]);
+    std::vector<double> d(n, 0.0);
+    std::vector<int64_t> pos(n, -1);  // scatter map of row i of L
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t o = L.rp[i];
+        double aii = 0.0;
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const int32_t c = A.ci[k];
+            if (c < i) {
+                L.ci[o] = c;
+                L.v[o] = A.v[k];
+                pos[c] = o;
+                ++o;
+            } else if (c == i) {
+                aii = A.v[k];
+            }
+        }
+        for (int64_t t = L.rp[i]; t < L.rp[i + 1]; ++t) {
+            const int32_t j = L.ci[t];
+            double sv = L.v[t];
+            for (int64_t q = L.rp[j]; q < L.rp[j + 1]; ++q) {  // k in row j (ascending), k < j
+                const int32_t k = L.ci[q];
+                const int64_t pk = pos[k];
+                if (pk >= L.rp[i] && pk < t) sv = sv - (L.v[pk] * d[k]) * L.v[q];
+            }
+            L.v[t] = sv / d[j];
+        }
+        double di = aii;
+        for (int64_t t = L.rp[i]; t < L.rp[i + 1]; ++t) di = di - (L.v[t] * L.v[t]) * d[L.ci[t]];
+        for (int64_t t = L.rp[i]; t < L.rp[i + 1]; ++t) pos[L.ci[t]] = -1;
+        if (!(di > 0.0)) return false;
+        d[i] = di;
+    }
+    // truncated inverse W (unit diagonal last in each row), with levels
+    Csr W;
+    W.nrows = W.ncols = n;
+    W.rp.assign(n + 1, 0);
+    std::vector<int32_t> wl;  // level of every kept entry
+    std::vector<double> acc(n, 0.0);
+    std::vector<int32_t> lev(n, 0);
+    std::vector<int64_t> mark(n, -1);
+    std::vector<int32_t> cols;
+    for (int64_t i = 0; i < n; ++i) {
+        cols.clear();
+        for (int64_t t = L.rp[i]; t < L.rp[i + 1]; ++t) {
+            const int32_t j = L.ci[t];
+            mark[j] = i;
+            acc[j] = 0.0;
+            lev[j] = 0;
+            cols.push_back(j);
+        }
+        for (int64_t t = L.rp[i]; t < L.rp[i + 1]; ++t) {
+            const int32_t k = L.ci[t];
+            const double lik = L.v[t];
+            for (int64_t q = W.rp[k]; q < W.rp[k + 1]; ++q) {
+                const int32_t j = W.ci[q];
+                const int32_t cl = wl[q] + 1;
+                // fill 0 keeps only the pattern of L: a non-structural column can never reach
+                // level 0, so its (discarded) accumulation is skipped — kept values unchanged
+                if (fill == 0 && mark[j] != i) continue;
+                if (mark[j] != i) {
+                    mark[j] = i;
+                    acc[j] = 0.0;
+                    lev[j] = cl;
+                    cols.push_back(j);
+                } else if (cl < lev[j]) {
+                    lev[j] = cl;
+                }
+                acc[j] = acc[j] + lik * W.v[q];
+            }
+        }
+        std::sort(cols.begin(), cols.end());
+        for (const int32_t j : cols)
+            if (lev[j] <= fill) {
+                W.ci.push_back(j);
+                W.v.push_back(-acc[j]);
+                wl.push_back(lev[j]);
+            }
+        W.ci.push_back((int32_t)i);
+        W.v.push_back(1.0);
+        wl.push_back(0);
+        W.rp[i + 1] = (int64_t)W.ci.size();
+    }
+    Z = transpose(W);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = W.rp[i]; k < W.rp[i + 1]; ++k) W.v[k] = W.v[k] / d[i];
+    Wd = std::move(W);
+    return true;
+}
+
 int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
           std::string& err) {
     auto t0 = std::chrono::steady_clock::now();

@@ -41,6 +41,7 @@ struct Level {
     std::vector<double> m;    // l1-Jacobi inverse diagonal 1/(sum_j |a_ij|)
     double omega = 0.0;
     int sweeps = 0;
+    Csr Wd, Z;                // INVK smoother (smoother == 1): D^{-1} W and Z = W^T
 };
 
 struct Hierarchy {
@@ -60,6 +61,10 @@ int build(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out,
 // The same build on the current CUDA device (setup_gpu.cu); A0 already validated.
 int build_gpu(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out, std::string& err);
 bool dense_inverse_host(const Csr& A, std::vector<double>& inv);
+// INVK smoother factors of A: IC(0) = ILU(0) in LDL^T form, W = L^{-1}
+// truncated to `fill` levels of positional fill, Wd = D^{-1} W, Z = W^T.  false on a
+// non-positive pivot.
+bool invk_factors(const Csr& A, int fill, Csr& Wd, Csr& Z);
 void tmark(const char* what);
 
 // Building blocks (exported for the setup self-tests).

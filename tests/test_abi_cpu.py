@@ -51,6 +51,7 @@ def test_config_default_matches_header(amg):
     assert c.cycle == 0  # V-cycle by default (the north_star path); K-cycle opt-in (NEXT-4)
     assert c.setup_device == 1  # GPU setup (NEXT-1), bit-identical to the host build
     assert c.tail_rows == 0  # persistent cooperative tail: experimental, off by default (slower)
+    assert (c.smoother, c.invk_fill) == (0, 1)  # l1-Jacobi by default; INVK opt-in (NEXT-3)
 
 
 def test_config_struct_layout_matches_header(amg):
