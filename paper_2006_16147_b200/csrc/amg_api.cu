@@ -1846,15 +1846,20 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
             set_err("amg_hierarchy_build: " + g_err);
             return fail(st);
         }
-        if (cfg.smoother == 1) {  // INVK factors of every non-coarsest level (host)
-            for (size_t l = 0; l + 1 < H.lv.size(); ++l) {
+        if (cfg.smoother == 1) {  // INVK factors of every non-coarsest level (host; levels in parallel,
+                                  // each factorisation is a sequential row recurrence)
+            const int nlf = (int)H.lv.size() - 1;
+            int bad = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : bad)
+            for (int l = 0; l < nlf; ++l) {
                 // reading I4: positional fill only on stencil-like levels (<= 27 entries/row)
                 const amgsetup::Csr& Al = H.lv[l].A;
                 const int f = ((double)Al.nnz() <= 27.0 * (double)Al.nrows) ? cfg.invk_fill : 0;
-                if (!amgsetup::invk_factors(Al, f, H.lv[l].Wd, H.lv[l].Z)) {
-                    set_err("amg_hierarchy_build: INVK: non-positive IC(0) pivot");
-                    return fail(AMG_ERR_NOT_SPD);
-                }
+                if (!amgsetup::invk_factors(Al, f, H.lv[l].Wd, H.lv[l].Z)) bad = 1;
+            }
+            if (bad) {
+                set_err("amg_hierarchy_build: INVK: non-positive IC(0) pivot");
+                return fail(AMG_ERR_NOT_SPD);
             }
             amgsetup::tmark("INVK factors");
         }
