@@ -612,7 +612,9 @@ struct TailEmitter {
         ops.push_back(o);
         bytes += 16.0 * (double)n;
     }
-    void fcg2(int l) {
+    // final_update: apply x += alpha p here (nested solves, consumed inside the program);
+    // the top-level solve leaves it to its launched consumer, which gathers x + alpha p
+    void fcg2(int l, bool final_update = true) {
         RankState& R = h->ranks[0];
         DevLevel& D = R.lv[l];
         const int64_t n = D.comp_n;
@@ -650,6 +652,7 @@ struct TailEmitter {
         ops.back().x = D.kp;
         ops.back().ks = D.kst;
         ops.back().fin = FIN_KALPHA;
+        if (!final_update) return;
         TailOp u2 = op(TK_KUPD2, 0);
         u2.n = n;
         u2.y = D.kx;
@@ -667,7 +670,7 @@ int build_tail(amg_hier_s* h) {
     h->tail_grid = std::max(1, std::min(nb, 6)) * h->ctx->nsm;
     TailEmitter E{h, {}, 0.0};
     RankState& R = h->ranks[0];
-    if (h->cfg.cycle == 1) E.fcg2(lt);
+    if (h->cfg.cycle == 1) E.fcg2(lt, false);
     else E.level(lt, R.lv[lt].b, R.lv[lt].mb, R.lv[lt].xa);
     int st;
     if ((st = dev_copy(&h->tail_prog, E.ops.data(), E.ops.size()))) return st;
@@ -694,8 +697,17 @@ void launch_tail(amg_hier_s* h, Launch& L) {
 
 // ------------------------------------------------------------- V-cycle / K-cycle
 void enqueue_fcg2(amg_hier_s* h, Launch& L, int l);
+// Where a cycle's fused dot goes: the PCG state (default) or a K-cycle level state.
+struct DotSink {
+    double* ks;
+    int kind;
+};
 void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf* mbvec, const VecOf& outv,
-                   bool dot, const VecOf* dwv);
+                   bool dot, const VecOf* dwv, const DotSink* sink = nullptr);
+RedCtx sink_red(amg_hier_s* h, RankState& R, int dkind, const DotSink* sink) {
+    if (sink) return RedCtx{R.partials, R.ticket, nullptr, nullptr, 0ull, sink->kind, sink->ks};
+    return dot_red(h, R, dkind, 0);
+}
 
 // Level l of the cycle with the INVK smoother (cfg.smoother == 1; single rank):
 // M^{-1} r = Z (Wd r), Wd = D^{-1} W, Z = W^T.  The iterate lives
@@ -705,7 +717,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
 //   b_{l+1} = R r; e = cycle(l+1); out += P-bar e; s2 times: r' = b - A out;
 //   out += Z (Wd r')   (the last one at level 0 also reduces the PCG/FCG dot).
 void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf& outv, bool dot,
-                        const VecOf* dwv) {
+                        const VecOf* dwv, const DotSink* sink) {
     const int dkind = dwv ? FIN_ZQ : FIN_RZ;
     const int nl = h->nlev();
     const int s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
@@ -721,7 +733,7 @@ void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, cons
         launch_mat(L, D.A, GVec{x}, EResid{b, D.r}, no_red(), "invk_resid", 3 * n8);
         launch_mat(L, D.Wd, GVec{D.r}, EStore{D.mb}, no_red(), "invk_w", 2 * n8);
         if (dt)
-            launch_mat(L, D.Z, GVec{D.mb}, EAddDot<true>{x, x, dwv ? (*dwv)(R) : b}, dot_red(h, R, dkind, 0),
+            launch_mat(L, D.Z, GVec{D.mb}, EAddDot<true>{x, x, dwv ? (*dwv)(R) : b}, sink_red(h, R, dkind, sink),
                        "invk_z_dot", 4 * n8);
         else
             launch_mat(L, D.Z, GVec{D.mb}, EAddDot<false>{x, x}, no_red(), "invk_z", 3 * n8);
@@ -735,9 +747,13 @@ void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, cons
                           : VecOf([l](RankState& R) { return R.lv[l + 1].xa; });
     if (kfcg) enqueue_fcg2(h, L, l + 1);
     else enqueue_level(h, L, l + 1, cb, nullptr, ev, false, nullptr);
-    launch_mat(L, D.P, GVec{ev(R)}, EProlongAdd{x, x}, no_red(), "prolong", 2 * n8 + 8.0 * (double)C.comp_n);
+    if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
+        launch_mat(L, D.P, GXap{C.kx, C.kp, C.kst}, EProlongAdd{x, x}, no_red(), "prolong",
+                   2 * n8 + 16.0 * (double)C.comp_n);
+    else
+        launch_mat(L, D.P, GVec{ev(R)}, EProlongAdd{x, x}, no_red(), "prolong", 2 * n8 + 8.0 * (double)C.comp_n);
     for (int sw = 0; sw < s2; ++sw) sweep(dot && sw == s2 - 1);
-    if (dot) dot_finish(h, L, dkind);
+    if (dot && !sink) dot_finish(h, L, dkind);
 }
 
 // out = B_l b: the part of the cycle rooted at level l (Eq. 3.1;
@@ -749,7 +765,7 @@ void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, cons
 // level l+1, or, for the K-cycle (cfg.cycle == 1) when level l+1 is not the
 // coarsest, two FCG iterations at level l+1 (enqueue_fcg2).
 void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf* mbvec, const VecOf& outv,
-                   bool dot, const VecOf* dwv) {
+                   bool dot, const VecOf* dwv, const DotSink* sink) {
     const int dkind = dwv ? FIN_ZQ : FIN_RZ;
     const int nl = h->nlev();
     const int s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
@@ -757,7 +773,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     const int nr = (int)h->ranks.size();
     auto ri_of = [&](RankState& R) { return (int)(&R - h->ranks.data()); };
     if (h->cfg.smoother == 1 && l < nl - 1) {
-        enqueue_level_invk(h, L, l, bvec, outv, dot, dwv);
+        enqueue_level_invk(h, L, l, bvec, outv, dot, dwv, sink);
         return;
     }
     if (l == nl - 1) {  // coarsest: z_L = B_L b_L (reading R2 or the coarse CG), replicated on every rank
@@ -766,11 +782,11 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             if (dot) {  // single-level hierarchy
                 L.begin("dot_rz", 16.0 * R.nL);
                 launch_k(k_dot, vec_grid(R.nL, nsm), kBlock, L.s, dwv ? (*dwv)(R) : bvec(R), outv(R), R.nL,
-                         dot_red(h, R, dkind, 0));
+                         sink_red(h, R, dkind, sink));
                 L.end();
             }
         }
-        if (dot) dot_finish(h, L, dkind);
+        if (dot && !sink) dot_finish(h, L, dkind);
         return;
     }
     std::vector<double*> xpre(nr, nullptr);
@@ -854,11 +870,20 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
         tmp[ri] = D.xb;     // the prolongation update is row-local: may run in place
         double* dst = (s2 % 2 == 1) ? tmp[ri] : fin[ri];
         const double n8 = 8.0 * (double)D.comp_n;
+        DevLevel& C = R.lv[l + 1];
         if (s1 == 1) {  // u = P-bar e only; the first post-sweep adds m o b (EPost1)
-            launch_mat(L, D.P, GVec{e}, EStore{dst + D.ep_off}, no_red(), "prolong", n8 + nc8);
+            if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
+                launch_mat(L, D.P, GXap{C.kx, C.kp, C.kst}, EStore{dst + D.ep_off}, no_red(), "prolong",
+                           n8 + 2 * nc8);
+            else
+                launch_mat(L, D.P, GVec{e}, EStore{dst + D.ep_off}, no_red(), "prolong", n8 + nc8);
         } else {
-            launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off}, no_red(), "prolong",
-                       2 * n8 + nc8);
+            if (kfcg)
+                launch_mat(L, D.P, GXap{C.kx, C.kp, C.kst}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off},
+                           no_red(), "prolong", 2 * n8 + 2 * nc8);
+            else
+                launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off}, no_red(), "prolong",
+                           2 * n8 + nc8);
         }
         cur[ri] = dst;
     }
@@ -885,10 +910,10 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
                 double* xx = xo + D.ep_off;
                 if (dt && abs)
                     launch_mat(L, D.A, GVec{xi}, EPost1<true, false, true>{uu, rr, bo, xx, nullptr, dw},
-                               dot_red(h, R, dkind, 0), "postsweep_dot", 4 * n8);
+                               sink_red(h, R, dkind, sink), "postsweep_dot", 4 * n8);
                 else if (dt)
                     launch_mat(L, D.A, GVec{xi}, EPost1<true, false, false>{uu, rr, bo, xx, m, dw},
-                               dot_red(h, R, dkind, 0), "postsweep_dot", 5 * n8);
+                               sink_red(h, R, dkind, sink), "postsweep_dot", 5 * n8);
                 else if (!mbvec && abs)
                     launch_mat(L, D.A, GVec{xi}, EPost1<false, false, true>{uu, rr, bo, xx}, no_red(), "postsweep",
                                4 * n8);
@@ -905,10 +930,10 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
                 if (abs)
                     launch_mat(L, D.A, GVec{xi},
                                ESweep<true, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, nullptr, dw},
-                               dot_red(h, R, dkind, 0), "postsweep_dot", 3 * n8);
+                               sink_red(h, R, dkind, sink), "postsweep_dot", 3 * n8);
                 else
                     launch_mat(L, D.A, GVec{xi}, ESweep<true, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m, dw},
-                               dot_red(h, R, dkind, 0), "postsweep_dot", 3 * n8 + mb8);
+                               sink_red(h, R, dkind, sink), "postsweep_dot", 3 * n8 + mb8);
             } else {
                 if (abs)
                     launch_mat(L, D.A, GVec{xi}, ESweep<false, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off},
@@ -920,7 +945,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             cur[ri] = xo;
         }
     }
-    if (dot) dot_finish(h, L, dkind);
+    if (dot && !sink) dot_finish(h, L, dkind);
 }
 
 // K-cycle coarse correction at level l (oracle kcycle_fcg2): two
@@ -941,28 +966,23 @@ void enqueue_fcg2(amg_hier_s* h, Launch& L, int l) {
     const VecOf kr = [l](RankState& R) { return R.lv[l].kr; };
     const VecOf kmb = [l](RankState& R) { return R.lv[l].kmb; };
     const VecOf kz = [l](RankState& R) { return R.lv[l].kz; };
-    // iteration 1: p = z = B_l b ; p^T r (r = b)
-    enqueue_level(h, L, l, bv, &mbv, kp, false, nullptr);
-    L.begin("kfcg_dot_pr", 2 * n8);
-    launch_k(k_dot, vec_grid(n, nsm), kBlock, L.s, D.kp, D.b, n, kred(FIN_KPR0));
-    L.end();
+    // iteration 1: p = z = B_l b with p^T r (r = b) fused into the cycle's last step
+    const DotSink s1{D.kst, FIN_KPR0};
+    enqueue_level(h, L, l, bv, &mbv, kp, true, nullptr, &s1);
     launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(FIN_KALPHA), "kfcg_spmv", 2 * n8);
     L.begin("kfcg_upd1", 7 * n8);
     launch_k(k_kupd1, vec_grid(n, nsm), kBlock, L.s, D.kx, D.kr, D.kmb, D.kp, D.kq, D.b, D.m, n,
              (const double*)D.kst);
     L.end();
-    // iteration 2: z = B_l r ; beta = -(z^T q)/(p^T q) ; p = z + beta p, p^T r ; q = A p, alpha ; x += alpha p
-    enqueue_level(h, L, l, kr, &kmb, kz, false, nullptr);
-    L.begin("kfcg_dot_zq", 2 * n8);
-    launch_k(k_dot, vec_grid(n, nsm), kBlock, L.s, D.kz, D.kq, n, kred(FIN_KBETA));
-    L.end();
+    // iteration 2: z = B_l r with z^T q fused -> beta ; p = z + beta p, p^T r ; q = A p, alpha.
+    // The final x += alpha p is formed by the consumer (the prolongation gathers x + alpha p).
+    const DotSink s2{D.kst, FIN_KBETA};
+    const VecOf kq = [l](RankState& R) { return R.lv[l].kq; };
+    enqueue_level(h, L, l, kr, &kmb, kz, true, &kq, &s2);
     L.begin("kfcg_pupd", 4 * n8);
     launch_k(k_kpupd, vec_grid(n, nsm), kBlock, L.s, D.kp, D.kz, D.kr, n, (const double*)D.kst, kred(FIN_KPR));
     L.end();
     launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(FIN_KALPHA), "kfcg_spmv", 2 * n8);
-    L.begin("kfcg_upd2", 3 * n8);
-    launch_k(k_kupd2, vec_grid(n, nsm), kBlock, L.s, D.kx, D.kp, n, (const double*)D.kst);
-    L.end();
 }
 
 // z0 = B b0 on the level-0 windows (the whole cycle).

@@ -252,6 +252,18 @@ __device__ __forceinline__ void bind(GPz& g) {
     g.pold = (it & 1) ? g.p1 : g.p0;
 }
 
+// e_j = x_j + alpha p_j: the K-cycle inner FCG's final update, formed where its
+// result is consumed (the prolongation); alpha = k[2] of the level's K state
+struct GXap {
+    static constexpr int kChunk = 4;
+    const double* __restrict__ x;
+    const double* __restrict__ p;
+    const double* k;
+    double alpha = 0.0;
+    __device__ __forceinline__ double operator()(int32_t j) const { return __ldg(x + j) + alpha * __ldg(p + j); }
+};
+__device__ __forceinline__ void bind(GXap& g) { g.alpha = g.k[2]; }
+
 // ------------------------------------------------------------- epilogues
 // An epilogue with `kAbs = true` also receives asum = sum_k |a_ik| of the row it
 // streams, i.e. the l1-Jacobi diagonal 1/m_i (nb = 1), so m_i is

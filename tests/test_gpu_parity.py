@@ -244,3 +244,22 @@ def test_full_c3_anisotropic_properties(ctx):
                                   size=(A.n_global, A.n_global)).cuda()
     res = bt - (Asp @ xs.unsqueeze(1)).squeeze(1)
     assert (torch.linalg.norm(res) / torch.linalg.norm(bt)).item() <= 1.5e-6
+
+
+def test_full_c4_hierarchy_and_vcycle_vs_oracle(ctx):
+    """BASELINE config 4 at full size (256^3) exactly as bench.py builds it (GPU setup,
+    default config): every level's aggregate map equals the oracle's bit for bit and one
+    V-cycle on a seeded vector agrees with the oracle's to 1e-12 (the oracle runs the
+    full-size V-cycle once, single-threaded)."""
+    amg = _amg()
+    A, b, meta = config_problem(4)
+    h = amg.Hierarchy(ctx, A)
+    ho = O.OracleHierarchy(A)
+    assert h.sizes() == ho.sizes()
+    for l in range(h.nlevels - 1):
+        assert np.array_equal(h.level_aggregates(l), ho.agg(l)), f"level {l}"
+    r = uniform_pm1(1004, A.n_global)
+    z = h.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    zo = ho.vcycle(r)
+    rel = np.linalg.norm(z - zo) / np.linalg.norm(zo)
+    assert rel <= VCYCLE_TOL, rel
