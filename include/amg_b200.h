@@ -92,8 +92,11 @@ typedef struct {
     int32_t setup_device;         /* 1 = build the hierarchy on the context's GPU (default; SURVEY.md
                                      §8f NEXT-1: suitor matching, expand-sort-compress canonical
                                      SpGEMM), bit-identical to 0 = the host build (C++/OpenMP).
-                                     amg_host_hierarchy_build honours it (current CUDA device) when
-                                     a cfg is passed and builds on the host when cfg is NULL. */
+                                     When the device build's working set (~40 B per stored entry of
+                                     A, x8) exceeds 70% of the free device memory the host build is
+                                     used instead (same result).  amg_host_hierarchy_build honours it
+                                     (current CUDA device) when a cfg is passed and builds on the
+                                     host when cfg is NULL. */
     int64_t tail_rows;            /* single-process contexts with a direct coarsest solve: the cycle
                                      rooted at the first level l >= 1 with n_l <= tail_rows runs as
                                      ONE cooperative persistent kernel (grid barriers between its

@@ -79,6 +79,10 @@ struct DevMat {
     int32_t* rp = nullptr;     // CSR
     int32_t* col = nullptr;
     double* val = nullptr;
+    // multi-rank overlap: launch units (slices for SELL/SDIA, rows for CSR) and the largest
+    // contiguous block of units whose gathers touch only owned columns ("interior": it can
+    // run while the halo is in flight); the rest ("head" / "tail") runs after the exchange
+    int64_t units = 0, ib0 = 0, ib1 = 0;
     // algorithmic bytes of one pass over the operator: 12 nnz + 4 (n+1)
     double model_bytes() const { return 12.0 * (double)nnz + 4.0 * (double)(nrows + 1); }
     // bytes the chosen device format actually stores for one pass
@@ -252,6 +256,10 @@ struct amg_hier_s {
     const double* apply_r = nullptr;
     double* apply_z = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // multi-rank: halo exchanges run on `comm` while the interior rows compute on the
+    // context stream (fork/join events)
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<KernelRec>* prof = nullptr;
     // persistent deep-level tail (single rank): first tail level, the compiled
     // program (device), its cooperative grid and reduction scratch
@@ -274,6 +282,9 @@ struct amg_hier_s {
         cudaFreeHost(st_host);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (comm) cudaStreamDestroy(comm);
     }
 };
 
@@ -331,26 +342,40 @@ struct Launch {
 };
 
 template <class G, class E>
-void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* name, double vec_bytes) {
+void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* name, double vec_bytes,
+                int part = 0) {
+    // part 0: all rows; 1: the interior units; 2: units before them; 3: units after them
+    const int64_t units = (M.fmt == FMT_SDIA || M.fmt == FMT_SELL) ? (M.nrows + 31) / 32 : M.nrows;
+    int64_t u0 = 0, u1 = units;
+    if (part == 1) {
+        u0 = M.ib0;
+        u1 = M.ib1;
+    } else if (part == 2) {
+        u1 = M.ib0;
+    } else if (part == 3) {
+        u0 = M.ib1;
+    }
+    if (part != 0 && u1 <= u0) return;
     const int nsm = L.h->ctx->nsm;
-    L.begin(name, M.model_bytes() + vec_bytes, M.stored_bytes() + vec_bytes);
+    const double frac = units ? (double)(u1 - u0) / (double)units : 1.0;
+    L.begin(name, frac * (M.model_bytes() + vec_bytes), frac * (M.stored_bytes() + vec_bytes));
     if (M.fmt == FMT_SDIA) {
         static const int cap = max_grid((const void*)k_sdia<G, E>, nsm);
-        const int64_t need = (M.nrows + kBlock - 1) / kBlock;
+        const int64_t need = ((u1 - u0) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
         launch_k(k_sdia<G, E>, grid, kBlock, L.s,
-                 SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor}, g, e, rc);
+                 SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor, u0, u1}, g, e, rc);
     } else if (M.fmt == FMT_SELL) {
         static const int cap = max_grid((const void*)k_sell<G, E>, nsm);
-        const int64_t need = (M.nrows + kBlock - 1) / kBlock;
+        const int64_t need = ((u1 - u0) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows}, g, e, rc);
+        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1}, g, e, rc);
     } else {
-        const CsrView v{M.rp, M.col, M.val, M.nrows};
-        const int64_t need = (M.nrows * M.vw + kBlock - 1) / kBlock;
+        const CsrView v{M.rp, M.col, M.val, M.nrows, u0, u1};
+        const int64_t need = ((u1 - u0) * M.vw + kBlock - 1) / kBlock;
         if (M.vw == kVWBlock) {
             static const int cap = max_grid((const void*)k_csrb<G, E>, nsm);
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(M.nrows, cap));
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(u1 - u0, cap));
             launch_k(k_csrb<G, E>, grid, kBlock, L.s, v, g, e, rc);
             L.end();
             return;
@@ -379,9 +404,13 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
 RedCtx no_red() { return RedCtx{nullptr, nullptr, nullptr, nullptr, 0ull, FIN_NONE, nullptr}; }
 
 // Dot epilogue context: fused finisher on one rank; local total (deferred) on many.
-RedCtx dot_red(amg_hier_s* h, RankState& R, int kind, unsigned long long cond) {
+// Multi-rank: three local slots (a kernel split into interior / head / tail parts writes
+// one slot per part); dot_finish sums all slots of all ranks in a fixed order.
+constexpr int kDotSlots = 3;
+int part_slot(int part) { return part <= 1 ? 0 : part - 1; }
+RedCtx dot_red(amg_hier_s* h, RankState& R, int kind, unsigned long long cond, int part = 0) {
     if (!h->multi()) return RedCtx{R.partials, R.ticket, nullptr, R.st, cond, kind, nullptr};
-    return RedCtx{R.partials, R.ticket, R.dot_local, nullptr, 0ull, FIN_NONE, nullptr};
+    return RedCtx{R.partials, R.ticket, R.dot_local + part_slot(part), nullptr, 0ull, FIN_NONE, nullptr};
 }
 
 // ------------------------------------------------------------- communication
@@ -391,22 +420,57 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind) {
     if (h->loopback) {
         for (auto& Rd : h->ranks)
             for (auto& Rs : h->ranks)
-                cudaMemcpyAsync(Rd.dot_all + Rs.rank, Rs.dot_local, sizeof(double), cudaMemcpyDeviceToDevice, L.s);
+                cudaMemcpyAsync(Rd.dot_all + kDotSlots * Rs.rank, Rs.dot_local, kDotSlots * sizeof(double),
+                                cudaMemcpyDeviceToDevice, L.s);
     } else {
         RankState& R = h->ranks[0];
-        ncclAllGather(R.dot_local, R.dot_all, 1, ncclDouble, h->ctx->nccl, L.s);
+        ncclAllGather(R.dot_local, R.dot_all, kDotSlots, ncclDouble, h->ctx->nccl, L.s);
     }
     for (auto& R : h->ranks) {
         RedCtx rc{nullptr, nullptr, nullptr, R.st, 0ull, kind, nullptr};
-        launch_k(k_finish, 1, 32, L.s, R.dot_all, h->np, rc);
+        launch_k(k_finish, 1, 32, L.s, R.dot_all, kDotSlots * h->np, rc);
+        cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);  // slots of skipped parts stay 0
     }
 }
 
 using VecOf = std::function<double*(RankState&)>;
 
-// Halo exchange of a level-l vector (window base pointer given per rank).
-void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) {
+// Halo exchange of a level-l vector (window base pointer given per rank) on stream `st`.
+void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec);
+void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) { exchange_on(h, L.s, l, vec); }
+
+// Overlapped exchange: fork the comm stream off the context stream, exchange there,
+// and let the caller launch the interior rows before exchange_end joins the streams.
+void exchange_begin(amg_hier_s* h, Launch& L, int l, const VecOf& vec) {
+    cudaEventRecord(h->ev_fork, L.s);
+    cudaStreamWaitEvent(h->comm, h->ev_fork, 0);
+    exchange_on(h, h->comm, l, vec);
+    cudaEventRecord(h->ev_join, h->comm);
+}
+void exchange_end(amg_hier_s* h, Launch& L) { cudaStreamWaitEvent(L.s, h->ev_join, 0); }
+
+// An operator application that gathers a level-lx vector xv: single rank / replicated:
+// one launch (part 0).  Distributed: exchange the halo on the comm stream while the
+// interior units (no halo columns) run, then the head and tail units (north_star (4):
+// "halo exchange ... overlapped with interior SpMV").
+using PartFn = std::function<void(RankState&, int)>;
+void overlapped(amg_hier_s* h, Launch& L, int lx, const VecOf& xv, bool dist, const PartFn& fn) {
+    if (!h->multi() || !dist) {
+        for (auto& R : h->ranks) fn(R, 0);
+        return;
+    }
+    exchange_begin(h, L, lx, xv);
+    for (auto& R : h->ranks) fn(R, 1);
+    exchange_end(h, L);
+    for (auto& R : h->ranks) {
+        fn(R, 2);
+        fn(R, 3);
+    }
+}
+
+void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec) {
     if (!h->multi()) return;
+    struct { cudaStream_t s; } L{st};
     const int nsm = h->ctx->nsm;
     bool any = false;
     for (auto& R : h->ranks) any |= (R.lv[l].ex.nsend > 0 || R.lv[l].ex.nrecv > 0);
@@ -433,8 +497,8 @@ void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) {
         for (int q = 0; q < h->np; ++q) {
             const int64_t ns = E.send_off[q + 1] - E.send_off[q];
             const int64_t nr = E.recv_off[q + 1] - E.recv_off[q];
-            if (ns) ncclSend(E.sbuf + E.send_off[q], ns, ncclDouble, q, h->ctx->nccl, L.s);
-            if (nr) ncclRecv(E.rbuf + E.recv_off[q], nr, ncclDouble, q, h->ctx->nccl, L.s);
+            if (ns) ncclSend(E.sbuf + E.send_off[q], ns, ncclDouble, q, h->ctx->nccl, st);
+            if (nr) ncclRecv(E.rbuf + E.recv_off[q], nr, ncclDouble, q, h->ctx->nccl, st);
         }
         ncclGroupEnd();
     }
@@ -795,55 +859,56 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     const bool am = (s1 == 1);
     if (am) mbvec = nullptr;
     // ---- down: pre-smoothing, residual, restriction
-    if (dist) exchange(h, L, l, mbvec ? *mbvec : bvec);
-    for (int ri = 0; ri < nr; ++ri) {
-        RankState& R = h->ranks[ri];
+    overlapped(h, L, l, mbvec ? *mbvec : bvec, dist, [&](RankState& R, int part) {
+        const int ri = ri_of(R);
         DevLevel& D = R.lv[l];
         const double* b = bvec(R);
         const double* be = b + D.ep_off;
         const double n8 = 8.0 * (double)D.comp_n;
         if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b) = b - (A diag(m)) b
-            launch_mat(L, D.Am, GVec{b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 2 * n8);
+            launch_mat(L, D.Am, GVec{b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 2 * n8, part);
         } else {  // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
             if (!mbvec)
-                launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
+                launch_mat(L, D.A, GMB{D.m, b}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8, part);
             else
-                launch_mat(L, D.A, GVec{(*mbvec)(R)}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8);
+                launch_mat(L, D.A, GVec{(*mbvec)(R)}, ESweep0{be, D.xa + D.ep_off}, no_red(), "sweep0", 3 * n8,
+                           part);
             xpre[ri] = D.xa;
         }
-    }
+    });
     if (s1 >= 2) {
         for (int s = 2; s < s1; ++s) {
-            if (dist) exchange(h, L, l, [&](RankState& R) { return xpre[ri_of(R)]; });
+            std::vector<double*> xnext(nr);
             for (int ri = 0; ri < nr; ++ri) {
-                RankState& R = h->ranks[ri];
+                DevLevel& D = h->ranks[ri].lv[l];
+                xnext[ri] = (xpre[ri] == D.xa) ? D.xb : D.xa;
+            }
+            overlapped(h, L, l, [&](RankState& R) { return xpre[ri_of(R)]; }, dist, [&](RankState& R, int part) {
+                const int ri = ri_of(R);
                 DevLevel& D = R.lv[l];
                 double* xi = xpre[ri];
-                double* xo = (xi == D.xa) ? D.xb : D.xa;
+                double* xo = xnext[ri];
                 launch_mat(L, D.A, GVec{xi}, ESweep<false>{xi + D.ep_off, bvec(R) + D.ep_off, xo + D.ep_off},
-                           no_red(), "presweep", 3 * 8.0 * (double)D.comp_n);
-                xpre[ri] = xo;
-            }
+                           no_red(), "presweep", 3 * 8.0 * (double)D.comp_n, part);
+            });
+            xpre = xnext;
         }
-        if (dist) exchange(h, L, l, [&](RankState& R) { return xpre[ri_of(R)]; });
-        for (int ri = 0; ri < nr; ++ri) {
-            RankState& R = h->ranks[ri];
+        overlapped(h, L, l, [&](RankState& R) { return xpre[ri_of(R)]; }, dist, [&](RankState& R, int part) {
             DevLevel& D = R.lv[l];
-            launch_mat(L, D.A, GVec{xpre[ri]}, EResid{bvec(R) + D.ep_off, D.r + D.ep_off}, no_red(), "resid",
-                       3 * 8.0 * (double)D.comp_n);
-        }
+            launch_mat(L, D.A, GVec{xpre[ri_of(R)]}, EResid{bvec(R) + D.ep_off, D.r + D.ep_off}, no_red(), "resid",
+                       3 * 8.0 * (double)D.comp_n, part);
+        });
     }
-    if (dist) exchange(h, L, l, [&](RankState& R) { return R.lv[l].r; });
-    for (auto& R : h->ranks) {
+    overlapped(h, L, l, [l](RankState& R) { return R.lv[l].r; }, dist, [&](RankState& R, int part) {
         DevLevel& D = R.lv[l];
         DevLevel& C = R.lv[l + 1];
         if (!C.coarsest && !am)
             launch_mat(L, D.R, GVec{D.r}, EStoreMB{C.b + D.rst_off, C.m + D.rst_off, C.mb + D.rst_off}, no_red(),
-                       "restrict", 8.0 * (double)D.comp_n + 24.0 * (double)D.rst_n);
+                       "restrict", 8.0 * (double)D.comp_n + 24.0 * (double)D.rst_n, part);
         else
             launch_mat(L, D.R, GVec{D.r}, EStore{C.b + D.rst_off}, no_red(), "restrict",
-                       8.0 * (double)D.comp_n + 8.0 * (double)D.rst_n);
-    }
+                       8.0 * (double)D.comp_n + 8.0 * (double)D.rst_n, part);
+    });
     if (h->ranks[0].lv[l + 1].replicated && dist) {  // first replicated level: gather the rhs
         exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].b; });
         if (!h->ranks[0].lv[l + 1].coarsest && !am)
@@ -859,43 +924,47 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     else if (kfcg) enqueue_fcg2(h, L, l + 1);
     else enqueue_level(h, L, l + 1, cb, &cmb, ev, false, nullptr);
     // ---- up: prolongation, post-smoothing
-    if (!h->ranks[0].lv[l + 1].replicated) exchange(h, L, l + 1, ev);
     std::vector<double*> cur(nr), fin(nr), tmp(nr);
     for (int ri = 0; ri < nr; ++ri) {
         RankState& R = h->ranks[ri];
         DevLevel& D = R.lv[l];
-        const double* e = ev(R);
-        const double nc8 = 8.0 * (double)R.lv[l + 1].comp_n;
         fin[ri] = outv(R);  // the level's result (read by level l-1)
         tmp[ri] = D.xb;     // the prolongation update is row-local: may run in place
-        double* dst = (s2 % 2 == 1) ? tmp[ri] : fin[ri];
-        const double n8 = 8.0 * (double)D.comp_n;
+        cur[ri] = (s2 % 2 == 1) ? tmp[ri] : fin[ri];
+    }
+    overlapped(h, L, l + 1, ev, !h->ranks[0].lv[l + 1].replicated, [&](RankState& R, int part) {
+        const int ri = ri_of(R);
+        DevLevel& D = R.lv[l];
         DevLevel& C = R.lv[l + 1];
+        const double* e = ev(R);
+        const double nc8 = 8.0 * (double)C.comp_n;
+        double* dst = cur[ri];
+        const double n8 = 8.0 * (double)D.comp_n;
         if (s1 == 1) {  // u = P-bar e only; the first post-sweep adds m o b (EPost1)
             if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
                 launch_mat(L, D.P, GXap{C.kx, C.kp, C.kst}, EStore{dst + D.ep_off}, no_red(), "prolong",
-                           n8 + 2 * nc8);
+                           n8 + 2 * nc8, part);
             else
-                launch_mat(L, D.P, GVec{e}, EStore{dst + D.ep_off}, no_red(), "prolong", n8 + nc8);
+                launch_mat(L, D.P, GVec{e}, EStore{dst + D.ep_off}, no_red(), "prolong", n8 + nc8, part);
         } else {
             if (kfcg)
                 launch_mat(L, D.P, GXap{C.kx, C.kp, C.kst}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off},
-                           no_red(), "prolong", 2 * n8 + 2 * nc8);
+                           no_red(), "prolong", 2 * n8 + 2 * nc8, part);
             else
                 launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off}, no_red(), "prolong",
-                           2 * n8 + nc8);
+                           2 * n8 + nc8, part);
         }
-        cur[ri] = dst;
-    }
+    });
     for (int s = 0; s < s2; ++s) {
         const bool last = (s == s2 - 1);
-        if (dist) exchange(h, L, l, [&](RankState& R) { return cur[ri_of(R)]; });
-        for (int ri = 0; ri < nr; ++ri) {
-            RankState& R = h->ranks[ri];
+        std::vector<double*> nxt(nr);
+        for (int ri = 0; ri < nr; ++ri) nxt[ri] = (cur[ri] == tmp[ri]) ? fin[ri] : tmp[ri];
+        overlapped(h, L, l, [&](RankState& R) { return cur[ri_of(R)]; }, dist, [&](RankState& R, int part) {
+            const int ri = ri_of(R);
             DevLevel& D = R.lv[l];
             const double* b = bvec(R);
             double* xi = cur[ri];
-            double* xo = (xi == tmp[ri]) ? fin[ri] : tmp[ri];
+            double* xo = nxt[ri];
             const double n8 = 8.0 * (double)D.comp_n;
             const bool dt = (dot && last);
             const double* dw = (dt && dwv) ? (*dwv)(R) + D.ep_off : nullptr;
@@ -903,47 +972,48 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
             const double mb8 = abs ? 0.0 : n8;
             double* m = D.m + D.ep_off;
+            auto red = [&]() { return sink ? sink_red(h, R, dkind, sink) : dot_red(h, R, dkind, 0, part); };
             if (s == 0 && s1 == 1) {
                 const double* bo = !mbvec ? b + D.ep_off : (*mbvec)(R) + D.ep_off;
                 const double* rr = D.r + D.ep_off;
                 double* uu = xi + D.ep_off;
                 double* xx = xo + D.ep_off;
                 if (dt && abs)
-                    launch_mat(L, D.A, GVec{xi}, EPost1<true, false, true>{uu, rr, bo, xx, nullptr, dw},
-                               sink_red(h, R, dkind, sink), "postsweep_dot", 4 * n8);
+                    launch_mat(L, D.A, GVec{xi}, EPost1<true, false, true>{uu, rr, bo, xx, nullptr, dw}, red(),
+                               "postsweep_dot", 4 * n8, part);
                 else if (dt)
-                    launch_mat(L, D.A, GVec{xi}, EPost1<true, false, false>{uu, rr, bo, xx, m, dw},
-                               sink_red(h, R, dkind, sink), "postsweep_dot", 5 * n8);
+                    launch_mat(L, D.A, GVec{xi}, EPost1<true, false, false>{uu, rr, bo, xx, m, dw}, red(),
+                               "postsweep_dot", 5 * n8, part);
                 else if (!mbvec && abs)
                     launch_mat(L, D.A, GVec{xi}, EPost1<false, false, true>{uu, rr, bo, xx}, no_red(), "postsweep",
-                               4 * n8);
+                               4 * n8, part);
                 else if (!mbvec)
                     launch_mat(L, D.A, GVec{xi}, EPost1<false, false, false>{uu, rr, bo, xx, m}, no_red(),
-                               "postsweep", 5 * n8);
+                               "postsweep", 5 * n8, part);
                 else if (abs)
                     launch_mat(L, D.A, GVec{xi}, EPost1<false, true, true>{uu, rr, bo, xx}, no_red(), "postsweep",
-                               4 * n8);
+                               4 * n8, part);
                 else
                     launch_mat(L, D.A, GVec{xi}, EPost1<false, true, false>{uu, rr, bo, xx, m}, no_red(),
-                               "postsweep", 5 * n8);
+                               "postsweep", 5 * n8, part);
             } else if (dt) {
                 if (abs)
                     launch_mat(L, D.A, GVec{xi},
-                               ESweep<true, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, nullptr, dw},
-                               sink_red(h, R, dkind, sink), "postsweep_dot", 3 * n8);
+                               ESweep<true, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, nullptr, dw}, red(),
+                               "postsweep_dot", 3 * n8, part);
                 else
                     launch_mat(L, D.A, GVec{xi}, ESweep<true, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m, dw},
-                               sink_red(h, R, dkind, sink), "postsweep_dot", 3 * n8 + mb8);
+                               red(), "postsweep_dot", 3 * n8 + mb8, part);
             } else {
                 if (abs)
                     launch_mat(L, D.A, GVec{xi}, ESweep<false, true>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off},
-                               no_red(), "postsweep", 3 * n8);
+                               no_red(), "postsweep", 3 * n8, part);
                 else
                     launch_mat(L, D.A, GVec{xi}, ESweep<false, false>{xi + D.ep_off, b + D.ep_off, xo + D.ep_off, m},
-                               no_red(), "postsweep", 3 * n8 + mb8);
+                               no_red(), "postsweep", 3 * n8 + mb8, part);
             }
-            cur[ri] = xo;
-        }
+        });
+        cur = nxt;
     }
     if (dot && !sink) dot_finish(h, L, dkind);
 }
@@ -1025,13 +1095,12 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
             L.end();
         }
         if (fcg) dot_finish(h, L, FIN_PR);
-        exchange(h, L, 0, [](RankState& R) { return R.pp; });
         const int pqk = fcg ? FIN_PQF : FIN_PQ;
-        for (auto& R : h->ranks) {
+        overlapped(h, L, 0, [](RankState& R) { return R.pp; }, true, [&](RankState& R, int part) {
             const DevLevel& D = R.L0();
-            launch_mat(L, D.A, GVec{R.pp}, ESpmvDot{R.pp + D.own_off, R.pq + D.own_off}, dot_red(h, R, pqk, 0),
-                       "spmv_dot", 16.0 * D.own_n);
-        }
+            launch_mat(L, D.A, GVec{R.pp}, ESpmvDot{R.pp + D.own_off, R.pq + D.own_off}, dot_red(h, R, pqk, 0, part),
+                       "spmv_dot", 16.0 * D.own_n, part);
+        });
         dot_finish(h, L, pqk);
     }
     for (auto& R : h->ranks) {
@@ -1088,7 +1157,27 @@ int dev_alloc(T** dst, size_t count) {
 // offsets, SELL-32 for short rows with little padding, CSR-vector (VW lanes per
 // row, or one block per row) otherwise.  `shift` maps local rows to the column
 // window frame (comp_begin - win_begin); `square` marks A_l.
-int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bool force_csr = false) {
+// Largest contiguous run of interior units (flag[u] = 1) -> [b0, b1)
+void interior_run(const std::vector<char>& flag, int64_t& b0, int64_t& b1) {
+    b0 = b1 = 0;
+    int64_t s = -1;
+    for (int64_t u = 0; u <= (int64_t)flag.size(); ++u) {
+        const bool in = u < (int64_t)flag.size() && flag[u];
+        if (in && s < 0) s = u;
+        if (!in && s >= 0) {
+            if (u - s > b1 - b0) {
+                b0 = s;
+                b1 = u;
+            }
+            s = -1;
+        }
+    }
+}
+
+// own_lo/own_hi: columns (window frame) owned by this rank for the gathered vector;
+// own_lo < 0: no split (single rank, replicated levels)
+int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bool force_csr = false,
+               int64_t own_lo = -1, int64_t own_hi = -1) {
     const int64_t n = M.nrows, nnz = M.nnz();
     D.nrows = n;
     D.ncols = M.ncols;
@@ -1157,11 +1246,37 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bo
                     }
                 }
             }
+            D.units = nsl;
+            if (own_lo >= 0) {  // a slice is interior when every lane's gathers (all slice offsets) are owned
+                std::vector<char> fl(nsl, 0);
+#pragma omp parallel for schedule(static)
+                for (int64_t s2 = 0; s2 < nsl; ++s2) {
+                    bool ok2 = true;
+                    for (int64_t r = s2 * 32; ok2 && r < std::min(n, s2 * 32 + 32); ++r)
+                        for (uint32_t k = sptr[s2]; ok2 && k < sptr[s2 + 1]; ++k) {
+                            const int64_t c = std::min<int64_t>(std::max<int64_t>(base(r) + offs[k], 0), M.ncols - 1);
+                            ok2 = (c >= own_lo && c < own_hi);
+                        }
+                    fl[s2] = ok2;
+                }
+                interior_run(fl, D.ib0, D.ib1);
+            }
             int st;
             if ((st = dev_copy(&D.sptr, sptr.data(), sptr.size()))) return st;
             if ((st = dev_copy(&D.offs, offs.data(), offs.size()))) return st;
             if ((st = dev_copy(&D.val, val.data(), val.size()))) return st;
             return AMG_OK;
+        }
+    }
+    // CSR rows (SELL pads with the row's own last column): row interior when all columns owned
+    std::vector<char> rowin;
+    if (own_lo >= 0) {
+        rowin.assign(n, 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t r = 0; r < n; ++r) {
+            bool ok2 = true;
+            for (int64_t k = M.rp[r]; ok2 && k < M.rp[r + 1]; ++k) ok2 = (M.ci[k] >= own_lo && M.ci[k] < own_hi);
+            rowin[r] = ok2;
         }
     }
     // SELL-32 (one thread per row, coalesced column-major slices) needs little padding and
@@ -1189,6 +1304,13 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bo
                 for (; k < width[s]; ++k) col[base + k * 32 + lane] = last;
             }
         }
+        D.units = nsl;
+        if (own_lo >= 0) {
+            std::vector<char> fl(nsl, 1);
+            for (int64_t r = 0; r < n; ++r)
+                if (!rowin[r]) fl[r / 32] = 0;
+            interior_run(fl, D.ib0, D.ib1);
+        }
         int st;
         if ((st = dev_copy(&D.sptr, sptr.data(), sptr.size()))) return st;
         if ((st = dev_copy(&D.col, col.data(), col.size()))) return st;
@@ -1208,6 +1330,8 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bo
     while (vw < 32 && (vw < want || vw * 8 < mean) && vw * 2 <= std::max(2.0, mean)) vw *= 2;
     if (mean >= 256.0 && (double)n < 18944.0) vw = kVWBlock;
     D.vw = vw;
+    D.units = n;
+    if (own_lo >= 0) interior_run(rowin, D.ib0, D.ib1);
     std::vector<int32_t> rp(n + 1);
     for (int64_t i = 0; i <= n; ++i) rp[i] = (int32_t)M.rp[i];
     int st;
@@ -1317,7 +1441,17 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
             D.rst_n = S.rst_end - S.rst_begin;
             D.rst_off = S.rst_begin - P.lv[l + 1].win_begin;
             const bool tcsr = h->tail_level >= 0 && l >= h->tail_level;  // tail levels: CSR for k_tail
-            if ((st = upload_mat(S.A, D.A, true, D.ep_off, tcsr))) return st;
+            // multi-rank overlap: owned window columns of the vectors the operators gather
+            int64_t lo = -1, hi = -1, clo = -1, chi = -1;
+            if (h->multi() && !S.replicated) {
+                lo = S.own_begin - S.win_begin;
+                hi = S.own_end - S.win_begin;
+            }
+            if (h->multi() && !P.lv[l + 1].replicated) {
+                clo = P.lv[l + 1].own_begin - P.lv[l + 1].win_begin;
+                chi = P.lv[l + 1].own_end - P.lv[l + 1].win_begin;
+            }
+            if ((st = upload_mat(S.A, D.A, true, D.ep_off, tcsr, lo, hi))) return st;
             if (h->cfg.smoother == 1) {
                 if ((st = upload_mat(S.Wd, D.Wd, true, D.ep_off))) return st;
                 if ((st = upload_mat(S.Z, D.Z, true, D.ep_off))) return st;
@@ -1326,10 +1460,10 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
 #pragma omp parallel for schedule(static)
                 for (int64_t i = 0; i < As.nrows; ++i)
                     for (int64_t k = As.rp[i]; k < As.rp[i + 1]; ++k) As.v[k] = As.v[k] * S.m[As.ci[k]];
-                if ((st = upload_mat(As, D.Am, true, D.ep_off, tcsr))) return st;
+                if ((st = upload_mat(As, D.Am, true, D.ep_off, tcsr, lo, hi))) return st;
             }
-            if ((st = upload_mat(S.P, D.P, false, 0, tcsr))) return st;
-            if ((st = upload_mat(S.R, D.R, false, 0, tcsr))) return st;
+            if ((st = upload_mat(S.P, D.P, false, 0, tcsr, clo, chi))) return st;
+            if ((st = upload_mat(S.R, D.R, false, 0, tcsr, lo, hi))) return st;
             if ((st = dev_copy(&D.m, S.m.data(), S.m.size()))) return st;
             if ((st = dev_alloc(&D.mb, wn))) return st;
             if ((st = dev_alloc(&D.r, wn))) return st;
@@ -1368,8 +1502,8 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
     if ((st = dev_alloc(&R.st, 1))) return st;
     if ((st = dev_alloc(&R.partials, kMaxPartials))) return st;
     if ((st = dev_alloc(&R.ticket, 1))) return st;
-    if ((st = dev_alloc(&R.dot_local, 1))) return st;
-    if ((st = dev_alloc(&R.dot_all, (size_t)h->np))) return st;
+    if ((st = dev_alloc(&R.dot_local, kDotSlots))) return st;
+    if ((st = dev_alloc(&R.dot_all, (size_t)kDotSlots * h->np))) return st;
     if (nl == 1) {  // single-level: level 0 is the coarsest; give it an operator for q = A p
         if ((st = upload_mat(P.lv[0].A, R.lv[0].A, true, 0))) return st;
     }
@@ -1562,6 +1696,16 @@ int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const do
     sc.post_sweeps = cfg.post_sweeps;
     sc.threads = cfg.setup_threads;
     sc.device = cfg.setup_device;
+    if (sc.device) {
+        // capacity: the expand-sort-compress products of the level-0 Galerkin step
+        // (~nnz(A) x 8 entries of P-bar per row, key + value, double-buffered sort) must fit
+        // in the free device memory; otherwise the (bit-identical) host build is used
+        size_t freeb = 0, totalb = 0;
+        if (cudaMemGetInfo(&freeb, &totalb) == cudaSuccess) {
+            const double need = 32.0 * 8.0 * (double)nnz + 64.0 * (double)nnz;
+            if (need > 0.7 * (double)freeb) sc.device = 0;
+        }
+    }
     std::string err;
     const int sst = amgsetup::build(std::move(A), std::move(wv), sc, H, err);
     if (sst != amgsetup::SETUP_OK) {
@@ -2055,6 +2199,11 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     }
     cudaEventCreate(&h->ev0);
     cudaEventCreate(&h->ev1);
+    if (h->multi()) {
+        CK(cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    }
     CK(cudaDeviceSynchronize());
     h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h;

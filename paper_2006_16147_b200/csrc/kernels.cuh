@@ -473,6 +473,7 @@ struct SellView {
     const int32_t* __restrict__ col;
     const double* __restrict__ val;
     int64_t n;
+    int64_t s0, s1;                     // slice range of this launch (multi-rank interior/boundary split)
 };
 
 // Row-chunk of exactly W entries of one slice (lane = row): the W value loads are
@@ -528,12 +529,11 @@ __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx
     pdl_begin();
     bind(g);
     bind(e);
-    const int64_t nslices = (A.n + 31) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
     double d = 0.0;
-    for (int64_t s = w0; s < nslices; s += nw) {
+    for (int64_t s = A.s0 + w0; s < A.s1; s += nw) {
         const uint32_t b0 = __ldg(A.sptr + s);
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
         const int32_t* c = A.col + (int64_t)b0 * 32 + lane;
@@ -560,6 +560,7 @@ struct SdiaView {
     int32_t ncols;
     int32_t shift;  // row -> column frame: col = row + shift + offset (multi-rank windows)
     const int32_t* __restrict__ anchor;  // rectangular operators: col = anchor[row] + offset
+    int64_t s0, s1;                      // slice range of this launch
 };
 
 template <class G, class E>
@@ -567,12 +568,11 @@ __global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx
     pdl_begin();
     bind(g);
     bind(e);
-    const int64_t nslices = (A.n + 31) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
     double d = 0.0;
-    for (int64_t s = w0; s < nslices; s += nw) {
+    for (int64_t s = A.s0 + w0; s < A.s1; s += nw) {
         const uint32_t b0 = __ldg(A.sptr + s);
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
         const int64_t row = (s << 5) + lane;
@@ -596,6 +596,7 @@ struct CsrView {
     const int32_t* __restrict__ ci;
     const double* __restrict__ v;
     int64_t n;
+    int64_t r0 = 0, r1 = 0;  // row range of this launch (k_csrv / k_csrb)
 };
 
 // One lane's share of a CSR row: entries k, k+S, k+2S, ... < k1 (S lanes per row),
@@ -637,11 +638,11 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
     const int64_t ng = ((int64_t)gridDim.x * kBlock) / VW;
     double d = 0.0;
     // every lane of a warp runs the same number of outer iterations (shuffles)
-    const int64_t iters = (A.n + ng - 1) / ng;
+    const int64_t iters = (A.r1 - A.r0 + ng - 1) / ng;
     for (int64_t it = 0; it < iters; ++it) {
-        const int64_t row = g0 + it * ng;
+        const int64_t row = A.r0 + g0 + it * ng;
         double acc = 0.0, asum = 0.0;
-        if (row < A.n) {
+        if (row < A.r1) {
             const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
             csr_lane_row<VW, E::kAbs>(A, k0 + sub, k1, g, acc, asum);
         }
@@ -650,7 +651,7 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
             acc += __shfl_xor_sync(0xffffffffu, acc, o, VW);
             if constexpr (E::kAbs) asum += __shfl_xor_sync(0xffffffffu, asum, o, VW);
         }
-        if (sub == 0 && row < A.n) d += apply_epi(e, row, acc, asum);
+        if (sub == 0 && row < A.r1) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
 }
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc)
     __shared__ double part[kBlock / 32], apart[kBlock / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double d = 0.0;
-    for (int64_t row = blockIdx.x; row < A.n; row += gridDim.x) {
+    for (int64_t row = A.r0 + blockIdx.x; row < A.r1; row += gridDim.x) {
         const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
         double acc = 0.0, asum = 0.0;
         csr_lane_row<kBlock, E::kAbs>(A, k0 + (int32_t)threadIdx.x, k1, g, acc, asum);

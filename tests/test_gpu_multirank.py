@@ -4,8 +4,10 @@ The hierarchy is partitioned into np row blocks exactly as across np GPUs; every
 rank's kernels run on its own window of each level, halos are packed, copied
 device-to-device (instead of NCCL send/recv) and unpacked, dot products are
 reduced per rank, all-gathered and summed in rank order, and the deep levels are
-replicated after a gather.  Same parity bars as the single-rank path against the
-CPU oracle.  (Ranks that wait on each other are never launched as concurrent
+replicated after a gather.  Every operator that gathers a distributed vector runs
+its interior rows (no halo columns) while the halo exchange is in flight on a second
+stream, then its boundary rows (north_star (4)).  Same parity bars as the single-rank
+path against the CPU oracle.  (Ranks that wait on each other are never launched as concurrent
 kernels on one GPU: the loopback transport is stream-ordered copies.)
 """
 import numpy as np
@@ -86,3 +88,22 @@ def test_too_small_for_ranks_is_an_error(ctx):
     A = poisson7(5, 4, 3)  # single-level hierarchy
     with pytest.raises(amg.AmgError):
         amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=2))
+
+
+def test_loopback_overlap_splits_operators_into_interior_and_boundary(ctx):
+    """With a z-slab partition every distributed operator launch is split: the interior
+    part (while the halo is exchanged) and the head/tail boundary parts after it, so the
+    level-0 residual appears as more than one launch per rank in a profiled V-cycle."""
+    import paper_2006_16147_b200 as amg
+    A, b, _ = config_problem(4, grid=(64, 64, 128))
+    h = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=2, replicate_below_bytes=0))
+    prof = h.profile_vcycle(1)
+    n_resid0 = sum(1 for k in prof if k["name"] == "resid0")
+    n_post = sum(1 for k in prof if k["name"].startswith("postsweep"))
+    # one launch per rank would give exactly 2 per level; the split gives interior + boundary
+    assert n_resid0 > 2 * (h.nlevels - 1) and n_post > 2 * (h.nlevels - 1), (n_resid0, n_post)
+    # and the split application equals the single-rank one to rounding
+    r = uniform_pm1(1500, A.n_global)
+    z = h.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    zs = amg.Hierarchy(ctx, A).precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    assert np.linalg.norm(z - zs) <= 1e-12 * np.linalg.norm(zs)
