@@ -1341,6 +1341,172 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bo
     return AMG_OK;
 }
 
+
+// ------------------------------------------------------------- device-side formats
+// Same decisions and layouts as upload_mat, computed on the device from a device CSR
+// (GPU-built hierarchies never leave the device: NEXT-1).
+__global__ void kc_slice_width(const int64_t* __restrict__ rp, int64_t n, int64_t nsl, uint32_t* width) {
+    for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nsl; sl += (int64_t)gridDim.x * blockDim.x) {
+        int64_t w = 0;
+        for (int64_t r = sl * 32; r < min(n, sl * 32 + 32); ++r) w = max(w, rp[r + 1] - rp[r]);
+        width[sl] = (uint32_t)w;
+    }
+}
+// warp per slice: the sorted union of the 32 rows' offsets col - base(row) by repeated
+// warp minima (rows are sorted, so each lane walks its row once); count or fill
+__global__ void kc_slice_offs(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              const double* __restrict__ v, int64_t n, int64_t nsl, int square, int64_t shift,
+                              uint32_t* dw, const uint32_t* __restrict__ sptr, int32_t* offs, double* val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t sl = w0; sl < nsl; sl += nw) {
+        const int64_t r = sl * 32 + lane;
+        int64_t p = 0, e = 0;
+        if (r < n) {
+            p = rp[r];
+            e = rp[r + 1];
+        }
+        const int64_t base = square ? r + shift : (p < e ? (int64_t)ci[p] : 0);
+        uint32_t k = 0;
+        const uint32_t b0 = sptr ? sptr[sl] : 0u;
+        for (;;) {
+            const int64_t cur = (p < e) ? (int64_t)ci[p] - base : INT64_MAX;
+            int64_t mn = cur;
+            for (int o = 16; o > 0; o >>= 1) mn = min(mn, (int64_t)__shfl_xor_sync(0xffffffffu, mn, o));
+            if (mn == INT64_MAX) break;
+            if (sptr) {
+                if (lane == 0) offs[b0 + k] = (int32_t)mn;
+                val[(int64_t)(b0 + k) * 32 + lane] = (cur == mn) ? v[p] : 0.0;
+            }
+            if (cur == mn) ++p;
+            ++k;
+        }
+        if (!sptr && lane == 0) dw[sl] = k;
+    }
+}
+__global__ void kc_anchor(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t n, int32_t* anc) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        anc[r] = rp[r + 1] > rp[r] ? ci[rp[r]] : 0;
+}
+__global__ void kc_sell_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                             const double* __restrict__ v, int64_t n, const uint32_t* __restrict__ sptr,
+                             const uint32_t* __restrict__ width, int32_t* col, double* val) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sl = r >> 5, lane = r & 31;
+        const int64_t base = (int64_t)sptr[sl] * 32;
+        int64_t k = 0;
+        int32_t last = 0;
+        for (int64_t t = rp[r]; t < rp[r + 1]; ++t, ++k) {
+            col[base + k * 32 + lane] = last = ci[t];
+            val[base + k * 32 + lane] = v[t];
+        }
+        for (; k < (int64_t)width[sl]; ++k) col[base + k * 32 + lane] = last;
+    }
+}
+__global__ void kc_rp32(const int64_t* __restrict__ rp, int64_t n, int32_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)rp[i];
+}
+__global__ void kc_scale_cols(const int32_t* __restrict__ ci, const double* __restrict__ v, int64_t nnz,
+                              const double* __restrict__ m, double* out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = v[k] * m[ci[k]];
+}
+
+int convert_mat(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t shift, bool force_csr, cudaStream_t s) {
+    const int64_t n = M.nrows, nnz = M.nnz;
+    D.nrows = n;
+    D.ncols = M.ncols;
+    D.nnz = nnz;
+    D.shift = (int32_t)shift;
+    const int64_t nsl = (n + 31) / 32;
+    const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((nsl * 32 + 255) / 256, 148 * 16));
+    uint32_t* dwidth = nullptr;
+    int st;
+    if ((st = dev_alloc(&dwidth, (size_t)nsl))) return st;
+    kc_slice_width<<<gs, 256, 0, s>>>(M.rp, n, nsl, dwidth);
+    std::vector<uint32_t> width(nsl);
+    CK(cudaMemcpyAsync(width.data(), dwidth, nsl * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int64_t padded = 0;
+    for (int64_t q = 0; q < nsl; ++q) padded += 32 * (int64_t)width[q];
+    const double mean = n ? (double)nnz / (double)n : 0.0;
+    if (!force_csr && nsl >= 148 * 16 && mean <= 64.0) {
+        uint32_t* ddw = nullptr;
+        if ((st = dev_alloc(&ddw, (size_t)nsl))) return st;
+        kc_slice_offs<<<gs, 256, 0, s>>>(M.rp, M.ci, M.v, n, nsl, square ? 1 : 0, shift, ddw, nullptr, nullptr,
+                                         nullptr);
+        std::vector<uint32_t> dw(nsl);
+        CK(cudaMemcpyAsync(dw.data(), ddw, nsl * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        cudaFree(ddw);
+        int64_t dpad = 0;
+        for (int64_t q = 0; q < nsl; ++q) dpad += 32 * (int64_t)dw[q];
+        const double sdia_bytes = 8.0 * (double)dpad + 4.0 * (double)dpad / 32.0 + (square ? 0.0 : 4.0 * (double)n);
+        const double sell_bytes = 12.0 * (double)padded;
+        const bool ok = square ? (double)dpad <= 1.02 * (double)padded + 64.0 : sdia_bytes <= 0.9 * sell_bytes;
+        if (ok && dpad / 32 < (int64_t)UINT32_MAX) {
+            D.fmt = FMT_SDIA;
+            D.stored = dpad;
+            std::vector<uint32_t> sptr(nsl + 1, 0);
+            for (int64_t q = 0; q < nsl; ++q) sptr[q + 1] = sptr[q] + dw[q];
+            if ((st = dev_copy(&D.sptr, sptr.data(), sptr.size()))) return st;
+            CK(cudaMalloc((void**)&D.offs, std::max<int64_t>(1, dpad / 32) * 4));
+            CK(cudaMalloc((void**)&D.val, std::max<int64_t>(1, dpad) * 8));
+            kc_slice_offs<<<gs, 256, 0, s>>>(M.rp, M.ci, M.v, n, nsl, square ? 1 : 0, shift, nullptr, D.sptr, D.offs,
+                                             D.val);
+            if (!square) {
+                CK(cudaMalloc((void**)&D.anchor, std::max<int64_t>(1, n) * 4));
+                kc_anchor<<<gs, 256, 0, s>>>(M.rp, M.ci, n, D.anchor);
+            }
+            CK(cudaStreamSynchronize(s));
+            cudaFree(dwidth);
+            D.units = nsl;
+            return AMG_OK;
+        }
+    }
+    const bool sell = !force_csr && (double)padded <= 1.10 * (double)nnz + 64.0 && nsl >= 148 * 16 &&
+                      padded / 32 < (int64_t)UINT32_MAX;
+    if (sell) {
+        D.fmt = FMT_SELL;
+        D.stored = padded;
+        std::vector<uint32_t> sptr(nsl + 1, 0);
+        for (int64_t q = 0; q < nsl; ++q) sptr[q + 1] = sptr[q] + width[q];
+        if ((st = dev_copy(&D.sptr, sptr.data(), sptr.size()))) return st;
+        if ((st = dev_alloc(&D.col, (size_t)std::max<int64_t>(1, padded)))) return st;
+        if ((st = dev_alloc(&D.val, (size_t)std::max<int64_t>(1, padded)))) return st;
+        kc_sell_fill<<<gs, 256, 0, s>>>(M.rp, M.ci, M.v, n, D.sptr, dwidth, D.col, D.val);
+        CK(cudaStreamSynchronize(s));
+        cudaFree(dwidth);
+        D.units = nsl;
+        return AMG_OK;
+    }
+    cudaFree(dwidth);
+    if (nnz >= (int64_t)INT32_MAX) {
+        set_err("operator too large for 32-bit CSR row pointers on one rank");
+        return AMG_ERR_ARG;
+    }
+    D.fmt = FMT_CSRV;
+    D.stored = nnz;
+    const double want = 148.0 * 2048.0 / (double)std::max<int64_t>(n, 1);
+    int vw = 2;
+    while (vw < 32 && (vw < want || vw * 8 < mean) && vw * 2 <= std::max(2.0, mean)) vw *= 2;
+    if (mean >= 256.0 && (double)n < 18944.0) vw = kVWBlock;
+    D.vw = vw;
+    D.units = n;
+    CK(cudaMalloc((void**)&D.rp, (n + 1) * 4));
+    kc_rp32<<<gs, 256, 0, s>>>(M.rp, n, D.rp);
+    CK(cudaMalloc((void**)&D.col, std::max<int64_t>(1, nnz) * 4));
+    CK(cudaMalloc((void**)&D.val, std::max<int64_t>(1, nnz) * 8));
+    if (nnz) {
+        CK(cudaMemcpyAsync(D.col, M.ci, nnz * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(D.val, M.v, nnz * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return AMG_OK;
+}
+
 // Coarse CG (cfg.coarse_solver == 1): CSR of the replicated A_L, its l1 diagonal,
 // and the cluster shape of k_coarse_cg.  CTAs: enough that each holds <= ~16k
 // entries (the SpMV is spread over 16 warps per CTA), more if the CTA's rows of
@@ -1419,7 +1585,8 @@ int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) 
 }
 
 // Uploads one rank's plan.  coarse_inv: the dense A_L^{-1}.
-int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<double>& coarse_inv, RankState& R) {
+int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<double>& coarse_inv, RankState& R,
+                const amgsetup::DeviceKeep* dk = nullptr) {
     const int nl = (int)P.lv.size();
     R.rank = P.rank;
     R.lv.resize(nl);
@@ -1451,23 +1618,43 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
                 clo = P.lv[l + 1].own_begin - P.lv[l + 1].win_begin;
                 chi = P.lv[l + 1].own_end - P.lv[l + 1].win_begin;
             }
-            if ((st = upload_mat(S.A, D.A, true, D.ep_off, tcsr, lo, hi))) return st;
-            if (h->cfg.smoother == 1) {
-                if ((st = upload_mat(S.Wd, D.Wd, true, D.ep_off))) return st;
-                if ((st = upload_mat(S.Z, D.Z, true, D.ep_off))) return st;
-            } else if (h->cfg.pre_sweeps == 1) {
-                amgsetup::Csr As = S.A;
+            if (dk) {  // GPU-built hierarchy: formats converted on the device (single rank)
+                cudaStream_t cs = h->ctx->stream;
+                if ((st = convert_mat(dk->A[l], D.A, true, D.ep_off, tcsr, cs))) return st;
+                if ((st = convert_mat(dk->P[l], D.P, false, 0, tcsr, cs))) return st;
+                if ((st = convert_mat(dk->R[l], D.R, false, 0, tcsr, cs))) return st;
+                CK(cudaMalloc((void**)&D.m, wn * 8));
+                CK(cudaMemcpyAsync(D.m, dk->m[l], wn * 8, cudaMemcpyDeviceToDevice, cs));
+                if (h->cfg.pre_sweeps == 1) {
+                    amgsetup::DevCsrRaw As = dk->A[l];
+                    CK(cudaMalloc((void**)&As.v, std::max<int64_t>(1, As.nnz) * 8));
+                    kc_scale_cols<<<148 * 16, 256, 0, cs>>>(dk->A[l].ci, dk->A[l].v, As.nnz, D.m, As.v);
+                    st = convert_mat(As, D.Am, true, D.ep_off, tcsr, cs);
+                    cudaFree(As.v);
+                    if (st) return st;
+                }
+                if ((st = dev_alloc(&D.mb, wn))) return st;
+                if ((st = dev_alloc(&D.r, wn))) return st;
+                if ((st = dev_alloc(&D.xb, wn))) return st;
+            } else {  // host-built hierarchy (or multi-rank plan): formats on the host
+                if ((st = upload_mat(S.A, D.A, true, D.ep_off, tcsr, lo, hi))) return st;
+                if (h->cfg.smoother == 1) {
+                    if ((st = upload_mat(S.Wd, D.Wd, true, D.ep_off))) return st;
+                    if ((st = upload_mat(S.Z, D.Z, true, D.ep_off))) return st;
+                } else if (h->cfg.pre_sweeps == 1) {
+                    amgsetup::Csr As = S.A;
 #pragma omp parallel for schedule(static)
-                for (int64_t i = 0; i < As.nrows; ++i)
-                    for (int64_t k = As.rp[i]; k < As.rp[i + 1]; ++k) As.v[k] = As.v[k] * S.m[As.ci[k]];
-                if ((st = upload_mat(As, D.Am, true, D.ep_off, tcsr, lo, hi))) return st;
+                    for (int64_t i = 0; i < As.nrows; ++i)
+                        for (int64_t k = As.rp[i]; k < As.rp[i + 1]; ++k) As.v[k] = As.v[k] * S.m[As.ci[k]];
+                    if ((st = upload_mat(As, D.Am, true, D.ep_off, tcsr, lo, hi))) return st;
+                }
+                if ((st = upload_mat(S.P, D.P, false, 0, tcsr, clo, chi))) return st;
+                if ((st = upload_mat(S.R, D.R, false, 0, tcsr, lo, hi))) return st;
+                if ((st = dev_copy(&D.m, S.m.data(), S.m.size()))) return st;
+                if ((st = dev_alloc(&D.mb, wn))) return st;
+                if ((st = dev_alloc(&D.r, wn))) return st;
+                if ((st = dev_alloc(&D.xb, wn))) return st;
             }
-            if ((st = upload_mat(S.P, D.P, false, 0, tcsr, clo, chi))) return st;
-            if ((st = upload_mat(S.R, D.R, false, 0, tcsr, lo, hi))) return st;
-            if ((st = dev_copy(&D.m, S.m.data(), S.m.size()))) return st;
-            if ((st = dev_alloc(&D.mb, wn))) return st;
-            if ((st = dev_alloc(&D.r, wn))) return st;
-            if ((st = dev_alloc(&D.xb, wn))) return st;
         }
         if ((st = dev_alloc(&D.b, wn))) return st;
         if ((st = dev_alloc(&D.xa, wn))) return st;
@@ -2006,6 +2193,8 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     int st = AMG_OK;
     if (nr == 1) {
         amgsetup::Hierarchy H;
+        // one process, l1-Jacobi: a GPU-built hierarchy stays on the device (formats converted there)
+        H.keep_device = (np == 1 && cfg.smoother == 0);
         if ((st = host_setup(n_global, rowptr, colind, values, w, cfg, H))) {
             set_err("amg_hierarchy_build: " + g_err);
             return fail(st);
@@ -2079,8 +2268,13 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         }
         amgsetup::tmark("partition");
         h->ranks.resize(np);
+        const amgsetup::DeviceKeep* dk = (np == 1 && !H.dev.A.empty()) ? &H.dev : nullptr;
         for (int g = 0; g < np; ++g)
-            if ((st = upload_rank(h, plans[g], H.coarse_inv, h->ranks[g]))) return fail(st);
+            if ((st = upload_rank(h, plans[g], H.coarse_inv, h->ranks[g], dk))) {
+                H.dev.free_all();
+                return fail(st);
+            }
+        H.dev.free_all();
         if (h->tail_level > 0 && (st = build_tail(h))) return fail(st);
         amgsetup::tmark("device formats + upload");
         for (int g = 0; g < np; ++g) h->ranks[g].user_off = h->loopback ? plans[g].lv[0].own_begin : 0;

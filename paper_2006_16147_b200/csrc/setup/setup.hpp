@@ -44,8 +44,24 @@ struct Level {
     Csr Wd, Z;                // INVK smoother (smoother == 1): D^{-1} W and Z = W^T
 };
 
+// Device-resident operators handed over by the GPU build (raw cudaMalloc'd arrays, freed
+// by the consumer with cudaFree): the host Hierarchy then carries only their row pointers.
+struct DevCsrRaw {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    int64_t* rp = nullptr;
+    int32_t* ci = nullptr;
+    double* v = nullptr;
+};
+struct DeviceKeep {
+    std::vector<DevCsrRaw> A, P, R;  // per level (P, R: non-coarsest levels)
+    std::vector<double*> m;          // l1-Jacobi inverse diagonals
+    void free_all();
+};
+
 struct Hierarchy {
     std::vector<Level> lv;
+    bool keep_device = false;        // GPU build: keep A_l, P-bar_l, R_l, m_l on the device (dev)
+    DeviceKeep dev;
     std::vector<double> coarse_inv;  // dense A_L^{-1}, row-major n_L x n_L
     double setup_s = 0.0;
 };

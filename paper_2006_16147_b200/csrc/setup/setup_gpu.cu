@@ -65,6 +65,12 @@ struct Buf {
         p = nullptr;
         n = 0;
     }
+    T* hand_over() {  // ownership leaves the buffer (freed later with cudaFree)
+        T* q = p;
+        p = nullptr;
+        n = 0;
+        return q;
+    }
     ~Buf() { release(); }
     Buf(const Buf&) = delete;
     Buf& operator=(const Buf&) = delete;
@@ -706,7 +712,45 @@ void matching(const DCsr& A, const Buf<double>& w, Buf<int32_t>& mate, cudaStrea
     LAUNCH(k_mates, n, s, sv.p, n, mate.p);
 }
 
+
+DevCsrRaw hand_over(DCsr& D) {
+    DevCsrRaw r;
+    r.nrows = D.nrows;
+    r.ncols = D.ncols;
+    r.nnz = D.nnz;
+    r.rp = D.rp.hand_over();
+    r.ci = D.ci.hand_over();
+    r.v = D.v.hand_over();
+    return r;
+}
+
+// host Csr carrying only the shape and the row pointers of a device matrix
+Csr rp_only(const DCsr& D, cudaStream_t s) {
+    Csr A;
+    A.nrows = D.nrows;
+    A.ncols = D.ncols;
+    A.rp.resize(D.nrows + 1);
+    GCK(cudaMemcpyAsync(A.rp.data(), D.rp.p, (D.nrows + 1) * 8, cudaMemcpyDeviceToHost, s));
+    GCK(cudaStreamSynchronize(s));
+    return A;
+}
+
 }  // namespace
+
+void DeviceKeep::free_all() {
+    for (auto* M : {&A, &P, &R})
+        for (auto& x : *M) {
+            cudaFree(x.rp);
+            cudaFree(x.ci);
+            cudaFree(x.v);
+        }
+    for (double* x : m) cudaFree(x);
+    A.clear();
+    P.clear();
+    R.clear();
+    m.clear();
+}
+
 
 // Full GPU build with the same results as amgsetup::build (validated input A0 on the
 // host; the hierarchy is copied back into `out` for partitioning / format upload).
@@ -717,6 +761,18 @@ int build_gpu(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& 
         return SETUP_ERR_ARG;
     }
     int code = SETUP_OK;
+    // keep freed blocks in the stream-ordered pool for the whole build (the default
+    // threshold 0 returns them to the driver at every synchronisation, and the next
+    // allocation maps fresh memory); trimmed again at the end
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = nullptr;
+    cudaDeviceGetDefaultMemPool(&pool, dev);
+    uint64_t keep_all = UINT64_MAX, old_thr = 0;
+    if (pool) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old_thr);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_all);
+    }
     try {
         out.lv.clear();
         out.lv.emplace_back();
@@ -732,6 +788,7 @@ int build_gpu(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& 
                 Buf<double> m(n, s);
                 LAUNCH(k_rowabs, n, s, A.rp.p, A.v.p, n, (const double*)nullptr, m.p, (double*)nullptr);
                 out.lv[l].m = download_vec(m, n, s);  // O7
+                if (out.keep_device) out.dev.m.push_back(m.hand_over());
             }
             if (n <= cfg.max_coarse_size || l == cfg.max_levels - 1) break;  // O1
             Buf<int32_t> cagg(n, s);
@@ -801,24 +858,43 @@ int build_gpu(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& 
             DCsr R = transpose(Pb, s);
             tmark("(gpu P-bar, galerkin)");
             L.agg = download_vec(cagg, n, s);
-            L.P = download(Pb, s);
-            L.R = download(R, s);
             L.sweeps = done;
             Level next;
-            next.A = download(Ac, s);
             next.w = download_vec(wc, nc, s);
+            if (out.keep_device) {  // operators stay on the device; the host keeps shapes + row pointers
+                L.P = rp_only(Pb, s);
+                L.R = rp_only(R, s);
+                next.A = rp_only(Ac, s);
+                GCK(cudaStreamSynchronize(s));
+                out.dev.P.push_back(hand_over(Pb));
+                out.dev.R.push_back(hand_over(R));
+                out.dev.A.push_back(hand_over(A));
+            } else {
+                L.P = download(Pb, s);
+                L.R = download(R, s);
+                next.A = download(Ac, s);
+            }
             out.lv.push_back(std::move(next));
             A = std::move(Ac);
             w = std::move(wc);
             tmark("(gpu download)");
         }
+        if (out.keep_device) {  // the coarsest: device copy kept, full host copy for the dense inverse
+            out.lv.back().A = download(A, s);
+            out.dev.A.push_back(hand_over(A));
+        }
         GCK(cudaStreamSynchronize(s));
     } catch (const std::string& e) {
         err = "build_gpu: " + e;
         code = SETUP_ERR_ARG;
+        out.dev.free_all();
     }
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
+    if (pool) {
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old_thr);
+        cudaMemPoolTrimTo(pool, 0);
+    }
     if (code != SETUP_OK) return code;
     if (!dense_inverse_host(out.lv.back().A, out.coarse_inv)) {  // O8
         err = "coarsest-level Cholesky failed (matrix not s.p.d.)";
