@@ -220,6 +220,8 @@ def run_ours(args):
     ctx = amg.Context(device=local, rank=rank, nranks=world, nccl_uid=uid, stream=stream.cuda_stream)
     method = method_settings(args, meta, world)
     extra = {} if args.tail_rows is None else {"tail_rows": args.tail_rows}
+    if args.tail_bytes is not None:
+        extra["tail_bytes"] = args.tail_bytes
     cfg = amg.make_config(**method["cfg"], **extra)
     t0 = time.perf_counter()
     h = amg.Hierarchy(ctx, A, cfg=cfg)
@@ -366,6 +368,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--method", choices=["default", "va3s5cs1", "ka1", "invk"], default="default")
     ap.add_argument("--tail-rows", type=int, default=None, help="override cfg.tail_rows (0 = no persistent tail)")
+    ap.add_argument("--tail-bytes", type=int, default=None, help="override cfg.tail_bytes (0 = no cluster tail)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -110,6 +110,10 @@ typedef struct {
                                      contexts only.  With one process HINVK = INVK. */
     int32_t invk_fill;            /* fill levels admitted in the inversion (default 1, Table 1
                                      caption PAPER.md:207) */
+    int64_t tail_bytes;           /* single-process, direct coarsest: the cycle rooted at the first
+                                     level from which all coarser operators take <= tail_bytes runs
+                                     as ONE thread-block-cluster kernel (<= 16 CTAs, hardware
+                                     cluster barriers between its operations).  0 = off. */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */

@@ -26,7 +26,8 @@ class amg_config_t(C.Structure):
                 ("use_graphs", C.c_int32), ("emulate_ranks", C.c_int32),
                 ("krylov", C.c_int32), ("coarse_solver", C.c_int32), ("coarse_maxit", C.c_int32),
                 ("coarse_rtol", C.c_double), ("cycle", C.c_int32), ("setup_device", C.c_int32),
-                ("tail_rows", C.c_int64), ("smoother", C.c_int32), ("invk_fill", C.c_int32)]
+                ("tail_rows", C.c_int64), ("smoother", C.c_int32), ("invk_fill", C.c_int32),
+                ("tail_bytes", C.c_int64)]
 
 
 class amg_report_t(C.Structure):

@@ -266,6 +266,7 @@ struct amg_hier_s {
     int tail_level = -1;
     TailOp* tail_prog = nullptr;
     int tail_nops = 0, tail_grid = 0;
+    bool tail_cluster = false;  // one thread-block cluster (tail_bytes) instead of a cooperative grid
     double* tail_partials = nullptr;
     double tail_bytes = 0.0;
 
@@ -729,9 +730,33 @@ struct TailEmitter {
 
 int build_tail(amg_hier_s* h) {
     const int lt = h->tail_level;
-    int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tail, kBlock, 0));
-    h->tail_grid = std::max(1, std::min(nb, 6)) * h->ctx->nsm;
+    if (h->tail_cluster) {
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(k_tail<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            attr = true;
+        }
+        int cl = 16;
+        for (; cl > 1; cl /= 2) {  // the largest cluster the device can co-schedule
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)cl);
+            lc.blockDim = dim3((unsigned)kBlock);
+            cudaLaunchAttribute at;
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = (unsigned)cl;
+            at.val.clusterDim.y = at.val.clusterDim.z = 1;
+            lc.attrs = &at;
+            lc.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, k_tail<true>, &lc) == cudaSuccess && ncl > 0) break;
+            cudaGetLastError();
+        }
+        h->tail_grid = cl;
+    } else {
+        int nb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tail<false>, kBlock, 0));
+        h->tail_grid = std::max(1, std::min(nb, 6)) * h->ctx->nsm;
+    }
     TailEmitter E{h, {}, 0.0};
     RankState& R = h->ranks[0];
     if (h->cfg.cycle == 1) E.fcg2(lt, false);
@@ -751,11 +776,20 @@ void launch_tail(amg_hier_s* h, Launch& L) {
     cfg.blockDim = dim3((unsigned)kBlock);
     cfg.stream = L.s;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    if (h->tail_cluster) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)h->tail_grid;
+        attr[0].val.clusterDim.y = attr[0].val.clusterDim.z = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_tail, (const TailOp*)h->tail_prog, (int32_t)h->tail_nops, h->tail_partials);
+    if (h->tail_cluster)
+        cudaLaunchKernelEx(&cfg, k_tail<true>, (const TailOp*)h->tail_prog, (int32_t)h->tail_nops, h->tail_partials);
+    else
+        cudaLaunchKernelEx(&cfg, k_tail<false>, (const TailOp*)h->tail_prog, (int32_t)h->tail_nops, h->tail_partials);
     L.end();
 }
 
@@ -2075,6 +2109,7 @@ void amg_config_default(amg_config_t* c) {
     c->cycle = 0;
     c->setup_device = 1;
     c->tail_rows = 0;
+    c->tail_bytes = 0;
     c->smoother = 0;
     c->invk_fill = 1;
 }
@@ -2226,8 +2261,19 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         for (size_t l = 0; l + 1 < nlv; ++l) h->agg.push_back(H.lv[l].agg);
         // persistent tail: the deep levels (n_l <= tail_rows, at least one non-coarsest)
         // run as one cooperative kernel; single process, direct coarsest solve
-        if (np == 1 && cfg.tail_rows > 0 && cfg.coarse_solver == 0 && cfg.smoother == 0 && nlv >= 3 &&
-            (cfg.cycle == 0 || cfg.pre_sweeps == 1)) {
+        const bool tail_ok = np == 1 && cfg.coarse_solver == 0 && cfg.smoother == 0 && nlv >= 3 &&
+                             (cfg.cycle == 0 || cfg.pre_sweeps == 1);
+        if (tail_ok && cfg.tail_bytes > 0) {
+            // cluster tail: the deepest levels whose operators (A, A diag(m), P-bar, R, the dense
+            // inverse) together take at most tail_bytes
+            double tot = 8.0 * (double)H.lv[nlv - 1].A.nrows * (double)H.lv[nlv - 1].A.nrows;
+            for (int l = (int)nlv - 2; l >= 1; --l) {
+                tot += 12.0 * (2.0 * (double)H.lv[l].A.nnz() + (double)H.lv[l].P.nnz() + (double)H.lv[l].R.nnz());
+                if (tot > (double)cfg.tail_bytes) break;
+                h->tail_level = l;
+            }
+            h->tail_cluster = h->tail_level > 0;
+        } else if (tail_ok && cfg.tail_rows > 0) {
             for (size_t l = 1; l + 1 < nlv; ++l)
                 if (H.lv[l].A.nrows <= cfg.tail_rows) {
                     h->tail_level = (int)l;

@@ -1166,8 +1166,21 @@ __device__ __forceinline__ double tail_spmv(const TailOp& o, double* wpart) {
     return d;
 }
 
+// CL = false: a cooperative grid over the whole GPU (grid barriers); CL = true: ONE
+// thread-block cluster (<= 16 CTAs, hardware cluster barriers) for deep levels whose
+// operators are a few MB — the same program interpreter either way.
+template <bool CL>
+__device__ __forceinline__ void tail_barrier() {
+    if constexpr (CL) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    } else {
+        cg::this_grid().sync();
+    }
+}
+
+template <bool CL>
 __global__ void __launch_bounds__(kBlock, 6) k_tail(const TailOp* __restrict__ prog, int32_t nops, double* partials) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ double wsum[kBlock / 32];
     __shared__ double wpart[2 * (kBlock / 32)];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1222,7 +1235,7 @@ __global__ void __launch_bounds__(kBlock, 6) k_tail(const TailOp* __restrict__ p
                 for (int w = 0; w < kBlock / 32; ++w) sb += wsum[w];
                 partials[blockIdx.x] = sb;
             }
-            grid.sync();
+            tail_barrier<CL>();
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 double tot = 0.0;
                 for (unsigned int bb = 0; bb < gridDim.x; ++bb) tot += ((volatile double*)partials)[bb];
@@ -1230,7 +1243,7 @@ __global__ void __launch_bounds__(kBlock, 6) k_tail(const TailOp* __restrict__ p
                 __threadfence();
             }
         }
-        grid.sync();
+        tail_barrier<CL>();
     }
 }
 

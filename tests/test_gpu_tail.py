@@ -27,11 +27,12 @@ def ctx():
 
 
 TAIL = 40000
+MODES = {"grid": dict(tail_rows=TAIL), "cluster": dict(tail_bytes=8 << 20)}
 
 
-def _pair(ctx, A, **kw):
+def _pair(ctx, A, mode, **kw):
     import paper_2006_16147_b200 as amg
-    return (amg.Hierarchy(ctx, A, cfg=amg.make_config(tail_rows=TAIL, **kw)),
+    return (amg.Hierarchy(ctx, A, cfg=amg.make_config(**MODES[mode], **kw)),
             amg.Hierarchy(ctx, A, cfg=amg.make_config(tail_rows=0, **kw)))
 
 
@@ -43,11 +44,12 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("mode", sorted(MODES))
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_tail_matches_launched_path_and_oracle(ctx, name):
+def test_tail_matches_launched_path_and_oracle(ctx, name, mode):
     build, kw, okw = CASES[name]
     A = build()
-    ht, hl = _pair(ctx, A, **kw)
+    ht, hl = _pair(ctx, A, mode, **kw)
     ho = O.OracleHierarchy(A, **{k: v for k, v in kw.items() if k not in ("cycle", "krylov")})
     if okw.get("cycle") == "K":
         ho.set_cycle("K")
@@ -68,11 +70,12 @@ def test_tail_matches_launched_path_and_oracle(ctx, name):
     assert (torch.linalg.norm(xt - xl) / torch.linalg.norm(xl)).item() <= 1e-10
 
 
-def test_tail_eager_equals_graph_and_is_deterministic(ctx):
+@pytest.mark.parametrize("mode", sorted(MODES))
+def test_tail_eager_equals_graph_and_is_deterministic(ctx, mode):
     import paper_2006_16147_b200 as amg
     A = poisson7(64, 64, 64)
-    hg = amg.Hierarchy(ctx, A, cfg=amg.make_config(tail_rows=TAIL))
-    he = amg.Hierarchy(ctx, A, cfg=amg.make_config(tail_rows=TAIL, use_graphs=0))
+    hg = amg.Hierarchy(ctx, A, cfg=amg.make_config(**MODES[mode]))
+    he = amg.Hierarchy(ctx, A, cfg=amg.make_config(**MODES[mode], use_graphs=0))
     r = torch.tensor(uniform_pm1(1302, A.n_global), device="cuda:0")
     zg = hg.precond_apply(r)
     assert torch.equal(zg, he.precond_apply(r))
