@@ -2376,8 +2376,13 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
                 set_err("amg_hierarchy_build: row blocks do not cover [0, n_global)");
                 return fail(AMG_ERR_ARG);
             }
+            std::vector<Blob>().swap(parts);  // the gathered blobs are no longer needed
             amgsetup::Hierarchy H;
-            if ((st = host_setup(n_global, gr.data(), gc.data(), gv.data(), gw.data(), cfg, H))) {
+            st = host_setup(n_global, gr.data(), gc.data(), gv.data(), gw.data(), cfg, H);
+            std::vector<int64_t>().swap(gr);  // host_setup keeps its own copy of A
+            std::vector<int64_t>().swap(gc);
+            std::vector<double>().swap(gv);
+            if (st) {
                 set_err("amg_hierarchy_build: " + g_err);
                 return fail(st);
             }
