@@ -11,6 +11,8 @@ from .problems import (  # noqa: F401
     CSR,
     poisson7,
     jump27,
+    random_spd,
+    diagonal_spd,
     uniform01,
     uniform_pm1,
     config_problem,

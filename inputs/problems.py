@@ -176,6 +176,50 @@ def jump27(N: int, nb: int = 8, seed: int = 50,
                np.concatenate(cols_parts), np.concatenate(vals_parts))
 
 
+# ------------------------------------------------------------ irregular graph
+def random_spd(n: int, deg: int = 6, window: int = 64, hubs: int = 0, hub_deg: int = 300,
+               shift: float = 1e-2, seed: int = 70) -> CSR:
+    """Irregular symmetric M-matrix (edge-case inputs, not a paper workload).
+
+    Each row i draws `deg` partners i + d, d uniform in [1, window] (dropped if
+    >= n); `hubs` evenly spaced rows each draw `hub_deg` partners anywhere.
+    Edge weights w in [0.1, 1.1); duplicate edges add.  a_ij = -w_ij,
+    a_ii = sum_j w_ij + shift * (1 + u_i), so A is symmetric, strictly
+    diagonally dominant and SPD, with a ragged row-length distribution (the
+    irregular-pattern edge cases of the format selection and the matching).
+    """
+    import scipy.sparse as sp
+    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
+    d = 1 + (uniform01(seed, n * deg) * window).astype(np.int64)
+    cols = rows + d
+    w = 0.1 + uniform01(seed + 1, n * deg)
+    keep = cols < n
+    rows, cols, w = rows[keep], cols[keep], w[keep]
+    if hubs and n > 1:
+        hr = np.repeat(np.linspace(0, n - 1, hubs).astype(np.int64), hub_deg)
+        hc = (uniform01(seed + 2, hr.size) * n).astype(np.int64)
+        hw = 0.1 + uniform01(seed + 3, hr.size)
+        ok = hr != hc
+        rows = np.concatenate([rows, hr[ok]])
+        cols = np.concatenate([cols, hc[ok]])
+        w = np.concatenate([w, hw[ok]])
+    W = sp.coo_matrix((w, (rows, cols)), shape=(n, n)).tocsr()
+    W = (W + W.T).tocsr()
+    W.sum_duplicates()
+    diag = np.asarray(W.sum(axis=1)).ravel() + shift * (1.0 + uniform01(seed + 4, n))
+    A = (sp.diags(diag) - W).tocsr()
+    A.sum_duplicates()
+    A.sort_indices()
+    return CSR(n, 0, n, A.indptr.astype(np.int64), A.indices.astype(np.int64),
+               A.data.astype(np.float64))
+
+
+def diagonal_spd(n: int, seed: int = 71) -> CSR:
+    """Diagonal SPD matrix a_ii = 1 + u_i (no couplings: the matching's empty-graph case)."""
+    return CSR(n, 0, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int64),
+               1.0 + uniform01(seed, n))
+
+
 # ------------------------------------------------------------------- configs
 CONFIGS = {
     # name: (grid builder, rhs, pre, post, maxsize_per_gpu)

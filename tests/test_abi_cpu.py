@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from inputs import config_problem, jump27, poisson7, uniform01
+from inputs import config_problem, diagonal_spd, jump27, poisson7, random_spd, uniform01
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -137,7 +137,8 @@ def _compare(amg, A, w=None, **cfg):
 
 
 @pytest.mark.parametrize("case", ["c1", "aniso_32", "jump_16", "ragged", "unsmoothed_20", "random_w",
-                                  "omega_text", "m4_sweeps", "c4_like_24x24x48"])
+                                  "omega_text", "m4_sweeps", "c4_like_24x24x48", "irregular_hubs",
+                                  "irregular_narrow", "line_1d", "plane_2d", "diagonal", "n1"])
 def test_host_setup_bit_exact_vs_oracle(amg, case):
     w, cfg = None, {}
     if case == "c1":
@@ -161,6 +162,18 @@ def test_host_setup_bit_exact_vs_oracle(amg, case):
     elif case == "m4_sweeps":
         A = poisson7(24, 24, 24)
         cfg = dict(sweeps_per_level=4, max_coarse_size=20)
+    elif case == "irregular_hubs":  # ragged rows 3..312 entries, long-range hub couplings
+        A = random_spd(6000, hubs=3)
+    elif case == "irregular_narrow":
+        A = random_spd(3000, deg=3, window=5)
+    elif case == "line_1d":  # 1-D chain: pairs only, cr 2 per sweep
+        A = poisson7(1000, 1, 1)
+    elif case == "plane_2d":
+        A = poisson7(40, 30, 1)
+    elif case == "diagonal":  # no couplings: nothing to match, single level
+        A = diagonal_spd(300)
+    elif case == "n1":
+        A = diagonal_spd(1)
     else:
         A = poisson7(24, 24, 48)
         cfg = dict(max_coarse_size=400)

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from inputs import config_problem, jump27, poisson7, uniform01, uniform_pm1
+from inputs import config_problem, diagonal_spd, jump27, poisson7, random_spd, uniform01, uniform_pm1
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -75,11 +75,30 @@ def _case(name):
         A = poisson7(5, 4, 3)
         b = uniform01(3, A.n_global)
         return A, b, {}, {}
+    if name == "irregular_hubs":  # ragged rows (3..312 entries), CSR-vector at every level
+        A = random_spd(20000, hubs=4)
+        return A, uniform_pm1(21, A.n_global), {}, {}
+    if name == "irregular_narrow":
+        A = random_spd(3000, deg=3, window=5)
+        return A, uniform01(22, A.n_global), {}, {}
+    if name == "line_1d_100k":  # 1-D chain; level 0 in SDIA (offsets -1, 0, 1)
+        A = poisson7(100000, 1, 1)
+        return A, uniform01(23, A.n_global), {}, {}
+    if name == "plane_2d_300":  # 2-D 5-point; level 0 in SDIA
+        A = poisson7(300, 300, 1)
+        return A, uniform_pm1(24, A.n_global), {}, {}
+    if name == "diagonal":  # no couplings: single level, dense coarsest
+        A = diagonal_spd(1000)
+        return A, uniform01(25, A.n_global), {}, {}
+    if name == "n1":
+        A = diagonal_spd(1)
+        return A, np.array([3.0]), {}, {}
     raise KeyError(name)
 
 
 CASES = ["c1", "c2", "c3_64", "c4_64x64x128", "c5_32", "ragged_17x13x11", "unsmoothed_24",
-         "omega_text_32", "single_level"]
+         "omega_text_32", "single_level", "irregular_hubs", "irregular_narrow", "line_1d_100k",
+         "plane_2d_300", "diagonal", "n1"]
 _cache = {}
 
 
