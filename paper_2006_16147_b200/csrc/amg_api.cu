@@ -1918,13 +1918,13 @@ int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const do
     sc.threads = cfg.setup_threads;
     sc.device = cfg.setup_device;
     if (sc.device) {
-        // capacity: the expand-sort-compress products of the level-0 Galerkin step
-        // (~nnz(A) x 8 entries of P-bar per row, key + value, double-buffered sort) must fit
-        // in the free device memory; otherwise the (bit-identical) host build is used
+        // capacity: A_0 and the level-0 Galerkin operands and results (A P-bar, its
+        // per-entry product offsets, P-bar^T, the kept device hierarchy: <= ~64 B per
+        // nonzero of A_0) plus one expand-sort-compress chunk (<= free/4, setup_gpu.cu)
+        // must fit in the free device memory; otherwise the bit-identical host build runs
         size_t freeb = 0, totalb = 0;
         if (cudaMemGetInfo(&freeb, &totalb) == cudaSuccess) {
-            const double need = 32.0 * 8.0 * (double)nnz + 64.0 * (double)nnz;
-            if (need > 0.7 * (double)freeb) sc.device = 0;
+            if (64.0 * (double)nnz > 0.6 * (double)freeb) sc.device = 0;
         }
     }
     std::string err;

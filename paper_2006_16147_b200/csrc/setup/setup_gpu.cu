@@ -23,7 +23,9 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -316,20 +318,6 @@ __global__ void k_rowof(const int64_t* rp, int64_t n, int32_t* row) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         for (int64_t k = rp[i]; k < rp[i + 1]; ++k) row[k] = (int32_t)i;
 }
-__global__ void k_expand(const int32_t* xrow, const int32_t* xci, const double* xv, int64_t xnnz, const int64_t* yrp,
-                         const int32_t* yci, const double* yv, const int64_t* off, uint64_t ncols, uint64_t* key,
-                         double* val) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < xnnz; k += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t j = xci[k];
-        const double x = xv[k];
-        const uint64_t base = (uint64_t)xrow[k] * ncols;
-        int64_t o = off[k];
-        for (int64_t t = yrp[j]; t < yrp[j + 1]; ++t, ++o) {
-            key[o] = base + (uint64_t)yci[t];
-            val[o] = __dmul_rn(x, yv[t]);
-        }
-    }
-}
 __global__ void k_runflag(const uint64_t* key, int64_t n, int64_t* flag) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
         flag[t] = (t == 0 || key[t] != key[t - 1]) ? 1 : 0;
@@ -563,6 +551,45 @@ DCsr spgemm_dense(const DCsr& X, const DCsr& Y, cudaStream_t s) {
     return C;
 }
 
+// X entries [k0, k1) of rows [r0, r1): key = (row - r0) * ncols + col
+__global__ void k_expand_rows(const int32_t* xrow, const int32_t* xci, const double* xv, int64_t k0, int64_t k1,
+                              int32_t r0, const int64_t* yrp, const int32_t* yci, const double* yv, const int64_t* off,
+                              int64_t off0, uint64_t ncols, uint64_t* key, double* val) {
+    for (int64_t k = k0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < k1; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = xci[k];
+        const double x = xv[k];
+        const uint64_t base = (uint64_t)(xrow[k] - r0) * ncols;
+        int64_t o = off[k] - off0;
+        for (int64_t t = yrp[j]; t < yrp[j + 1]; ++t, ++o) {
+            key[o] = base + (uint64_t)yci[t];
+            val[o] = __dmul_rn(x, yv[t]);
+        }
+    }
+}
+__global__ void k_row_off(const int64_t* xrp, const int64_t* off, int64_t n, int64_t* rowoff) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+        rowoff[i] = off[xrp[i]];
+}
+
+// Products per chunk of the expand-sort-compress SpGEMM: bounds the transient
+// memory (key + value, double-buffered sort, run flags: ~48 B per product) so
+// that large operators (27-point, multi-GPU-sized level 0) build on one device.
+// AMG_SPGEMM_CHUNK overrides (tests force many chunks on small inputs).
+int64_t spgemm_chunk_products() {
+    if (const char* e = std::getenv("AMG_SPGEMM_CHUNK")) {
+        const long long v = std::atoll(e);
+        if (v > 0) return (int64_t)v;
+    }
+    size_t fr = 0, tot = 0;
+    int64_t cap = (int64_t)1 << 28;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) cap = std::min<int64_t>(cap, (int64_t)(fr / 4 / 48));
+    return std::max<int64_t>(cap, (int64_t)1 << 20);
+}
+
+// C = X Y, rows in chunks of at most spgemm_chunk_products() products (a row is
+// never split).  Within a chunk the stable radix sort keeps the products of an
+// output entry in expansion order (ascending X entry, then ascending Y entry), so
+// the result is independent of the chunking and equal to the one-pass result (C3).
 DCsr spgemm(const DCsr& X, const DCsr& Y, cudaStream_t s) {
     if (Y.ncols <= kDenseMax && Y.ncols > 0) return spgemm_dense(X, Y, s);
     DCsr C;
@@ -572,32 +599,85 @@ DCsr spgemm(const DCsr& X, const DCsr& Y, cudaStream_t s) {
     GCK(cudaMemsetAsync(cnt.p + X.nnz, 0, 8, s));
     LAUNCH(k_prod_count, X.nnz, s, X.ci.p, X.nnz, Y.rp.p, cnt.p);
     excl_scan(cnt.p, off.p, X.nnz + 1, s);
-    const int64_t np = dev_get(off.p + X.nnz, s);
     cnt.release();
+    std::vector<int64_t> rowoff, xrp;
+    {
+        Buf<int64_t> ro(X.nrows + 1, s);
+        LAUNCH(k_row_off, X.nrows + 1, s, X.rp.p, off.p, X.nrows, ro.p);
+        rowoff = download_vec(ro, X.nrows + 1, s);
+        xrp = download_vec(X.rp, X.nrows + 1, s);
+    }
     Buf<int32_t> xrow(X.nnz, s);
     LAUNCH(k_rowof, X.nrows, s, X.rp.p, X.nrows, xrow.p);
-    Buf<uint64_t> key(np, s);
-    Buf<double> val(np, s);
     const uint64_t ncols = (uint64_t)std::max<int64_t>(1, Y.ncols);
-    LAUNCH(k_expand, X.nnz, s, xrow.p, X.ci.p, X.v.p, X.nnz, Y.rp.p, Y.ci.p, Y.v.p, off.p, ncols, key.p, val.p);
+    const int64_t budget = spgemm_chunk_products();
+    Buf<unsigned long long> rc(C.nrows, s);
+    GCK(cudaMemsetAsync(rc.p, 0, std::max<int64_t>(1, C.nrows) * 8, s));
+    std::vector<Buf<int32_t>> pci;
+    std::vector<Buf<double>> pv;
+    std::vector<int64_t> pn;
+    for (int64_t r0 = 0; r0 < X.nrows;) {
+        int64_t r1 = r0 + 1;
+        {  // the longest run of rows within the budget (at least one row)
+            int64_t lo = r0 + 1, hi = X.nrows;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) / 2;
+                if (rowoff[mid] - rowoff[r0] <= budget) lo = mid;
+                else hi = mid - 1;
+            }
+            r1 = lo;
+        }
+        const int64_t np = rowoff[r1] - rowoff[r0];
+        const int64_t k0 = xrp[r0], k1 = xrp[r1];
+        Buf<int32_t> cci;
+        Buf<double> cv;
+        int64_t nr = 0;
+        if (np > 0) {
+            Buf<uint64_t> key(np, s);
+            Buf<double> val(np, s);
+            LAUNCH(k_expand_rows, k1 - k0, s, xrow.p, X.ci.p, X.v.p, k0, k1, (int32_t)r0, Y.rp.p, Y.ci.p, Y.v.p, off.p,
+                   rowoff[r0], ncols, key.p, val.p);
+            sort_pairs(key, val, np, bits_for((uint64_t)(r1 - r0) * ncols), s);
+            Buf<int64_t> flag(np + 1, s), pos(np + 1, s);
+            GCK(cudaMemsetAsync(flag.p + np, 0, 8, s));
+            LAUNCH(k_runflag, np, s, key.p, np, flag.p);
+            excl_scan(flag.p, pos.p, np + 1, s);
+            nr = dev_get(pos.p + np, s);
+            Buf<int64_t> start(nr, s);
+            LAUNCH(k_runstart, np, s, flag.p, pos.p, np, start.p);
+            flag.release();
+            pos.release();
+            cci.alloc(nr, s);
+            cv.alloc(nr, s);
+            LAUNCH(k_runsum, nr, s, key.p, val.p, start.p, nr, np, ncols, cci.p, cv.p, rc.p + r0);
+        }
+        pci.push_back(std::move(cci));
+        pv.push_back(std::move(cv));
+        pn.push_back(nr);
+        r0 = r1;
+    }
     xrow.release();
     off.release();
-    sort_pairs(key, val, np, bits_for((uint64_t)std::max<int64_t>(1, X.nrows) * ncols), s);
-    Buf<int64_t> flag(np + 1, s), pos(np + 1, s);
-    GCK(cudaMemsetAsync(flag.p + np, 0, 8, s));
-    LAUNCH(k_runflag, np, s, key.p, np, flag.p);
-    excl_scan(flag.p, pos.p, np + 1, s);
-    const int64_t nr = dev_get(pos.p + np, s);
-    Buf<int64_t> start(nr, s);
-    LAUNCH(k_runstart, np, s, flag.p, pos.p, np, start.p);
-    flag.release();
-    pos.release();
-    C.nnz = nr;
-    C.ci.alloc(nr, s);
-    C.v.alloc(nr, s);
-    Buf<unsigned long long> rc(C.nrows, s);
-    GCK(cudaMemsetAsync(rc.p, 0, C.nrows * 8, s));
-    LAUNCH(k_runsum, nr, s, key.p, val.p, start.p, nr, np, ncols, C.ci.p, C.v.p, rc.p);
+    int64_t tot = 0;
+    for (int64_t x : pn) tot += x;
+    C.nnz = tot;
+    if (pci.size() == 1) {
+        C.ci = std::move(pci[0]);
+        C.v = std::move(pv[0]);
+    } else {
+        C.ci.alloc(tot, s);
+        C.v.alloc(tot, s);
+        int64_t o = 0;
+        for (size_t c = 0; c < pci.size(); ++c) {
+            if (pn[c]) {
+                GCK(cudaMemcpyAsync(C.ci.p + o, pci[c].p, pn[c] * 4, cudaMemcpyDeviceToDevice, s));
+                GCK(cudaMemcpyAsync(C.v.p + o, pv[c].p, pn[c] * 8, cudaMemcpyDeviceToDevice, s));
+            }
+            o += pn[c];
+            pci[c].release();
+            pv[c].release();
+        }
+    }
     rp_from_counts(rc.p, C.nrows, C.rp, s);
     return C;
 }

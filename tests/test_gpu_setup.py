@@ -7,13 +7,14 @@ under the canonical arithmetic contract C1-C5, so every aggregate map, every coa
 operator A_l and every smoothed prolongator P-bar_l must equal the host build's bit for
 bit, and the aggregate maps must equal the oracle's.
 """
+import os
 import time
 
 import numpy as np
 import pytest
 
 import oracle as O
-from inputs import config_problem, jump27, poisson7, uniform01
+from inputs import config_problem, jump27, poisson7, random_spd, uniform01
 from test_abi_cpu import HostH
 
 torch = pytest.importorskip("torch")
@@ -49,11 +50,22 @@ def _case(name):
         return poisson7(32, 32, 32), None, dict(prol_omega_scale=1.0)
     if name == "maxsize_2400_64":
         return poisson7(64, 64, 64), None, dict(max_coarse_size=2400)
+    # row-chunked expand-sort-compress SpGEMM (AMG_SPGEMM_CHUNK products per chunk):
+    # hundreds of chunks at the level-0 Galerkin step, single rows over the budget
+    if name == "c2_128_chunked":
+        return config_problem(2)[0], None, {}
+    if name == "jump27_48_chunked":
+        return jump27(48), None, {}
+    if name == "irregular_200k_chunked":
+        return random_spd(200000, hubs=8), None, {}
     raise KeyError(name)
 
 
+CHUNK = {"c2_128_chunked": 200000, "jump27_48_chunked": 100000, "irregular_200k_chunked": 150}
+
 CASES = ["c1", "c2_128", "aniso_48_2x2", "jump27_32", "ragged_17x13x11", "unsmoothed_40", "four_sweeps_48",
-         "random_w_24", "omega_text_32", "maxsize_2400_64"]
+         "random_w_24", "omega_text_32", "maxsize_2400_64", "c2_128_chunked", "jump27_48_chunked",
+         "irregular_200k_chunked"]
 
 
 def _same(a, b):
@@ -64,7 +76,12 @@ def _same(a, b):
 def test_gpu_setup_bit_identical_to_host_setup(amg, name):
     A, w, kw = _case(name)
     hh = HostH(amg, A, w=w, setup_device=0, **kw)
-    hg = HostH(amg, A, w=w, setup_device=1, **kw)
+    if name in CHUNK:
+        os.environ["AMG_SPGEMM_CHUNK"] = str(CHUNK[name])
+    try:
+        hg = HostH(amg, A, w=w, setup_device=1, **kw)
+    finally:
+        os.environ.pop("AMG_SPGEMM_CHUNK", None)
     assert hh.code == 0 and hg.code == 0, amg.amg_last_error()
     assert hg.nlevels == hh.nlevels
     for l in range(hh.nlevels):
