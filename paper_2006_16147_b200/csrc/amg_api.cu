@@ -731,11 +731,8 @@ struct TailEmitter {
 int build_tail(amg_hier_s* h) {
     const int lt = h->tail_level;
     if (h->tail_cluster) {
-        static bool attr = false;
-        if (!attr) {
-            CK(cudaFuncSetAttribute(k_tail<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            attr = true;
-        }
+        // function attributes are per device: set on every build (cheap, thread-safe)
+        CK(cudaFuncSetAttribute(k_tail<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         int cl = 16;
         for (; cl > 1; cl /= 2) {  // the largest cluster the device can co-schedule
             cudaLaunchConfig_t lc = {};
@@ -1553,12 +1550,9 @@ int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) 
         set_err("coarse CG: the coarsest matrix is too large (n_L <= 16384 required)");
         return AMG_ERR_ARG;
     }
-    static bool attr_done = false;
-    if (!attr_done) {
-        CK(cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        CK(cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_done = true;
-    }
+    // function attributes are per device: set on every build (cheap, thread-safe)
+    CK(cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     const size_t budget = 200 * 1024;
     auto plan = [&](int ncta, std::vector<int32_t>& split, size_t& smem_base, size_t& smem_a) {
         split.assign(ncta + 1, 0);

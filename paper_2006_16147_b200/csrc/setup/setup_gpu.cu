@@ -528,12 +528,9 @@ DCsr spgemm_dense(const DCsr& X, const DCsr& Y, cudaStream_t s) {
     C.ncols = Y.ncols;
     const int nc = (int)Y.ncols;
     const size_t sm_cnt = (size_t)nc, sm_val = (size_t)nc * 9;
-    static bool attr = false;
-    if (!attr) {
-        GCK(cudaFuncSetAttribute(k_spgemm_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseMax * 9));
-        GCK(cudaFuncSetAttribute(k_spgemm_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseMax * 9));
-        attr = true;
-    }
+    // function attributes are per device: set on every call (cheap, thread-safe)
+    GCK(cudaFuncSetAttribute(k_spgemm_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseMax * 9));
+    GCK(cudaFuncSetAttribute(k_spgemm_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseMax * 9));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(X.nrows, 148 * 8));
     Buf<int64_t> cnt(X.nrows + 1, s);
     GCK(cudaMemsetAsync(cnt.p + X.nrows, 0, 8, s));
