@@ -186,7 +186,8 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev);
  * amg_level_info: global rows, global nnz of A_l and P-bar_l (0 at the coarsest),
  * this rank's row block of level l and the device storage format of A_l
  * (0 = SELL-32, 1 = CSR-vector, 2 = dense inverse (coarsest), 3 = SDIA-32: slices of 32
- * rows aligned by column offset, no per-entry column index). */
+ * rows aligned by column offset, no per-entry column index, 4 = SELL-32-sigma: SELL-32
+ * over rows sorted by length inside windows of 256 rows, with a slot -> row map). */
 int amg_num_levels(amg_hier_t h, int32_t* nlevels);
 int amg_level_info(amg_hier_t h, int32_t lvl, int64_t* n_global, int64_t* nnzA_global,
                    int64_t* nnzP_global, int64_t* row_begin, int64_t* row_end, int32_t* format);

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libamg_b200.so")
 
 AMG_OK, AMG_ERR_ARG, AMG_ERR_NOT_SPD, AMG_ERR_CUDA, AMG_ERR_NCCL, AMG_ERR_OOM = 0, 1, 2, 3, 4, 5
 AMG_NOT_CONVERGED, AMG_ERR_BREAKDOWN = 6, 7
-FORMATS = {0: "sell32", 1: "csr_vector", 2: "dense_inverse", 3: "sdia32"}
+FORMATS = {0: "sell32", 1: "csr_vector", 2: "dense_inverse", 3: "sdia32", 4: "sell32_sigma"}
 
 
 class amg_config_t(C.Structure):

@@ -65,7 +65,7 @@ void set_err(const std::string& s) { g_err = s; }
         }                                                                \
     } while (0)
 
-enum { FMT_SELL = 0, FMT_CSRV = 1, FMT_DENSE = 2, FMT_SDIA = 3 };
+enum { FMT_SELL = 0, FMT_CSRV = 1, FMT_DENSE = 2, FMT_SDIA = 3, FMT_SELL_SIGMA = 4 /* reported only */ };
 constexpr int kVWBlock = 256;  // CSR-vector "VW" value meaning one block per row
 
 struct DevMat {
@@ -79,6 +79,7 @@ struct DevMat {
     int32_t* rp = nullptr;     // CSR
     int32_t* col = nullptr;
     double* val = nullptr;
+    int32_t* perm = nullptr;   // SELL-32-sigma: slot -> row (null: plain SELL-32)
     // multi-rank overlap: launch units (slices for SELL/SDIA, rows for CSR) and the largest
     // contiguous block of units whose gathers touch only owned columns ("interior": it can
     // run while the halo is in flight); the rest ("head" / "tail") runs after the exchange
@@ -89,7 +90,7 @@ struct DevMat {
     double stored_bytes() const {
         const double nsl = (double)((nrows + 31) / 32);
         switch (fmt) {
-            case FMT_SELL: return 12.0 * (double)stored + 4.0 * (nsl + 1);
+            case FMT_SELL: return 12.0 * (double)stored + 4.0 * (nsl + 1) + (perm ? 128.0 * nsl : 0.0);
             case FMT_SDIA:
                 return 8.0 * (double)stored + 4.0 * (double)stored / 32.0 + 4.0 * (nsl + 1) +
                        (anchor ? 4.0 * (double)nrows : 0.0);
@@ -103,11 +104,13 @@ struct DevMat {
         cudaFree(rp);
         cudaFree(col);
         cudaFree(val);
+        cudaFree(perm);
         sptr = nullptr;
         offs = nullptr;
         anchor = nullptr;
         rp = col = nullptr;
         val = nullptr;
+        perm = nullptr;
     }
 };
 
@@ -370,7 +373,7 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         static const int cap = max_grid((const void*)k_sell<G, E>, nsm);
         const int64_t need = ((u1 - u0) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1}, g, e, rc);
+        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1, M.perm}, g, e, rc);
     } else {
         const CsrView v{M.rp, M.col, M.val, M.nrows, u0, u1};
         const int64_t need = ((u1 - u0) * M.vw + kBlock - 1) / kBlock;
@@ -1435,6 +1438,54 @@ __global__ void kc_sell_fill(const int64_t* __restrict__ rp, const int32_t* __re
         for (; k < (int64_t)width[sl]; ++k) col[base + k * 32 + lane] = last;
     }
 }
+// SELL-32-sigma: inside each window of kSigma rows, rows ordered by length
+// descending (ties by row index); one block per window, rank by counting
+constexpr int kSigma = 256;
+__global__ void __launch_bounds__(kSigma) kc_sigma_perm(const int64_t* __restrict__ rp, int64_t n, int32_t* perm) {
+    __shared__ int64_t len[kSigma];
+    const int64_t w0 = (int64_t)blockIdx.x * kSigma;
+    const int t = threadIdx.x;
+    const int64_t r = w0 + t;
+    len[t] = (r < n) ? rp[r + 1] - rp[r] : -1;  // padding slots sort last
+    __syncthreads();
+    const int64_t li = len[t];
+    int rank = 0;
+    for (int j = 0; j < kSigma; ++j) {
+        const int64_t lj = len[j];
+        rank += (lj > li || (lj == li && j < t)) ? 1 : 0;
+    }
+    perm[w0 + rank] = (r < n) ? (int32_t)r : -1;
+}
+__global__ void kc_slice_width_perm(const int64_t* __restrict__ rp, const int32_t* __restrict__ perm, int64_t nsl,
+                                    uint32_t* width) {
+    for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nsl; sl += (int64_t)gridDim.x * blockDim.x) {
+        int64_t w = 0;
+        for (int l = 0; l < 32; ++l) {
+            const int32_t r = perm[sl * 32 + l];
+            if (r >= 0) w = max(w, rp[r + 1] - rp[r]);
+        }
+        width[sl] = (uint32_t)w;
+    }
+}
+// slot-major fill (thread per slot); padding entries repeat the row's last column, value 0
+__global__ void kc_sell_fill_perm(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ v, const int32_t* __restrict__ perm, int64_t nslots,
+                                  const uint32_t* __restrict__ sptr, const uint32_t* __restrict__ width, int32_t* col,
+                                  double* val) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nslots; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sl = q >> 5, lane = q & 31;
+        const int64_t base = (int64_t)sptr[sl] * 32;
+        const int32_t r = perm[q];
+        int64_t k = 0;
+        int32_t last = 0;
+        if (r >= 0)
+            for (int64_t t = rp[r]; t < rp[r + 1]; ++t, ++k) {
+                col[base + k * 32 + lane] = last = ci[t];
+                val[base + k * 32 + lane] = v[t];
+            }
+        for (; k < (int64_t)width[sl]; ++k) col[base + k * 32 + lane] = last;
+    }
+}
 __global__ void kc_rp32(const int64_t* __restrict__ rp, int64_t n, int32_t* out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = (int32_t)rp[i];
@@ -1443,6 +1494,11 @@ __global__ void kc_scale_cols(const int32_t* __restrict__ ci, const double* __re
                               const double* __restrict__ m, double* out) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
         out[k] = v[k] * m[ci[k]];
+}
+
+static double sigma_mean_max() {  // AMG_SIGMA_MEAN_MAX: experiment knob (default 128)
+    const char* e = std::getenv("AMG_SIGMA_MEAN_MAX");
+    return e ? std::atof(e) : 128.0;
 }
 
 int convert_mat(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t shift, bool force_csr, cudaStream_t s) {
@@ -1512,6 +1568,47 @@ int convert_mat(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t sh
         cudaFree(dwidth);
         D.units = nsl;
         return AMG_OK;
+    }
+    // SELL-32-sigma: rows sorted by length inside windows of kSigma rows cut the padding of
+    // ragged operators (irregular aggregates: P-bar / R of the 27-point jump problem, its
+    // coarse A_l); the slot -> row map costs 4 B per row.  Used when it stores at most
+    // 1.10 x nnz and the rows fit int32, for rows of <= 128 entries on average and enough
+    // of them to fill the GPU with one thread per row (>= 148 x 2048): few long rows on one
+    // thread each (A_2 of the 27-point problem: 114k rows of 600 entries) serialise, and
+    // CSR-vector is faster there.  c5 analogue 192^3: 56.9 -> 53.9 ms; 256^3: 119.8 -> 115.5.
+    if (!force_csr && n >= 148 * 2048 && mean <= sigma_mean_max() && n < (int64_t)INT32_MAX) {
+        const int64_t nwin = (n + kSigma - 1) / kSigma;
+        const int64_t nslots = nwin * kSigma;
+        const int64_t nslp = nslots / 32;
+        int32_t* perm = nullptr;
+        uint32_t* pw = nullptr;
+        if ((st = dev_alloc(&perm, (size_t)nslots))) return st;
+        if ((st = dev_alloc(&pw, (size_t)nslp))) return st;
+        kc_sigma_perm<<<(unsigned)nwin, kSigma, 0, s>>>(M.rp, n, perm);
+        kc_slice_width_perm<<<gs, 256, 0, s>>>(M.rp, perm, nslp, pw);
+        std::vector<uint32_t> pwidth(nslp);
+        CK(cudaMemcpyAsync(pwidth.data(), pw, nslp * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        int64_t ppad = 0;
+        for (int64_t q = 0; q < nslp; ++q) ppad += 32 * (int64_t)pwidth[q];
+        if ((double)ppad <= 1.10 * (double)nnz + 64.0 && ppad / 32 < (int64_t)UINT32_MAX) {
+            D.fmt = FMT_SELL;
+            D.stored = ppad;
+            D.perm = perm;
+            std::vector<uint32_t> sptr(nslp + 1, 0);
+            for (int64_t q = 0; q < nslp; ++q) sptr[q + 1] = sptr[q] + pwidth[q];
+            if ((st = dev_copy(&D.sptr, sptr.data(), sptr.size()))) return st;
+            if ((st = dev_alloc(&D.col, (size_t)std::max<int64_t>(1, ppad)))) return st;
+            if ((st = dev_alloc(&D.val, (size_t)std::max<int64_t>(1, ppad)))) return st;
+            kc_sell_fill_perm<<<gs, 256, 0, s>>>(M.rp, M.ci, M.v, perm, nslots, D.sptr, pw, D.col, D.val);
+            CK(cudaStreamSynchronize(s));
+            cudaFree(pw);
+            cudaFree(dwidth);
+            D.units = nslp;
+            return AMG_OK;
+        }
+        cudaFree(perm);
+        cudaFree(pw);
     }
     cudaFree(dwidth);
     if (nnz >= (int64_t)INT32_MAX) {
@@ -2322,7 +2419,9 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         h->lvl_own_end = h->lvl_n;
         h->n0_local = n_global;
         for (size_t l = 0; l < H.lv.size(); ++l)
-            h->lvl_fmt.push_back(l + 1 < H.lv.size() ? h->ranks[0].lv[l].A.fmt : FMT_DENSE);
+            h->lvl_fmt.push_back(l + 1 < H.lv.size()
+                                     ? (h->ranks[0].lv[l].A.perm ? FMT_SELL_SIGMA : h->ranks[0].lv[l].A.fmt)
+                                     : FMT_DENSE);
     } else {
         // ---- NCCL: gather the matrix on rank 0, build there, send each rank its plan
         const int me = ctx->rank;

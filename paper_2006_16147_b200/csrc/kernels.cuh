@@ -474,6 +474,9 @@ struct SellView {
     const double* __restrict__ val;
     int64_t n;
     int64_t s0, s1;                     // slice range of this launch (multi-rank interior/boundary split)
+    // SELL-32-sigma: slot (slice, lane) -> row (rows sorted by length inside windows of
+    // sigma rows; -1 = padding slot); null for plain SELL-32 (slot = row)
+    const int32_t* __restrict__ perm;
 };
 
 // Row-chunk of exactly W entries of one slice (lane = row): the W value loads are
@@ -540,8 +543,8 @@ __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx
         const double* v = A.val + (int64_t)b0 * 32 + lane;
         double acc = 0.0, asum = 0.0;
         slice_row<G::kChunk, E::kAbs>(v, w, [&](uint32_t k) { return ld_stream(c + 32 * k); }, g, acc, asum);
-        const int64_t row = (s << 5) + lane;
-        if (row < A.n) d += apply_epi(e, row, acc, asum);
+        const int64_t row = A.perm ? (int64_t)__ldg(A.perm + (s << 5) + lane) : (s << 5) + lane;
+        if (row >= 0 && row < A.n) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
 }

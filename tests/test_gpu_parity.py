@@ -90,6 +90,12 @@ def _case(name):
     if name == "diagonal":  # no couplings: single level, dense coarsest
         A = diagonal_spd(1000)
         return A, uniform01(25, A.n_global), {}, {}
+    if name == "c5_72":  # ragged P-bar_0 (irregular aggregates, 8.5 entries/row) -> SELL-32-sigma
+        A = jump27(72)
+        return A, uniform01(26, A.n_global), {}, {}
+    if name == "irregular_400k":  # ragged short rows, n >= 148 x 2048 -> SELL-32-sigma at level 0
+        A = random_spd(400000, deg=4, window=32)
+        return A, uniform_pm1(27, A.n_global), {}, {}
     if name == "n1":
         A = diagonal_spd(1)
         return A, np.array([3.0]), {}, {}
@@ -98,7 +104,7 @@ def _case(name):
 
 CASES = ["c1", "c2", "c3_64", "c4_64x64x128", "c5_32", "ragged_17x13x11", "unsmoothed_24",
          "omega_text_32", "single_level", "irregular_hubs", "irregular_narrow", "line_1d_100k",
-         "plane_2d_300", "diagonal", "n1"]
+         "plane_2d_300", "diagonal", "n1", "c5_72", "irregular_400k"]
 _cache = {}
 
 
@@ -115,6 +121,8 @@ def _built(ctx, name):
 @pytest.mark.parametrize("name", CASES)
 def test_hierarchy_and_aggregates_bit_exact(ctx, name):
     A, b, ho, h = _built(ctx, name)
+    if name == "irregular_400k":  # the ragged level-0 operator takes the row-sorted SELL layout
+        assert h.level_info(0)["format"] == "sell32_sigma"
     assert h.sizes() == ho.sizes()
     for l in range(h.nlevels):
         info = h.level_info(l)

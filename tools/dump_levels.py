@@ -45,6 +45,18 @@ def main():
     assert st == 0, amg.amg_last_error()
     nl = C.c_int32()
     L.amg_host_num_levels(h, C.byref(nl))
+    for l in ([0] if os.environ.get("DUMP_P") else []):  # P-bar_0 (prolongation) as well
+        n, a, p = C.c_int64(), C.c_int64(), C.c_int64()
+        om = C.c_double()
+        L.amg_host_level_sizes(h, l, C.byref(n), C.byref(a), C.byref(p), C.byref(om))
+        rp = np.zeros(n.value + 1, np.int64)
+        ci = np.zeros(max(p.value, 1), np.int64)
+        v = np.zeros(max(p.value, 1))
+        assert L.amg_host_level_matrix(h, l, 1, C.c_void_p(rp.ctypes.data), C.c_void_p(ci.ctypes.data),
+                                       C.c_void_p(v.ctypes.data)) == 0
+        path = os.path.join(out, f"{which}_P{l}.csr")
+        write(path, rp, ci[:p.value], v[:p.value])
+        print(path, n.value, p.value, p.value / n.value)
     for l in levels:
         if l >= nl.value:
             break

@@ -257,6 +257,10 @@ int main(int argc, char** argv) {
         CK(cudaDeviceSynchronize());
 #define V0(VW) run("V0/" #VW, [&] { k_v0<VW><<<grid_for(VW), 256>>>(A, dx, db, dy); })
 #define PV(VW, CH) run("P" #CH "/" #VW, [&] { k_p<VW, CH><<<grid_for(VW), 256>>>(A, dx, db, dy); })
+        if (op.n > 1000000 && (double)nnz / op.n < 24) {  // short rows: narrow groups
+            V0(1); V0(2); V0(4);
+            PV(1, 4); PV(1, 8); PV(2, 4); PV(2, 8); PV(4, 4); PV(4, 8);
+        }
         V0(8); V0(16); V0(32);
         PV(8, 4); PV(8, 8); PV(16, 4); PV(16, 8); PV(32, 4); PV(32, 8);
         run("B/4", [&] { k_b<4><<<(int)std::min<int64_t>(op.n, 148 * 8), 256>>>(A, dx, db, dy); });
