@@ -69,6 +69,52 @@ __global__ void __launch_bounds__(256) k_v0(M A, const double* __restrict__ x, c
     }
 }
 
+// V0 + software pipelining across a warp's rows: the next row's pointers and the
+// current row's epilogue operand are loaded before the current row's entries
+template <int VW>
+__global__ void __launch_bounds__(256) k_v0p(M A, const double* __restrict__ x, const double* __restrict__ b,
+                                             double* __restrict__ y) {
+    const int64_t gid = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const int sub = threadIdx.x % VW;
+    const int64_t g0 = gid / VW, ng = ((int64_t)gridDim.x * 256) / VW;
+    const int64_t iters = (A.n + ng - 1) / ng;
+    int32_t nk0 = 0, nk1 = 0;
+    if (g0 < A.n) {
+        nk0 = __ldg(A.rp + g0);
+        nk1 = __ldg(A.rp + g0 + 1);
+    }
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t row = g0 + it * ng;
+        const int32_t k0 = nk0, k1 = nk1;
+        const int64_t nrow = row + ng;
+        if (nrow < A.n) {
+            nk0 = __ldg(A.rp + nrow);
+            nk1 = __ldg(A.rp + nrow + 1);
+        }
+        double acc = 0.0, bi = 0.0;
+        if (row < A.n) {
+            if (sub == 0) bi = b[row];
+            int32_t k = k0 + sub;
+            for (; k + 3 * VW < k1; k += 4 * VW) {
+                double a[4], xx[4];
+                int32_t c[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a[j] = ld_stream(A.v + k + j * VW);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) c[j] = ld_stream(A.ci + k + j * VW);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) xx[j] = __ldg(x + c[j]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc += a[j] * xx[j];
+            }
+            for (; k < k1; k += VW) acc += ld_stream(A.v + k) * __ldg(x + ld_stream(A.ci + k));
+        }
+#pragma unroll
+        for (int o = VW / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, VW);
+        if (sub == 0 && row < A.n) y[row] = bi - acc;
+    }
+}
+
 template <int VW, int CH>
 __global__ void __launch_bounds__(256) k_p(M A, const double* __restrict__ x, const double* __restrict__ b,
                                            double* __restrict__ y) {
@@ -262,6 +308,9 @@ int main(int argc, char** argv) {
             PV(1, 4); PV(1, 8); PV(2, 4); PV(2, 8); PV(4, 4); PV(4, 8);
         }
         V0(8); V0(16); V0(32);
+        run("V0P/8", [&] { k_v0p<8><<<grid_for(8), 256>>>(A, dx, db, dy); });
+        run("V0P/16", [&] { k_v0p<16><<<grid_for(16), 256>>>(A, dx, db, dy); });
+        run("V0P/32", [&] { k_v0p<32><<<grid_for(32), 256>>>(A, dx, db, dy); });
         PV(8, 4); PV(8, 8); PV(16, 4); PV(16, 8); PV(32, 4); PV(32, 8);
         run("B/4", [&] { k_b<4><<<(int)std::min<int64_t>(op.n, 148 * 8), 256>>>(A, dx, db, dy); });
         run("B/1", [&] { k_b<1><<<(int)std::min<int64_t>(op.n, 148 * 8), 256>>>(A, dx, db, dy); });
