@@ -214,3 +214,40 @@ def test_host_setup_errors(amg):
     A.colind = A.colind.copy()
     A.colind[0], A.colind[1] = A.colind[1], A.colind[0]  # unsorted row
     assert HostH(amg, A).code == 1
+
+
+def test_null_handles_and_bad_arguments_are_status_codes(amg):
+    """Every entry point answers a NULL handle / NULL output / bad argument with
+    AMG_ERR_ARG (1) and a message, never a crash (include/amg_b200.h: status codes
+    only, no exceptions across the ABI)."""
+    L = amg.lib
+    null = C.c_void_p()
+    i32, i64, f64 = C.c_int32(), C.c_int64(), C.c_double()
+    from paper_2006_16147_b200 import _abi
+    rep = C.byref(_abi.amg_report_t())
+    buf = np.zeros(16)
+    p = C.c_void_p(buf.ctypes.data)
+    calls = {
+        "amg_solve": lambda: L.amg_solve(null, p, p, C.c_double(1e-6), C.c_int32(10), rep),
+        "amg_solve_host": lambda: L.amg_solve_host(null, p, p, C.c_double(1e-6), C.c_int32(10), rep),
+        "amg_precond_apply": lambda: L.amg_precond_apply(null, p, p),
+        "amg_num_levels": lambda: L.amg_num_levels(null, C.byref(i32)),
+        "amg_level_info": lambda: L.amg_level_info(null, 0, C.byref(i64), C.byref(i64), C.byref(i64),
+                                                   C.byref(i64), C.byref(i64), C.byref(i32)),
+        "amg_level_aggregates": lambda: L.amg_level_aggregates(null, 0, p),
+        "amg_hierarchy_report": lambda: L.amg_hierarchy_report(null, rep),
+        "amg_host_num_levels": lambda: L.amg_host_num_levels(null, C.byref(i32)),
+        "amg_host_level_sizes": lambda: L.amg_host_level_sizes(null, 0, C.byref(i64), C.byref(i64),
+                                                               C.byref(i64), C.byref(f64)),
+        "amg_host_level_aggregates": lambda: L.amg_host_level_aggregates(null, 0, p),
+    }
+    for name, call in calls.items():
+        assert call() == 1, name
+        assert amg.amg_last_error(), name
+    # a valid host hierarchy rejects out-of-range levels and a bad matrix selector
+    h = HostH(amg, poisson7(6, 6, 6))
+    assert h.code == 0
+    nl = h.nlevels
+    assert L.amg_host_level_sizes(h.h, nl, C.byref(i64), C.byref(i64), C.byref(i64), C.byref(f64)) == 1
+    assert L.amg_host_level_aggregates(h.h, nl - 1, p) == 1  # the coarsest has no aggregates
+    assert L.amg_host_level_matrix(h.h, 0, 7, p, p, p) == 1
