@@ -110,3 +110,17 @@ def test_loopback_overlap_splits_operators_into_interior_and_boundary(ctx):
     z = h.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
     zs = amg.Hierarchy(ctx, A).precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
     assert np.linalg.norm(z - zs) <= 1e-12 * np.linalg.norm(zs)
+
+
+def test_loopback_profile_vcycle_and_report(ctx):
+    """The instrumented V-cycle (per-kernel events, bench.py's roofline source) and the
+    report work on the multi-rank path too (what bench.py calls under torchrun)."""
+    import paper_2006_16147_b200 as amg
+    A, b, _ = config_problem(4, grid=(32, 32, 64))
+    h = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=2, replicate_below_bytes=0))
+    prof = h.profile_vcycle(2)
+    assert prof and all(k["ms"] > 0 and k["bytes"] > 0 for k in prof)
+    names = {k["name"] for k in prof}
+    assert {"resid0", "restrict", "prolong", "postsweep"} <= names
+    rep = h.report()
+    assert rep["vcycle_bytes_model"] > 0 and rep["nlevels"] == h.nlevels
