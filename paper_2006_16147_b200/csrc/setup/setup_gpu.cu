@@ -340,59 +340,67 @@ __global__ void k_runsum(const uint64_t* key, const double* val, const int64_t* 
     }
 }
 
-// ---- SpGEMM with a dense per-row accumulator (narrow outputs, ncols <= kDenseMax):
+// ---- SpGEMM with a dense per-row accumulator (outputs of <= kDenseBlocks x kDenseMax
+// columns, processed in column blocks of <= kDenseMax):
 // one block per output row; for each entry j of row i of X in ascending order the
 // block's threads add x_ij*y_jK into acc[K] for the (distinct) K of row j of Y, with
 // a barrier between entries — so every acc[K] receives its products in exactly the
 // arrival order of C3.  Touched columns are emitted in ascending order with a block
 // scan.  VALUES = false: count only.
 constexpr int kDenseMax = 16384;
+// outputs up to kDenseBlocks x kDenseMax columns use the column-blocked dense accumulator
+constexpr int kDenseBlocks = 4;
 constexpr int DB = 256;
 
 template <bool VALUES>
 __global__ void __launch_bounds__(DB) k_spgemm_dense(const int64_t* xrp, const int32_t* xci, const double* xv,
                                                      int64_t nrows, const int64_t* yrp, const int32_t* yci,
-                                                     const double* yv, int32_t ncols, int64_t* cnt,
+                                                     const double* yv, int32_t ncols, int32_t cb, int64_t* cnt,
                                                      const int64_t* crp, int32_t* cci, double* cv) {
+    // output columns in blocks of cb (<= kDenseMax): the row is traversed once per block,
+    // so every output entry still sums its products in ascending X-entry order (C3)
     extern __shared__ __align__(16) unsigned char sm[];
     double* acc = (double*)sm;
-    unsigned char* flag = (unsigned char*)(acc + (VALUES ? ncols : 0));
+    unsigned char* flag = (unsigned char*)(acc + (VALUES ? cb : 0));
     typedef cub::BlockScan<int, DB> Scan;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ int total;
     for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
-        for (int c = threadIdx.x; c < ncols; c += DB) {
-            if (VALUES) acc[c] = 0.0;
-            flag[c] = 0;
-        }
-        __syncthreads();
-        for (int64_t e = xrp[i]; e < xrp[i + 1]; ++e) {
-            const int32_t j = xci[e];
-            const double x = xv[e];
-            for (int64_t t = yrp[j] + threadIdx.x; t < yrp[j + 1]; t += DB) {
-                const int32_t K = yci[t];
-                if (VALUES) acc[K] = __dadd_rn(acc[K], __dmul_rn(x, yv[t]));
-                flag[K] = 1;
-            }
-            __syncthreads();
-        }
         int64_t out = VALUES ? crp[i] : 0;
-        for (int c0 = 0; c0 < ncols; c0 += DB) {
-            const int c = c0 + threadIdx.x;
-            const int f = (c < ncols) ? flag[c] : 0;
-            int pos, agg;
-            Scan(tmp).ExclusiveSum(f, pos, agg);
-            if (VALUES && f) {
-                cci[out + pos] = c;
-                cv[out + pos] = acc[c];
+        for (int32_t c0 = 0; c0 < ncols; c0 += cb) {
+            const int32_t w = min(cb, ncols - c0);
+            for (int c = threadIdx.x; c < w; c += DB) {
+                if (VALUES) acc[c] = 0.0;
+                flag[c] = 0;
             }
-            out += agg;
             __syncthreads();
+            for (int64_t e = xrp[i]; e < xrp[i + 1]; ++e) {
+                const int32_t j = xci[e];
+                const double x = xv[e];
+                for (int64_t t = yrp[j] + threadIdx.x; t < yrp[j + 1]; t += DB) {
+                    const int32_t K = yci[t] - c0;
+                    if (K >= 0 && K < w) {
+                        if (VALUES) acc[K] = __dadd_rn(acc[K], __dmul_rn(x, yv[t]));
+                        flag[K] = 1;
+                    }
+                }
+                __syncthreads();
+            }
+            for (int cc = 0; cc < w; cc += DB) {
+                const int c = cc + threadIdx.x;
+                const int f = (c < w) ? flag[c] : 0;
+                int pos, agg;
+                Scan(tmp).ExclusiveSum(f, pos, agg);
+                if (VALUES && f) {
+                    cci[out + pos] = c0 + c;
+                    cv[out + pos] = acc[c];
+                }
+                out += agg;
+                __syncthreads();
+            }
         }
         if (!VALUES && threadIdx.x == 0) cnt[i] = out;
         __syncthreads();
     }
-    (void)total;
 }
 
 // ---- transpose (stable)
@@ -527,23 +535,25 @@ DCsr spgemm_dense(const DCsr& X, const DCsr& Y, cudaStream_t s) {
     C.nrows = X.nrows;
     C.ncols = Y.ncols;
     const int nc = (int)Y.ncols;
-    const size_t sm_cnt = (size_t)nc, sm_val = (size_t)nc * 9;
+    const int nb = (nc + kDenseMax - 1) / kDenseMax;  // column blocks
+    const int cb = (nc + nb - 1) / nb;
+    const size_t sm_cnt = (size_t)cb, sm_val = (size_t)cb * 9;
     // function attributes are per device: set on every call (cheap, thread-safe)
     GCK(cudaFuncSetAttribute(k_spgemm_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseMax * 9));
     GCK(cudaFuncSetAttribute(k_spgemm_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseMax * 9));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(X.nrows, 148 * 8));
     Buf<int64_t> cnt(X.nrows + 1, s);
     GCK(cudaMemsetAsync(cnt.p + X.nrows, 0, 8, s));
-    k_spgemm_dense<false><<<grid, DB, sm_cnt, s>>>(X.rp.p, X.ci.p, X.v.p, X.nrows, Y.rp.p, Y.ci.p, Y.v.p, nc, cnt.p,
-                                                   nullptr, nullptr, nullptr);
+    k_spgemm_dense<false><<<grid, DB, sm_cnt, s>>>(X.rp.p, X.ci.p, X.v.p, X.nrows, Y.rp.p, Y.ci.p, Y.v.p, nc, cb,
+                                                   cnt.p, nullptr, nullptr, nullptr);
     GCK(cudaGetLastError());
     C.rp.alloc(X.nrows + 1, s);
     excl_scan(cnt.p, C.rp.p, X.nrows + 1, s);
     C.nnz = dev_get(C.rp.p + X.nrows, s);
     C.ci.alloc(C.nnz, s);
     C.v.alloc(C.nnz, s);
-    k_spgemm_dense<true><<<grid, DB, sm_val, s>>>(X.rp.p, X.ci.p, X.v.p, X.nrows, Y.rp.p, Y.ci.p, Y.v.p, nc, nullptr,
-                                                  C.rp.p, C.ci.p, C.v.p);
+    k_spgemm_dense<true><<<grid, DB, sm_val, s>>>(X.rp.p, X.ci.p, X.v.p, X.nrows, Y.rp.p, Y.ci.p, Y.v.p, nc, cb,
+                                                  nullptr, C.rp.p, C.ci.p, C.v.p);
     GCK(cudaGetLastError());
     return C;
 }
@@ -588,7 +598,7 @@ int64_t spgemm_chunk_products() {
 // output entry in expansion order (ascending X entry, then ascending Y entry), so
 // the result is independent of the chunking and equal to the one-pass result (C3).
 DCsr spgemm(const DCsr& X, const DCsr& Y, cudaStream_t s) {
-    if (Y.ncols <= kDenseMax && Y.ncols > 0) return spgemm_dense(X, Y, s);
+    if (Y.ncols <= kDenseBlocks * kDenseMax && Y.ncols > 0) return spgemm_dense(X, Y, s);
     DCsr C;
     C.nrows = X.nrows;
     C.ncols = Y.ncols;
