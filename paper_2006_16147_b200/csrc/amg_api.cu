@@ -158,6 +158,7 @@ struct DevLevel {
     // K-cycle FCG vectors of this level (cfg.cycle == 1, levels 1..nl-2) and its
     // device scalars {p^T r, p^T q, alpha, beta, stop}
     double *kx = nullptr, *kr = nullptr, *kmb = nullptr, *kz = nullptr, *kp = nullptr, *kq = nullptr;
+    double* kp2 = nullptr;  // the inner FCG's second direction (written while kp is gathered)
     double* kst = nullptr;
     Exch ex;
     void release() {
@@ -167,7 +168,7 @@ struct DevLevel {
         Am.release();
         Wd.release();
         Z.release();
-        for (double* v : {kx, kr, kmb, kz, kp, kq, kst}) cudaFree(v);
+        for (double* v : {kx, kr, kmb, kz, kp, kq, kst, kp2}) cudaFree(v);
         cudaFree(m);
         cudaFree(b);
         cudaFree(mb);
@@ -795,10 +796,17 @@ void launch_tail(amg_hier_s* h, Launch& L) {
 
 // ------------------------------------------------------------- V-cycle / K-cycle
 void enqueue_fcg2(amg_hier_s* h, Launch& L, int l);
+// K-cycle inner FCG without the vector-update kernel (one pre-sweep, l1-Jacobi): the
+// second application forms r = b - alpha_1 q_1 itself, the consumer forms x (GXap2)
+inline bool kcycle_fused(const amg_hier_s* h) { return h->cfg.pre_sweeps == 1 && h->cfg.smoother == 0; }
 // Where a cycle's fused dot goes: the PCG state (default) or a K-cycle level state.
 struct DotSink {
     double* ks;
     int kind;
+    // K-cycle, s1 == 1: the application's right-hand side is b - alpha q (k = ks), formed by
+    // its first kernel, which also writes it to the application's b vector
+    const double* kb = nullptr;
+    const double* kq = nullptr;
 };
 void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf* mbvec, const VecOf& outv,
                    bool dot, const VecOf* dwv, const DotSink* sink = nullptr);
@@ -846,7 +854,7 @@ void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, cons
     if (kfcg) enqueue_fcg2(h, L, l + 1);
     else enqueue_level(h, L, l + 1, cb, nullptr, ev, false, nullptr);
     if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
-        launch_mat(L, D.P, GXap{C.kx, C.kp, C.kst}, EProlongAdd{x, x}, no_red(), "prolong",
+        launch_mat(L, D.P, GXap{C.kx, C.kp2, C.kst}, EProlongAdd{x, x}, no_red(), "prolong",
                    2 * n8 + 16.0 * (double)C.comp_n);
     else
         launch_mat(L, D.P, GVec{ev(R)}, EProlongAdd{x, x}, no_red(), "prolong", 2 * n8 + 8.0 * (double)C.comp_n);
@@ -899,7 +907,11 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
         const double* b = bvec(R);
         const double* be = b + D.ep_off;
         const double n8 = 8.0 * (double)D.comp_n;
-        if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b) = b - (A diag(m)) b
+        if (s1 == 1 && sink && sink->kb) {  // K-cycle: rhs = b - alpha_1 q_1 formed and stored here
+            launch_mat(L, D.Am, GBaq{sink->kb, sink->kq, sink->ks},
+                       EResidK{sink->kb, sink->kq, sink->ks, const_cast<double*>(b), D.r}, no_red(), "resid0",
+                       4 * n8, part);
+        } else if (s1 == 1) {  // x = m o b is never stored: r = b - A (m o b) = b - (A diag(m)) b
             launch_mat(L, D.Am, GVec{b}, EResid{be, D.r + D.ep_off}, no_red(), "resid0", 2 * n8, part);
         } else {  // x2 = m b + m (b - A (m b)): the first two sweeps from x = 0 in one pass
             if (!mbvec)
@@ -958,6 +970,12 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
     else if (kfcg) enqueue_fcg2(h, L, l + 1);
     else enqueue_level(h, L, l + 1, cb, &cmb, ev, false, nullptr);
     // ---- up: prolongation, post-smoothing
+    // the inner FCG's last direction: kp2 (launched inner solve), kp (the persistent tail's)
+    auto kpfin = [&](DevLevel& C) -> const double* {
+        return (h->tail_nops > 0 && l + 1 == h->tail_level) ? C.kp : C.kp2;
+    };
+    // the launched (not tail-run) inner solve without its update kernel: x was never formed
+    auto kfused = [&](DevLevel&) { return kcycle_fused(h) && !(h->tail_nops > 0 && l + 1 == h->tail_level); };
     std::vector<double*> cur(nr), fin(nr), tmp(nr);
     for (int ri = 0; ri < nr; ++ri) {
         RankState& R = h->ranks[ri];
@@ -975,14 +993,20 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
         double* dst = cur[ri];
         const double n8 = 8.0 * (double)D.comp_n;
         if (s1 == 1) {  // u = P-bar e only; the first post-sweep adds m o b (EPost1)
-            if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
-                launch_mat(L, D.P, GXap{C.kx, C.kp, C.kst}, EStore{dst + D.ep_off}, no_red(), "prolong",
+            if (kfcg && kfused(C))  // e = alpha_1 p_1 + alpha_2 p_2 of the inner FCG, formed in the gather
+                launch_mat(L, D.P, GXap2{C.kp, C.kp2, C.kst}, EStore{dst + D.ep_off}, no_red(), "prolong",
+                           n8 + 2 * nc8, part);
+            else if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
+                launch_mat(L, D.P, GXap{C.kx, kpfin(C), C.kst}, EStore{dst + D.ep_off}, no_red(), "prolong",
                            n8 + 2 * nc8, part);
             else
                 launch_mat(L, D.P, GVec{e}, EStore{dst + D.ep_off}, no_red(), "prolong", n8 + nc8, part);
         } else {
-            if (kfcg)
-                launch_mat(L, D.P, GXap{C.kx, C.kp, C.kst}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off},
+            if (kfcg && kfused(C))
+                launch_mat(L, D.P, GXap2{C.kp, C.kp2, C.kst}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off},
+                           no_red(), "prolong", 2 * n8 + 2 * nc8, part);
+            else if (kfcg)
+                launch_mat(L, D.P, GXap{C.kx, kpfin(C), C.kst}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off},
                            no_red(), "prolong", 2 * n8 + 2 * nc8, part);
             else
                 launch_mat(L, D.P, GVec{e}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off}, no_red(), "prolong",
@@ -1073,20 +1097,25 @@ void enqueue_fcg2(amg_hier_s* h, Launch& L, int l) {
     // iteration 1: p = z = B_l b with p^T r (r = b) fused into the cycle's last step
     const DotSink s1{D.kst, FIN_KPR0};
     enqueue_level(h, L, l, bv, &mbv, kp, true, nullptr, &s1);
-    launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(FIN_KALPHA), "kfcg_spmv", 2 * n8);
-    L.begin("kfcg_upd1", 7 * n8);
-    launch_k(k_kupd1, vec_grid(n, nsm), kBlock, L.s, D.kx, D.kr, D.kmb, D.kp, D.kq, D.b, D.m, n,
-             (const double*)D.kst);
-    L.end();
+    const bool fused = kcycle_fused(h);
+    launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(fused ? FIN_KALPHA1 : FIN_KALPHA), "kfcg_spmv",
+               2 * n8);
+    if (!fused) {  // x = alpha p ; r = b - alpha q ; m o r (the SWEEP0 path gathers it)
+        L.begin("kfcg_upd1", 7 * n8);
+        launch_k(k_kupd1, vec_grid(n, nsm), kBlock, L.s, D.kx, D.kr, D.kmb, D.kp, D.kq, D.b, D.m, n,
+                 (const double*)D.kst);
+        L.end();
+    }
     // iteration 2: z = B_l r with z^T q fused -> beta ; p = z + beta p, p^T r ; q = A p, alpha.
     // The final x += alpha p is formed by the consumer (the prolongation gathers x + alpha p).
-    const DotSink s2{D.kst, FIN_KBETA};
+    // fused: r = b - alpha_1 q_1 is formed (and stored in kr) by the application's first kernel,
+    // x = alpha_1 p_1 + alpha_2 p_2 by the consumer (GXap2)
+    const DotSink s2{D.kst, FIN_KBETA, fused ? D.b : nullptr, fused ? D.kq : nullptr};
     const VecOf kq = [l](RankState& R) { return R.lv[l].kq; };
     enqueue_level(h, L, l, kr, &kmb, kz, true, &kq, &s2);
-    L.begin("kfcg_pupd", 4 * n8);
-    launch_k(k_kpupd, vec_grid(n, nsm), kBlock, L.s, D.kp, D.kz, D.kr, n, (const double*)D.kst, kred(FIN_KPR));
-    L.end();
-    launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(FIN_KALPHA), "kfcg_spmv", 2 * n8);
+    // p = z + beta p formed inside q = A p (new p into kp2), p^T q and p^T r in one reduction
+    launch_mat(L, D.A, GKpz{D.kz, D.kp, D.kst}, EKSpmvPupd{D.kz, D.kp, D.kp2, D.kq, D.kr, D.kst},
+               kred(FIN_KALPHA2), "kfcg_spmv_pupd", 5 * n8);
 }
 
 // z0 = B b0 on the level-0 windows (the whole cycle).
@@ -1784,7 +1813,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
         if ((st = dev_alloc(&D.b, wn))) return st;
         if ((st = dev_alloc(&D.xa, wn))) return st;
         if (h->cfg.cycle == 1 && l >= 1 && l + 1 < nl) {
-            for (double** v : {&D.kx, &D.kr, &D.kmb, &D.kz, &D.kp, &D.kq})
+            for (double** v : {&D.kx, &D.kr, &D.kmb, &D.kz, &D.kp, &D.kq, &D.kp2})
                 if ((st = dev_alloc(v, wn))) return st;
             if ((st = dev_alloc(&D.kst, 8))) return st;
         }
@@ -1812,7 +1841,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
     if (!h->multi() && (st = dev_alloc(&R.pp2, w0))) return st;
     if ((st = dev_alloc(&R.pq, w0))) return st;
     if ((st = dev_alloc(&R.st, 1))) return st;
-    if ((st = dev_alloc(&R.partials, kMaxPartials))) return st;
+    if ((st = dev_alloc(&R.partials, 2 * kMaxPartials))) return st;  // two-dot reductions: 2 per block
     if ((st = dev_alloc(&R.ticket, 1))) return st;
     if ((st = dev_alloc(&R.dot_local, kDotSlots))) return st;
     if ((st = dev_alloc(&R.dot_all, (size_t)kDotSlots * h->np))) return st;

@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace cg = cooperative_groups;
 
 namespace amgk {
@@ -52,7 +54,7 @@ struct PcgState {
 // per-level state k[] = {p^T r, p^T q, alpha, beta, stop}.
 enum FinishKind : int32_t {
     FIN_NONE = 0, FIN_BNORM = 1, FIN_RZ = 2, FIN_PQ = 3, FIN_RR = 4, FIN_ZQ = 5, FIN_PR = 6, FIN_PQF = 7,
-    FIN_KPR0 = 8, FIN_KPR = 9, FIN_KALPHA = 10, FIN_KBETA = 11
+    FIN_KPR0 = 8, FIN_KPR = 9, FIN_KALPHA = 10, FIN_KBETA = 11, FIN_KALPHA2 = 12, FIN_KALPHA1 = 13
 };
 // Multi-rank: a dot kernel only writes its local total (rc.out, kind FIN_NONE);
 // the per-rank totals are all-gathered and k_finish sums them in rank order.
@@ -84,6 +86,16 @@ __device__ __forceinline__ void finish(const RedCtx& rc, double total) {
                 k[1] = total;
                 break;
             case FIN_KBETA: k[3] = (k[4] != 0.0) ? 0.0 : -total / k[1]; break;
+            case FIN_KALPHA1:  // the first inner iteration's alpha, also kept as alpha_1 = k[5]
+                if (k[4] != 0.0 || !(total > 0.0)) {
+                    k[2] = 0.0;
+                    k[4] = 1.0;
+                } else {
+                    k[2] = k[0] / total;
+                }
+                k[1] = total;
+                k[5] = k[2];
+                break;
             default: break;
         }
         return;
@@ -154,6 +166,16 @@ __device__ __forceinline__ void finish(const RedCtx& rc, double total) {
     }
 }
 
+// FIN_KALPHA2 (K-cycle, fused direction update): t0 = p^T q, t1 = p^T r; then as FIN_KALPHA.
+__device__ __forceinline__ void finish2(const RedCtx& rc, double t0, double t1) {
+    if (rc.ks && rc.kind == FIN_KALPHA2) {
+        rc.ks[0] = t1;
+        RedCtx r1 = rc;
+        r1.kind = FIN_KALPHA;
+        finish(r1, t0);
+    }
+}
+
 // Deterministic grid reduction: fixed per-block tree, fixed-order sum of the
 // block partials by the last block to arrive.
 __device__ __forceinline__ void grid_reduce(double v, const RedCtx& rc) {
@@ -185,6 +207,61 @@ __device__ __forceinline__ void grid_reduce(double v, const RedCtx& rc) {
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += wsum[w];
         *rc.ticket = 0u;
         finish(rc, tot);
+    }
+}
+
+// Two dots at once (same fixed trees, partials interleaved: 2 doubles per block).
+__device__ __forceinline__ void finish2(const RedCtx& rc, double t0, double t1);
+__device__ __forceinline__ void grid_reduce(double2 v, const RedCtx& rc) {
+    __shared__ double wsum[2][kBlock / 32];
+    __shared__ bool last;
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        wsum[0][wid] = v.x;
+        wsum[1][wid] = v.y;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += wsum[0][w];
+            b += wsum[1][w];
+        }
+        rc.partials[2 * blockIdx.x] = a;
+        rc.partials[2 * blockIdx.x + 1] = b;
+        __threadfence();
+        unsigned int t = atomicAdd(rc.ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double a = 0.0, b = 0.0;
+    for (unsigned int q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
+        a += ((volatile double*)rc.partials)[2 * q];
+        b += ((volatile double*)rc.partials)[2 * q + 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+        wsum[0][wid] = a;
+        wsum[1][wid] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ta = 0.0, tb = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            ta += wsum[0][w];
+            tb += wsum[1][w];
+        }
+        *rc.ticket = 0u;
+        finish2(rc, ta, tb);
     }
 }
 
@@ -264,12 +341,66 @@ struct GXap {
 };
 __device__ __forceinline__ void bind(GXap& g) { g.alpha = g.k[2]; }
 
+// p_j = z_j + beta p_j: the K-cycle inner FCG's second direction formed in the
+// gather of q = A p (beta = k[3] of the level's K state); cf. GPz for the outer PCG
+struct GKpz {
+    static constexpr int kChunk = 4;
+    const double* __restrict__ z;
+    const double* __restrict__ p;
+    const double* k;
+    double beta = 0.0;
+    __device__ __forceinline__ double operator()(int32_t j) const { return __ldg(z + j) + beta * __ldg(p + j); }
+};
+__device__ __forceinline__ void bind(GKpz& g) { g.beta = g.k[3]; }
+
+// e_j = alpha_1 p1_j + alpha_2 p2_j: the K-cycle inner FCG's result x = alpha_1 p_1 +
+// alpha_2 p_2 (x_0 = 0), formed only where it is consumed (the prolongation)
+struct GXap2 {
+    static constexpr int kChunk = 4;
+    const double* __restrict__ p1;
+    const double* __restrict__ p2;
+    const double* k;
+    double a1 = 0.0, a2 = 0.0;
+    __device__ __forceinline__ double operator()(int32_t j) const { return a1 * __ldg(p1 + j) + a2 * __ldg(p2 + j); }
+};
+__device__ __forceinline__ void bind(GXap2& g) {
+    g.a1 = g.k[5];
+    g.a2 = g.k[2];
+}
+// b_j - alpha q_j: the K-cycle inner residual r_1 = b - alpha_1 q_1, formed in the gather
+// of the second cycle application's first kernel (alpha = k[2])
+struct GBaq {
+    static constexpr int kChunk = 4;
+    const double* __restrict__ b;
+    const double* __restrict__ q;
+    const double* k;
+    double alpha = 0.0;
+    __device__ __forceinline__ double operator()(int32_t j) const { return __ldg(b + j) - alpha * __ldg(q + j); }
+};
+__device__ __forceinline__ void bind(GBaq& g) { g.alpha = g.k[2]; }
+
 // ------------------------------------------------------------- epilogues
+// Epilogues that reduce two dot products at once declare `using dot_t = double2;`
+// (the K-cycle's fused direction update: p^T q and p^T r in one pass).
+__device__ __forceinline__ double2& operator+=(double2& a, const double2& b) {
+    a.x += b.x;
+    a.y += b.y;
+    return a;
+}
+template <class E, class = void>
+struct DotOf {
+    using type = double;
+};
+template <class E>
+struct DotOf<E, std::void_t<typename E::dot_t>> {
+    using type = typename E::dot_t;
+};
+
 // An epilogue with `kAbs = true` also receives asum = sum_k |a_ik| of the row it
 // streams, i.e. the l1-Jacobi diagonal 1/m_i (nb = 1), so m_i is
 // recomputed in registers instead of being read from HBM.
 template <class E>
-__device__ __forceinline__ double apply_epi(const E& e, int64_t i, double s, double asum) {
+__device__ __forceinline__ auto apply_epi(const E& e, int64_t i, double s, double asum) {
     if constexpr (E::kAbs) return e(i, s, asum);
     else return e(i, s);
 }
@@ -285,6 +416,25 @@ struct EResid {
         return 0.0;
     }
 };
+// rhs = b - alpha q ; r = rhs - s            (EResid whose right-hand side is the K-cycle
+// inner residual b - alpha_1 q_1, materialised here for the rest of the cycle)
+struct EResidK {
+    static constexpr bool kDot = false;
+    static constexpr bool kAbs = false;
+    const double* __restrict__ b;
+    const double* __restrict__ q;
+    const double* k;
+    double* __restrict__ rhs;
+    double* __restrict__ r;
+    double alpha = 0.0;
+    __device__ __forceinline__ double operator()(int64_t i, double s) const {
+        const double bi = b[i] - alpha * q[i];
+        rhs[i] = bi;
+        r[i] = bi - s;
+        return 0.0;
+    }
+};
+__device__ __forceinline__ void bind(EResidK& e) { e.alpha = e.k[2]; }
 // x' = x + m (b - s)                        (l1-Jacobi sweep, out of place)
 // ABS = true: m_i = 1/asum from the streamed row (short rows); false: m_i read
 // from `m` (long rows, where the extra per-entry |a| chain costs more than 8 B/row).
@@ -467,6 +617,29 @@ struct ESpmvDot {
     }
 };
 
+// q = A p with p = z + beta p_old formed per row (the owner writes p into pnew, a
+// second buffer: neighbours still gather p_old), reducing p^T q and p^T r together
+// (FIN_KALPHA2): the K-cycle's k_kpupd folded into its q = A p
+struct EKSpmvPupd {
+    static constexpr bool kDot = true;
+    static constexpr bool kAbs = false;
+    using dot_t = double2;
+    const double* __restrict__ z;
+    const double* __restrict__ pold;
+    double* __restrict__ pnew;
+    double* __restrict__ q;
+    const double* __restrict__ r;
+    const double* k;
+    double beta = 0.0;
+    __device__ __forceinline__ double2 operator()(int64_t i, double s) const {
+        const double pi = z[i] + beta * pold[i];
+        pnew[i] = pi;
+        q[i] = s;
+        return make_double2(pi * s, pi * r[i]);
+    }
+};
+__device__ __forceinline__ void bind(EKSpmvPupd& e) { e.beta = e.k[3]; }
+
 // ------------------------------------------------------------ SELL-32 kernel
 struct SellView {
     const uint32_t* __restrict__ sptr;  // nslices+1, offsets in units of 32 entries
@@ -535,7 +708,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
-    double d = 0.0;
+    typename DotOf<E>::type d{};
     for (int64_t s = A.s0 + w0; s < A.s1; s += nw) {
         const uint32_t b0 = __ldg(A.sptr + s);
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
@@ -574,7 +747,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
-    double d = 0.0;
+    typename DotOf<E>::type d{};
     for (int64_t s = A.s0 + w0; s < A.s1; s += nw) {
         const uint32_t b0 = __ldg(A.sptr + s);
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
@@ -639,7 +812,7 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
     const int sub = threadIdx.x % VW;
     const int64_t g0 = gid / VW;
     const int64_t ng = ((int64_t)gridDim.x * kBlock) / VW;
-    double d = 0.0;
+    typename DotOf<E>::type d{};
     // every lane of a warp runs the same number of outer iterations (shuffles)
     const int64_t iters = (A.r1 - A.r0 + ng - 1) / ng;
     for (int64_t it = 0; it < iters; ++it) {
@@ -669,7 +842,7 @@ __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc)
     bind(e);
     __shared__ double part[kBlock / 32], apart[kBlock / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double d = 0.0;
+    typename DotOf<E>::type d{};
     for (int64_t row = A.r0 + blockIdx.x; row < A.r1; row += gridDim.x) {
         const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
         double acc = 0.0, asum = 0.0;
