@@ -1137,13 +1137,15 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
     enqueue_vcycle(h, L, [](RankState& R) { return R.pr; }, [](RankState& R) { return R.pz; }, true,
                    fcg ? &qv : nullptr);
     if (!fcg && !h->multi() && h->nlev() > 1) {
-        // p = z + beta p fused into q = A p (p double-buffered, selected on the device)
+        // p = z + beta p fused into q = A p (p double-buffered, selected on the device).  (The
+        // FCG variant, reducing p^T r there as well, measured 1 % slower: its SDIA/SELL kernels
+        // spill under the 32-register bound, so FCG keeps k_pupdate_fcg.)
         RankState& R = h->ranks[0];
         const DevLevel& D = R.L0();
         launch_mat(L, D.A, GPz{R.pz, R.pp, R.pp2, R.st},
                    ESpmvDotPz{R.pz, R.pp, R.pp2, R.pq, x_user + R.user_off, R.st}, dot_red(h, R, FIN_PQ, 0),
                    "spmv_dot_pupd", 48.0 * D.own_n);
-    } else {  // multi-rank or FCG: separate direction update, halo of p, q = A p
+    } else {  // multi-rank, FCG or one level: separate direction update, halo of p, q = A p
         for (auto& R : h->ranks) {
             const DevLevel& D = R.L0();
             if (fcg) {
