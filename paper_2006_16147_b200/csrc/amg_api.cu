@@ -149,6 +149,10 @@ struct DevLevel {
     DevMat Am;
     // INVK smoother (cfg.smoother == 1): D^{-1} W and Z = W^T
     DevMat Wd, Z;
+    // Compact small level (one pre- and one post-sweep, single rank): Rc = R (I - A diag(m)) and
+    // Pc = (I - diag(m) A) P-bar, so the level is s = S2(b), b_{l+1} = Rc b, out = s + Pc e
+    bool compact = false;
+    DevMat Rc, Pc;
     double* m = nullptr;   // window-sized vectors
     double* b = nullptr;
     double* mb = nullptr;
@@ -168,6 +172,8 @@ struct DevLevel {
         Am.release();
         Wd.release();
         Z.release();
+        Rc.release();
+        Pc.release();
         for (double* v : {kx, kr, kmb, kz, kp, kq, kst, kp2}) cudaFree(v);
         cudaFree(m);
         cudaFree(b);
@@ -862,6 +868,54 @@ void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, cons
     if (dot && !sink) dot_finish(h, L, dkind);
 }
 
+// Compact small level (see compact_level_ok): s = S2(b) = m b + m (b - A (m b)) into r;
+// b_{l+1} = Rc b; coarse correction e; out = s + Pc e (+ the K-cycle dot of a sink).
+void enqueue_level_compact(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf& outv, bool dot,
+                           const VecOf* dwv, const DotSink* sink) {
+    const int nl = h->nlev();
+    RankState& R = h->ranks[0];
+    DevLevel& D = R.lv[l];
+    DevLevel& C = R.lv[l + 1];
+    const double* b = bvec(R);
+    double* out = outv(R);
+    const double n8 = 8.0 * (double)D.comp_n, nc8 = 8.0 * (double)C.comp_n;
+    // the smoothing branch s = S2(b) runs on the second stream, concurrently with the
+    // restriction and the whole coarse correction; the post kernel joins it
+    cudaEventRecord(h->ev_fork, L.s);
+    cudaStreamWaitEvent(h->comm, h->ev_fork, 0);
+    {
+        Launch Ls{h, h->comm};
+        launch_mat(Ls, D.A, GMB{D.m, b}, ESweep0{b, D.r}, no_red(), "sweep0_c", 3 * n8);
+    }
+    cudaEventRecord(h->ev_join, h->comm);
+    launch_mat(L, D.Rc, GVec{b}, EStore{C.b}, no_red(), "restrict_c", n8 + nc8);
+    const bool kfcg = h->cfg.cycle == 1 && l + 1 < nl - 1;
+    const VecOf cb = [l](RankState& R) { return R.lv[l + 1].b; };
+    const VecOf cmb = [l](RankState& R) { return R.lv[l + 1].mb; };
+    const VecOf ev = kfcg ? VecOf([l](RankState& R) { return R.lv[l + 1].kx; })
+                          : VecOf([l](RankState& R) { return R.lv[l + 1].xa; });
+    if (h->tail_nops > 0 && l + 1 == h->tail_level) launch_tail(h, L);
+    else if (kfcg) enqueue_fcg2(h, L, l + 1);
+    else enqueue_level(h, L, l + 1, cb, &cmb, ev, false, nullptr);
+    const bool tailc = h->tail_nops > 0 && l + 1 == h->tail_level;
+    // joins this level's smoothing branch (a deeper compact level re-records ev_join later on the
+    // same second stream, which orders after this level's branch: still a correct dependency)
+    cudaStreamWaitEvent(L.s, h->ev_join, 0);
+    auto post = [&](auto g) {
+        if (dot) {
+            const int dkind = dwv ? FIN_ZQ : FIN_RZ;
+            launch_mat(L, D.Pc, g, EAddDot<true>{D.r, out, dwv ? (*dwv)(R) : b}, sink_red(h, R, dkind, sink),
+                       "prolong_post_c", 3 * n8 + nc8);
+            if (!sink) dot_finish(h, L, dkind);
+        } else {
+            launch_mat(L, D.Pc, g, EAddDot<false>{D.r, out}, no_red(), "prolong_post_c", 2 * n8 + nc8);
+        }
+    };
+    if (kfcg && kcycle_fused(h) && !tailc) post(GXap2{C.kp, C.kp2, C.kst});
+    else if (kfcg) post(GXap{C.kx, tailc ? C.kp : C.kp2, C.kst});
+    else post(GVec{ev(R)});
+}
+
 // out = B_l b: the part of the cycle rooted at level l (Eq. 3.1;
 // SURVEY.md §8c O10).  bvec / outv give each rank's level-l WINDOW base pointers;
 // mbvec gives m o b for levels >= 1 (the restriction writes it) and is null at
@@ -893,6 +947,10 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             }
         }
         if (dot && !sink) dot_finish(h, L, dkind);
+        return;
+    }
+    if (h->ranks[0].lv[l].compact && !(sink && sink->kb)) {
+        enqueue_level_compact(h, L, l, bvec, outv, dot, dwv, sink);
         return;
     }
     std::vector<double*> xpre(nr, nullptr);
@@ -1741,6 +1799,73 @@ int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) 
 }
 
 // Uploads one rank's plan.  coarse_inv: the dense A_L^{-1}.
+// ------------------------------------------------------------- compact small levels
+// With one pre- and one post-sweep the level's cycle is (Eq. 3.1, x1 = m o b, R9):
+//   x1 = m b;  b_{l+1} = R (b - A x1);  e = B_{l+1} b_{l+1};  u = x1 + P e;  out = u + m (b - A u)
+//      = [m b + m (b - A (m b))] + (P - diag(m) A P) e  =  S2(b) + Pc e,  b_{l+1} = R (I - A diag m) b = Rc b.
+// On small levels (latency-bound) this is 3 kernels instead of 4, the restriction independent of
+// the smoothing.  Same arithmetic up to rounding order; Rc and Pc are formed once on the host.
+constexpr int64_t kCompactRows = 8192;
+bool compact_level_ok(const amg_hier_s* h, int l, int nl, int64_t n) {
+    return !h->multi() && h->cfg.pre_sweeps == 1 && h->cfg.post_sweeps == 1 && h->cfg.smoother == 0 && l >= 1 &&
+           l + 1 < nl && n <= kCompactRows && !(h->tail_level >= 0 && l >= h->tail_level);
+}
+amgsetup::Csr csr_from_device(const amgsetup::DevCsrRaw& D, cudaStream_t s) {
+    amgsetup::Csr C;
+    C.nrows = D.nrows;
+    C.ncols = D.ncols;
+    C.rp.resize(D.nrows + 1);
+    C.ci.resize(D.nnz);
+    C.v.resize(D.nnz);
+    cudaMemcpyAsync(C.rp.data(), D.rp, (D.nrows + 1) * 8, cudaMemcpyDeviceToHost, s);
+    if (D.nnz) {
+        cudaMemcpyAsync(C.ci.data(), D.ci, D.nnz * 4, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(C.v.data(), D.v, D.nnz * 8, cudaMemcpyDeviceToHost, s);
+    }
+    cudaStreamSynchronize(s);
+    return C;
+}
+// Y = X - diag(lm) Z W  (dense accumulator per row; lm = nullptr: no left scaling; cm: right
+// scaling of Z's columns).  Rc = R - R (A diag m): X = R, Z = R, W = A, cm = m.
+// Pc = P - diag(m) A P: X = P, Z = A, W = P, lm = m.
+amgsetup::Csr minus_product(const amgsetup::Csr& X, const amgsetup::Csr& Z, const amgsetup::Csr& W,
+                            const double* lm, const double* cm) {
+    amgsetup::Csr Y;
+    Y.nrows = X.nrows;
+    Y.ncols = X.ncols;
+    Y.rp.assign(X.nrows + 1, 0);
+    std::vector<double> acc(X.ncols, 0.0);
+    std::vector<char> used(X.ncols, 0);
+    std::vector<int32_t> cols;
+    for (int64_t i = 0; i < X.nrows; ++i) {
+        cols.clear();
+        for (int64_t k = X.rp[i]; k < X.rp[i + 1]; ++k) {
+            const int32_t c = X.ci[k];
+            if (!used[c]) used[c] = 1, cols.push_back(c);
+            acc[c] += X.v[k];
+        }
+        const double li = lm ? lm[i] : 1.0;
+        for (int64_t k = Z.rp[i]; k < Z.rp[i + 1]; ++k) {
+            const int32_t j = Z.ci[k];
+            const double zij = li * Z.v[k];
+            for (int64_t t = W.rp[j]; t < W.rp[j + 1]; ++t) {
+                const int32_t c = W.ci[t];
+                if (!used[c]) used[c] = 1, cols.push_back(c);
+                acc[c] -= zij * W.v[t] * (cm ? cm[c] : 1.0);
+            }
+        }
+        std::sort(cols.begin(), cols.end());
+        for (int32_t c : cols) {
+            Y.ci.push_back(c);
+            Y.v.push_back(acc[c]);
+            acc[c] = 0.0;
+            used[c] = 0;
+        }
+        Y.rp[i + 1] = (int64_t)Y.ci.size();
+    }
+    return Y;
+}
+
 int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<double>& coarse_inv, RankState& R,
                 const amgsetup::DeviceKeep* dk = nullptr) {
     const int nl = (int)P.lv.size();
@@ -1811,6 +1936,26 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
                 if ((st = dev_alloc(&D.r, wn))) return st;
                 if ((st = dev_alloc(&D.xb, wn))) return st;
             }
+        }
+        if (compact_level_ok(h, l, nl, D.comp_n)) {
+            amgsetup::Csr A, Pb, Rt;
+            std::vector<double> m(D.comp_n);
+            if (dk) {
+                A = csr_from_device(dk->A[l], h->ctx->stream);
+                Pb = csr_from_device(dk->P[l], h->ctx->stream);
+                Rt = csr_from_device(dk->R[l], h->ctx->stream);
+                CK(cudaMemcpy(m.data(), dk->m[l], m.size() * 8, cudaMemcpyDeviceToHost));
+            } else {
+                A = S.A;
+                Pb = S.P;
+                Rt = S.R;
+                m = S.m;
+            }
+            const amgsetup::Csr Rc = minus_product(Rt, Rt, A, nullptr, m.data());
+            const amgsetup::Csr Pc = minus_product(Pb, A, Pb, m.data(), nullptr);
+            if ((st = upload_mat(Rc, D.Rc, false, 0))) return st;
+            if ((st = upload_mat(Pc, D.Pc, false, 0))) return st;
+            D.compact = true;
         }
         if ((st = dev_alloc(&D.b, wn))) return st;
         if ((st = dev_alloc(&D.xa, wn))) return st;
@@ -2568,11 +2713,10 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     }
     cudaEventCreate(&h->ev0);
     cudaEventCreate(&h->ev1);
-    if (h->multi()) {
-        CK(cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-    }
+    // second stream: halo exchanges (multi-rank) / the smoothing branch of compact levels
+    CK(cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     CK(cudaDeviceSynchronize());
     h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h;
