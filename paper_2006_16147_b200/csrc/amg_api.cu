@@ -883,12 +883,21 @@ void enqueue_level_compact(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, c
     // restriction and the whole coarse correction; the post kernel joins it
     cudaEventRecord(h->ev_fork, L.s);
     cudaStreamWaitEvent(h->comm, h->ev_fork, 0);
+    const bool krhs = sink && sink->kb;  // K-cycle second application: rhs = b - alpha q, stored in b
     {
         Launch Ls{h, h->comm};
-        launch_mat(Ls, D.A, GMB{D.m, b}, ESweep0{b, D.r}, no_red(), "sweep0_c", 3 * n8);
+        if (krhs)
+            launch_mat(Ls, D.A, GMBaq{D.m, sink->kb, sink->kq, sink->ks},
+                       ESweep0K{sink->kb, sink->kq, sink->ks, const_cast<double*>(b), D.r}, no_red(), "sweep0_c",
+                       5 * n8);
+        else
+            launch_mat(Ls, D.A, GMB{D.m, b}, ESweep0{b, D.r}, no_red(), "sweep0_c", 3 * n8);
     }
     cudaEventRecord(h->ev_join, h->comm);
-    launch_mat(L, D.Rc, GVec{b}, EStore{C.b}, no_red(), "restrict_c", n8 + nc8);
+    if (krhs)
+        launch_mat(L, D.Rc, GBaq{sink->kb, sink->kq, sink->ks}, EStore{C.b}, no_red(), "restrict_c", 2 * n8 + nc8);
+    else
+        launch_mat(L, D.Rc, GVec{b}, EStore{C.b}, no_red(), "restrict_c", n8 + nc8);
     const bool kfcg = h->cfg.cycle == 1 && l + 1 < nl - 1;
     const VecOf cb = [l](RankState& R) { return R.lv[l + 1].b; };
     const VecOf cmb = [l](RankState& R) { return R.lv[l + 1].mb; };
@@ -949,7 +958,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
         if (dot && !sink) dot_finish(h, L, dkind);
         return;
     }
-    if (h->ranks[0].lv[l].compact && !(sink && sink->kb)) {
+    if (h->ranks[0].lv[l].compact) {
         enqueue_level_compact(h, L, l, bvec, outv, dot, dwv, sink);
         return;
     }

@@ -379,6 +379,20 @@ struct GBaq {
 };
 __device__ __forceinline__ void bind(GBaq& g) { g.alpha = g.k[2]; }
 
+// m_j (b_j - alpha q_j): GMB over the K-cycle's second right-hand side (alpha = k[2])
+struct GMBaq {
+    static constexpr int kChunk = 4;
+    const double* __restrict__ m;
+    const double* __restrict__ b;
+    const double* __restrict__ q;
+    const double* k;
+    double alpha = 0.0;
+    __device__ __forceinline__ double operator()(int32_t j) const {
+        return __ldg(m + j) * (__ldg(b + j) - alpha * __ldg(q + j));
+    }
+};
+__device__ __forceinline__ void bind(GMBaq& g) { g.alpha = g.k[2]; }
+
 // ------------------------------------------------------------- epilogues
 // Epilogues that reduce two dot products at once declare `using dot_t = double2;`
 // (the K-cycle's fused direction update: p^T q and p^T r in one pass).
@@ -493,6 +507,26 @@ struct ESweep0 {
         return 0.0;
     }
 };
+// the compact level's smoothing term for the K-cycle's second application, whose rhs is
+// b - alpha q: rhs_i = b_i - alpha q_i is stored, xo = m rhs + m (rhs - s), m from the row (ABS);
+// s = A (m o rhs) comes from the GMBaq gather
+struct ESweep0K {
+    static constexpr bool kDot = false;
+    static constexpr bool kAbs = true;
+    const double* __restrict__ b;
+    const double* __restrict__ q;
+    const double* k;
+    double* __restrict__ rhs;
+    double* __restrict__ xo;
+    double alpha = 0.0;
+    __device__ __forceinline__ double operator()(int64_t i, double s, double asum) const {
+        const double mi = 1.0 / asum, bi = b[i] - alpha * q[i];
+        rhs[i] = bi;
+        xo[i] = mi * bi + mi * (bi - s);
+        return 0.0;
+    }
+};
+__device__ __forceinline__ void bind(ESweep0K& e) { e.alpha = e.k[2]; }
 // y = s                                     (restriction b_{l+1} = P-bar^T r)
 struct EStore {
     static constexpr bool kDot = false;
