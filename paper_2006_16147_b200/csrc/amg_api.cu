@@ -153,6 +153,8 @@ struct DevLevel {
     // Pc = (I - diag(m) A) P-bar, so the level is s = S2(b), b_{l+1} = Rc b, out = s + Pc e
     bool compact = false;
     DevMat Rc, Pc;
+    // collapsed (the compact level just above a direct coarsest solve): M = Pc A_L^{-1} Rc dense
+    double* Mc = nullptr;
     double* m = nullptr;   // window-sized vectors
     double* b = nullptr;
     double* mb = nullptr;
@@ -174,6 +176,8 @@ struct DevLevel {
         Z.release();
         Rc.release();
         Pc.release();
+        cudaFree(Mc);
+        Mc = nullptr;
         for (double* v : {kx, kr, kmb, kz, kp, kq, kst, kp2}) cudaFree(v);
         cudaFree(m);
         cudaFree(b);
@@ -868,6 +872,35 @@ void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, cons
     if (dot && !sink) dot_finish(h, L, dkind);
 }
 
+// Collapsed level (compact, above a direct coarsest solve): out = S2(b) + M b in ONE kernel.
+void enqueue_level_collapsed(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf& outv, bool dot,
+                             const VecOf* dwv, const DotSink* sink) {
+    RankState& R = h->ranks[0];
+    DevLevel& D = R.lv[l];
+    const double* b = bvec(R);
+    double* out = outv(R);
+    const int64_t n = D.comp_n;
+    const CsrView A{D.A.rp, D.A.col, D.A.val, n, 0, n};
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, kMaxPartials));
+    const double bytes = 8.0 * (double)n * (double)n + D.A.model_bytes() + 32.0 * (double)n;
+    const bool krhs = sink && sink->kb;
+    const double* dw = (dot && dwv) ? (*dwv)(R) : nullptr;
+    const int dkind = dwv ? FIN_ZQ : FIN_RZ;
+    const RedCtx red = dot ? sink_red(h, R, dkind, sink) : no_red();
+    L.begin("collapsed", bytes);
+    if (krhs) {
+        const GBaq g{sink->kb, sink->kq, sink->ks};
+        if (dot) launch_k(k_collapsed<GBaq, true, true>, grid, kBlock, L.s, A, D.m, D.Mc, g, const_cast<double*>(b), out, dw, red);
+        else launch_k(k_collapsed<GBaq, false, true>, grid, kBlock, L.s, A, D.m, D.Mc, g, const_cast<double*>(b), out, dw, red);
+    } else {
+        const GVec g{b};
+        if (dot) launch_k(k_collapsed<GVec, true, false>, grid, kBlock, L.s, A, D.m, D.Mc, g, (double*)nullptr, out, dw, red);
+        else launch_k(k_collapsed<GVec, false, false>, grid, kBlock, L.s, A, D.m, D.Mc, g, (double*)nullptr, out, dw, red);
+    }
+    L.end();
+    if (dot && !sink) dot_finish(h, L, dkind);
+}
+
 // Compact small level (see compact_level_ok): s = S2(b) = m b + m (b - A (m b)) into r;
 // b_{l+1} = Rc b; coarse correction e; out = s + Pc e (+ the K-cycle dot of a sink).
 void enqueue_level_compact(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf& outv, bool dot,
@@ -956,6 +989,10 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             }
         }
         if (dot && !sink) dot_finish(h, L, dkind);
+        return;
+    }
+    if (h->ranks[0].lv[l].Mc) {
+        enqueue_level_collapsed(h, L, l, bvec, outv, dot, dwv, sink);
         return;
     }
     if (h->ranks[0].lv[l].compact) {
@@ -1815,6 +1852,7 @@ int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) 
 // On small levels (latency-bound) this is 3 kernels instead of 4, the restriction independent of
 // the smoothing.  Same arithmetic up to rounding order; Rc and Pc are formed once on the host.
 constexpr int64_t kCompactRows = 8192;
+constexpr int64_t kCollapseRows = 2048;  // dense M of the collapsed level: <= 32 MB
 bool compact_level_ok(const amg_hier_s* h, int l, int nl, int64_t n) {
     return !h->multi() && h->cfg.pre_sweeps == 1 && h->cfg.post_sweeps == 1 && h->cfg.smoother == 0 && l >= 1 &&
            l + 1 < nl && n <= kCompactRows && !(h->tail_level >= 0 && l >= h->tail_level);
@@ -1965,6 +2003,24 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
             if ((st = upload_mat(Rc, D.Rc, false, 0))) return st;
             if ((st = upload_mat(Pc, D.Pc, false, 0))) return st;
             D.compact = true;
+            // the level above a direct coarsest solve: the whole rest of the cycle is the linear
+            // map b -> S2(b) + Pc A_L^{-1} Rc b; M = Pc A_L^{-1} Rc formed here (dense, n <= 2048)
+            const int64_t nc = P.lv[l + 1].n_global, n = D.comp_n;
+            if (l + 2 == nl && h->cfg.coarse_solver == 0 && n <= kCollapseRows && D.A.fmt == FMT_CSRV &&
+                (int64_t)coarse_inv.size() == nc * nc) {
+                std::vector<double> T((size_t)nc * n, 0.0), M((size_t)n * n, 0.0);
+                for (int64_t c = 0; c < nc; ++c)  // T = A_L^{-1} Rc
+                    for (int64_t k = Rc.rp[c]; k < Rc.rp[c + 1]; ++k)
+                        for (int64_t a = 0; a < nc; ++a) T[a * n + Rc.ci[k]] += coarse_inv[a * nc + c] * Rc.v[k];
+                for (int64_t i = 0; i < n; ++i)  // M = Pc T
+                    for (int64_t k = Pc.rp[i]; k < Pc.rp[i + 1]; ++k) {
+                        const double pv = Pc.v[k];
+                        const double* Ta = T.data() + (size_t)Pc.ci[k] * n;
+                        double* Mi = M.data() + (size_t)i * n;
+                        for (int64_t j = 0; j < n; ++j) Mi[j] += pv * Ta[j];
+                    }
+                if ((st = dev_copy(&D.Mc, M.data(), M.size()))) return st;
+            }
         }
         if ((st = dev_alloc(&D.b, wn))) return st;
         if ((st = dev_alloc(&D.xa, wn))) return st;
