@@ -8,6 +8,7 @@ for c in 1 2 3; do timeout 900 python bench.py --config $c --no-cpu-baseline > g
 timeout 900 python bench.py --config 5 --grid 192x192x192 --no-cpu-baseline > gpurun_out/snap_c5_192.json 2>/dev/null
 AMG_SETUP_TIMING=1 timeout 900 python bench.py --config 5 --grid 256x256x256 --no-cpu-baseline > gpurun_out/snap_c5_256.json 2> gpurun_out/snap_c5_256.err
 for m in va3s5cs1 ka1 invk; do timeout 900 python bench.py --method $m --no-cpu-baseline > gpurun_out/snap_c4_$m.json 2>/dev/null; done
+timeout 900 python bench.py --method ka1 --config 2 --no-cpu-baseline > gpurun_out/snap_c2_ka1.json 2>/dev/null
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/snap_ref.json 2>/dev/null
 bash tools/profile_round.sh > gpurun_out/prof_round.log 2>&1
 echo snapshot done
