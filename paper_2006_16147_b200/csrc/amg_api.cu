@@ -1880,35 +1880,50 @@ amgsetup::Csr minus_product(const amgsetup::Csr& X, const amgsetup::Csr& Z, cons
     amgsetup::Csr Y;
     Y.nrows = X.nrows;
     Y.ncols = X.ncols;
-    Y.rp.assign(X.nrows + 1, 0);
-    std::vector<double> acc(X.ncols, 0.0);
-    std::vector<char> used(X.ncols, 0);
-    std::vector<int32_t> cols;
-    for (int64_t i = 0; i < X.nrows; ++i) {
-        cols.clear();
-        for (int64_t k = X.rp[i]; k < X.rp[i + 1]; ++k) {
-            const int32_t c = X.ci[k];
-            if (!used[c]) used[c] = 1, cols.push_back(c);
-            acc[c] += X.v[k];
-        }
-        const double li = lm ? lm[i] : 1.0;
-        for (int64_t k = Z.rp[i]; k < Z.rp[i + 1]; ++k) {
-            const int32_t j = Z.ci[k];
-            const double zij = li * Z.v[k];
-            for (int64_t t = W.rp[j]; t < W.rp[j + 1]; ++t) {
-                const int32_t c = W.ci[t];
+    std::vector<std::vector<int32_t>> rc(X.nrows);
+    std::vector<std::vector<double>> rv(X.nrows);
+#pragma omp parallel
+    {
+        std::vector<double> acc(X.ncols, 0.0);
+        std::vector<char> used(X.ncols, 0);
+        std::vector<int32_t> cols;
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < X.nrows; ++i) {
+            cols.clear();
+            for (int64_t k = X.rp[i]; k < X.rp[i + 1]; ++k) {
+                const int32_t c = X.ci[k];
                 if (!used[c]) used[c] = 1, cols.push_back(c);
-                acc[c] -= zij * W.v[t] * (cm ? cm[c] : 1.0);
+                acc[c] += X.v[k];
+            }
+            const double li = lm ? lm[i] : 1.0;
+            for (int64_t k = Z.rp[i]; k < Z.rp[i + 1]; ++k) {
+                const int32_t j = Z.ci[k];
+                const double zij = li * Z.v[k];
+                for (int64_t t = W.rp[j]; t < W.rp[j + 1]; ++t) {
+                    const int32_t c = W.ci[t];
+                    if (!used[c]) used[c] = 1, cols.push_back(c);
+                    acc[c] -= zij * W.v[t] * (cm ? cm[c] : 1.0);
+                }
+            }
+            std::sort(cols.begin(), cols.end());
+            rc[i].reserve(cols.size());
+            rv[i].reserve(cols.size());
+            for (int32_t c : cols) {
+                rc[i].push_back(c);
+                rv[i].push_back(acc[c]);
+                acc[c] = 0.0;
+                used[c] = 0;
             }
         }
-        std::sort(cols.begin(), cols.end());
-        for (int32_t c : cols) {
-            Y.ci.push_back(c);
-            Y.v.push_back(acc[c]);
-            acc[c] = 0.0;
-            used[c] = 0;
-        }
-        Y.rp[i + 1] = (int64_t)Y.ci.size();
+    }
+    Y.rp.assign(X.nrows + 1, 0);
+    for (int64_t i = 0; i < X.nrows; ++i) Y.rp[i + 1] = Y.rp[i] + (int64_t)rc[i].size();
+    Y.ci.resize(Y.rp[X.nrows]);
+    Y.v.resize(Y.rp[X.nrows]);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < X.nrows; ++i) {
+        std::copy(rc[i].begin(), rc[i].end(), Y.ci.begin() + Y.rp[i]);
+        std::copy(rv[i].begin(), rv[i].end(), Y.v.begin() + Y.rp[i]);
     }
     return Y;
 }
@@ -2012,6 +2027,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
                 for (int64_t c = 0; c < nc; ++c)  // T = A_L^{-1} Rc
                     for (int64_t k = Rc.rp[c]; k < Rc.rp[c + 1]; ++k)
                         for (int64_t a = 0; a < nc; ++a) T[a * n + Rc.ci[k]] += coarse_inv[a * nc + c] * Rc.v[k];
+#pragma omp parallel for schedule(static)
                 for (int64_t i = 0; i < n; ++i)  // M = Pc T
                     for (int64_t k = Pc.rp[i]; k < Pc.rp[i + 1]; ++k) {
                         const double pv = Pc.v[k];
