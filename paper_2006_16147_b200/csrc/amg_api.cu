@@ -880,22 +880,21 @@ void enqueue_level_collapsed(amg_hier_s* h, Launch& L, int l, const VecOf& bvec,
     const double* b = bvec(R);
     double* out = outv(R);
     const int64_t n = D.comp_n;
-    const CsrView A{D.A.rp, D.A.col, D.A.val, n, 0, n};
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, kMaxPartials));
-    const double bytes = 8.0 * (double)n * (double)n + D.A.model_bytes() + 32.0 * (double)n;
     const bool krhs = sink && sink->kb;
     const double* dw = (dot && dwv) ? (*dwv)(R) : nullptr;
     const int dkind = dwv ? FIN_ZQ : FIN_RZ;
     const RedCtx red = dot ? sink_red(h, R, dkind, sink) : no_red();
-    L.begin("collapsed", bytes);
+    L.begin("collapsed", 8.0 * (double)n * (double)n + 16.0 * (double)n);
     if (krhs) {
         const GBaq g{sink->kb, sink->kq, sink->ks};
-        if (dot) launch_k(k_collapsed<GBaq, true, true>, grid, kBlock, L.s, A, D.m, D.Mc, g, const_cast<double*>(b), out, dw, red);
-        else launch_k(k_collapsed<GBaq, false, true>, grid, kBlock, L.s, A, D.m, D.Mc, g, const_cast<double*>(b), out, dw, red);
+        double* rhs = const_cast<double*>(b);
+        if (dot) launch_k(k_collapsed<GBaq, true, true>, grid, kBlock, L.s, (const double*)D.Mc, n, g, rhs, out, dw, red);
+        else launch_k(k_collapsed<GBaq, false, true>, grid, kBlock, L.s, (const double*)D.Mc, n, g, rhs, out, dw, red);
     } else {
         const GVec g{b};
-        if (dot) launch_k(k_collapsed<GVec, true, false>, grid, kBlock, L.s, A, D.m, D.Mc, g, (double*)nullptr, out, dw, red);
-        else launch_k(k_collapsed<GVec, false, false>, grid, kBlock, L.s, A, D.m, D.Mc, g, (double*)nullptr, out, dw, red);
+        if (dot) launch_k(k_collapsed<GVec, true, false>, grid, kBlock, L.s, (const double*)D.Mc, n, g, (double*)nullptr, out, dw, red);
+        else launch_k(k_collapsed<GVec, false, false>, grid, kBlock, L.s, (const double*)D.Mc, n, g, (double*)nullptr, out, dw, red);
     }
     L.end();
     if (dot && !sink) dot_finish(h, L, dkind);
@@ -1852,7 +1851,71 @@ int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) 
 // On small levels (latency-bound) this is 3 kernels instead of 4, the restriction independent of
 // the smoothing.  Same arithmetic up to rounding order; Rc and Pc are formed once on the host.
 constexpr int64_t kCompactRows = 8192;
-constexpr int64_t kCollapseRows = 2048;  // dense M of the collapsed level: <= 32 MB
+constexpr int64_t kCollapseRows = 2048;  // dense B of the collapsed level: <= 32 MB
+bool collapse_level_ok(const amg_hier_s* h, int l, int nl, int64_t n) {
+    return !h->multi() && h->cfg.smoother == 0 && h->cfg.coarse_solver == 0 && l >= 1 && l + 2 == nl &&
+           n <= kCollapseRows && !(h->tail_level >= 0 && l >= h->tail_level);
+}
+// C = X D (X sparse n x k CSR, D dense k x w row-major) -> dense n x w
+std::vector<double> sp_dense(const amgsetup::Csr& X, const std::vector<double>& D, int64_t w) {
+    std::vector<double> C((size_t)X.nrows * w, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < X.nrows; ++i) {
+        double* Ci = C.data() + (size_t)i * w;
+        for (int64_t k = X.rp[i]; k < X.rp[i + 1]; ++k) {
+            const double x = X.v[k];
+            const double* Dk = D.data() + (size_t)X.ci[k] * w;
+            for (int64_t j = 0; j < w; ++j) Ci[j] += x * Dk[j];
+        }
+    }
+    return C;
+}
+// The cycle rooted at level l (s1 pre- / s2 post-sweeps of l1-Jacobi, exact coarsest solve
+// A_L^{-1} = Cinv one level down) as a dense matrix B (Eq. 3.1, R9): with E = I - diag(m) A,
+//   Spre = sum_{t<s1} E^t diag(m);  U = Spre + P-bar Cinv R (I - A Spre);
+//   B = U, then s2 times B <- E B + diag(m).
+std::vector<double> dense_level_operator(const amgsetup::Csr& A, const amgsetup::Csr& Pb, const amgsetup::Csr& Rt,
+                                         const std::vector<double>& m, const std::vector<double>& Cinv, int s1,
+                                         int s2) {
+    const int64_t n = A.nrows, nc = Rt.nrows;
+    auto diag_m = [&]() {
+        std::vector<double> D((size_t)n * n, 0.0);
+        for (int64_t i = 0; i < n; ++i) D[(size_t)i * n + i] = m[i];
+        return D;
+    };
+    auto applyE = [&](const std::vector<double>& X) {  // E X = X - diag(m) (A X)
+        std::vector<double> AX = sp_dense(A, X, n), Y(X);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = 0; j < n; ++j) Y[(size_t)i * n + j] -= m[i] * AX[(size_t)i * n + j];
+        return Y;
+    };
+    std::vector<double> G = diag_m(), Spre = G;
+    for (int t = 1; t < s1; ++t) {
+        G = applyE(G);
+        for (size_t q = 0; q < Spre.size(); ++q) Spre[q] += G[q];
+    }
+    std::vector<double> W = sp_dense(A, Spre, n);  // W = I - A Spre
+    for (size_t q = 0; q < W.size(); ++q) W[q] = -W[q];
+    for (int64_t i = 0; i < n; ++i) W[(size_t)i * n + i] += 1.0;
+    const std::vector<double> V = sp_dense(Rt, W, n);  // nc x n
+    std::vector<double> Y((size_t)nc * n, 0.0);      // Y = Cinv V
+#pragma omp parallel for schedule(static)
+    for (int64_t a = 0; a < nc; ++a)
+        for (int64_t c = 0; c < nc; ++c) {
+            const double ca = Cinv[(size_t)a * nc + c];
+            const double* Vc = V.data() + (size_t)c * n;
+            double* Ya = Y.data() + (size_t)a * n;
+            for (int64_t j = 0; j < n; ++j) Ya[j] += ca * Vc[j];
+        }
+    std::vector<double> B = sp_dense(Pb, Y, n);  // U = Spre + P-bar Y
+    for (size_t q = 0; q < B.size(); ++q) B[q] += Spre[q];
+    for (int t = 0; t < s2; ++t) {
+        B = applyE(B);
+        for (int64_t i = 0; i < n; ++i) B[(size_t)i * n + i] += m[i];
+    }
+    return B;
+}
 bool compact_level_ok(const amg_hier_s* h, int l, int nl, int64_t n) {
     return !h->multi() && h->cfg.pre_sweeps == 1 && h->cfg.post_sweeps == 1 && h->cfg.smoother == 0 && l >= 1 &&
            l + 1 < nl && n <= kCompactRows && !(h->tail_level >= 0 && l >= h->tail_level);
@@ -2018,25 +2081,26 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
             if ((st = upload_mat(Rc, D.Rc, false, 0))) return st;
             if ((st = upload_mat(Pc, D.Pc, false, 0))) return st;
             D.compact = true;
-            // the level above a direct coarsest solve: the whole rest of the cycle is the linear
-            // map b -> S2(b) + Pc A_L^{-1} Rc b; M = Pc A_L^{-1} Rc formed here (dense, n <= 2048)
-            const int64_t nc = P.lv[l + 1].n_global, n = D.comp_n;
-            if (l + 2 == nl && h->cfg.coarse_solver == 0 && n <= kCollapseRows && D.A.fmt == FMT_CSRV &&
-                (int64_t)coarse_inv.size() == nc * nc) {
-                std::vector<double> T((size_t)nc * n, 0.0), M((size_t)n * n, 0.0);
-                for (int64_t c = 0; c < nc; ++c)  // T = A_L^{-1} Rc
-                    for (int64_t k = Rc.rp[c]; k < Rc.rp[c + 1]; ++k)
-                        for (int64_t a = 0; a < nc; ++a) T[a * n + Rc.ci[k]] += coarse_inv[a * nc + c] * Rc.v[k];
-#pragma omp parallel for schedule(static)
-                for (int64_t i = 0; i < n; ++i)  // M = Pc T
-                    for (int64_t k = Pc.rp[i]; k < Pc.rp[i + 1]; ++k) {
-                        const double pv = Pc.v[k];
-                        const double* Ta = T.data() + (size_t)Pc.ci[k] * n;
-                        double* Mi = M.data() + (size_t)i * n;
-                        for (int64_t j = 0; j < n; ++j) Mi[j] += pv * Ta[j];
-                    }
-                if ((st = dev_copy(&D.Mc, M.data(), M.size()))) return st;
+        }
+        if (collapse_level_ok(h, l, nl, D.comp_n) &&
+            (int64_t)coarse_inv.size() == P.lv[l + 1].n_global * P.lv[l + 1].n_global) {
+            // the level above a direct coarsest solve: its whole cycle is a fixed linear map B
+            amgsetup::Csr A, Pb, Rt;
+            std::vector<double> m(D.comp_n);
+            if (dk) {
+                A = csr_from_device(dk->A[l], h->ctx->stream);
+                Pb = csr_from_device(dk->P[l], h->ctx->stream);
+                Rt = csr_from_device(dk->R[l], h->ctx->stream);
+                CK(cudaMemcpy(m.data(), dk->m[l], m.size() * 8, cudaMemcpyDeviceToHost));
+            } else {
+                A = S.A;
+                Pb = S.P;
+                Rt = S.R;
+                m = S.m;
             }
+            const std::vector<double> B =
+                dense_level_operator(A, Pb, Rt, m, coarse_inv, h->cfg.pre_sweeps, h->cfg.post_sweeps);
+            if ((st = dev_copy(&D.Mc, B.data(), B.size()))) return st;
         }
         if ((st = dev_alloc(&D.b, wn))) return st;
         if ((st = dev_alloc(&D.xa, wn))) return st;

@@ -998,54 +998,31 @@ __global__ void __launch_bounds__(kBlock) k_unpack(double* __restrict__ v, const
         v[idx[k]] = buf[k];
 }
 
-// The level just above the coarsest, collapsed (compact level + direct coarsest solve):
-//   out = m b + m (b - A (m o b)) + M b,  M = Pc A_L^{-1} Rc  (dense, precomputed)
-// one warp per row: the sparse row of A (m recomputed from it: the l1 diagonal) and the dense
-// row of M, both gathering b through G (GVec, or GBaq for the K-cycle's b - alpha q, whose
-// values are then stored in rhs); DOT reduces dw_i out_i (dw = nullptr: the rhs itself).
+// The level just above a direct coarsest solve, collapsed: the whole rest of the cycle from
+// that level is a fixed linear map, out = B b with B dense (formed at setup), one 256-thread
+// block per row; G gathers b (GVec, or GBaq for the K-cycle's b - alpha q, whose values are then
+// stored in rhs); DOT reduces dw_i out_i (dw = nullptr: the rhs itself).
 template <class G, bool DOT, bool STORE_RHS>
-__global__ void __launch_bounds__(kBlock) k_collapsed(CsrView A, const double* __restrict__ m,
-                                                      const double* __restrict__ M, G g, double* __restrict__ rhs,
-                                                      double* __restrict__ out, const double* __restrict__ dw,
-                                                      RedCtx rc) {
-    // one 256-thread block per row (a warp per row left the dense row's loads latency-bound)
+__global__ void __launch_bounds__(kBlock) k_collapsed(const double* __restrict__ B, int64_t n, G g,
+                                                      double* __restrict__ rhs, double* __restrict__ out,
+                                                      const double* __restrict__ dw, RedCtx rc) {
     pdl_begin();
     bind(g);
-    __shared__ double part[3][kBlock / 32];
-    const int64_t n = A.n;
+    __shared__ double part[kBlock / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double d = 0.0;
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        double acc1 = 0.0, asum = 0.0, acc2 = 0.0;
-        for (int32_t k = __ldg(A.rp + i) + (int32_t)threadIdx.x; k < __ldg(A.rp + i + 1); k += kBlock) {
-            const int32_t c = __ldg(A.ci + k);
-            const double a = __ldg(A.v + k);
-            acc1 += a * (__ldg(m + c) * g(c));
-            asum += fabs(a);
-        }
-        const double* Mi = M + i * n;
-        for (int64_t j = threadIdx.x; j < n; j += kBlock) acc2 += __ldg(Mi + j) * g((int32_t)j);
-        for (int o = 16; o > 0; o >>= 1) {
-            acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
-            asum += __shfl_xor_sync(0xffffffffu, asum, o);
-            acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
-        }
-        if (lane == 0) {
-            part[0][wid] = acc1;
-            part[1][wid] = asum;
-            part[2][wid] = acc2;
-        }
+        const double* Bi = B + i * n;
+        double acc = 0.0;
+        for (int64_t j = threadIdx.x; j < n; j += kBlock) acc += __ldg(Bi + j) * g((int32_t)j);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) part[wid] = acc;
         __syncthreads();
         if (threadIdx.x == 0) {
-            double s1 = 0.0, sa = 0.0, s2 = 0.0;
-            for (int w = 0; w < kBlock / 32; ++w) {
-                s1 += part[0][w];
-                sa += part[1][w];
-                s2 += part[2][w];
-            }
-            const double bi = g((int32_t)i), mi = 1.0 / sa;
-            const double v = mi * bi + mi * (bi - s1) + s2;
+            double v = 0.0;
+            for (int w = 0; w < kBlock / 32; ++w) v += part[w];
             out[i] = v;
+            const double bi = (STORE_RHS || (DOT && !dw)) ? g((int32_t)i) : 0.0;
             if constexpr (STORE_RHS) rhs[i] = bi;
             if constexpr (DOT) d += (dw ? dw[i] : bi) * v;
         }
