@@ -290,3 +290,24 @@ def test_full_c4_hierarchy_and_vcycle_vs_oracle(ctx):
     zo = ho.vcycle(r)
     rel = np.linalg.norm(z - zo) / np.linalg.norm(zo)
     assert rel <= VCYCLE_TOL, rel
+
+
+def test_compact_and_collapsed_levels_are_taken(ctx):
+    """c2's deep levels run in the compact form (S2(b) on the second stream, Rc restriction,
+    Pc prolongation+post) and the level above the coarsest as one dense GEMV; the parity cases
+    above check their numbers against the oracle, this checks the paths are actually used."""
+    amg = _amg()
+    A, b, _ = config_problem(2)
+    h = amg.Hierarchy(ctx, A)
+    names = [k["name"] for k in h.profile_vcycle(1)]
+    assert "collapsed" in names and "restrict_c" in names and "sweep0_c" in names
+    assert names.count("collapsed") == 1 and "coarse_gemv" not in names
+    # and 2/2 sweeps collapse too (general dense level operator)
+    A3 = poisson7(32, 32, 32, (1.0, 1.0, 0.01))
+    h3 = amg.Hierarchy(ctx, A3, cfg=amg.make_config(pre_sweeps=2, post_sweeps=2))
+    ho = O.OracleHierarchy(A3, pre_sweeps=2, post_sweeps=2)
+    assert "collapsed" in [k["name"] for k in h3.profile_vcycle(1)]
+    r = uniform_pm1(4242, A3.n_global)
+    z = h3.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    zo = ho.vcycle(r)
+    assert np.linalg.norm(z - zo) / np.linalg.norm(zo) <= VCYCLE_TOL
