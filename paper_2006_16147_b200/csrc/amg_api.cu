@@ -1496,7 +1496,9 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bo
     const double want = 148.0 * 2048.0 / (double)std::max<int64_t>(n, 1);
     int vw = 2;
     while (vw < 32 && (vw < want || vw * 8 < mean) && vw * 2 <= std::max(2.0, mean)) vw *= 2;
-    if (mean >= 256.0 && (double)n < 18944.0) vw = kVWBlock;
+    // block per row: few long rows, or rows long enough (>= 1024) to give every thread of a block
+    // several entries (c5 A_3 at 256^3: 34k rows x 2,695 -> 5.6 vs 4.5 TB/s in spmv_lab3)
+    if ((mean >= 256.0 && (double)n < 18944.0) || mean >= 1024.0) vw = kVWBlock;
     D.vw = vw;
     D.units = n;
     if (own_lo >= 0) interior_run(rowin, D.ib0, D.ib1);
@@ -1754,7 +1756,9 @@ int convert_mat(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t sh
     const double want = 148.0 * 2048.0 / (double)std::max<int64_t>(n, 1);
     int vw = 2;
     while (vw < 32 && (vw < want || vw * 8 < mean) && vw * 2 <= std::max(2.0, mean)) vw *= 2;
-    if (mean >= 256.0 && (double)n < 18944.0) vw = kVWBlock;
+    // block per row: few long rows, or rows long enough (>= 1024) to give every thread of a block
+    // several entries (c5 A_3 at 256^3: 34k rows x 2,695 -> 5.6 vs 4.5 TB/s in spmv_lab3)
+    if ((mean >= 256.0 && (double)n < 18944.0) || mean >= 1024.0) vw = kVWBlock;
     D.vw = vw;
     D.units = n;
     CK(cudaMalloc((void**)&D.rp, (n + 1) * 4));
