@@ -178,6 +178,18 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
 int amg_solve_host(amg_hier_t h, const double* b_host, double* x_host, double rtol,
                    int32_t maxit, amg_report_t* rep);
 
+/* nrhs independent solves with the same hierarchy on HOST buffers: right-hand side k is
+ * B_host[k*n .. k*n+n-1] (n = this rank's local rows), its solution goes to X_host at the
+ * same offset.  The copies are pipelined with the solves (b_{k+1} travels host->device and
+ * x_{k-1} device->host while solve k runs, two device buffer pairs, a copy stream); every
+ * solve is exactly amg_solve's (bitwise the same x).  For the overlap B_host / X_host should
+ * be pinned (cudaHostAlloc / cudaHostRegister); pageable buffers still give correct results.
+ * `reps` may be NULL or hold nrhs reports (solve_s of each = the batch time / nrhs).  Returns
+ * the first non-AMG_OK status of the batch (AMG_NOT_CONVERGED / AMG_ERR_BREAKDOWN: x valid).
+ * Multi-rank contexts or use_graphs = 0: the solves run one after another (amg_solve_host). */
+int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, double* X_host, double rtol,
+                         int32_t maxit, amg_report_t* reps);
+
 /* One application of the preconditioner z = B r, i.e. one V-cycle
  * (Eq. 3.1).  Device buffers, local rows. */
 int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev);

@@ -146,6 +146,21 @@ class Hierarchy:
         check(code, "amg_solve_host", ok=(AMG_OK, AMG_NOT_CONVERGED))
         return x, rep.as_dict()
 
+    def solve_host_batch(self, B: np.ndarray, X: np.ndarray | None = None, rtol: float = 1e-6,
+                         maxit: int = 500):
+        """amg_solve_host_batch: nrhs solves on host buffers (rows of B, C-contiguous), copies
+        pipelined with the solves (pin B and X, e.g. torch.empty(...).pin_memory(), for overlap)."""
+        if not (isinstance(B, np.ndarray) and B.dtype == np.float64 and B.flags.c_contiguous):
+            B = np.ascontiguousarray(B, dtype=np.float64)
+        nrhs = B.shape[0] if B.ndim == 2 else 1
+        if X is None:
+            X = np.empty_like(B)
+        reps = (amg_report_t * max(1, nrhs))()
+        code = lib.amg_solve_host_batch(self.h, int(nrhs), _ptr(B), _ptr(X), float(rtol), int(maxit),
+                                        C.cast(reps, C.c_void_p))
+        check(code, "amg_solve_host_batch", ok=(AMG_OK, AMG_NOT_CONVERGED))
+        return X, [reps[k].as_dict() for k in range(nrhs)]
+
     def precond_apply(self, r, z=None):
         """amg_precond_apply: one V-cycle z = B r on CUDA tensors."""
         import torch

@@ -266,6 +266,11 @@ struct amg_hier_s {
     cudaGraphExec_t solve_exec = nullptr;
     const double* solve_b = nullptr;
     double* solve_x = nullptr;
+    // pipelined host batch (amg_solve_host_batch): two device (b, x) pairs and their graphs
+    double* bb[2] = {nullptr, nullptr};
+    double* bx[2] = {nullptr, nullptr};
+    cudaGraphExec_t batch_exec[2] = {nullptr, nullptr};
+    cudaStream_t cstream = nullptr, dstream = nullptr;  // host->device / device->host copies
     cudaGraphExec_t apply_exec = nullptr;
     const double* apply_r = nullptr;
     double* apply_z = nullptr;
@@ -290,6 +295,13 @@ struct amg_hier_s {
         cudaFree(tail_prog);
         cudaFree(tail_partials);
         if (solve_exec) cudaGraphExecDestroy(solve_exec);
+        for (int q = 0; q < 2; ++q) {
+            if (batch_exec[q]) cudaGraphExecDestroy(batch_exec[q]);
+            cudaFree(bb[q]);
+            cudaFree(bx[q]);
+        }
+        if (cstream) cudaStreamDestroy(cstream);
+        if (dstream) cudaStreamDestroy(dstream);
         if (apply_exec) cudaGraphExecDestroy(apply_exec);
         for (auto& R : ranks) R.release();
         cudaFree(hb);
@@ -2193,12 +2205,21 @@ void hier_stats(amg_hier_s* h, const amgsetup::Hierarchy& H) {
     byte_model(h, H);
 }
 
+int build_solve_exec(amg_hier_s* h, const double* b, double* x, cudaGraphExec_t* out);
 int ensure_solve_graph(amg_hier_s* h, const double* b, double* x) {
     if (h->solve_exec && h->solve_b == b && h->solve_x == x) return AMG_OK;
     if (h->solve_exec) {
         cudaGraphExecDestroy(h->solve_exec);
         h->solve_exec = nullptr;
     }
+    int st = build_solve_exec(h, b, x, &h->solve_exec);
+    if (st) return st;
+    h->solve_b = b;
+    h->solve_x = x;
+    return AMG_OK;
+}
+// the whole solve as one graph: prologue, WHILE node over the PCG body, final x update
+int build_solve_exec(amg_hier_s* h, const double* b, double* x, cudaGraphExec_t* out) {
     cudaStream_t s = h->ctx->stream;
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
@@ -2227,10 +2248,8 @@ int ensure_solve_graph(amg_hier_s* h, const double* b, double* x) {
     CK(cudaStreamBeginCaptureToGraph(s, g, &wnode, nullptr, 1, cudaStreamCaptureModeThreadLocal));
     enqueue_pcg_final(h, L, x);
     CK(cudaStreamEndCapture(s, &g));
-    CK(cudaGraphInstantiate(&h->solve_exec, g, 0));
+    CK(cudaGraphInstantiate(out, g, 0));
     CK(cudaGraphDestroy(g));
-    h->solve_b = b;
-    h->solve_x = x;
     return AMG_OK;
 }
 
@@ -2931,6 +2950,101 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
         set_err("amg_solve: breakdown, p^T A p <= 0");
     }
     if (rep) rep->status = code;
+    return code;
+}
+
+int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, double* X_host, double rtol,
+                         int32_t maxit, amg_report_t* reps) {
+    if (!h || nrhs < 0 || (nrhs > 0 && (!B_host || !X_host)) || rtol < 0.0 || maxit < 0) {
+        set_err("amg_solve_host_batch: bad argument");
+        return AMG_ERR_ARG;
+    }
+    CK(cudaSetDevice(h->ctx->device));
+    const int64_t n = h->n0_local;
+    int code = AMG_OK;
+    if (h->multi() || !h->cfg.use_graphs) {  // no pipelining: one solve after another
+        for (int32_t k = 0; k < nrhs; ++k) {
+            const int c = amg_solve_host(h, B_host + k * n, X_host + k * n, rtol, maxit, reps ? reps + k : nullptr);
+            if (c != AMG_OK && c != AMG_NOT_CONVERGED && c != AMG_ERR_BREAKDOWN) return c;
+            if (code == AMG_OK) code = c;
+        }
+        return code;
+    }
+    int st;
+    for (int q = 0; q < 2; ++q) {
+        if (!h->bb[q] && (st = dev_alloc(&h->bb[q], n))) return st;
+        if (!h->bx[q] && (st = dev_alloc(&h->bx[q], n))) return st;
+        if (!h->batch_exec[q] && (st = build_solve_exec(h, h->bb[q], h->bx[q], &h->batch_exec[q]))) return st;
+    }
+    if (!h->cstream) CK(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    if (!h->dstream) CK(cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking));
+    // separate copy streams: b_{k+1} must not queue behind x_k's copy (which waits for solve k)
+    cudaStream_t s = h->ctx->stream, cs = h->cstream, ds = h->dstream;
+    PcgState* sts = nullptr;  // [0]: the initial state, [1 + k]: solve k's final state
+    CK(cudaMallocHost((void**)&sts, sizeof(PcgState) * (size_t)(nrhs + 1)));
+    PcgState init{};
+    init.rtol = rtol;
+    init.maxit = maxit;
+    sts[0] = init;
+    cudaEvent_t h2d[2], solved[2], d2h[2];
+    for (int q = 0; q < 2; ++q) {
+        cudaEventCreateWithFlags(&h2d[q], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&solved[q], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&d2h[q], cudaEventDisableTiming);
+    }
+    RankState& R = h->ranks[0];
+    CK(cudaEventRecord(h->ev0, s));
+    CK(cudaStreamWaitEvent(cs, h->ev0, 0));
+    CK(cudaStreamWaitEvent(ds, h->ev0, 0));
+    for (int32_t k = 0; k < nrhs; ++k) {
+        const int q = k & 1;
+        // b_k -> bb[q] once solve k-2 (the last reader of bb[q]) is done
+        if (k >= 2) CK(cudaStreamWaitEvent(cs, solved[q], 0));
+        CK(cudaMemcpyAsync(h->bb[q], B_host + k * n, sizeof(double) * n, cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(h2d[q], cs));
+        // solve k once b_k is there and x_{k-2} has left bx[q]
+        CK(cudaStreamWaitEvent(s, h2d[q], 0));
+        if (k >= 2) CK(cudaStreamWaitEvent(s, d2h[q], 0));
+        CK(cudaMemcpyAsync(R.st, &sts[0], sizeof(PcgState), cudaMemcpyHostToDevice, s));
+        CK(cudaGraphLaunch(h->batch_exec[q], s));
+        CK(cudaMemcpyAsync(&sts[1 + k], R.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(solved[q], s));
+        // x_k -> host while the next solves run
+        CK(cudaStreamWaitEvent(ds, solved[q], 0));
+        CK(cudaMemcpyAsync(X_host + k * n, h->bx[q], sizeof(double) * n, cudaMemcpyDeviceToHost, ds));
+        CK(cudaEventRecord(d2h[q], ds));
+    }
+    CK(cudaStreamWaitEvent(s, d2h[0], 0));
+    CK(cudaStreamWaitEvent(s, d2h[1], 0));
+    CK(cudaEventRecord(h->ev1, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(cs));
+    CK(cudaStreamSynchronize(ds));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    for (int32_t k = 0; k < nrhs; ++k) {
+        const PcgState& S = sts[1 + k];
+        int c = AMG_OK;
+        if (S.status == ST_MAXIT) c = AMG_NOT_CONVERGED;
+        if (S.status == ST_BREAKDOWN) c = AMG_ERR_BREAKDOWN;
+        if (code == AMG_OK) code = c;
+        if (reps) {
+            fill_report(h, reps + k);
+            reps[k].iterations = S.iter;
+            reps[k].final_relres = S.relres;
+            reps[k].converged = (S.status == ST_CONVERGED || S.status == ST_ZERO_RHS) ? 1 : 0;
+            reps[k].solve_s = ms * 1e-3 / (double)std::max(1, nrhs);
+            reps[k].status = c;
+        }
+    }
+    for (int q = 0; q < 2; ++q) {
+        cudaEventDestroy(h2d[q]);
+        cudaEventDestroy(solved[q]);
+        cudaEventDestroy(d2h[q]);
+    }
+    cudaFreeHost(sts);
+    if (code == AMG_ERR_BREAKDOWN) set_err("amg_solve_host_batch: breakdown, p^T A p <= 0");
+    CK(cudaGetLastError());
     return code;
 }
 

@@ -311,3 +311,25 @@ def test_compact_and_collapsed_levels_are_taken(ctx):
     z = h3.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
     zo = ho.vcycle(r)
     assert np.linalg.norm(z - zo) / np.linalg.norm(zo) <= VCYCLE_TOL
+
+
+def test_solve_host_batch_equals_single_solves(ctx):
+    """amg_solve_host_batch (copies pipelined with the solves over two device buffer pairs)
+    returns exactly the solutions and reports of one amg_solve_host per right-hand side."""
+    amg = _amg()
+    A, _, _ = config_problem(2)
+    h = amg.Hierarchy(ctx, A)
+    n = A.n_global
+    B = np.stack([uniform01(300 + k, n) for k in range(5)])
+    B[3] = 0.0  # a zero right-hand side inside the batch
+    Bp = torch.tensor(B).pin_memory().numpy()
+    Xp = torch.empty(B.shape, dtype=torch.float64).pin_memory().numpy()
+    X, reps = h.solve_host_batch(Bp, Xp, rtol=1e-6)
+    for k in range(B.shape[0]):
+        xk, rk = h.solve_host(B[k].copy(), rtol=1e-6)
+        assert np.array_equal(X[k], xk), k
+        assert reps[k]["iterations"] == rk["iterations"] and reps[k]["converged"] == rk["converged"]
+    assert reps[3]["iterations"] == 0 and not X[3].any()
+    # pageable buffers: same results
+    X2, _ = h.solve_host_batch(B.copy(), rtol=1e-6)
+    assert np.array_equal(X2, X)
