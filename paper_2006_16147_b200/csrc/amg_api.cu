@@ -155,6 +155,7 @@ struct DevLevel {
     DevMat Rc, Pc;
     // collapsed (the compact level just above a direct coarsest solve): M = Pc A_L^{-1} Rc dense
     double* Mc = nullptr;
+    double* AMc = nullptr;  // K-cycle inner level: A_l B (the first inner SpMV folded into the cycle)
     double* m = nullptr;   // window-sized vectors
     double* b = nullptr;
     double* mb = nullptr;
@@ -178,6 +179,8 @@ struct DevLevel {
         Pc.release();
         cudaFree(Mc);
         Mc = nullptr;
+        cudaFree(AMc);
+        AMc = nullptr;
         for (double* v : {kx, kr, kmb, kz, kp, kq, kst, kp2}) cudaFree(v);
         cudaFree(m);
         cudaFree(b);
@@ -1211,10 +1214,17 @@ void enqueue_fcg2(amg_hier_s* h, Launch& L, int l) {
     const VecOf kz = [l](RankState& R) { return R.lv[l].kz; };
     // iteration 1: p = z = B_l b with p^T r (r = b) fused into the cycle's last step
     const DotSink s1{D.kst, FIN_KPR0};
-    enqueue_level(h, L, l, bv, &mbv, kp, true, nullptr, &s1);
     const bool fused = kcycle_fused(h);
-    launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(fused ? FIN_KALPHA1 : FIN_KALPHA), "kfcg_spmv",
-               2 * n8);
+    if (D.AMc && fused) {  // collapsed level: p = B b and q = (A B) b in one kernel
+        L.begin("collapsed_kq", 16.0 * (double)n * (double)n + 24.0 * (double)n);
+        launch_k(k_collapsed_kq, (int)std::max<int64_t>(1, std::min<int64_t>(n, kMaxPartials)), kBlock, L.s,
+                 (const double*)D.Mc, (const double*)D.AMc, n, (const double*)D.b, D.kp, D.kq, kred(FIN_KPR0ALPHA1));
+        L.end();
+    } else {
+        enqueue_level(h, L, l, bv, &mbv, kp, true, nullptr, &s1);
+        launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp, D.kq}, kred(fused ? FIN_KALPHA1 : FIN_KALPHA), "kfcg_spmv",
+                   2 * n8);
+    }
     if (!fused) {  // x = alpha p ; r = b - alpha q ; m o r (the SWEEP0 path gathers it)
         L.begin("kfcg_upd1", 7 * n8);
         launch_k(k_kupd1, vec_grid(n, nsm), kBlock, L.s, D.kx, D.kr, D.kmb, D.kp, D.kq, D.b, D.m, n,
@@ -2117,6 +2127,10 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
             const std::vector<double> B =
                 dense_level_operator(A, Pb, Rt, m, coarse_inv, h->cfg.pre_sweeps, h->cfg.post_sweeps);
             if ((st = dev_copy(&D.Mc, B.data(), B.size()))) return st;
+            if (h->cfg.cycle == 1 && l + 2 == nl && l >= 1) {  // an inner FCG level: also A B
+                const std::vector<double> AB = sp_dense(A, B, D.comp_n);
+                if ((st = dev_copy(&D.AMc, AB.data(), AB.size()))) return st;
+            }
         }
         if ((st = dev_alloc(&D.b, wn))) return st;
         if ((st = dev_alloc(&D.xa, wn))) return st;

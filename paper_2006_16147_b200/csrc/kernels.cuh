@@ -54,7 +54,7 @@ struct PcgState {
 // per-level state k[] = {p^T r, p^T q, alpha, beta, stop}.
 enum FinishKind : int32_t {
     FIN_NONE = 0, FIN_BNORM = 1, FIN_RZ = 2, FIN_PQ = 3, FIN_RR = 4, FIN_ZQ = 5, FIN_PR = 6, FIN_PQF = 7,
-    FIN_KPR0 = 8, FIN_KPR = 9, FIN_KALPHA = 10, FIN_KBETA = 11, FIN_KALPHA2 = 12, FIN_KALPHA1 = 13
+    FIN_KPR0 = 8, FIN_KPR = 9, FIN_KALPHA = 10, FIN_KBETA = 11, FIN_KALPHA2 = 12, FIN_KALPHA1 = 13, FIN_KPR0ALPHA1 = 14
 };
 // Multi-rank: a dot kernel only writes its local total (rc.out, kind FIN_NONE);
 // the per-rank totals are all-gathered and k_finish sums them in rank order.
@@ -167,11 +167,19 @@ __device__ __forceinline__ void finish(const RedCtx& rc, double total) {
 }
 
 // FIN_KALPHA2 (K-cycle, fused direction update): t0 = p^T q, t1 = p^T r; then as FIN_KALPHA.
+// FIN_KPR0ALPHA1 (K-cycle, collapsed inner level, first iteration): t0 = p^T q, t1 = p^T b;
+// a new inner solve starts (as FIN_KPR0 with t1), then as FIN_KALPHA1 with t0.
 __device__ __forceinline__ void finish2(const RedCtx& rc, double t0, double t1) {
     if (rc.ks && rc.kind == FIN_KALPHA2) {
         rc.ks[0] = t1;
         RedCtx r1 = rc;
         r1.kind = FIN_KALPHA;
+        finish(r1, t0);
+    } else if (rc.ks && rc.kind == FIN_KPR0ALPHA1) {
+        rc.ks[4] = 0.0;
+        rc.ks[0] = t1;
+        RedCtx r1 = rc;
+        r1.kind = FIN_KALPHA1;
         finish(r1, t0);
     }
 }
@@ -1029,6 +1037,51 @@ __global__ void __launch_bounds__(kBlock) k_collapsed(const double* __restrict__
         __syncthreads();
     }
     if constexpr (DOT) grid_reduce(d, rc);
+}
+
+// The K-cycle's first inner iteration on a collapsed level: p = z = B b and q = A p = (A B) b
+// in one kernel (two dense rows per block), reducing p^T q and p^T b together (FIN_KPR0ALPHA1)
+// — the cycle application and the inner FCG's first SpMV in one launch.
+__global__ void __launch_bounds__(kBlock) k_collapsed_kq(const double* __restrict__ B,
+                                                         const double* __restrict__ AB, int64_t n,
+                                                         const double* __restrict__ b, double* __restrict__ p,
+                                                         double* __restrict__ q, RedCtx rc) {
+    pdl_begin();
+    __shared__ double part[2][kBlock / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double2 d = make_double2(0.0, 0.0);
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const double* Bi = B + i * n;
+        const double* Ai = AB + i * n;
+        double z = 0.0, w = 0.0;
+        for (int64_t j = threadIdx.x; j < n; j += kBlock) {
+            const double bj = __ldg(b + j);
+            z += __ldg(Bi + j) * bj;
+            w += __ldg(Ai + j) * bj;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            z += __shfl_xor_sync(0xffffffffu, z, o);
+            w += __shfl_xor_sync(0xffffffffu, w, o);
+        }
+        if (lane == 0) {
+            part[0][wid] = z;
+            part[1][wid] = w;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double zs = 0.0, ws = 0.0;
+            for (int k = 0; k < kBlock / 32; ++k) {
+                zs += part[0][k];
+                ws += part[1][k];
+            }
+            p[i] = zs;
+            q[i] = ws;
+            d.x += zs * ws;
+            d.y += zs * b[i];
+        }
+        __syncthreads();
+    }
+    grid_reduce(d, rc);
 }
 
 // Coarsest level: z = A_L^{-1} b, dense row-major inverse, one warp per row.
