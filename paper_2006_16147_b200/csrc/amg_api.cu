@@ -1237,6 +1237,18 @@ void enqueue_fcg2(amg_hier_s* h, Launch& L, int l) {
     // x = alpha_1 p_1 + alpha_2 p_2 by the consumer (GXap2)
     const DotSink s2{D.kst, FIN_KBETA, fused ? D.b : nullptr, fused ? D.kq : nullptr};
     const VecOf kq = [l](RankState& R) { return R.lv[l].kq; };
+    if (D.AMc && fused) {  // collapsed level: z = B r1, w = A z = (AB) r1, then p2 / q2 by vectors
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, kMaxPartials));
+        L.begin("collapsed_kw", 16.0 * (double)n * (double)n + 40.0 * (double)n);
+        launch_k(k_collapsed_kw, grid, kBlock, L.s, (const double*)D.Mc, (const double*)D.AMc, n,
+                 GBaq{D.b, D.kq, D.kst}, D.kr, D.kz, D.kmb, (const double*)D.kq, kred(FIN_KBETA));
+        L.end();
+        L.begin("kfcg_pq2", 56.0 * (double)n);
+        launch_k(k_kpq2, vec_grid(n, nsm), kBlock, L.s, (const double*)D.kz, (const double*)D.kp, D.kp2,
+                 (const double*)D.kmb, D.kq, (const double*)D.kr, n, (const double*)D.kst, kred(FIN_KALPHA2));
+        L.end();
+        return;
+    }
     enqueue_level(h, L, l, kr, &kmb, kz, true, &kq, &s2);
     // p = z + beta p formed inside q = A p (new p into kp2), p^T q and p^T r in one reduction
     launch_mat(L, D.A, GKpz{D.kz, D.kp, D.kst}, EKSpmvPupd{D.kz, D.kp, D.kp2, D.kq, D.kr, D.kst},

@@ -1084,6 +1084,70 @@ __global__ void __launch_bounds__(kBlock) k_collapsed_kq(const double* __restric
     grid_reduce(d, rc);
 }
 
+// The K-cycle's second inner iteration on a collapsed level: with rhs r1 = b - alpha_1 q1
+// (stored), z = B r1 and w = (A B) r1 = A z in one kernel, reducing z^T q1 (FIN_KBETA).
+__global__ void __launch_bounds__(kBlock) k_collapsed_kw(const double* __restrict__ B,
+                                                         const double* __restrict__ AB, int64_t n, GBaq g,
+                                                         double* __restrict__ rhs, double* __restrict__ z,
+                                                         double* __restrict__ w, const double* __restrict__ q1,
+                                                         RedCtx rc) {
+    pdl_begin();
+    bind(g);
+    __shared__ double part[2][kBlock / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double d = 0.0;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const double* Bi = B + i * n;
+        const double* Ai = AB + i * n;
+        double zs = 0.0, ws = 0.0;
+        for (int64_t j = threadIdx.x; j < n; j += kBlock) {
+            const double gj = g((int32_t)j);
+            zs += __ldg(Bi + j) * gj;
+            ws += __ldg(Ai + j) * gj;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            zs += __shfl_xor_sync(0xffffffffu, zs, o);
+            ws += __shfl_xor_sync(0xffffffffu, ws, o);
+        }
+        if (lane == 0) {
+            part[0][wid] = zs;
+            part[1][wid] = ws;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = 0.0, c = 0.0;
+            for (int k = 0; k < kBlock / 32; ++k) {
+                a += part[0][k];
+                c += part[1][k];
+            }
+            z[i] = a;
+            w[i] = c;
+            rhs[i] = g((int32_t)i);
+            d += q1[i] * a;
+        }
+        __syncthreads();
+    }
+    grid_reduce(d, rc);
+}
+// ... then p2 = z + beta p1 (into p2), q2 = w + beta q1 (in place), p2^T q2 and p2^T r1 (FIN_KALPHA2)
+__global__ void __launch_bounds__(kBlock) k_kpq2(const double* __restrict__ z, const double* __restrict__ p1,
+                                                 double* __restrict__ p2, const double* __restrict__ w,
+                                                 double* __restrict__ q, const double* __restrict__ r1, int64_t n,
+                                                 const double* __restrict__ k, RedCtx rc) {
+    pdl_begin();
+    const double beta = k[3];
+    double2 d = make_double2(0.0, 0.0);
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        const double pi = z[i] + beta * p1[i];
+        const double qi = w[i] + beta * q[i];
+        p2[i] = pi;
+        q[i] = qi;
+        d.x += pi * qi;
+        d.y += pi * r1[i];
+    }
+    grid_reduce(d, rc);
+}
+
 // Coarsest level: z = A_L^{-1} b, dense row-major inverse, one warp per row.
 __global__ void __launch_bounds__(kBlock) k_dense_gemv(const double* __restrict__ Ainv, const double* __restrict__ b,
                                                        double* __restrict__ z, int64_t n) {
