@@ -63,8 +63,22 @@ struct ohier {
     int32_t cycle;
     /* smoother: 0 = l1-Jacobi; 1 = INVK */
     int32_t smoother;
+    /* coarse CG preconditioner: 0 = l1-Jacobi diagonal of A_L (VA3S5CS1); 1 = the INVK /
+     * HINVK factors of A_L (VA3S3CS1: "we apply HINVK also as preconditioner of the CG
+     * method at the coarsest level") */
+    int32_t coarse_prec;
     int64_t coarse_visits;  /* coarsest solves performed (instrumentation) */
+    int64_t visits[64];     /* cycle applications rooted at each level (instrumentation) */
 };
+
+/* Solve-phase threads (SURVEY §8d (ii) "OpenMP all-core" oracle timing).  1 (default) is
+ * the parity reference: every loop sequential, every dot summed in index order.  With
+ * g_threads > 1 the row loops run in parallel (same arithmetic per entry) and dots are
+ * summed per fixed chunk in index order, then over the chunks in order: deterministic,
+ * but rounded differently from the sequential sum.  Setup is always sequential. */
+static int g_threads = 1;
+#define OR_CHUNKS 256
+void or_set_threads(int32_t t) { g_threads = t > 1 ? t : 1; }
 
 /* ------------------------------------------------------------------ helpers */
 static double dot(int64_t n, const double* a, const double* b);
@@ -145,6 +159,7 @@ static double diag_of(const ocsr* A, int64_t i) {
 /* ---------------------------------------------------------------- sparse core */
 /* y = A x, each row summed in ascending column order from +0.0. */
 void or_spmv(const ocsr* A, const double* x, double* y) {
+#pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
     for (int64_t i = 0; i < A->nrows; ++i) {
         double s = 0.0;
         for (int64_t k = A->rp[i]; k < A->rp[i + 1]; ++k) s += A->v[k] * x[A->ci[k]];
@@ -721,18 +736,31 @@ double or_avg_cr(const ohier* h) {
 /* Coarsest iterative solve: CG from x0 = 0
  * preconditioned by the l1-Jacobi diagonal of A_L, stopped as soon as the
  * relative residual is less than rtol, or after maxit iterations. */
-static void coarse_pcg(const ocsr* A, const double* m, int64_t n, double rtol, int32_t maxit, const double* b,
-                       double* x) {
+/* z = M^{-1} r of the coarse CG: the l1-Jacobi diagonal m, or (Wd != NULL) the INVK
+ * factors z = Z (Wd r) (VA3S3CS1). */
+static void coarse_prec_apply(const double* m, const ocsr* Wd, const ocsr* Z, int64_t n, const double* r,
+                              double* z, double* t) {
+    if (Wd) {
+        or_spmv(Wd, r, t);
+        or_spmv(Z, t, z);
+    } else {
+        for (int64_t i = 0; i < n; ++i) z[i] = m[i] * r[i];
+    }
+}
+
+static void coarse_pcg(const ocsr* A, const double* m, const ocsr* Wd, const ocsr* Z, int64_t n, double rtol,
+                       int32_t maxit, const double* b, double* x) {
     double* r = (double*)xmalloc(sizeof(double) * (size_t)n);
     double* z = (double*)xmalloc(sizeof(double) * (size_t)n);
     double* p = (double*)xmalloc(sizeof(double) * (size_t)n);
     double* q = (double*)xmalloc(sizeof(double) * (size_t)n);
+    double* t = (double*)xmalloc(sizeof(double) * (size_t)n);
     for (int64_t i = 0; i < n; ++i) {
         x[i] = 0.0;
         r[i] = b[i];
-        z[i] = m[i] * r[i];
-        p[i] = z[i];
     }
+    coarse_prec_apply(m, Wd, Z, n, r, z, t);
+    for (int64_t i = 0; i < n; ++i) p[i] = z[i];
     double bnorm = sqrt(dot(n, b, b));
     double rho = dot(n, r, z);
     if (bnorm > 0.0) {
@@ -746,9 +774,10 @@ static void coarse_pcg(const ocsr* A, const double* m, int64_t n, double rtol, i
                 r[i] = r[i] - alpha * q[i];
             }
             if (sqrt(dot(n, r, r)) / bnorm < rtol) break;
-            for (int64_t i = 0; i < n; ++i) z[i] = m[i] * r[i];
+            coarse_prec_apply(m, Wd, Z, n, r, z, t);
             double rho_new = dot(n, r, z);
             double beta = rho_new / rho;
+            #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
             for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
             rho = rho_new;
         }
@@ -757,6 +786,7 @@ static void coarse_pcg(const ocsr* A, const double* m, int64_t n, double rtol, i
     free(z);
     free(p);
     free(q);
+    free(t);
 }
 
 void or_set_coarse_cg(ohier* h, int32_t on, double rtol, int32_t maxit) {
@@ -917,13 +947,14 @@ static ocsr* invk_inverse(const ocsr* L, int32_t fill) {
     return W;
 }
 
-/* INVK factors of level l: Wd = D^{-1} W (row i scaled by 1/d_i) and Z = W^T, so
- * that M^{-1} r = W^T D^{-1} W r = Z (Wd r).  Returns 0 on an IC(0) breakdown. */
-static int invk_level(olevel* Lv, int32_t fill) {
+/* INVK factors of level l from the matrix B (A_l or its block-diagonal part):
+ * Wd = D^{-1} W (row i scaled by 1/d_i) and Z = W^T, so that
+ * M^{-1} r = W^T D^{-1} W r = Z (Wd r).  Returns 0 on an IC(0) breakdown. */
+static int invk_level(olevel* Lv, const ocsr* B, int32_t fill) {
     int64_t n = Lv->n;
     double* d = (double*)xmalloc(sizeof(double) * (size_t)n);
     ocsr* L = NULL;
-    if (!ic0(Lv->A, &L, d)) {
+    if (!ic0(B, &L, d)) {
         free(d);
         return 0;
     }
@@ -937,23 +968,95 @@ static int invk_level(olevel* Lv, int32_t fill) {
     return 1;
 }
 
-int32_t or_set_smoother(ohier* h, int32_t kind, int32_t fill) {
+/* The matrix whose INVK factors the smoother uses, in the parallel block-Jacobi setting
+ * of PAPER.md:165-170 and 178-181 ("we will always consider the case of computing the
+ * decomposition M for the diagonal blocks A_pp of A"; "the l1-modification ... computing
+ * the approximate inverse of the A_pp + D_l1,p blocks"): entries a_ij with owner(i) !=
+ * owner(j) are dropped; with l1 = 1, row i's diagonal gains sum_{j: owner(j) != owner(i)}
+ * |a_ij| (Eq. 3.5, the off-block l1 weights, summed in ascending column order).  One block
+ * (owner == NULL) leaves A unchanged: HINVK = l1-INVK = INVK. */
+static ocsr* block_diag_part(const ocsr* A, const int32_t* owner, int32_t l1) {
+    int64_t n = A->nrows;
+    ocsr* B = csr_alloc(n, n, A->rp[n]);
+    int64_t o = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double off = 0.0;
+        for (int64_t k = A->rp[i]; k < A->rp[i + 1]; ++k)
+            if (owner && owner[A->ci[k]] != owner[i]) off = off + fabs(A->v[k]);
+        for (int64_t k = A->rp[i]; k < A->rp[i + 1]; ++k) {
+            int64_t j = A->ci[k];
+            if (owner && owner[j] != owner[i]) continue;
+            B->ci[o] = j;
+            B->v[o] = (j == i && l1) ? A->v[k] + off : A->v[k];
+            ++o;
+        }
+        B->rp[i + 1] = o;
+    }
+    return B;
+}
+
+/* Block owner of every row of every level (R18): level 0 rows belong to the blocks
+ * [bounds0[p], bounds0[p+1]); a coarse row belongs to the block that owns the minimum
+ * member of its aggregate. */
+static int32_t** level_owners(const ohier* h, int32_t nblocks, const int64_t* bounds0) {
+    int32_t** own = (int32_t**)xcalloc((size_t)h->nl, sizeof(int32_t*));
+    for (int32_t l = 0; l < h->nl; ++l) {
+        int64_t n = h->lv[l].n;
+        own[l] = (int32_t*)xmalloc(sizeof(int32_t) * (size_t)n);
+        if (l == 0) {
+            for (int32_t p = 0; p < nblocks; ++p)
+                for (int64_t i = bounds0[p]; i < bounds0[p + 1]; ++i) own[0][i] = p;
+        } else {
+            const olevel* F = &h->lv[l - 1];
+            for (int64_t g = 0; g < n; ++g) own[l][g] = -1;
+            for (int64_t i = 0; i < F->n; ++i) /* ascending i: the first member seen is the minimum */
+                if (own[l][F->agg[i]] < 0) own[l][F->agg[i]] = own[l - 1][i];
+        }
+    }
+    return own;
+}
+
+int32_t or_set_smoother_ex(ohier* h, int32_t kind, int32_t fill, int32_t nblocks, const int64_t* bounds0,
+                           int32_t l1, const int32_t* fill_per_level) {
     h->smoother = kind;
-    if (kind != 1) return OR_OK;
-    for (int32_t l = 0; l + 1 < h->nl; ++l) {
+    if (kind != 1 && !h->coarse_prec) return OR_OK;
+    if (nblocks < 1 || (nblocks > 1 && (!bounds0 || bounds0[0] != 0 || bounds0[nblocks] != h->lv[0].n)))
+        return OR_ERR_ARG;
+    for (int32_t p = 0; nblocks > 1 && p < nblocks; ++p)
+        if (bounds0[p + 1] < bounds0[p]) return OR_ERR_ARG;
+    int32_t** own = nblocks > 1 ? level_owners(h, nblocks, bounds0) : NULL;
+    int32_t st = OR_OK;
+    /* every non-coarsest level (smoother), and the coarsest when it is the coarse CG's
+     * preconditioner */
+    for (int32_t l = 0; l < h->nl; ++l) {
         olevel* Lv = &h->lv[l];
         or_csr_free(Lv->Wd);
         or_csr_free(Lv->Z);
         Lv->Wd = Lv->Z = NULL;
-        /* reading I4: fill is admitted on stencil-like levels (<= 27 entries per row);
-         * denser coarse levels keep the pattern of L (fill 0), otherwise the level-1
-         * pattern of an already dense row fills in the whole triangle */
-        int64_t nnz = Lv->A->rp[Lv->n];
-        int32_t f = ((double)nnz <= 27.0 * (double)Lv->n) ? fill : 0;
-        if (!invk_level(Lv, f)) return OR_ERR_NOT_SPD;
+        if (l == h->nl - 1 ? !h->coarse_prec : kind != 1) continue;
+        /* "a single level of fill-in in the inversion" on every level; a
+         * per-level override exists only to express the library's non-default knob */
+        int32_t f = fill_per_level ? fill_per_level[l] : fill;
+        ocsr* B = block_diag_part(Lv->A, own ? own[l] : NULL, l1);
+        int ok = invk_level(Lv, B, f);
+        or_csr_free(B);
+        if (!ok) {
+            st = OR_ERR_NOT_SPD;
+            break;
+        }
     }
-    return OR_OK;
+    if (own) {
+        for (int32_t l = 0; l < h->nl; ++l) free(own[l]);
+        free(own);
+    }
+    return st;
 }
+
+int32_t or_set_smoother(ohier* h, int32_t kind, int32_t fill) {
+    return or_set_smoother_ex(h, kind, fill, 1, NULL, 0, NULL);
+}
+
+void or_set_coarse_prec(ohier* h, int32_t kind) { h->coarse_prec = kind; }
 
 const ocsr* or_level_invk(const ohier* h, int32_t l, int32_t which) {
     return which == 0 ? h->lv[l].Wd : h->lv[l].Z;
@@ -967,11 +1070,13 @@ static void smooth_apply(const ohier* h, const olevel* Lv, const double* res, do
         or_spmv(Lv->Wd, res, tmp);
         or_spmv(Lv->Z, tmp, out);
     } else {
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) out[i] = Lv->m[i] * res[i];
     }
 }
 
 int64_t or_coarse_visits(const ohier* h) { return h->coarse_visits; }
+int64_t or_level_visits(const ohier* h, int32_t l) { return (l >= 0 && l < 64) ? h->visits[l] : 0; }
 
 /* K-cycle coarse correction ("at each level except the fine and the
  * coarsest ones we apply two iterations of a Flexible Conjugate Gradient (FCG)
@@ -1000,12 +1105,14 @@ static void kcycle_fcg2(const ohier* h, int32_t l, const double* b, double* x) {
             memcpy(p, z, sizeof(double) * (size_t)n);
         } else {
             double beta = -dot(n, z, q) / pq;
+            #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
             for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
         }
         or_spmv(L->A, p, q);
         pq = dot(n, p, q);
         if (!(pq > 0.0)) break;
         double alpha = dot(n, p, r) / pq;
+#pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) {
             x[i] = x[i] + alpha * p[i];
             r[i] = r[i] - alpha * q[i];
@@ -1024,10 +1131,11 @@ static void kcycle_fcg2(const ohier* h, int32_t l, const double* b, double* x) {
 static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
     const olevel* L = &h->lv[l];
     int64_t n = L->n;
+    if (l < 64) ((ohier*)h)->visits[l] += 1;
     if (l == h->nl - 1) {
         ((ohier*)h)->coarse_visits += 1;
         if (h->coarse_cg)
-            coarse_pcg(L->A, L->m, n, h->coarse_rtol, h->coarse_maxit, b, x);
+            coarse_pcg(L->A, L->m, h->coarse_prec ? L->Wd : NULL, L->Z, n, h->coarse_rtol, h->coarse_maxit, b, x);
         else
             cholesky_solve(n, L->L, b, x);
         return;
@@ -1039,12 +1147,15 @@ static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
     smooth_apply(h, L, b, x, tmp); /* first pre-sweep from x = 0: x = M^{-1} b */
     for (int32_t s = 1; s < h->pre; ++s) {
         or_spmv(L->A, x, t);
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
         smooth_apply(h, L, t, u, tmp);
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) xn[i] = x[i] + u[i];
         memcpy(x, xn, sizeof(double) * (size_t)n);
     }
     or_spmv(L->A, x, t);
+    #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
     for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
     int64_t nc = h->lv[l + 1].n;
     double* bc = (double*)xmalloc(sizeof(double) * (size_t)nc);
@@ -1055,11 +1166,14 @@ static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
     else
         vcycle_rec(h, l + 1, bc, ec);
     or_spmv(L->P, ec, t);
+    #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
     for (int64_t i = 0; i < n; ++i) x[i] = x[i] + t[i];
     for (int32_t s = 0; s < h->post; ++s) { /* post-smoothing with M^T = M */
         or_spmv(L->A, x, t);
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
         smooth_apply(h, L, t, u, tmp);
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) xn[i] = x[i] + u[i];
         memcpy(x, xn, sizeof(double) * (size_t)n);
     }
@@ -1074,6 +1188,19 @@ static void vcycle_rec(const ohier* h, int32_t l, const double* b, double* x) {
 void or_vcycle(const ohier* h, const double* r, double* z) { vcycle_rec(h, 0, r, z); }
 
 static double dot(int64_t n, const double* a, const double* b) {
+    if (g_threads > 1 && n >= 4 * OR_CHUNKS) {
+        double part[OR_CHUNKS];
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+        for (int c = 0; c < OR_CHUNKS; ++c) {
+            int64_t i0 = n * c / OR_CHUNKS, i1 = n * (c + 1) / OR_CHUNKS;
+            double s = 0.0;
+            for (int64_t i = i0; i < i1; ++i) s += a[i] * b[i];
+            part[c] = s;
+        }
+        double s = 0.0;
+        for (int c = 0; c < OR_CHUNKS; ++c) s += part[c];
+        return s;
+    }
     double s = 0.0;
     for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
     return s;
@@ -1115,6 +1242,7 @@ int32_t or_pcg(const ohier* h, const double* b, double* x, double rtol, int32_t 
             break;
         }
         double alpha = rho / pq;
+#pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) {
             x[i] = x[i] + alpha * p[i];
             r[i] = r[i] - alpha * q[i];
@@ -1130,6 +1258,7 @@ int32_t or_pcg(const ohier* h, const double* b, double* x, double rtol, int32_t 
         or_vcycle(h, r, z);
         double rho_new = dot(n, r, z);
         double beta = rho_new / rho;
+        #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
         rho = rho_new;
     }
@@ -1179,6 +1308,7 @@ int32_t or_fcg(const ohier* h, const double* b, double* x, double rtol, int32_t 
             memcpy(p, z, sizeof(double) * (size_t)n);
         } else {
             double beta = -dot(n, z, q) / pq_prev;
+            #pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
             for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
         }
         or_spmv(A, p, q);
@@ -1188,6 +1318,7 @@ int32_t or_fcg(const ohier* h, const double* b, double* x, double rtol, int32_t 
             break;
         }
         double alpha = dot(n, p, r) / pq;
+#pragma omp parallel for schedule(static) if (g_threads > 1) num_threads(g_threads)
         for (int64_t i = 0; i < n; ++i) {
             x[i] = x[i] + alpha * p[i];
             r[i] = r[i] - alpha * q[i];

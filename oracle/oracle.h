@@ -90,8 +90,24 @@ void    or_set_cycle(ohier* h, int32_t cycle);
  * Returns OR_ERR_NOT_SPD on a non-positive IC(0) pivot.  or_level_invk returns
  * D^{-1} W (which = 0) or Z = W^T (which = 1) of level l. */
 int32_t or_set_smoother(ohier* h, int32_t kind, int32_t fill);
+/* The paper's parallel block-Jacobi forms: the INVK factors of the
+ * diagonal blocks A_pp (HINVK), or of A_pp + D_l1,p (l1 = 1, l1-INVK), with nblocks row
+ * blocks [bounds0[p], bounds0[p+1]) at level 0 and coarse rows owned by the block of their
+ * aggregate's minimum member (R18).  fill_per_level (NULL = `fill` everywhere) overrides
+ * the fill of each level.  Also builds the coarsest level's factors when the coarse CG
+ * uses them (or_set_coarse_prec, call it first). */
+int32_t or_set_smoother_ex(ohier* h, int32_t kind, int32_t fill, int32_t nblocks, const int64_t* bounds0,
+                           int32_t l1, const int32_t* fill_per_level);
+/* coarse CG preconditioner: 0 = l1-Jacobi (VA3S5CS1), 1 = the INVK factors of A_L (VA3S3CS1,
+ * PAPER.md:420) */
+void    or_set_coarse_prec(ohier* h, int32_t kind);
 const ocsr* or_level_invk(const ohier* h, int32_t l, int32_t which);
 int64_t or_coarse_visits(const ohier* h);
+/* cycle applications rooted at level l since the build (K-opc weights) */
+int64_t or_level_visits(const ohier* h, int32_t l);
+/* solve-phase threads: 1 = the sequential parity reference (default); > 1 = OpenMP row
+ * loops and fixed-chunk dots (SURVEY §8d (ii) all-core timing only) */
+void    or_set_threads(int32_t t);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ def build_oracle(force: bool = False) -> str:
     src = os.path.join(_HERE, "oracle.c")
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
             os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
                                "-o", _SO, src, "-lm"])
     return _SO
 
@@ -78,6 +78,10 @@ def lib():
                                C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                C.POINTER(C.c_double), _vp]),
         "or_set_coarse_cg": (None, [_vp, C.c_int32, C.c_double, C.c_int32]),
+        "or_set_smoother_ex": (C.c_int32, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32, _vp]),
+        "or_set_coarse_prec": (None, [_vp, C.c_int32]),
+        "or_level_visits": (C.c_int64, [_vp, C.c_int32]),
+        "or_set_threads": (None, [C.c_int32]),
         "or_set_cycle": (None, [_vp, C.c_int32]),
         "or_set_smoother": (C.c_int32, [_vp, C.c_int32, C.c_int32]),
         "or_level_invk": (_vp, [_vp, C.c_int32, C.c_int32]),
@@ -305,11 +309,33 @@ class OracleHierarchy:
         """'V' (Eq. 3.1) or 'K' (K-cycle: two FCG(1) iterations per intermediate level)."""
         lib().or_set_cycle(self.h, {"V": 0, "K": 1}[kind])
 
-    def set_smoother(self, kind="l1jacobi", fill=1):
-        """'l1jacobi' or 'invk' (`fill` levels in the inversion)."""
-        st = lib().or_set_smoother(self.h, {"l1jacobi": 0, "invk": 1}[kind], int(fill))
+    def set_smoother(self, kind="l1jacobi", fill=1, blocks=None, l1=False, fill_per_level=None):
+        """'l1jacobi' or 'invk' (`fill` levels in the inversion).
+        blocks: level-0 row bounds [0, b1, ..., n] of the parallel block-Jacobi setting (HINVK on
+        the diagonal blocks); l1=True: l1-INVK (A_pp + D_l1,p)."""
+        nb = 1 if blocks is None else len(blocks) - 1
+        self._bounds = None if blocks is None else np.ascontiguousarray(blocks, dtype=np.int64)
+        self._fills = None if fill_per_level is None else np.ascontiguousarray(fill_per_level, dtype=np.int32)
+        st = lib().or_set_smoother_ex(
+            self.h, {"l1jacobi": 0, "invk": 1}[kind], int(fill), nb,
+            None if self._bounds is None else self._bounds.ctypes.data_as(C.c_void_p), int(bool(l1)),
+            None if self._fills is None else self._fills.ctypes.data_as(C.c_void_p))
         if st != OR_OK:
             raise RuntimeError(f"or_set_smoother failed with status {st}")
+
+    def set_coarse_prec(self, kind="l1jacobi"):
+        """Coarse CG preconditioner: 'l1jacobi' (VA3S5CS1) or 'invk' (VA3S3CS1).
+        Call before set_smoother, which builds the coarsest level's factors."""
+        lib().or_set_coarse_prec(self.h, {"l1jacobi": 0, "invk": 1}[kind])
+
+    def level_visits(self, l):
+        """Cycle applications rooted at level l since the build."""
+        return lib().or_level_visits(self.h, int(l))
+
+    @staticmethod
+    def set_threads(t):
+        """Solve-phase threads: 1 = sequential parity reference; > 1 = OpenMP (timing only)."""
+        lib().or_set_threads(int(t))
 
     def invk(self, l, which):
         """which = 0: D^{-1} W; 1: Z = W^T (INVK factors of level l, borrowed)."""
