@@ -24,6 +24,13 @@
  *    apply are collective over the ranks of the context.
  *  - Indices: global int64 on input; rows are contiguous blocks [row_begin, row_end).
  *  - fp64 throughout (the paper never states precision).
+ *  - Threads: a hierarchy owns per-solve state (its CUDA graphs, the PCG vectors, the
+ *    staging buffers of the host-buffer calls).  amg_solve, amg_solve_host,
+ *    amg_solve_host_batch, amg_precond_apply and amg_profile_vcycle take a per-hierarchy
+ *    lock, so calls from several threads on ONE hierarchy are serialised, not concurrent
+ *    (a divergence from SPEC.md's "concurrent solves on shared immutable hierarchies":
+ *    for concurrency build one hierarchy per thread / stream).  Different hierarchies are
+ *    independent.  amg_hierarchy_destroy must not race with calls on the same hierarchy.
  */
 #ifndef AMG_B200_H
 #define AMG_B200_H

@@ -119,9 +119,12 @@ class Hierarchy:
     def solve(self, b, x=None, rtol: float = 1e-6, maxit: int = 500):
         """amg_solve on CUDA tensors (fp64, this rank's rows)."""
         import torch
-        assert b.dtype == torch.float64 and b.is_cuda and b.is_contiguous()
+        if not (b.dtype == torch.float64 and b.is_cuda and b.is_contiguous() and b.numel() == self.n_local):
+            raise ValueError(f"b must be a contiguous float64 CUDA tensor of {self.n_local} entries")
         if x is None:
             x = torch.empty_like(b)
+        elif not (x.dtype == torch.float64 and x.is_cuda and x.is_contiguous() and x.numel() == self.n_local):
+            raise ValueError(f"x must be a contiguous float64 CUDA tensor of {self.n_local} entries")
         torch.cuda.current_stream(b.device).synchronize()
         rep = amg_report_t()
         code = lib.amg_solve(self.h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), float(rtol),
@@ -139,8 +142,13 @@ class Hierarchy:
     def solve_host(self, b: np.ndarray, x: np.ndarray | None = None, rtol: float = 1e-6, maxit: int = 500):
         """amg_solve_host: host buffers, H2D/D2H copies inside the call."""
         b = np.ascontiguousarray(b, dtype=np.float64)
+        if b.shape != (self.n_local,):
+            raise ValueError(f"b must have shape ({self.n_local},), got {b.shape}")
         if x is None:
             x = np.empty_like(b)
+        elif not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous
+                  and x.shape == b.shape and x.flags.writeable):
+            raise ValueError("x must be a writeable C-contiguous float64 array of b's shape")
         rep = amg_report_t()
         code = lib.amg_solve_host(self.h, _ptr(b), _ptr(x), float(rtol), int(maxit), C.byref(rep))
         check(code, "amg_solve_host", ok=(AMG_OK, AMG_NOT_CONVERGED))
@@ -152,9 +160,14 @@ class Hierarchy:
         pipelined with the solves (pin B and X, e.g. torch.empty(...).pin_memory(), for overlap)."""
         if not (isinstance(B, np.ndarray) and B.dtype == np.float64 and B.flags.c_contiguous):
             B = np.ascontiguousarray(B, dtype=np.float64)
+        if B.ndim not in (1, 2) or B.shape[-1] != self.n_local:
+            raise ValueError(f"B must have shape (n,) or (nrhs, n) with n = {self.n_local}, got {B.shape}")
         nrhs = B.shape[0] if B.ndim == 2 else 1
         if X is None:
             X = np.empty_like(B)
+        elif not (isinstance(X, np.ndarray) and X.dtype == np.float64 and X.flags.c_contiguous
+                  and X.shape == B.shape and X.flags.writeable):
+            raise ValueError("X must be a writeable C-contiguous float64 array of B's shape")
         reps = (amg_report_t * max(1, nrhs))()
         code = lib.amg_solve_host_batch(self.h, int(nrhs), _ptr(B), _ptr(X), float(rtol), int(maxit),
                                         C.cast(reps, C.c_void_p))
@@ -164,9 +177,12 @@ class Hierarchy:
     def precond_apply(self, r, z=None):
         """amg_precond_apply: one V-cycle z = B r on CUDA tensors."""
         import torch
-        assert r.dtype == torch.float64 and r.is_cuda and r.is_contiguous()
+        if not (r.dtype == torch.float64 and r.is_cuda and r.is_contiguous() and r.numel() == self.n_local):
+            raise ValueError(f"r must be a contiguous float64 CUDA tensor of {self.n_local} entries")
         if z is None:
             z = torch.empty_like(r)
+        elif not (z.dtype == torch.float64 and z.is_cuda and z.is_contiguous() and z.numel() == self.n_local):
+            raise ValueError(f"z must be a contiguous float64 CUDA tensor of {self.n_local} entries")
         torch.cuda.current_stream(r.device).synchronize()
         check(lib.amg_precond_apply(self.h, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr())),
               "amg_precond_apply")

@@ -32,7 +32,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/amg_b200.h"
@@ -250,6 +252,9 @@ struct amg_ctx_s {
     bool own_stream = false;
     int nsm = 148;
     ncclComm_t nccl = nullptr;
+    // launch caps (SM count x resident blocks) per kernel, computed once per context
+    std::unordered_map<const void*, int> caps;
+    std::mutex caps_mu;
 };
 
 struct amg_hier_s {
@@ -292,6 +297,13 @@ struct amg_hier_s {
     double* tail_partials = nullptr;
     double tail_bytes = 0.0;
 
+    // one solve / apply at a time per hierarchy: the graphs, PCG vectors and staging buffers
+    // are per-hierarchy state (include/amg_b200.h, "Threads")
+    std::recursive_mutex mu;
+    // first NCCL failure of an enqueue pass (exchange / all-gather), reported as AMG_ERR_NCCL
+    ncclResult_t nccl_status = ncclSuccess;
+    std::string nccl_what;
+
     bool multi() const { return np > 1; }
     int nlev() const { return (int)ranks[0].lv.size(); }
     ~amg_hier_s() {
@@ -327,6 +339,15 @@ int max_grid(const void* fn, int nsm) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kBlock, 0);
     if (nb < 1) nb = 1;
     return std::min(nb * nsm, kMaxPartials);
+}
+// per-context cache of max_grid (the SM count is the context device's)
+int ctx_cap(amg_ctx_s* c, const void* fn) {
+    std::lock_guard<std::mutex> g(c->caps_mu);
+    auto it = c->caps.find(fn);
+    if (it != c->caps.end()) return it->second;
+    const int v = max_grid(fn, c->nsm);
+    c->caps.emplace(fn, v);
+    return v;
 }
 
 int vec_grid(int64_t n, int nsm) {
@@ -386,17 +407,16 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         u0 = M.ib1;
     }
     if (part != 0 && u1 <= u0) return;
-    const int nsm = L.h->ctx->nsm;
     const double frac = units ? (double)(u1 - u0) / (double)units : 1.0;
     L.begin(name, frac * (M.model_bytes() + vec_bytes), frac * (M.stored_bytes() + vec_bytes));
     if (M.fmt == FMT_SDIA) {
-        static const int cap = max_grid((const void*)k_sdia<G, E>, nsm);
+        const int cap = ctx_cap(L.h->ctx, (const void*)k_sdia<G, E>);
         const int64_t need = ((u1 - u0) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
         launch_k(k_sdia<G, E>, grid, kBlock, L.s,
                  SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor, u0, u1}, g, e, rc);
     } else if (M.fmt == FMT_SELL) {
-        static const int cap = max_grid((const void*)k_sell<G, E>, nsm);
+        const int cap = ctx_cap(L.h->ctx, (const void*)k_sell<G, E>);
         const int64_t need = ((u1 - u0) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
         launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1, M.perm}, g, e, rc);
@@ -404,7 +424,7 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         const CsrView v{M.rp, M.col, M.val, M.nrows, u0, u1};
         const int64_t need = ((u1 - u0) * M.vw + kBlock - 1) / kBlock;
         if (M.vw == kVWBlock) {
-            static const int cap = max_grid((const void*)k_csrb<G, E>, nsm);
+            const int cap = ctx_cap(L.h->ctx, (const void*)k_csrb<G, E>);
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(u1 - u0, cap));
             launch_k(k_csrb<G, E>, grid, kBlock, L.s, v, g, e, rc);
             L.end();
@@ -413,7 +433,7 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         switch (M.vw) {
 #define VWCASE(W)                                                                 \
     case W: {                                                                     \
-        static const int cap = max_grid((const void*)k_csrv<W, G, E>, nsm);       \
+        const int cap = ctx_cap(L.h->ctx, (const void*)k_csrv<W, G, E>);           \
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap)); \
         launch_k(k_csrv<W, G, E>, grid, kBlock, L.s, v, g, e, rc);                   \
         break;                                                                    \
@@ -444,6 +464,14 @@ RedCtx dot_red(amg_hier_s* h, RankState& R, int kind, unsigned long long cond, i
 }
 
 // ------------------------------------------------------------- communication
+// Records the first NCCL failure of an enqueue pass (checked by the ABI entry points).
+void nccl_note(amg_hier_s* h, ncclResult_t r, const char* what) {
+    if (r != ncclSuccess && h->nccl_status == ncclSuccess) {
+        h->nccl_status = r;
+        h->nccl_what = std::string(what) + ": " + ncclGetErrorString(r);
+    }
+}
+
 // Multi-rank: gather every rank's dot total to every rank, then finish in rank order.
 void dot_finish(amg_hier_s* h, Launch& L, int kind) {
     if (!h->multi()) return;
@@ -454,7 +482,8 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind) {
                                 cudaMemcpyDeviceToDevice, L.s);
     } else {
         RankState& R = h->ranks[0];
-        ncclAllGather(R.dot_local, R.dot_all, kDotSlots, ncclDouble, h->ctx->nccl, L.s);
+        nccl_note(h, ncclAllGather(R.dot_local, R.dot_all, kDotSlots, ncclDouble, h->ctx->nccl, L.s),
+                  "ncclAllGather (dot totals)");
     }
     for (auto& R : h->ranks) {
         RedCtx rc{nullptr, nullptr, nullptr, R.st, 0ull, kind, nullptr};
@@ -523,14 +552,14 @@ void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec) {
     } else {
         RankState& R = h->ranks[0];
         const Exch& E = R.lv[l].ex;
-        ncclGroupStart();
+        nccl_note(h, ncclGroupStart(), "ncclGroupStart (halo)");
         for (int q = 0; q < h->np; ++q) {
             const int64_t ns = E.send_off[q + 1] - E.send_off[q];
             const int64_t nr = E.recv_off[q + 1] - E.recv_off[q];
-            if (ns) ncclSend(E.sbuf + E.send_off[q], ns, ncclDouble, q, h->ctx->nccl, st);
-            if (nr) ncclRecv(E.rbuf + E.recv_off[q], nr, ncclDouble, q, h->ctx->nccl, st);
+            if (ns) nccl_note(h, ncclSend(E.sbuf + E.send_off[q], ns, ncclDouble, q, h->ctx->nccl, st), "ncclSend (halo)");
+            if (nr) nccl_note(h, ncclRecv(E.rbuf + E.recv_off[q], nr, ncclDouble, q, h->ctx->nccl, st), "ncclRecv (halo)");
         }
-        ncclGroupEnd();
+        nccl_note(h, ncclGroupEnd(), "ncclGroupEnd (halo)");
     }
     for (auto& R : h->ranks) {
         const Exch& E = R.lv[l].ex;
@@ -2139,7 +2168,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
             const std::vector<double> B =
                 dense_level_operator(A, Pb, Rt, m, coarse_inv, h->cfg.pre_sweeps, h->cfg.post_sweeps);
             if ((st = dev_copy(&D.Mc, B.data(), B.size()))) return st;
-            if (h->cfg.cycle == 1 && l + 2 == nl && l >= 1) {  // an inner FCG level: also A B
+            if (h->cfg.cycle == 1 && kcycle_fused(h) && l + 2 == nl && l >= 1) {  // an inner FCG level: also A B
                 const std::vector<double> AB = sp_dense(A, B, D.comp_n);
                 if ((st = dev_copy(&D.AMc, AB.data(), AB.size()))) return st;
             }
@@ -2316,6 +2345,14 @@ int ensure_apply_graph(amg_hier_s* h, const double* r, double* z) {
     h->apply_r = r;
     h->apply_z = z;
     return AMG_OK;
+}
+
+// AMG_ERR_NCCL if an enqueue pass since the last call recorded an NCCL failure.
+int take_nccl_status(amg_hier_s* h) {
+    if (h->nccl_status == ncclSuccess) return AMG_OK;
+    set_err(h->nccl_what);
+    h->nccl_status = ncclSuccess;
+    return AMG_ERR_NCCL;
 }
 
 void fill_report(amg_hier_s* h, amg_report_t* rep) {
@@ -2930,8 +2967,10 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
         set_err("amg_solve: bad argument");
         return AMG_ERR_ARG;
     }
+    std::lock_guard<std::recursive_mutex> guard(h->mu);
     CK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
+    h->nccl_status = ncclSuccess;
     PcgState init{};
     init.rtol = rtol;
     init.maxit = maxit;
@@ -2947,12 +2986,15 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
         CK(cudaStreamSynchronize(s));
     } else {
         Launch L{h, s};
+        int e;
         enqueue_pcg_init(h, L, b_dev, x_dev, 0);
+        if ((e = take_nccl_status(h))) return e;
         for (;;) {
             CK(cudaMemcpyAsync(h->st_host, h->ranks[0].st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             if (h->st_host->status != ST_RUNNING) break;
             enqueue_pcg_body(h, L, x_dev, 0);
+            if ((e = take_nccl_status(h))) return e;
         }
         enqueue_pcg_final(h, L, x_dev);
         CK(cudaEventRecord(h->ev1, s));
@@ -2985,6 +3027,7 @@ int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, doubl
         set_err("amg_solve_host_batch: bad argument");
         return AMG_ERR_ARG;
     }
+    std::lock_guard<std::recursive_mutex> guard(h->mu);
     CK(cudaSetDevice(h->ctx->device));
     const int64_t n = h->n0_local;
     int code = AMG_OK;
@@ -3006,17 +3049,35 @@ int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, doubl
     if (!h->dstream) CK(cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking));
     // separate copy streams: b_{k+1} must not queue behind x_k's copy (which waits for solve k)
     cudaStream_t s = h->ctx->stream, cs = h->cstream, ds = h->dstream;
-    PcgState* sts = nullptr;  // [0]: the initial state, [1 + k]: solve k's final state
-    CK(cudaMallocHost((void**)&sts, sizeof(PcgState) * (size_t)(nrhs + 1)));
+    // every exit path (including a failing CK below) drains the three streams before the
+    // pinned state array and the events go away: queued copies may still reference them
+    struct BatchRes {
+        cudaStream_t s, cs, ds;
+        PcgState* sts = nullptr;
+        cudaEvent_t h2d[2] = {}, solved[2] = {}, d2h[2] = {};
+        ~BatchRes() {
+            cudaStreamSynchronize(s);
+            cudaStreamSynchronize(cs);
+            cudaStreamSynchronize(ds);
+            for (int q = 0; q < 2; ++q)
+                for (cudaEvent_t e : {h2d[q], solved[q], d2h[q]})
+                    if (e) cudaEventDestroy(e);
+            if (sts) cudaFreeHost(sts);
+        }
+    } res{s, cs, ds};
+    CK(cudaMallocHost((void**)&res.sts, sizeof(PcgState) * (size_t)(nrhs + 1)));
+    PcgState* sts = res.sts;  // [0]: the initial state, [1 + k]: solve k's final state
     PcgState init{};
     init.rtol = rtol;
     init.maxit = maxit;
     sts[0] = init;
-    cudaEvent_t h2d[2], solved[2], d2h[2];
+    cudaEvent_t* h2d = res.h2d;
+    cudaEvent_t* solved = res.solved;
+    cudaEvent_t* d2h = res.d2h;
     for (int q = 0; q < 2; ++q) {
-        cudaEventCreateWithFlags(&h2d[q], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&solved[q], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&d2h[q], cudaEventDisableTiming);
+        CK(cudaEventCreateWithFlags(&h2d[q], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&solved[q], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&d2h[q], cudaEventDisableTiming));
     }
     RankState& R = h->ranks[0];
     CK(cudaEventRecord(h->ev0, s));
@@ -3063,12 +3124,6 @@ int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, doubl
             reps[k].status = c;
         }
     }
-    for (int q = 0; q < 2; ++q) {
-        cudaEventDestroy(h2d[q]);
-        cudaEventDestroy(solved[q]);
-        cudaEventDestroy(d2h[q]);
-    }
-    cudaFreeHost(sts);
     if (code == AMG_ERR_BREAKDOWN) set_err("amg_solve_host_batch: breakdown, p^T A p <= 0");
     CK(cudaGetLastError());
     return code;
@@ -3080,6 +3135,7 @@ int amg_solve_host(amg_hier_t h, const double* b_host, double* x_host, double rt
         set_err("amg_solve_host: bad argument");
         return AMG_ERR_ARG;
     }
+    std::lock_guard<std::recursive_mutex> guard(h->mu);
     CK(cudaSetDevice(h->ctx->device));
     int st;
     if (!h->hb && (st = dev_alloc(&h->hb, h->n0_local))) return st;
@@ -3098,8 +3154,10 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
         set_err("amg_precond_apply: bad argument");
         return AMG_ERR_ARG;
     }
+    std::lock_guard<std::recursive_mutex> guard(h->mu);
     CK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
+    h->nccl_status = ncclSuccess;
     if (h->cfg.use_graphs && !h->multi()) {
         int e = ensure_apply_graph(h, r_dev, z_dev);
         if (e) return e;
@@ -3107,6 +3165,7 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
     } else {
         Launch L{h, s};
         enqueue_apply(h, L, r_dev, z_dev);
+        if (int e = take_nccl_status(h)) return e;
     }
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
@@ -3157,6 +3216,7 @@ int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out
         set_err("amg_profile_vcycle: bad argument");
         return AMG_ERR_ARG;
     }
+    std::lock_guard<std::recursive_mutex> guard(h->mu);
     CK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
     for (auto& R : h->ranks) CK(cudaMemsetAsync(R.pr, 0, sizeof(double) * R.lv[0].win_n, s));
