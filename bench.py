@@ -7,6 +7,10 @@ l1-Jacobi 1/1, direct coarsest solve).  A "step" is one full PCG solve.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
+With --gpus N > 1 and no WORLD_SIZE in the environment, bench.py re-launches itself
+under `python -m torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL
+communicator init logged with NCCL_DEBUG=INFO / SUBSYS=INIT) and checks world == N.
+
 Prints ONE JSON line on rank 0.  `value` = unknowns solved per second over all
 ranks (n_global / device time per solve, max over ranks).  The hierarchy and
 inputs are resident in HBM before the timed region; the hierarchy (GBs) is far
@@ -31,7 +35,6 @@ sys.path.insert(0, ROOT)
 METRIC = "AMG-PCG solve s & ms/iter at rtol 1e-6; V-cycle HBM GB/s; weak-scaling eff 1/2/4/8"
 UNIT = "dof/s (unknowns solved to rtol 1e-6 per second)"
 NOMINAL_HBM_GBS = 8000.0
-CPU_SAMPLE_GRID = (96, 96, 96)
 
 
 def measured_peaks():
@@ -44,8 +47,11 @@ def measured_peaks():
 
 
 def workload_name(cfg, grid):
-    return {1: "c1_poisson7_16^3", 2: "c2_poisson7_128^3_u01", 3: "c3_aniso7_256^3_2x2sweeps",
-            4: "c4_poisson7_256^3_per_gpu_weak", 5: "c5_jump27_512^3"}[cfg] + f"_grid{grid[0]}x{grid[1]}x{grid[2]}"
+    """The BASELINE config family and the grid that actually ran (a smaller analogue names
+    its own grid, never the config's full size)."""
+    g = f"{grid[0]}x{grid[1]}x{grid[2]}"
+    return {1: "c1_poisson7", 2: "c2_poisson7_u01", 3: "c3_aniso7_2x2sweeps",
+            4: "c4_poisson7_per_gpu_weak", 5: "c5_jump27"}[cfg] + f"_grid{g}"
 
 
 # ------------------------------------------------------------------ clocks
@@ -100,12 +106,31 @@ def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch with torchrun "
+                         f"--nproc-per-node {args.gpus}, or without WORLD_SIZE to self-launch)")
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         backend = "gloo" if args.impl == "reference" else "nccl"
         dist.init_process_group(backend=backend)
+        assert dist.get_world_size() == args.gpus
     return world, rank, local
+
+
+def self_launch(argv, n):
+    """Re-exec this script under torch.distributed.run with n ranks on this node."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + argv
+    print("bench.py: self-launch: " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 def barrier(world):
@@ -125,48 +150,131 @@ def allmax(world, v):
 
 
 # ------------------------------------------------------------------ oracle
-def oracle_sample(rtol, nsolves=1):
-    """The CPU oracle, as it stands, on a bounded sample of the workload family:
-    the same 7-point generator and settings on a 96^3 grid (b = 1)."""
-    import oracle as O
-    from inputs import poisson7
-    A = poisson7(*CPU_SAMPLE_GRID)
-    t0 = time.perf_counter()
-    h = O.OracleHierarchy(A)
-    setup = time.perf_counter() - t0
-    b = np.ones(A.n_global)
-    times, its = [], []
-    for _ in range(nsolves):
+def host_record():
+    """CPU model, core count and RAM of the host the oracle runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    ram = round(int(line.split()[1]) / 2 ** 20, 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "ram_gib": ram}
+
+
+class OracleSample:
+    """The CPU oracle, as it stands, on the benched workload itself (BASELINE config 4 grid of
+    one GPU's share): the hierarchy is built single-threaded (untimed), then
+      * all-core: one full PCG solve to rtol with the oracle's OpenMP row loops (SURVEY §8d (ii));
+      * single-thread: `st_its` timed PCG iterations of the sequential parity oracle (bounded
+        sample), converted to a solve with the iteration count of the full solve."""
+
+    def __init__(self, args, grid):
+        import oracle as O
+        from inputs import config_problem
+        self.O = O
+        A, b, meta = config_problem(args.config, grid=grid)
+        self.n = A.n_global
+        self.b = b
+        kw = {}
+        if getattr(args, "method", "default") != "default":
+            raise SystemExit("the oracle reference arm is defined for --method default")
+        kw = dict(pre_sweeps=meta["sweeps"][0], post_sweeps=meta["sweeps"][1],
+                  max_coarse_size=meta["max_coarse_size"])
         t0 = time.perf_counter()
-        _, info = h.pcg(b, rtol=rtol, maxit=500)
-        times.append(time.perf_counter() - t0)
-        its.append(info["iterations"])
-    return A.n_global, setup, times, its
+        self.h = O.OracleHierarchy(A, **kw)
+        self.setup_s = time.perf_counter() - t0
+        self.rtol = args.rtol
+        self.cores = os.cpu_count() or 1
+
+    def full_solve(self, threads):
+        self.O.OracleHierarchy.set_threads(threads)
+        try:
+            t0 = time.perf_counter()
+            _, info = self.h.pcg(self.b, rtol=self.rtol, maxit=500)
+            return time.perf_counter() - t0, info["iterations"]
+        finally:
+            self.O.OracleHierarchy.set_threads(1)
+
+    def iterations_sample(self, its, threads=1):
+        """Seconds per PCG iteration from a fixed-count run of `its` iterations."""
+        self.O.OracleHierarchy.set_threads(threads)
+        try:
+            t0 = time.perf_counter()
+            self.h.pcg(self.b, rtol=0.0, maxit=its)
+            return (time.perf_counter() - t0) / its
+        finally:
+            self.O.OracleHierarchy.set_threads(1)
+
+
+def cpu_baseline_record(args, grid, st_its=2):
+    S = OracleSample(args, grid)
+    t_all, its = S.full_solve(S.cores)
+    t_it1 = S.iterations_sample(st_its, 1)
+    return {"value": S.n / t_all, "unit": UNIT, "cores": S.cores, "kind": "oracle",
+            "sample": (f"the benched workload itself ({grid[0]}x{grid[1]}x{grid[2]}, {S.n} unknowns): oracle "
+                       f"hierarchy built single-thread (setup {S.setup_s:.1f} s, untimed), then one full PCG "
+                       f"solve to rtol {args.rtol} ({its} its) with the oracle's OpenMP row loops on "
+                       f"{S.cores} threads: {t_all:.2f} s"),
+            "iterations": its, "solve_s": t_all, "setup_s": S.setup_s,
+            "single_thread": {"value": S.n / (t_it1 * its), "unit": UNIT, "cores": 1,
+                              "sample": f"{st_its} timed PCG iterations of the sequential parity oracle "
+                                        f"({t_it1:.2f} s/iteration) x the {its} iterations of the full solve"},
+            "host": host_record()}
 
 
 def run_reference(args):
     world, rank, _ = dist_init(args)
     if rank != 0:
         return 0
-    n, setup, times, its = oracle_sample(args.rtol, args.warmup + args.steps)
-    timed = times[args.warmup:]
-    sec = sum(timed) / len(timed)
-    value = n / sec
+    grid = per_gpu_grid(args)
+    S = OracleSample(args, grid)
+    # warm-up: one full all-core solve (gives the iteration count the value is quoted at)
+    t_full, its = S.full_solve(S.cores)
+    for _ in range(max(0, args.warmup - 1)):
+        S.iterations_sample(2, S.cores)
+    per_it = [S.iterations_sample(2, S.cores) for _ in range(args.steps)]
+    sec = its * statistics.mean(per_it) * world  # a CPU does the N-GPU job's N shares one after another
+    value = S.n * world / sec
+    wl_grid = tuple(args.grid) if args.grid is not None else (grid[0], grid[1], grid[2] * world)
+    cfg = {"workload": workload_name(args.config, wl_grid),
+           "n_global": S.n * world, "rtol": args.rtol, "method": "default",
+           "sample": (f"oracle on {S.cores} host threads (OpenMP row loops); each step = 2 PCG iterations "
+                      f"of the {grid[0]}x{grid[1]}x{grid[2]} per-GPU problem, solve time = {its} iterations "
+                      f"(its full solve in warm-up: {t_full:.2f} s)"
+                      + (f"; N = {world}: {world} such shares processed one after another" if world > 1 else ""))}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, (256, 256, 256 * args.gpus)),
-                   "sample": f"oracle PCG solve of the {CPU_SAMPLE_GRID} grid of the same generator",
-                   "rtol": args.rtol},
-        "iterations": its[-1],
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"single-thread fp64 C oracle, full PCG solve on {CPU_SAMPLE_GRID} "
-                                   f"(setup {setup:.1f} s untimed)"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+        "iterations": its,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": S.cores, "kind": "oracle",
+                         "sample": cfg["sample"], "setup_s": S.setup_s, "host": host_record()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def per_gpu_grid(args):
+    """One GPU's share of the workload (config 4: 256^3 per GPU; --grid overrides the GLOBAL
+    grid as in run_ours, whose z-extent the ranks split)."""
+    from inputs.problems import CONFIGS
+    if args.grid is not None:
+        g = tuple(args.grid)
+        return (g[0], g[1], g[2] // args.gpus)
+    return tuple(CONFIGS[args.config]["grid"])
 
 
 # ------------------------------------------------------------------ ours
@@ -182,6 +290,13 @@ def method_settings(args, meta, world):
                                             "FCG(1), coarsest l1-Jacobi CG (1e-4, 30 its)",
                 "cfg": dict(pre_sweeps=4, post_sweeps=4, max_coarse_size=12 * 200 * world, krylov=1,
                             coarse_solver=1, coarse_rtol=1e-4, coarse_maxit=30)}
+    if args.method == "va3s3cs1":
+        return {"name": "va3s3cs1", "desc": "3 matching sweeps/level, smoothed P (omega=4/3/||D^-1A||), FCG(1), "
+                                            "1/1 HINVK sweeps (IC(0) + 1 fill level in the inversion, one block "
+                                            "per GPU), coarsest CG preconditioned by HINVK (1e-4, 30 its)",
+                "cfg": dict(pre_sweeps=1, post_sweeps=1, max_coarse_size=12 * 200 * world, krylov=1,
+                            smoother=1, invk_fill=1, coarse_solver=1, coarse_prec=1, coarse_rtol=1e-4,
+                            coarse_maxit=30)}
     if args.method == "invk":
         return {"name": "invk", "desc": "3 matching sweeps/level, smoothed P (omega=4/3/||D^-1A||), INVK smoother "
                                         "(IC(0) + 1 level of fill in the inversion), PCG, direct coarsest",
@@ -202,8 +317,6 @@ def run_ours(args):
     import torch
 
     world, rank, local = dist_init(args)
-    if world != args.gpus:
-        print(f"--gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     torch.cuda.set_device(local)
     import paper_2006_16147_b200 as amg
     from inputs import config_problem
@@ -273,18 +386,20 @@ def run_ours(args):
     bytes_it = hrep["iteration_bytes_model"]
     peak, peak_src = measured_peaks()
 
-    # per-kernel timing (instrumented eager V-cycles on the same stream) -> dominant kernel
+    # per-kernel timing (instrumented eager V-cycles / whole iterations on the solve stream):
+    # the dominant kernel of an ITERATION (the V-cycle kernels, q = A p, the vector updates)
     prof = h.profile_vcycle(10)
-    per_v = len(prof)
-    dom = max(prof, key=lambda k: k["ms"])
-    dom_gbs = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
-    dom_stored_gbs = dom["stored_bytes"] / (dom["ms"] * 1e-3) / 1e9
+    prof_it = h.profile_iteration(bt, 10)
+    dom = max(prof_it, key=lambda k: k["ms"])
+    dom_gbs = dom["stored_bytes"] / (dom["ms"] * 1e-3) / 1e9
+    dom_model_gbs = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             tr = json.load(f)
-        traffic = tr.get(f"c{args.config}:{dom['name']}")
+        traffic = tr.get(f"c{args.config}:{dom['name']}") if meta["grid"] == (256, 256, 256) else None
+    it_ms = sum(k["ms"] for k in prof_it)
 
     # e2e through the public API with host buffers: every step copies its b host->device and
     # its x device->host; amg_solve_host_batch pipelines those copies with the solves
@@ -298,13 +413,10 @@ def run_ours(args):
     h.solve_host_batch(Bh, Xh, rtol=args.rtol, maxit=args.maxit)
     e2e_s = allmax(world, (time.perf_counter() - t0) / args.steps)
 
-    # CPU oracle baseline (rank 0, N = 1 only)
+    # CPU oracle baseline (rank 0, N = 1 only): the oracle on this same workload
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nS, setupS, timesS, itsS = oracle_sample(args.rtol, 1)
-        cpu = {"value": nS / timesS[0], "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"single-thread fp64 C oracle, one full PCG solve ({itsS[0]} its) on the "
-                         f"{CPU_SAMPLE_GRID} grid of the same generator, setup {setupS:.1f} s untimed"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and method["name"] == "default":
+        cpu = cpu_baseline_record(args, tuple(meta["grid"]))
 
     if rank == 0:
         value = n_global / (ms_per_step * 1e-3)
@@ -329,14 +441,18 @@ def run_ours(args):
             "iteration_bytes_model": bytes_it,
             "roofline": {"bound": "hbm", "kernel": dom["name"], "achieved": dom_gbs, "peak": peak,
                          "unit": "GB/s", "frac": dom_gbs / peak, "traffic": traffic,
-                         "bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"],
-                         "stored_bytes_per_launch": dom["stored_bytes"],
-                         "achieved_stored_GBps": dom_stored_gbs, "frac_stored": dom_stored_gbs / peak,
-                         "note": "achieved uses SURVEY 8(d) algorithmic bytes (12 B/nnz); SDIA-32 stores no "
-                                 "per-entry column index, so the compulsory (stored) bytes are smaller",
-                         "share_of_vcycle": dom["ms"] / sum(k["ms"] for k in prof),
+                         "bytes": "stored: what the chosen device format and the fused epilogue move per "
+                                  "launch (SDIA-32 values + slice offsets, gathered/written vectors once)",
+                         "stored_bytes_per_launch": dom["stored_bytes"], "ms_per_launch": dom["ms"],
+                         "model_bytes_per_launch": dom["bytes"], "achieved_model_GBps": dom_model_gbs,
+                         "model_note": "SURVEY 8(d) algorithmic bytes charge 12 B/nnz incl. a 4 B column index "
+                                       "SDIA-32 does not store, hence model GB/s can exceed the peak",
+                         "share_of_iteration": dom["ms"] / it_ms,
                          "peak_source": peak_src,
-                         "timing": "CUDA events on the solve stream, instrumented V-cycles after the timed region"},
+                         "timing": "CUDA events on the solve stream around every kernel of 10 instrumented "
+                                   "eager PCG iterations after the timed region"},
+            "kernels_per_iteration": [(k["name"], round(k["ms"], 4), round(k["stored_bytes"] / (k["ms"] * 1e-3) / 1e9, 1))
+                                      for k in prof_it],
             "kernels_per_vcycle": [(k["name"], round(k["ms"], 4), round(k["bytes"] / (k["ms"] * 1e-3) / 1e9, 1),
                                     round(k["stored_bytes"] / (k["ms"] * 1e-3) / 1e9, 1)) for k in prof],
             "vcycle_stored_bytes": sum(k["stored_bytes"] for k in prof),
@@ -344,10 +460,9 @@ def run_ours(args):
             "e2e": {"value": n_global / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * bh.shape[0] * world,
                     "d2h_bytes_per_step": 8 * bh.shape[0] * world, "s_per_step": e2e_s,
                     "api": "amg_solve_host_batch (pinned host b/x per step, copies pipelined with the solves)"},
-            # per solve: prologue + per iteration (cycle kernels + q = A p [+ p-update] + r-update)
-            # + the deferred final x update; single-rank PCG fuses the p-update into q = A p
-            "gpu_launches": args.steps * (2 + iters * (per_v + (2 if (method["cfg"].get("krylov", 0) == 0
-                                                                    and world == 1) else 3))),
+            # per solve: prologue + per iteration (the kernels one profiled iteration launched)
+            # + the deferred final x update
+            "gpu_launches": args.steps * (2 + iters * len(prof_it)),
             "clocks": ck,
         }
         print(json.dumps(line), flush=True)
@@ -369,7 +484,7 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--maxit", type=int, default=500)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--method", choices=["default", "va3s5cs1", "ka1", "invk"], default="default")
+    ap.add_argument("--method", choices=["default", "va3s5cs1", "va3s3cs1", "ka1", "invk"], default="default")
     ap.add_argument("--tail-rows", type=int, default=None, help="override cfg.tail_rows (0 = no persistent tail)")
     ap.add_argument("--tail-bytes", type=int, default=None, help="override cfg.tail_bytes (0 = no cluster tail)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -377,6 +492,8 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("note: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(sys.argv[1:], args.gpus))
     sys.exit(run_reference(args) if args.impl == "reference" else run_ours(args))
 
 

@@ -113,14 +113,35 @@ typedef struct {
     int32_t smoother;             /* 0 = l1-Jacobi (default); 1 = INVK (
                                      SURVEY.md §8f NEXT-3): IC(0) = ILU(0) in LDL^T form, W = L^{-1}
                                      with `invk_fill` levels of positional fill, a smoothing step is
-                                     x += W^T D^{-1} W (b - A x) (two extra SpMVs).  Single-rank
-                                     contexts only.  With one process HINVK = INVK. */
+                                     x += W^T D^{-1} W (b - A x) (two extra SpMVs), computed per
+                                     diagonal block (HINVK / l1-INVK, see invk_l1 / invk_blocks).  With
+                                     one block (one process) HINVK = INVK. */
     int32_t invk_fill;            /* fill levels admitted in the inversion (default 1, Table 1
                                      caption PAPER.md:207) */
     int64_t tail_bytes;           /* single-process, direct coarsest: the cycle rooted at the first
                                      level from which all coarser operators take <= tail_bytes runs
                                      as ONE thread-block-cluster kernel (<= 16 CTAs, hardware
                                      cluster barriers between its operations).  0 = off. */
+    /* --- block-Jacobi INVK forms and the VA3S3CS1 coarse solver --- */
+    int32_t invk_l1;              /* smoother == 1: 0 = HINVK, the INVK factors of every rank's
+                                     diagonal block A_pp; 1 = l1-INVK, the factors of
+                                     A_pp + D_l1,p (Eq. 3.5 weights of the couplings outside the block,
+                                     PAPER.md:180-181).  With one block both are plain INVK. */
+    int32_t invk_blocks;          /* number of diagonal blocks: 0 (default) = one per rank of the
+                                     partition (nranks, or emulate_ranks); k > 0 = k equal level-0 row
+                                     blocks with coarse rows in the block of their aggregate's minimum
+                                     member (R18): the paper's k-process block-Jacobi setting on one GPU
+                                     (single-rank contexts; multi-rank contexts need 0 or nranks) */
+    int32_t invk_dense_cut;       /* 0 (default) = "a single level of fill-in in the inversion" on every
+                                     level.  c > 0: levels with more than c stored entries
+                                     per row of A_l keep only the pattern of L (fill 0) -- a NON-paper
+                                     setup-cost knob (the level-1 fill of a dense coarse row fills most of
+                                     the triangle), documented as a deviation in DESIGN.md §8e */
+    int32_t coarse_prec;          /* coarse_solver == 1: preconditioner of the coarse CG; 0 = l1-Jacobi
+                                     diagonal of A_L (VA3S5CS1, default); 1 = the (H)INVK factors of A_L
+                                     with the smoother's blocks / l1 / fill (VA3S3CS1: "we apply HINVK also
+                                     as preconditioner of the CG method at the coarsest level",
+                                     PAPER.md:420) */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */
@@ -227,6 +248,15 @@ int amg_hierarchy_report(amg_hier_t h, amg_report_t* rep);
 int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out,
                        double* bytes_out, double* stored_bytes_out, const char** names_out,
                        int32_t* count);
+
+/* The same probe over whole solver iterations (the V-cycle, q = A p with its dots, the
+ * vector updates): runs the solver's prologue on b_dev / x_dev (device, local rows; x_dev is
+ * overwritten), one warm-up iteration, then `napply` iterations in fixed-count mode with CUDA
+ * events around every kernel, and reports the kernels of one iteration in launch order.  Used
+ * to name the dominant kernel of an iteration for the roofline. */
+int amg_profile_iteration(amg_hier_t h, const double* b_dev, double* x_dev, int32_t napply, int32_t cap,
+                          double* ms_out, double* bytes_out, double* stored_bytes_out, const char** names_out,
+                          int32_t* count);
 
 /* ---- Host-only view of the setup phase (no device needed with setup_device = 0) ----
  * Runs exactly the setup that amg_hierarchy_build runs (the same C++ code) on a

@@ -199,3 +199,22 @@ class Hierarchy:
         k = min(cnt.value, cap)
         return [dict(name=names[i].decode(), ms=float(ms[i]), bytes=float(by[i]), stored_bytes=float(sb[i]))
                 for i in range(k)]
+
+    def profile_iteration(self, b, napply: int = 10, cap: int = 512):
+        """amg_profile_iteration: per-kernel device times of whole solver iterations (b: CUDA tensor;
+        a scratch x is used)."""
+        import torch
+        if not (b.dtype == torch.float64 and b.is_cuda and b.is_contiguous() and b.numel() == self.n_local):
+            raise ValueError(f"b must be a contiguous float64 CUDA tensor of {self.n_local} entries")
+        x = torch.empty_like(b)
+        torch.cuda.current_stream(b.device).synchronize()
+        ms = np.zeros(cap)
+        by = np.zeros(cap)
+        sb = np.zeros(cap)
+        names = (C.c_char_p * cap)()
+        cnt = C.c_int32()
+        check(lib.amg_profile_iteration(self.h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), napply, cap,
+                                        _ptr(ms), _ptr(by), _ptr(sb), names, C.byref(cnt)), "amg_profile_iteration")
+        k = min(cnt.value, cap)
+        return [dict(name=names[i].decode(), ms=float(ms[i]), bytes=float(by[i]), stored_bytes=float(sb[i]))
+                for i in range(k)]

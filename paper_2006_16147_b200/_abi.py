@@ -27,7 +27,8 @@ class amg_config_t(C.Structure):
                 ("krylov", C.c_int32), ("coarse_solver", C.c_int32), ("coarse_maxit", C.c_int32),
                 ("coarse_rtol", C.c_double), ("cycle", C.c_int32), ("setup_device", C.c_int32),
                 ("tail_rows", C.c_int64), ("smoother", C.c_int32), ("invk_fill", C.c_int32),
-                ("tail_bytes", C.c_int64)]
+                ("tail_bytes", C.c_int64), ("invk_l1", C.c_int32), ("invk_blocks", C.c_int32),
+                ("invk_dense_cut", C.c_int32), ("coarse_prec", C.c_int32)]
 
 
 class amg_report_t(C.Structure):
@@ -65,6 +66,8 @@ _SIG = {
     "amg_hierarchy_report": (C.c_int, [_vp, C.POINTER(amg_report_t)]),
     "amg_profile_vcycle": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp,
                                      C.POINTER(C.c_int32)]),
+    "amg_profile_iteration": (C.c_int, [_vp, _vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp,
+                                        C.POINTER(C.c_int32)]),
     "amg_last_error": (C.c_char_p, []),
     "amg_nccl_unique_id": (C.c_int, [_vp]),
     "amg_host_hierarchy_build": (C.c_int, [C.c_int64, _vp, _vp, _vp, _vp, C.POINTER(amg_config_t),

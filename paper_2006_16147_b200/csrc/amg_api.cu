@@ -219,6 +219,9 @@ struct RankState {
     // the per-CTA row split and the cluster launch shape of k_coarse_cg
     int32_t *cg_rp = nullptr, *cg_ci = nullptr, *cg_split = nullptr;
     double *cg_v = nullptr, *cg_m = nullptr;
+    // coarse CG preconditioned by the (H)INVK factors of A_L (coarse_prec == 1, VA3S3CS1)
+    int32_t *cg_wrp = nullptr, *cg_wci = nullptr, *cg_zrp = nullptr, *cg_zci = nullptr;
+    double *cg_wv = nullptr, *cg_zv = nullptr;
     int64_t cg_nnz = 0;
     int cg_ncta = 1, cg_smem_a = 0;
     size_t cg_smem = 0;
@@ -229,6 +232,9 @@ struct RankState {
         cudaFree(cg_split);
         cudaFree(cg_v);
         cudaFree(cg_m);
+        for (int32_t* p : {cg_wrp, cg_wci, cg_zrp, cg_zci}) cudaFree(p);
+        cudaFree(cg_wv);
+        cudaFree(cg_zv);
         cudaFree(cinv);
         cudaFree(pr);
         cudaFree(pz);
@@ -279,6 +285,13 @@ struct amg_hier_s {
     double* bx[2] = {nullptr, nullptr};
     cudaGraphExec_t batch_exec[2] = {nullptr, nullptr};
     cudaStream_t cstream = nullptr, dstream = nullptr;  // host->device / device->host copies
+    // solve graph shape: GM_WHILE = one graph per solve (a device-side WHILE node over the
+    // iteration, no host round trip); GM_ITER = one graph per iteration launched from a host loop
+    // with one status read each (the fallback of NCCL contexts if the WHILE graph cannot be built
+    // or instantiated, decided collectively; AMG_MULTI_GRAPH=iter forces it)
+    int graph_mode = 0;
+    cudaGraphExec_t iter_exec = nullptr;
+    double* iter_x = nullptr;
     cudaGraphExec_t apply_exec = nullptr;
     const double* apply_r = nullptr;
     double* apply_z = nullptr;
@@ -318,6 +331,7 @@ struct amg_hier_s {
         if (cstream) cudaStreamDestroy(cstream);
         if (dstream) cudaStreamDestroy(dstream);
         if (apply_exec) cudaGraphExecDestroy(apply_exec);
+        if (iter_exec) cudaGraphExecDestroy(iter_exec);
         for (auto& R : ranks) R.release();
         cudaFree(hb);
         cudaFree(hx);
@@ -473,7 +487,7 @@ void nccl_note(amg_hier_s* h, ncclResult_t r, const char* what) {
 }
 
 // Multi-rank: gather every rank's dot total to every rank, then finish in rank order.
-void dot_finish(amg_hier_s* h, Launch& L, int kind) {
+void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0) {
     if (!h->multi()) return;
     if (h->loopback) {
         for (auto& Rd : h->ranks)
@@ -486,24 +500,27 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind) {
                   "ncclAllGather (dot totals)");
     }
     for (auto& R : h->ranks) {
-        RedCtx rc{nullptr, nullptr, nullptr, R.st, 0ull, kind, nullptr};
+        // every rank computes the same status; in loopback each sets the (shared) WHILE condition
+        RedCtx rc{nullptr, nullptr, nullptr, R.st, cond, kind, nullptr};
         launch_k(k_finish, 1, 32, L.s, R.dot_all, kDotSlots * h->np, rc);
         cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);  // slots of skipped parts stay 0
     }
 }
 
 using VecOf = std::function<double*(RankState&)>;
+// custom unpack of a received halo (rank, its exchange plan, stream); null: v[idx] = buf
+using UnpackFn = std::function<void(RankState&, const Exch&, cudaStream_t)>;
 
 // Halo exchange of a level-l vector (window base pointer given per rank) on stream `st`.
-void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec);
+void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const UnpackFn* unpack = nullptr);
 void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) { exchange_on(h, L.s, l, vec); }
 
 // Overlapped exchange: fork the comm stream off the context stream, exchange there,
 // and let the caller launch the interior rows before exchange_end joins the streams.
-void exchange_begin(amg_hier_s* h, Launch& L, int l, const VecOf& vec) {
+void exchange_begin(amg_hier_s* h, Launch& L, int l, const VecOf& vec, const UnpackFn* unpack = nullptr) {
     cudaEventRecord(h->ev_fork, L.s);
     cudaStreamWaitEvent(h->comm, h->ev_fork, 0);
-    exchange_on(h, h->comm, l, vec);
+    exchange_on(h, h->comm, l, vec, unpack);
     cudaEventRecord(h->ev_join, h->comm);
 }
 void exchange_end(amg_hier_s* h, Launch& L) { cudaStreamWaitEvent(L.s, h->ev_join, 0); }
@@ -513,12 +530,21 @@ void exchange_end(amg_hier_s* h, Launch& L) { cudaStreamWaitEvent(L.s, h->ev_joi
 // interior units (no halo columns) run, then the head and tail units (north_star (4):
 // "halo exchange ... overlapped with interior SpMV").
 using PartFn = std::function<void(RankState&, int)>;
-void overlapped(amg_hier_s* h, Launch& L, int lx, const VecOf& xv, bool dist, const PartFn& fn) {
+// distributed levels with fewer rows per rank are not split into interior / boundary launches:
+// their operator passes are a few microseconds, shorter than the exchange they would overlap
+constexpr int64_t kSplitRows = 4096;
+void overlapped(amg_hier_s* h, Launch& L, int lx, const VecOf& xv, bool dist, const PartFn& fn,
+                const UnpackFn* unpack = nullptr) {
     if (!h->multi() || !dist) {
         for (auto& R : h->ranks) fn(R, 0);
         return;
     }
-    exchange_begin(h, L, lx, xv);
+    if (h->ranks[0].lv[lx].comp_n < kSplitRows) {  // tiny distributed level: the split only adds launches
+        exchange_on(h, L.s, lx, xv, unpack);
+        for (auto& R : h->ranks) fn(R, 0);
+        return;
+    }
+    exchange_begin(h, L, lx, xv, unpack);
     for (auto& R : h->ranks) fn(R, 1);
     exchange_end(h, L);
     for (auto& R : h->ranks) {
@@ -527,7 +553,7 @@ void overlapped(amg_hier_s* h, Launch& L, int lx, const VecOf& xv, bool dist, co
     }
 }
 
-void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec) {
+void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const UnpackFn* unpack) {
     if (!h->multi()) return;
     struct { cudaStream_t s; } L{st};
     const int nsm = h->ctx->nsm;
@@ -563,7 +589,9 @@ void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec) {
     }
     for (auto& R : h->ranks) {
         const Exch& E = R.lv[l].ex;
-        if (E.nrecv) launch_k(k_unpack, vec_grid(E.nrecv, nsm), kBlock, L.s, vec(R), E.recv_idx, E.rbuf, E.nrecv);
+        if (!E.nrecv) continue;
+        if (unpack) (*unpack)(R, E, L.s);
+        else launch_k(k_unpack, vec_grid(E.nrecv, nsm), kBlock, L.s, vec(R), E.recv_idx, E.rbuf, E.nrecv);
     }
 }
 
@@ -580,7 +608,8 @@ void launch_coarse(amg_hier_s* h, Launch& L, RankState& R, const double* b, doub
     // bytes of ONE pass over A_L (the iteration count is data dependent; latency-bound)
     L.begin("coarse_cg", 12.0 * (double)R.cg_nnz + 4.0 * (double)(R.nL + 1) + 24.0 * (double)R.nL);
     const CoarseCG A{R.cg_rp, R.cg_ci, R.cg_v, R.cg_m, R.cg_split, (int32_t)R.nL, R.cg_ncta, R.cg_smem_a,
-                     h->cfg.coarse_maxit, h->cfg.coarse_rtol};
+                     h->cfg.coarse_maxit, h->cfg.coarse_rtol, R.cg_wrp, R.cg_wci, R.cg_wv, R.cg_zrp, R.cg_zci,
+                     R.cg_zv};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)R.cg_ncta);
     cfg.blockDim = dim3((unsigned)kCgBlock);
@@ -869,111 +898,149 @@ RedCtx sink_red(amg_hier_s* h, RankState& R, int dkind, const DotSink* sink) {
     return dot_red(h, R, dkind, 0);
 }
 
-// Level l of the cycle with the INVK smoother (cfg.smoother == 1; single rank):
-// M^{-1} r = Z (Wd r), Wd = D^{-1} W, Z = W^T.  The iterate lives
-// in `out` throughout (every update is row-local), Wd r in the level's mb buffer
-// (m o b is not used with INVK), residuals in r:
+// Level l of the cycle with the INVK smoother (cfg.smoother == 1): M^{-1} r = Z (Wd r),
+// Wd = D^{-1} W, Z = W^T of the rank's diagonal block (HINVK / l1-INVK).
+// The iterate lives in `out` throughout (every update is row-local), Wd r in the level's mb
+// buffer (m o b is not used with INVK), residuals in r:
 //   out = Z (Wd b); [s1-1 times: r' = b - A out; out += Z (Wd r')]; r = b - A out;
 //   b_{l+1} = R r; e = cycle(l+1); out += P-bar e; s2 times: r' = b - A out;
 //   out += Z (Wd r')   (the last one at level 0 also reduces the PCG/FCG dot).
+// Several ranks: the factors are block-diagonal over the ranks' rows, so only the residual
+// SpMVs, the restriction and the prolongation exchange halos (overlapped with their interior
+// rows); Wd and Z run on the rank's own rows.
 void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf& outv, bool dot,
                         const VecOf* dwv, const DotSink* sink) {
     const int dkind = dwv ? FIN_ZQ : FIN_RZ;
     const int nl = h->nlev();
     const int s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
-    RankState& R = h->ranks[0];
-    DevLevel& D = R.lv[l];
-    DevLevel& C = R.lv[l + 1];
-    const double* b = bvec(R);
-    double* x = outv(R);
-    const double n8 = 8.0 * (double)D.comp_n;
-    launch_mat(L, D.Wd, GVec{b}, EStore{D.mb}, no_red(), "invk_w", 2 * n8);
-    launch_mat(L, D.Z, GVec{D.mb}, EStore{x}, no_red(), "invk_z", 2 * n8);
-    auto sweep = [&](bool dt) {
-        launch_mat(L, D.A, GVec{x}, EResid{b, D.r}, no_red(), "invk_resid", 3 * n8);
-        launch_mat(L, D.Wd, GVec{D.r}, EStore{D.mb}, no_red(), "invk_w", 2 * n8);
-        if (dt)
-            launch_mat(L, D.Z, GVec{D.mb}, EAddDot<true>{x, x, dwv ? (*dwv)(R) : b}, sink_red(h, R, dkind, sink),
-                       "invk_z_dot", 4 * n8);
-        else
-            launch_mat(L, D.Z, GVec{D.mb}, EAddDot<false>{x, x}, no_red(), "invk_z", 3 * n8);
+    const bool dist = !h->ranks[0].lv[l].replicated;
+    const bool cdist = !h->ranks[0].lv[l + 1].replicated;
+    auto n8 = [l](RankState& R) { return 8.0 * (double)R.lv[l].comp_n; };
+    // out (+)= Z (Wd src) on every rank's computed rows
+    auto precond = [&](const VecOf& src, bool add, bool dt) {
+        for (auto& R : h->ranks) {
+            DevLevel& D = R.lv[l];
+            double* x = outv(R) + D.ep_off;
+            launch_mat(L, D.Wd, GVec{src(R)}, EStore{D.mb + D.ep_off}, no_red(), "invk_w", 2 * n8(R));
+            if (dt)
+                launch_mat(L, D.Z, GVec{D.mb}, EAddDot<true>{x, x, dwv ? (*dwv)(R) + D.ep_off : bvec(R) + D.ep_off},
+                           sink ? sink_red(h, R, dkind, sink) : dot_red(h, R, dkind, 0), "invk_z_dot", 4 * n8(R));
+            else if (add)
+                launch_mat(L, D.Z, GVec{D.mb}, EAddDot<false>{x, x}, no_red(), "invk_z", 3 * n8(R));
+            else
+                launch_mat(L, D.Z, GVec{D.mb}, EStore{x}, no_red(), "invk_z", 2 * n8(R));
+        }
     };
-    for (int sw = 1; sw < s1; ++sw) sweep(false);
-    launch_mat(L, D.A, GVec{x}, EResid{b, D.r}, no_red(), "resid", 3 * n8);
-    launch_mat(L, D.R, GVec{D.r}, EStore{C.b}, no_red(), "restrict", n8 + 8.0 * (double)C.comp_n);
+    const VecOf rv = [l](RankState& R) { return R.lv[l].r; };
+    auto resid = [&](const char* name) {  // r = b - A out (halo of out)
+        overlapped(h, L, l, outv, dist, [&](RankState& R, int part) {
+            DevLevel& D = R.lv[l];
+            launch_mat(L, D.A, GVec{outv(R)}, EResid{bvec(R) + D.ep_off, D.r + D.ep_off}, no_red(), name,
+                       3 * n8(R), part);
+        });
+    };
+    precond(bvec, false, false);
+    for (int sw = 1; sw < s1; ++sw) {
+        resid("invk_resid");
+        precond(rv, true, false);
+    }
+    resid("resid");
+    overlapped(h, L, l, rv, dist, [&](RankState& R, int part) {
+        DevLevel& D = R.lv[l];
+        launch_mat(L, D.R, GVec{D.r}, EStore{R.lv[l + 1].b + D.rst_off}, no_red(), "restrict",
+                   n8(R) + 8.0 * (double)D.rst_n, part);
+    });
+    if (!cdist && dist)  // first replicated level: gather the restricted rhs
+        exchange(h, L, l + 1, [&](RankState& R) { return R.lv[l + 1].b; });
     const bool kfcg = h->cfg.cycle == 1 && l + 1 < nl - 1;
     const VecOf cb = [l](RankState& R) { return R.lv[l + 1].b; };
     const VecOf ev = kfcg ? VecOf([l](RankState& R) { return R.lv[l + 1].kx; })
                           : VecOf([l](RankState& R) { return R.lv[l + 1].xa; });
     if (kfcg) enqueue_fcg2(h, L, l + 1);
     else enqueue_level(h, L, l + 1, cb, nullptr, ev, false, nullptr);
-    if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
-        launch_mat(L, D.P, GXap{C.kx, C.kp2, C.kst}, EProlongAdd{x, x}, no_red(), "prolong",
-                   2 * n8 + 16.0 * (double)C.comp_n);
-    else
-        launch_mat(L, D.P, GVec{ev(R)}, EProlongAdd{x, x}, no_red(), "prolong", 2 * n8 + 8.0 * (double)C.comp_n);
-    for (int sw = 0; sw < s2; ++sw) sweep(dot && sw == s2 - 1);
+    overlapped(h, L, l + 1, ev, cdist, [&](RankState& R, int part) {
+        DevLevel& D = R.lv[l];
+        DevLevel& C = R.lv[l + 1];
+        double* x = outv(R) + D.ep_off;
+        if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
+            launch_mat(L, D.P, GXap{C.kx, C.kp2, C.kst}, EProlongAdd{x, x}, no_red(), "prolong",
+                       2 * n8(R) + 16.0 * (double)C.comp_n, part);
+        else
+            launch_mat(L, D.P, GVec{ev(R)}, EProlongAdd{x, x}, no_red(), "prolong",
+                       2 * n8(R) + 8.0 * (double)C.comp_n, part);
+    });
+    for (int sw = 0; sw < s2; ++sw) {
+        resid("invk_resid");
+        precond(rv, true, dot && sw == s2 - 1);
+    }
     if (dot && !sink) dot_finish(h, L, dkind);
 }
 
 // Collapsed level (compact, above a direct coarsest solve): out = S2(b) + M b in ONE kernel.
+// Single rank, or a replicated level of a multi-rank hierarchy (every rank computes all rows).
 void enqueue_level_collapsed(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf& outv, bool dot,
                              const VecOf* dwv, const DotSink* sink) {
-    RankState& R = h->ranks[0];
-    DevLevel& D = R.lv[l];
-    const double* b = bvec(R);
-    double* out = outv(R);
-    const int64_t n = D.comp_n;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, kMaxPartials));
-    const bool krhs = sink && sink->kb;
-    const double* dw = (dot && dwv) ? (*dwv)(R) : nullptr;
     const int dkind = dwv ? FIN_ZQ : FIN_RZ;
-    const RedCtx red = dot ? sink_red(h, R, dkind, sink) : no_red();
-    L.begin("collapsed", 8.0 * (double)n * (double)n + 16.0 * (double)n);
-    if (krhs) {
-        const GBaq g{sink->kb, sink->kq, sink->ks};
-        double* rhs = const_cast<double*>(b);
-        if (dot) launch_k(k_collapsed<GBaq, true, true>, grid, kBlock, L.s, (const double*)D.Mc, n, g, rhs, out, dw, red);
-        else launch_k(k_collapsed<GBaq, false, true>, grid, kBlock, L.s, (const double*)D.Mc, n, g, rhs, out, dw, red);
-    } else {
-        const GVec g{b};
-        if (dot) launch_k(k_collapsed<GVec, true, false>, grid, kBlock, L.s, (const double*)D.Mc, n, g, (double*)nullptr, out, dw, red);
-        else launch_k(k_collapsed<GVec, false, false>, grid, kBlock, L.s, (const double*)D.Mc, n, g, (double*)nullptr, out, dw, red);
+    for (auto& R : h->ranks) {
+        DevLevel& D = R.lv[l];
+        const double* b = bvec(R);
+        double* out = outv(R);
+        const int64_t n = D.comp_n;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, kMaxPartials));
+        const bool krhs = sink && sink->kb;
+        const double* dw = (dot && dwv) ? (*dwv)(R) : nullptr;
+        const RedCtx red = dot ? sink_red(h, R, dkind, sink) : no_red();
+        L.begin("collapsed", 8.0 * (double)n * (double)n + 16.0 * (double)n);
+        if (krhs) {
+            const GBaq g{sink->kb, sink->kq, sink->ks};
+            double* rhs = const_cast<double*>(b);
+            if (dot) launch_k(k_collapsed<GBaq, true, true>, grid, kBlock, L.s, (const double*)D.Mc, n, g, rhs, out, dw, red);
+            else launch_k(k_collapsed<GBaq, false, true>, grid, kBlock, L.s, (const double*)D.Mc, n, g, rhs, out, dw, red);
+        } else {
+            const GVec g{b};
+            if (dot) launch_k(k_collapsed<GVec, true, false>, grid, kBlock, L.s, (const double*)D.Mc, n, g, (double*)nullptr, out, dw, red);
+            else launch_k(k_collapsed<GVec, false, false>, grid, kBlock, L.s, (const double*)D.Mc, n, g, (double*)nullptr, out, dw, red);
+        }
+        L.end();
     }
-    L.end();
     if (dot && !sink) dot_finish(h, L, dkind);
 }
 
 // Compact small level (see compact_level_ok): s = S2(b) = m b + m (b - A (m b)) into r;
 // b_{l+1} = Rc b; coarse correction e; out = s + Pc e (+ the K-cycle dot of a sink).
+// Single rank, or a replicated level of a multi-rank hierarchy (no halo below it).
 void enqueue_level_compact(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf& outv, bool dot,
                            const VecOf* dwv, const DotSink* sink) {
     const int nl = h->nlev();
-    RankState& R = h->ranks[0];
-    DevLevel& D = R.lv[l];
-    DevLevel& C = R.lv[l + 1];
-    const double* b = bvec(R);
-    double* out = outv(R);
-    const double n8 = 8.0 * (double)D.comp_n, nc8 = 8.0 * (double)C.comp_n;
+    const bool krhs = sink && sink->kb;  // K-cycle second application: rhs = b - alpha q, stored in b
     // the smoothing branch s = S2(b) runs on the second stream, concurrently with the
     // restriction and the whole coarse correction; the post kernel joins it
     cudaEventRecord(h->ev_fork, L.s);
     cudaStreamWaitEvent(h->comm, h->ev_fork, 0);
-    const bool krhs = sink && sink->kb;  // K-cycle second application: rhs = b - alpha q, stored in b
     {
         Launch Ls{h, h->comm};
-        if (krhs)
-            launch_mat(Ls, D.A, GMBaq{D.m, sink->kb, sink->kq, sink->ks},
-                       ESweep0K{sink->kb, sink->kq, sink->ks, const_cast<double*>(b), D.r}, no_red(), "sweep0_c",
-                       5 * n8);
-        else
-            launch_mat(Ls, D.A, GMB{D.m, b}, ESweep0{b, D.r}, no_red(), "sweep0_c", 3 * n8);
+        for (auto& R : h->ranks) {
+            DevLevel& D = R.lv[l];
+            const double* b = bvec(R);
+            const double n8 = 8.0 * (double)D.comp_n;
+            if (krhs)
+                launch_mat(Ls, D.A, GMBaq{D.m, sink->kb, sink->kq, sink->ks},
+                           ESweep0K{sink->kb, sink->kq, sink->ks, const_cast<double*>(b), D.r}, no_red(), "sweep0_c",
+                           5 * n8);
+            else
+                launch_mat(Ls, D.A, GMB{D.m, b}, ESweep0{b, D.r}, no_red(), "sweep0_c", 3 * n8);
+        }
     }
     cudaEventRecord(h->ev_join, h->comm);
-    if (krhs)
-        launch_mat(L, D.Rc, GBaq{sink->kb, sink->kq, sink->ks}, EStore{C.b}, no_red(), "restrict_c", 2 * n8 + nc8);
-    else
-        launch_mat(L, D.Rc, GVec{b}, EStore{C.b}, no_red(), "restrict_c", n8 + nc8);
+    for (auto& R : h->ranks) {
+        DevLevel& D = R.lv[l];
+        DevLevel& C = R.lv[l + 1];
+        const double n8 = 8.0 * (double)D.comp_n, nc8 = 8.0 * (double)C.comp_n;
+        if (krhs)
+            launch_mat(L, D.Rc, GBaq{sink->kb, sink->kq, sink->ks}, EStore{C.b}, no_red(), "restrict_c", 2 * n8 + nc8);
+        else
+            launch_mat(L, D.Rc, GVec{bvec(R)}, EStore{C.b}, no_red(), "restrict_c", n8 + nc8);
+    }
     const bool kfcg = h->cfg.cycle == 1 && l + 1 < nl - 1;
     const VecOf cb = [l](RankState& R) { return R.lv[l + 1].b; };
     const VecOf cmb = [l](RankState& R) { return R.lv[l + 1].mb; };
@@ -986,19 +1053,25 @@ void enqueue_level_compact(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, c
     // joins this level's smoothing branch (a deeper compact level re-records ev_join later on the
     // same second stream, which orders after this level's branch: still a correct dependency)
     cudaStreamWaitEvent(L.s, h->ev_join, 0);
-    auto post = [&](auto g) {
-        if (dot) {
-            const int dkind = dwv ? FIN_ZQ : FIN_RZ;
-            launch_mat(L, D.Pc, g, EAddDot<true>{D.r, out, dwv ? (*dwv)(R) : b}, sink_red(h, R, dkind, sink),
-                       "prolong_post_c", 3 * n8 + nc8);
-            if (!sink) dot_finish(h, L, dkind);
-        } else {
-            launch_mat(L, D.Pc, g, EAddDot<false>{D.r, out}, no_red(), "prolong_post_c", 2 * n8 + nc8);
-        }
-    };
-    if (kfcg && kcycle_fused(h) && !tailc) post(GXap2{C.kp, C.kp2, C.kst});
-    else if (kfcg) post(GXap{C.kx, tailc ? C.kp : C.kp2, C.kst});
-    else post(GVec{ev(R)});
+    const int dkind = dwv ? FIN_ZQ : FIN_RZ;
+    for (auto& R : h->ranks) {
+        DevLevel& D = R.lv[l];
+        DevLevel& C = R.lv[l + 1];
+        const double* b = bvec(R);
+        double* out = outv(R);
+        const double n8 = 8.0 * (double)D.comp_n, nc8 = 8.0 * (double)C.comp_n;
+        auto post = [&](auto g) {
+            if (dot)
+                launch_mat(L, D.Pc, g, EAddDot<true>{D.r, out, dwv ? (*dwv)(R) : b}, sink_red(h, R, dkind, sink),
+                           "prolong_post_c", 3 * n8 + nc8);
+            else
+                launch_mat(L, D.Pc, g, EAddDot<false>{D.r, out}, no_red(), "prolong_post_c", 2 * n8 + nc8);
+        };
+        if (kfcg && kcycle_fused(h) && !tailc) post(GXap2{C.kp, C.kp2, C.kst});
+        else if (kfcg) post(GXap{C.kx, tailc ? C.kp : C.kp2, C.kst});
+        else post(GVec{ev(R)});
+    }
+    if (dot && !sink) dot_finish(h, L, dkind);
 }
 
 // out = B_l b: the part of the cycle rooted at level l (Eq. 3.1;
@@ -1302,16 +1375,26 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
     const VecOf qv = [](RankState& R) { return R.pq; };
     enqueue_vcycle(h, L, [](RankState& R) { return R.pr; }, [](RankState& R) { return R.pz; }, true,
                    fcg ? &qv : nullptr);
-    if (!fcg && !h->multi() && h->nlev() > 1) {
+    if (!fcg && h->nlev() > 1) {
         // p = z + beta p fused into q = A p (p double-buffered, selected on the device).  (The
         // FCG variant, reducing p^T r there as well, measured 1 % slower: its SDIA/SELL kernels
-        // spill under the 32-register bound, so FCG keeps k_pupdate_fcg.)
-        RankState& R = h->ranks[0];
-        const DevLevel& D = R.L0();
-        launch_mat(L, D.A, GPz{R.pz, R.pp, R.pp2, R.st},
-                   ESpmvDotPz{R.pz, R.pp, R.pp2, R.pq, x_user + R.user_off, R.st}, dot_red(h, R, FIN_PQ, 0),
-                   "spmv_dot_pupd", 48.0 * D.own_n);
-    } else {  // multi-rank, FCG or one level: separate direction update, halo of p, q = A p
+        // spill under the 32-register bound, so FCG keeps k_pupdate_fcg.)  Several ranks: the
+        // halo of z is exchanged and its unpack also forms p_new = z + beta p_old at the halo
+        // positions (p_old's halo arrived with the previous iteration's z), so the gathers see
+        // the same p_new as the owners write.
+        const UnpackFn pz_unpack = [&](RankState& R, const Exch& E, cudaStream_t s) {
+            launch_k(k_unpack_pz, vec_grid(E.nrecv, nsm), kBlock, s, R.pz, R.pp, R.pp2, E.recv_idx, E.rbuf, E.nrecv,
+                     (const PcgState*)R.st);
+        };
+        overlapped(h, L, 0, [](RankState& R) { return R.pz; }, true, [&](RankState& R, int part) {
+            const DevLevel& D = R.L0();
+            const int64_t o = D.own_off;
+            launch_mat(L, D.A, GPz{R.pz, R.pp, R.pp2, R.st},
+                       ESpmvDotPz{R.pz + o, R.pp + o, R.pp2 + o, R.pq + o, x_user + R.user_off, R.st},
+                       dot_red(h, R, FIN_PQ, 0, part), "spmv_dot_pupd", 48.0 * D.own_n, part);
+        }, &pz_unpack);
+        dot_finish(h, L, FIN_PQ);
+    } else {  // FCG or one level: separate direction update, halo of p, q = A p
         for (auto& R : h->ranks) {
             const DevLevel& D = R.L0();
             if (fcg) {
@@ -1341,16 +1424,16 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
                  dot_red(h, R, FIN_RR, cond));
         L.end();
     }
-    dot_finish(h, L, FIN_RR);
+    dot_finish(h, L, FIN_RR, cond);
 }
 
 void enqueue_pcg_final(amg_hier_s* h, Launch& L, double* x_user) {
     for (auto& R : h->ranks) {
         const DevLevel& D = R.L0();
         L.begin("xfinal", 24.0 * D.own_n);
-        const bool fused = h->cfg.krylov != 1 && !h->multi() && h->nlev() > 1;
+        const bool fused = h->cfg.krylov != 1 && h->nlev() > 1;
         launch_k(k_xfinal, vec_grid(D.own_n, h->ctx->nsm), kBlock, L.s, x_user + R.user_off,
-                 (const double*)(R.pp + D.own_off), fused ? (const double*)R.pp2 : (const double*)nullptr,
+                 (const double*)(R.pp + D.own_off), fused ? (const double*)(R.pp2 + D.own_off) : (const double*)nullptr,
                  D.own_n, (const PcgState*)R.st);
         L.end();
     }
@@ -1365,7 +1448,7 @@ void enqueue_pcg_init(amg_hier_s* h, Launch& L, const double* b_user, double* x_
                                                                         dot_red(h, R, FIN_BNORM, cond));
         L.end();
     }
-    dot_finish(h, L, FIN_BNORM);
+    dot_finish(h, L, FIN_BNORM, cond);
 }
 
 // ------------------------------------------------------------- upload
@@ -1844,6 +1927,12 @@ int convert_mat(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t sh
 int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) {
     const amgsetup::Csr& A = C.A;
     const int64_t n = A.nrows, nnz = A.nnz();
+    const bool invk = h->cfg.coarse_prec == 1;
+    if (invk && (C.Wd.nrows != n || C.Z.nrows != n || C.Wd.nnz() >= (int64_t)INT32_MAX ||
+                 C.Z.nnz() >= (int64_t)INT32_MAX)) {
+        set_err("coarse CG: the INVK factors of the coarsest matrix are missing or too large");
+        return AMG_ERR_ARG;
+    }
     if (n > 16384 || nnz >= (int64_t)INT32_MAX) {
         set_err("coarse CG: the coarsest matrix is too large (n_L <= 16384 required)");
         return AMG_ERR_ARG;
@@ -1865,7 +1954,7 @@ int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) 
             own = std::max<int64_t>(own, split[c + 1] - split[c]);
             ann = std::max<int64_t>(ann, A.rp[split[c + 1]] - A.rp[split[c]]);
         }
-        smem_base = 8 * (size_t)n + 32 * (size_t)own;
+        smem_base = 8 * (size_t)n * (invk ? 3 : 1) + 32 * (size_t)own;
         smem_a = 12 * (size_t)ann;
     };
     int ncta = (int)std::min<int64_t>(16, std::max<int64_t>(1, (nnz + 16383) / 16384));
@@ -1907,6 +1996,18 @@ int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) 
     if ((st = dev_copy(&R.cg_v, A.v.data(), A.v.size()))) return st;
     if ((st = dev_copy(&R.cg_m, C.m.data(), C.m.size()))) return st;
     if ((st = dev_copy(&R.cg_split, split.data(), split.size()))) return st;
+    if (invk) {
+        auto up = [&](const amgsetup::Csr& M, int32_t** rpd, int32_t** cid, double** vd) {
+            std::vector<int32_t> r32(M.nrows + 1);
+            for (int64_t i = 0; i <= M.nrows; ++i) r32[i] = (int32_t)M.rp[i];
+            int e;
+            if ((e = dev_copy(rpd, r32.data(), r32.size()))) return e;
+            if ((e = dev_copy(cid, M.ci.data(), M.ci.size()))) return e;
+            return dev_copy(vd, M.v.data(), M.v.size());
+        };
+        if ((st = up(C.Wd, &R.cg_wrp, &R.cg_wci, &R.cg_wv))) return st;
+        if ((st = up(C.Z, &R.cg_zrp, &R.cg_zci, &R.cg_zv))) return st;
+    }
     return AMG_OK;
 }
 
@@ -1919,8 +2020,9 @@ int upload_coarse_cg(amg_hier_s* h, const amgsetup::RankLevel& C, RankState& R) 
 // the smoothing.  Same arithmetic up to rounding order; Rc and Pc are formed once on the host.
 constexpr int64_t kCompactRows = 8192;
 constexpr int64_t kCollapseRows = 2048;  // dense B of the collapsed level: <= 32 MB
-bool collapse_level_ok(const amg_hier_s* h, int l, int nl, int64_t n) {
-    return !h->multi() && h->cfg.smoother == 0 && h->cfg.coarse_solver == 0 && l >= 1 && l + 2 == nl &&
+// (multi-rank: on replicated levels only -- every rank computes all their rows; `rep`)
+bool collapse_level_ok(const amg_hier_s* h, int l, int nl, int64_t n, bool rep) {
+    return (!h->multi() || rep) && h->cfg.smoother == 0 && h->cfg.coarse_solver == 0 && l >= 1 && l + 2 == nl &&
            n <= kCollapseRows && !(h->tail_level >= 0 && l >= h->tail_level);
 }
 // C = X D (X sparse n x k CSR, D dense k x w row-major) -> dense n x w
@@ -1983,8 +2085,8 @@ std::vector<double> dense_level_operator(const amgsetup::Csr& A, const amgsetup:
     }
     return B;
 }
-bool compact_level_ok(const amg_hier_s* h, int l, int nl, int64_t n) {
-    return !h->multi() && h->cfg.pre_sweeps == 1 && h->cfg.post_sweeps == 1 && h->cfg.smoother == 0 && l >= 1 &&
+bool compact_level_ok(const amg_hier_s* h, int l, int nl, int64_t n, bool rep) {
+    return (!h->multi() || rep) && h->cfg.pre_sweeps == 1 && h->cfg.post_sweeps == 1 && h->cfg.smoother == 0 && l >= 1 &&
            l + 1 < nl && n <= kCompactRows && !(h->tail_level >= 0 && l >= h->tail_level);
 }
 amgsetup::Csr csr_from_device(const amgsetup::DevCsrRaw& D, cudaStream_t s) {
@@ -2129,7 +2231,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
                 if ((st = dev_alloc(&D.xb, wn))) return st;
             }
         }
-        if (compact_level_ok(h, l, nl, D.comp_n)) {
+        if (compact_level_ok(h, l, nl, D.comp_n, S.replicated)) {
             amgsetup::Csr A, Pb, Rt;
             std::vector<double> m(D.comp_n);
             if (dk) {
@@ -2149,7 +2251,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
             if ((st = upload_mat(Pc, D.Pc, false, 0))) return st;
             D.compact = true;
         }
-        if (collapse_level_ok(h, l, nl, D.comp_n) &&
+        if (collapse_level_ok(h, l, nl, D.comp_n, S.replicated) &&
             (int64_t)coarse_inv.size() == P.lv[l + 1].n_global * P.lv[l + 1].n_global) {
             // the level above a direct coarsest solve: its whole cycle is a fixed linear map B
             amgsetup::Csr A, Pb, Rt;
@@ -2201,7 +2303,7 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
     if ((st = dev_alloc(&R.pr, w0))) return st;
     if ((st = dev_alloc(&R.pz, w0))) return st;
     if ((st = dev_alloc(&R.pp, w0))) return st;
-    if (!h->multi() && (st = dev_alloc(&R.pp2, w0))) return st;
+    if ((st = dev_alloc(&R.pp2, w0))) return st;
     if ((st = dev_alloc(&R.pq, w0))) return st;
     if ((st = dev_alloc(&R.st, 1))) return st;
     if ((st = dev_alloc(&R.partials, 2 * kMaxPartials))) return st;  // two-dot reductions: 2 per block
@@ -2261,6 +2363,21 @@ void hier_stats(amg_hier_s* h, const amgsetup::Hierarchy& H) {
 }
 
 int build_solve_exec(amg_hier_s* h, const double* b, double* x, cudaGraphExec_t* out);
+enum { GM_WHILE = 0, GM_ITER = 1 };
+// NCCL contexts: every rank must take the same graph shape (the captured collectives must
+// match), so a local failure is agreed on with an eager all-reduce (min) of the success flags.
+int agree_ok(amg_hier_s* h, int ok_local, int* ok_all) {
+    *ok_all = ok_local;
+    if (!h->multi() || h->loopback) return AMG_OK;
+    int* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(int)));
+    CK(cudaMemcpy(d, &ok_local, sizeof(int), cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(d, d, 1, ncclInt, ncclMin, h->ctx->nccl, h->ctx->stream));
+    CK(cudaStreamSynchronize(h->ctx->stream));
+    CK(cudaMemcpy(ok_all, d, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return AMG_OK;
+}
 int ensure_solve_graph(amg_hier_s* h, const double* b, double* x) {
     if (h->solve_exec && h->solve_b == b && h->solve_x == x) return AMG_OK;
     if (h->solve_exec) {
@@ -2268,9 +2385,48 @@ int ensure_solve_graph(amg_hier_s* h, const double* b, double* x) {
         h->solve_exec = nullptr;
     }
     int st = build_solve_exec(h, b, x, &h->solve_exec);
+    if (h->multi() && !h->loopback) {  // NCCL: collective decision, fall back to one graph per iteration
+        int all = 0, e;
+        if ((e = agree_ok(h, st == AMG_OK ? 1 : 0, &all))) return e;
+        if (!all) {
+            if (h->solve_exec) cudaGraphExecDestroy(h->solve_exec);
+            h->solve_exec = nullptr;
+            cudaGetLastError();
+            h->graph_mode = GM_ITER;
+            return AMG_OK;
+        }
+    }
     if (st) return st;
     h->solve_b = b;
     h->solve_x = x;
+    return AMG_OK;
+}
+// GM_ITER: the iteration body as a plain graph (captured collectives, no conditional node)
+int ensure_iter_graph(amg_hier_s* h, double* x) {
+    if (h->iter_exec && h->iter_x == x) return AMG_OK;
+    if (h->iter_exec) {
+        cudaGraphExecDestroy(h->iter_exec);
+        h->iter_exec = nullptr;
+    }
+    cudaStream_t s = h->ctx->stream;
+    Launch L{h, s};
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    enqueue_pcg_body(h, L, x, 0);
+    const cudaError_t ec = cudaStreamEndCapture(s, &g);
+    cudaError_t ei = cudaErrorUnknown;
+    if (ec == cudaSuccess) ei = cudaGraphInstantiate(&h->iter_exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    int all = 0, e;
+    if ((e = agree_ok(h, (ec == cudaSuccess && ei == cudaSuccess) ? 1 : 0, &all))) return e;
+    if (!all) {
+        if (h->iter_exec && ei == cudaSuccess) cudaGraphExecDestroy(h->iter_exec);
+        h->iter_exec = nullptr;
+        cudaGetLastError();
+        h->graph_mode = 2;  // eager
+        return AMG_OK;
+    }
+    h->iter_x = x;
     return AMG_OK;
 }
 // the whole solve as one graph: prologue, WHILE node over the PCG body, final x update
@@ -2434,6 +2590,44 @@ int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const do
     return AMG_OK;
 }
 
+// INVK factors of every non-coarsest level (smoother == 1) and of the
+// coarsest (coarse CG preconditioned by them, coarse_prec == 1), in the parallel
+// block-Jacobi setting: the blocks are the ranks' rows (rank_bounds, level 0; R18 above), or
+// cfg.invk_blocks equal level-0 blocks; HINVK factors A_pp, l1-INVK A_pp + D_l1,p.  Host,
+// levels in parallel (each factorisation is a sequential row recurrence).
+int invk_build(const amg_config_t& cfg, amgsetup::Hierarchy& H, const std::vector<int64_t>& rank_bounds) {
+    const int nlv = (int)H.lv.size();
+    const bool smooth = cfg.smoother == 1, coarse = cfg.coarse_solver == 1 && cfg.coarse_prec == 1;
+    if (!smooth && !coarse) return AMG_OK;
+    std::vector<int64_t> b0 = rank_bounds;
+    const int64_t n0 = H.lv[0].A.nrows;
+    if (cfg.invk_blocks > 0) {
+        b0.assign(cfg.invk_blocks + 1, 0);
+        for (int g = 0; g <= cfg.invk_blocks; ++g) b0[g] = n0 * g / cfg.invk_blocks;
+    }
+    const bool blocks = b0.size() > 2;
+    const std::vector<std::vector<int32_t>> own =
+        blocks ? amgsetup::level_blocks(H, b0) : std::vector<std::vector<int32_t>>(nlv);
+    int bad = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : bad)
+    for (int l = 0; l < nlv; ++l) {
+        if (l == nlv - 1 ? !coarse : !smooth) continue;
+        const amgsetup::Csr& Al = H.lv[l].A;
+        // "a single level of fill-in in the inversion" on every level, unless the
+        // non-paper invk_dense_cut knob drops the fill of dense levels
+        const int f = (cfg.invk_dense_cut > 0 && (double)Al.nnz() > (double)cfg.invk_dense_cut * (double)Al.nrows)
+                          ? 0 : cfg.invk_fill;
+        const amgsetup::Csr B = amgsetup::block_diagonal_part(Al, own[l], cfg.invk_l1 == 1);
+        if (!amgsetup::invk_factors(B, f, H.lv[l].Wd, H.lv[l].Z)) bad = 1;
+    }
+    if (bad) {
+        set_err("amg_hierarchy_build: INVK: non-positive IC(0) pivot");
+        return AMG_ERR_NOT_SPD;
+    }
+    amgsetup::tmark("INVK factors");
+    return AMG_OK;
+}
+
 // ---------------------------------------------------- plan (de)serialisation
 struct Blob {
     std::vector<char> b;
@@ -2503,6 +2697,8 @@ void serialize(const amgsetup::RankPlan& P, const std::vector<double>& cinv, con
         B.put_csr(L.P);
         B.put_csr(L.R);
         B.putv(L.m);
+        B.put_csr(L.Wd);
+        B.put_csr(L.Z);
     }
     B.putv(cinv);
     for (int l = 0; l + 1 < nl; ++l) B.putv(agg_own[l]);
@@ -2532,6 +2728,8 @@ void deserialize(Blob& B, amgsetup::RankPlan& P, std::vector<double>& cinv, std:
         B.get_csr(L.P);
         B.get_csr(L.R);
         B.getv(L.m);
+        B.get_csr(L.Wd);
+        B.get_csr(L.Z);
     }
     B.getv(cinv);
     agg.assign(nl > 0 ? nl - 1 : 0, {});
@@ -2610,6 +2808,10 @@ void amg_config_default(amg_config_t* c) {
     c->tail_bytes = 0;
     c->smoother = 0;
     c->invk_fill = 1;
+    c->invk_l1 = 0;
+    c->invk_blocks = 0;
+    c->invk_dense_cut = 0;
+    c->coarse_prec = 0;
 }
 
 int amg_nccl_unique_id(void* out128) {
@@ -2694,9 +2896,17 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         set_err("amg_hierarchy_build: smoother must be 0 (l1-Jacobi) or 1 (INVK), invk_fill >= 0");
         return AMG_ERR_ARG;
     }
-    if (cfg.smoother == 1 && (ctx->nranks > 1 || cfg.emulate_ranks > 1)) {
-        set_err("amg_hierarchy_build: the INVK smoother is implemented for single-rank contexts only");
+    if ((cfg.invk_l1 != 0 && cfg.invk_l1 != 1) || cfg.invk_blocks < 0 || cfg.invk_dense_cut < 0 ||
+        (cfg.coarse_prec != 0 && cfg.coarse_prec != 1)) {
+        set_err("amg_hierarchy_build: invk_l1 / coarse_prec must be 0 or 1, invk_blocks / invk_dense_cut >= 0");
         return AMG_ERR_ARG;
+    }
+    {
+        const int npart = ctx->nranks > 1 ? ctx->nranks : std::max(1, cfg.emulate_ranks);
+        if (npart > 1 && cfg.invk_blocks != 0 && cfg.invk_blocks != npart) {
+            set_err("amg_hierarchy_build: with several ranks the INVK blocks are the ranks' (invk_blocks 0 or np)");
+            return AMG_ERR_ARG;
+        }
     }
     if (cfg.cycle == 1 && (ctx->nranks > 1 || cfg.emulate_ranks > 1)) {
         set_err("amg_hierarchy_build: the K-cycle is implemented for single-rank contexts only");
@@ -2722,32 +2932,19 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         delete h;
         return code;
     };
-    if (h->multi()) h->cfg.use_graphs = 0;  // multi-rank solves run eagerly (host loop)
     int st = AMG_OK;
     if (nr == 1) {
         amgsetup::Hierarchy H;
         // one process, l1-Jacobi: a GPU-built hierarchy stays on the device (formats converted there)
-        H.keep_device = (np == 1 && cfg.smoother == 0);
+        H.keep_device = (np == 1 && cfg.smoother == 0 && !(cfg.coarse_solver == 1 && cfg.coarse_prec == 1));
         if ((st = host_setup(n_global, rowptr, colind, values, w, cfg, H))) {
             set_err("amg_hierarchy_build: " + g_err);
             return fail(st);
         }
-        if (cfg.smoother == 1) {  // INVK factors of every non-coarsest level (host; levels in parallel,
-                                  // each factorisation is a sequential row recurrence)
-            const int nlf = (int)H.lv.size() - 1;
-            int bad = 0;
-#pragma omp parallel for schedule(dynamic, 1) reduction(max : bad)
-            for (int l = 0; l < nlf; ++l) {
-                // reading I4: positional fill only on stencil-like levels (<= 27 entries/row)
-                const amgsetup::Csr& Al = H.lv[l].A;
-                const int f = ((double)Al.nnz() <= 27.0 * (double)Al.nrows) ? cfg.invk_fill : 0;
-                if (!amgsetup::invk_factors(Al, f, H.lv[l].Wd, H.lv[l].Z)) bad = 1;
-            }
-            if (bad) {
-                set_err("amg_hierarchy_build: INVK: non-positive IC(0) pivot");
-                return fail(AMG_ERR_NOT_SPD);
-            }
-            amgsetup::tmark("INVK factors");
+        {
+            std::vector<int64_t> b0(np + 1);
+            for (int g = 0; g <= np; ++g) b0[g] = n_global * g / np;
+            if ((st = invk_build(cfg, H, b0))) return fail(st);
         }
         amgsetup::tmark("(hierarchy built)");
         std::vector<int64_t> bounds(np + 1);
@@ -2886,6 +3083,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
                 set_err("amg_hierarchy_build: " + g_err);
                 return fail(st);
             }
+            if ((st = invk_build(cfg, H, bounds))) return fail(st);
             std::vector<amgsetup::RankPlan> plans;
             std::string err;
             if (!amgsetup::partition(H, bounds, cfg.replicate_below_bytes, plans, err)) {
@@ -2938,6 +3136,8 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         for (size_t l = 0; l < P.lv.size(); ++l)
             h->lvl_fmt.push_back(l + 1 < P.lv.size() ? h->ranks[0].lv[l].A.fmt : FMT_DENSE);
     }
+    if (const char* gm = std::getenv("AMG_MULTI_GRAPH"))
+        if (h->multi() && std::strcmp(gm, "iter") == 0) h->graph_mode = GM_ITER;
     if (cudaMallocHost((void**)&h->st_host, sizeof(PcgState)) != cudaSuccess) {
         set_err("cudaMallocHost failed");
         return fail(AMG_ERR_OOM);
@@ -2977,14 +3177,24 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
     *h->st_host = init;
     for (auto& R : h->ranks) CK(cudaMemcpyAsync(R.st, h->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord(h->ev0, s));
-    if (h->cfg.use_graphs && !h->multi()) {
+    if (h->cfg.use_graphs && h->graph_mode == GM_WHILE) {
         int e = ensure_solve_graph(h, b_dev, x_dev);
         if (e) return e;
+        if ((e = take_nccl_status(h))) return e;
+    }
+    if (h->cfg.use_graphs && h->graph_mode == GM_ITER) {
+        int e = ensure_iter_graph(h, x_dev);
+        if (e) return e;
+        if ((e = take_nccl_status(h))) return e;
+    }
+    if (h->cfg.use_graphs && h->graph_mode == GM_WHILE) {
         CK(cudaGraphLaunch(h->solve_exec, s));
         CK(cudaEventRecord(h->ev1, s));
         CK(cudaMemcpyAsync(h->st_host, h->ranks[0].st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     } else {
+        // one graph per iteration (GM_ITER) or eager launches, one status read per iteration
+        const bool it_graph = h->cfg.use_graphs && h->graph_mode == GM_ITER;
         Launch L{h, s};
         int e;
         enqueue_pcg_init(h, L, b_dev, x_dev, 0);
@@ -2993,8 +3203,12 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
             CK(cudaMemcpyAsync(h->st_host, h->ranks[0].st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             if (h->st_host->status != ST_RUNNING) break;
-            enqueue_pcg_body(h, L, x_dev, 0);
-            if ((e = take_nccl_status(h))) return e;
+            if (it_graph) {
+                CK(cudaGraphLaunch(h->iter_exec, s));
+            } else {
+                enqueue_pcg_body(h, L, x_dev, 0);
+                if ((e = take_nccl_status(h))) return e;
+            }
         }
         enqueue_pcg_final(h, L, x_dev);
         CK(cudaEventRecord(h->ev1, s));
@@ -3158,7 +3372,7 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
     CK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
     h->nccl_status = ncclSuccess;
-    if (h->cfg.use_graphs && !h->multi()) {
+    if (h->cfg.use_graphs && (!h->multi() || h->loopback)) {
         int e = ensure_apply_graph(h, r_dev, z_dev);
         if (e) return e;
         CK(cudaGraphLaunch(h->apply_exec, s));
@@ -3231,6 +3445,55 @@ int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out
     h->prof = nullptr;
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
+    const int per = (int)(recs.size() / napply);
+    *count = per;
+    for (int k = 0; k < per && k < cap; ++k) {
+        double tot = 0.0;
+        for (int a = 0; a < napply; ++a) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, recs[a * per + k].e0, recs[a * per + k].e1);
+            tot += ms;
+        }
+        if (ms_out) ms_out[k] = tot / napply;
+        if (bytes_out) bytes_out[k] = recs[k].bytes;
+        if (stored_bytes_out) stored_bytes_out[k] = recs[k].stored_bytes;
+        if (names_out) names_out[k] = recs[k].name;
+    }
+    for (auto& r : recs) {
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+    }
+    return AMG_OK;
+}
+
+int amg_profile_iteration(amg_hier_t h, const double* b_dev, double* x_dev, int32_t napply, int32_t cap,
+                          double* ms_out, double* bytes_out, double* stored_bytes_out, const char** names_out,
+                          int32_t* count) {
+    if (!h || !b_dev || !x_dev || napply < 1 || !count) {
+        set_err("amg_profile_iteration: bad argument");
+        return AMG_ERR_ARG;
+    }
+    std::lock_guard<std::recursive_mutex> guard(h->mu);
+    CK(cudaSetDevice(h->ctx->device));
+    cudaStream_t s = h->ctx->stream;
+    h->nccl_status = ncclSuccess;
+    PcgState init{};
+    init.rtol = 0.0;  // fixed-count: every profiled body runs the whole iteration
+    init.maxit = napply + 2;
+    *h->st_host = init;
+    for (auto& R : h->ranks) CK(cudaMemcpyAsync(R.st, h->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+    std::vector<KernelRec> recs;
+    Launch L{h, s};
+    enqueue_pcg_init(h, L, b_dev, x_dev, 0);
+    enqueue_pcg_body(h, L, x_dev, 0);  // warm-up iteration
+    CK(cudaStreamSynchronize(s));
+    h->prof = &recs;
+    for (int a = 0; a < napply; ++a) enqueue_pcg_body(h, L, x_dev, 0);
+    h->prof = nullptr;
+    enqueue_pcg_final(h, L, x_dev);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    if (int e = take_nccl_status(h)) return e;
     const int per = (int)(recs.size() / napply);
     *count = per;
     for (int k = 0; k < per && k < cap; ++k) {

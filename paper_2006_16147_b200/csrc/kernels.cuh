@@ -1006,6 +1006,27 @@ __global__ void __launch_bounds__(kBlock) k_unpack(double* __restrict__ v, const
         v[idx[k]] = buf[k];
 }
 
+// Halo unpack of z for the fused direction update (several ranks): z[idx] = buf and, at the
+// same halo positions, p_new = z + beta p_old (p_new = z on the first iteration), with the p
+// double buffer selected by the iteration parity exactly as GPz / ESpmvDotPz do.
+__global__ void __launch_bounds__(kBlock) k_unpack_pz(double* __restrict__ z, double* p0, double* p1,
+                                                      const int32_t* __restrict__ idx,
+                                                      const double* __restrict__ buf, int64_t n,
+                                                      const PcgState* __restrict__ st) {
+    pdl_begin();
+    const int32_t it = st->iter;
+    const bool first = (it == 0);
+    const double beta = st->beta;
+    const double* pold = (it & 1) ? p1 : p0;
+    double* pnew = (it & 1) ? p0 : p1;
+    for (int64_t k = (int64_t)blockIdx.x * kBlock + threadIdx.x; k < n; k += (int64_t)gridDim.x * kBlock) {
+        const int32_t j = idx[k];
+        const double zj = buf[k];
+        z[j] = zj;
+        pnew[j] = first ? zj : zj + beta * pold[j];
+    }
+}
+
 // The level just above a direct coarsest solve, collapsed: the whole rest of the cycle from
 // that level is a fixed linear map, out = B b with B dense (formed at setup), one 256-thread
 // block per row; G gathers b (GVec, or GBaq for the K-cycle's b - alpha q, whose values are then
@@ -1228,6 +1249,14 @@ struct CoarseCG {
     int32_t smem_a;                    // 1: the CTA's rows of A_L are staged in shared memory
     int32_t maxit;
     double rtol;
+    // VA3S3CS1: the preconditioner is z = Z (Wd r), the (H)INVK factors of A_L
+    // (CSR, int32 row pointers); nullptr: the l1-Jacobi diagonal m
+    const int32_t* __restrict__ wrp;
+    const int32_t* __restrict__ wci;
+    const double* __restrict__ wv;
+    const int32_t* __restrict__ zrp;
+    const int32_t* __restrict__ zci;
+    const double* __restrict__ zv;
 };
 
 constexpr int kCgBlock = 512;
@@ -1280,6 +1309,31 @@ __device__ __forceinline__ void cg_allreduce(double (&v)[NV], double* wsum /*[NV
     }
 }
 
+// every CTA copies the peers' slices [split[c], split[c+1]) of the full-length shared vector
+// `full` into its own copy (after a cluster barrier that published them)
+__device__ __forceinline__ void cg_gather(double* full, const int32_t* split, int ncta, uint32_t me) {
+    for (int c = 0; c < ncta; ++c) {
+        if (c == (int)me) continue;
+        const int32_t c0 = split[c], c1 = split[c + 1];
+        const double* src = peer_smem(full, (uint32_t)c);
+        for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) full[i] = src[i];
+    }
+}
+
+// y_i = sum_k M_ik v_k on the own rows [r0, r0 + nown) (warp per row, ascending k per lane)
+__device__ __forceinline__ void cg_rows(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                        const double* __restrict__ v, const double* vfull, int32_t r0,
+                                        int32_t nown, double* y) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int i = wid; i < nown; i += nwarp) {
+        const int32_t a0 = rp[r0 + i], a1 = rp[r0 + i + 1];
+        double s = 0.0;
+        for (int k = a0 + lane; k < a1; k += 32) s += __ldg(v + k) * vfull[__ldg(ci + k)];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) y[i] = s;
+    }
+}
+
 __global__ void __launch_bounds__(kCgBlock, 1) k_coarse_cg(CoarseCG A, const double* __restrict__ b,
                                                            double* __restrict__ x) {
     pdl_begin();
@@ -1290,9 +1344,13 @@ __global__ void __launch_bounds__(kCgBlock, 1) k_coarse_cg(CoarseCG A, const dou
     const uint32_t me = ncta > 1 ? cluster_rank() : 0u;
     const int32_t r0 = A.split[me], r1 = A.split[me + 1], nown = r1 - r0;
     const int n = A.n;
-    // shared layout: pfull[n] | r[nown] | x[nown] | q[nown] | m[nown] | (vals | cols)
+    const bool invk = A.wrp != nullptr;
+    // shared layout: pfull[n] | (INVK: vfull[n] | tfull[n]) | r[nown] | x[nown] | q[nown] |
+    // m[nown] (l1-Jacobi) or z[nown] (INVK) | (vals | cols)
     double* pfull = (double*)cg_smem;
-    double* rs = pfull + n;
+    double* vfull = pfull + n;  // INVK: r of all rows, then t = Wd r of all rows in tfull
+    double* tfull = vfull + n;
+    double* rs = invk ? tfull + n : pfull + n;
     double* xs = rs + nown;
     double* qs = xs + nown;
     double* ms = qs + nown;
@@ -1308,17 +1366,46 @@ __global__ void __launch_bounds__(kCgBlock, 1) k_coarse_cg(CoarseCG A, const dou
     const double* vals = A.smem_a ? av : A.v + k0;
     const int32_t* cols = A.smem_a ? ac : A.ci + k0;
     double* ps = pfull + r0;
-    // x = 0, r = b, z = m r, p = z; ||b||^2 and rho = r^T z
+    // INVK: z = Z (Wd r) into ms; Wd and Z couple rows of other CTAs, so r and t = Wd r are
+    // published through distributed shared memory (two cluster barriers)
+    auto precond = [&]() {
+        for (int i = threadIdx.x; i < nown; i += blockDim.x) vfull[r0 + i] = rs[i];
+        cg_sync(ncta);
+        if (ncta > 1) cg_gather(vfull, A.split, ncta, me);
+        __syncthreads();
+        cg_rows(A.wrp, A.wci, A.wv, vfull, r0, nown, tfull + r0);
+        cg_sync(ncta);
+        if (ncta > 1) cg_gather(tfull, A.split, ncta, me);
+        __syncthreads();
+        cg_rows(A.zrp, A.zci, A.zv, tfull, r0, nown, ms);
+        __syncthreads();
+    };
+    // x = 0, r = b, z = M^{-1} r, p = z; ||b||^2 and rho = r^T z
     double red[2] = {0.0, 0.0};
-    for (int i = threadIdx.x; i < nown; i += blockDim.x) {
-        const double bi = b[r0 + i], mi = A.m[r0 + i];
-        rs[i] = bi;
-        xs[i] = 0.0;
-        ms[i] = mi;
-        const double zi = mi * bi;
-        ps[i] = zi;
-        red[0] += bi * bi;
-        red[1] += bi * zi;
+    if (invk) {
+        for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+            rs[i] = b[r0 + i];
+            xs[i] = 0.0;
+        }
+        __syncthreads();
+        precond();
+        for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+            const double bi = rs[i], zi = ms[i];
+            ps[i] = zi;
+            red[0] += bi * bi;
+            red[1] += bi * zi;
+        }
+    } else {
+        for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+            const double bi = b[r0 + i], mi = A.m[r0 + i];
+            rs[i] = bi;
+            xs[i] = 0.0;
+            ms[i] = mi;
+            const double zi = mi * bi;
+            ps[i] = zi;
+            red[0] += bi * bi;
+            red[1] += bi * zi;
+        }
     }
     cg_allreduce<2>(red, wsum, slots[1], ncta);
     const double bnorm = sqrt(red[0]);
@@ -1329,12 +1416,7 @@ __global__ void __launch_bounds__(kCgBlock, 1) k_coarse_cg(CoarseCG A, const dou
             // (A) publish / gather p
             cg_sync(ncta);
             if (ncta > 1) {
-                for (int c = 0; c < ncta; ++c) {
-                    if (c == (int)me) continue;
-                    const int32_t c0 = A.split[c], c1 = A.split[c + 1];
-                    const double* src = peer_smem(pfull, (uint32_t)c);
-                    for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) pfull[i] = src[i];
-                }
+                cg_gather(pfull, A.split, ncta, me);
                 __syncthreads();
             }
             // q = A p on the own rows (warp per row), p^T q
@@ -1353,17 +1435,34 @@ __global__ void __launch_bounds__(kCgBlock, 1) k_coarse_cg(CoarseCG A, const dou
             if (!(pq[0] > 0.0)) break;
             const double alpha = rho / pq[0];
             double rr[2] = {0.0, 0.0};
-            for (int i = threadIdx.x; i < nown; i += blockDim.x) {
-                xs[i] = xs[i] + alpha * ps[i];
-                const double ri = rs[i] - alpha * qs[i];
-                rs[i] = ri;
-                rr[0] += ri * ri;
-                rr[1] += ri * (ms[i] * ri);
+            if (invk) {  // z = M^{-1} r is formed before the stop test (discarded on the last step)
+                for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+                    xs[i] = xs[i] + alpha * ps[i];
+                    rs[i] = rs[i] - alpha * qs[i];
+                }
+                __syncthreads();
+                precond();
+                for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+                    const double ri = rs[i];
+                    rr[0] += ri * ri;
+                    rr[1] += ri * ms[i];
+                }
+            } else {
+                for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+                    xs[i] = xs[i] + alpha * ps[i];
+                    const double ri = rs[i] - alpha * qs[i];
+                    rs[i] = ri;
+                    rr[0] += ri * ri;
+                    rr[1] += ri * (ms[i] * ri);
+                }
             }
             cg_allreduce<2>(rr, wsum, slots[1], ncta);  // (C)
             if (sqrt(rr[0]) / bnorm < A.rtol) break;
             const double beta = rr[1] / rho;
-            for (int i = threadIdx.x; i < nown; i += blockDim.x) ps[i] = ms[i] * rs[i] + beta * ps[i];
+            if (invk)
+                for (int i = threadIdx.x; i < nown; i += blockDim.x) ps[i] = ms[i] + beta * ps[i];
+            else
+                for (int i = threadIdx.x; i < nown; i += blockDim.x) ps[i] = ms[i] * rs[i] + beta * ps[i];
             rho = rr[1];
         }
     }

@@ -177,6 +177,12 @@ bool partition(const Hierarchy& H, const std::vector<int64_t>& rb0, int64_t rep_
             L.recv_ids = ids;  // ascending ids are already grouped by owner (contiguous blocks)
             // local operators in window frames
             L.A = slice_rows(H.lv[l].A, L.comp_begin, L.comp_end, L.win_begin, L.win_end - L.win_begin);
+            // INVK factors are block-diagonal over the owners (HINVK / l1-INVK): their columns stay
+            // inside the rows this rank computes, so they need no halo
+            if (!H.lv[l].Wd.rp.empty()) {
+                L.Wd = slice_rows(H.lv[l].Wd, L.comp_begin, L.comp_end, L.win_begin, L.win_end - L.win_begin);
+                L.Z = slice_rows(H.lv[l].Z, L.comp_begin, L.comp_end, L.win_begin, L.win_end - L.win_begin);
+            }
             L.m.assign(H.lv[l].m.begin() + L.win_begin, H.lv[l].m.begin() + L.win_end);
         }
         for (int l = 0; l + 1 < nl; ++l) {

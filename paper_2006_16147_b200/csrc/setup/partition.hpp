@@ -37,7 +37,7 @@ struct RankLevel {
     Csr P;  // rows [comp_begin, comp_end), columns in the level-(l+1) window frame
     Csr R;  // rows [rst_begin, rst_end) of level l+1, columns in the level-l window frame
     std::vector<double> m;  // l1-Jacobi inverse diagonal over the whole window
-    Csr Wd, Z;              // INVK factors (single rank only)
+    Csr Wd, Z;              // INVK factors (rows [comp_begin, comp_end), block-diagonal: no halo)
 };
 
 struct RankPlan {

@@ -534,6 +534,55 @@ bool dense_inverse_host(const Csr& A, std::vector<double>& inv) { return dense_i
 // L), then the truncated inverse by the row recurrence w_i = e_i - sum_k l_ik w_k with
 // a dense accumulator and per-column fill levels; summation orders as the readings
 // I1-I3 state (k ascending; within a row of W, ascending columns).
+Csr block_diagonal_part(const Csr& A, const std::vector<int32_t>& owner, bool l1) {
+    if (owner.empty()) return A;
+    const int64_t n = A.nrows;
+    std::vector<int64_t> cnt(n + 1, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t c = 0;
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) c += (owner[A.ci[k]] == owner[i]);
+        cnt[i + 1] = c;
+    }
+    Csr B;
+    B.nrows = B.ncols = n;
+    B.rp.assign(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) B.rp[i + 1] = B.rp[i] + cnt[i + 1];
+    B.ci.resize(B.rp[n]);
+    B.v.resize(B.rp[n]);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double dl1 = 0.0;  // sum of |a_ij| outside the block, ascending j
+        if (l1)
+            for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
+                if (owner[A.ci[k]] != owner[i]) dl1 = dl1 + std::fabs(A.v[k]);
+        int64_t o = B.rp[i];
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const int32_t j = A.ci[k];
+            if (owner[j] != owner[i]) continue;
+            B.ci[o] = j;
+            B.v[o] = (l1 && j == i) ? A.v[k] + dl1 : A.v[k];
+            ++o;
+        }
+    }
+    return B;
+}
+
+std::vector<std::vector<int32_t>> level_blocks(const Hierarchy& H, const std::vector<int64_t>& bounds0) {
+    const size_t nl = H.lv.size();
+    std::vector<std::vector<int32_t>> own(nl);
+    own[0].resize(H.lv[0].A.nrows);
+    for (size_t p = 0; p + 1 < bounds0.size(); ++p)
+        for (int64_t i = bounds0[p]; i < bounds0[p + 1]; ++i) own[0][i] = (int32_t)p;
+    for (size_t l = 0; l + 1 < nl; ++l) {
+        own[l + 1].assign(H.lv[l + 1].A.nrows, -1);
+        const auto& agg = H.lv[l].agg;
+        for (int64_t i = 0; i < (int64_t)agg.size(); ++i)  // ascending: the first member is the minimum
+            if (own[l + 1][agg[i]] < 0) own[l + 1][agg[i]] = own[l][i];
+    }
+    return own;
+}
+
 bool invk_factors(const Csr& A, int fill, Csr& Wd, Csr& Z) {
     const int64_t n = A.nrows;
     Csr L;

@@ -81,6 +81,13 @@ bool dense_inverse_host(const Csr& A, std::vector<double>& inv);
 // truncated to `fill` levels of positional fill, Wd = D^{-1} W, Z = W^T.  false on a
 // non-positive pivot.
 bool invk_factors(const Csr& A, int fill, Csr& Wd, Csr& Z);
+// The paper's parallel block-Jacobi setting: the matrix whose INVK factors a
+// rank uses is its diagonal block A_pp (HINVK) or A_pp + D_l1,p (l1 = true, l1-INVK, Eq. 3.5
+// weights of the couplings outside the block).  owner[i] = block of row i (empty: one block).
+Csr block_diagonal_part(const Csr& A, const std::vector<int32_t>& owner, bool l1);
+// Block of every row of every level: level-0 rows by `bounds0` (nb+1 ascending boundaries), a
+// coarse row by the block of its aggregate's minimum member (R18, as the rank partition).
+std::vector<std::vector<int32_t>> level_blocks(const Hierarchy& H, const std::vector<int64_t>& bounds0);
 void tmark(const char* what);
 
 // Building blocks (exported for the setup self-tests).

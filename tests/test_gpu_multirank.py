@@ -124,3 +124,50 @@ def test_loopback_profile_vcycle_and_report(ctx):
     assert {"resid0", "restrict", "prolong", "postsweep"} <= names
     rep = h.report()
     assert rep["vcycle_bytes_model"] > 0 and rep["nlevels"] == h.nlevels
+
+
+@pytest.mark.parametrize("np_", [2, 4])
+def test_loopback_graph_equals_eager_and_oracle(ctx, np_):
+    """The multi-rank PCG is ONE graph per solve (a device-side WHILE node over the iteration,
+    halo copies / exchanges and the rank-ordered dot finishers inside it): bitwise the same x
+    and iteration count as the eager host loop, and the oracle's iterations +-1."""
+    import paper_2006_16147_b200 as amg
+    A, b, _ = config_problem(4, grid=(48, 48, 96))
+    bt = torch.tensor(b, device="cuda:0")
+    hg = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=np_))
+    he = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=np_, use_graphs=0))
+    xg, rg = hg.solve(bt)
+    xe, re_ = he.solve(bt)
+    assert rg["iterations"] == re_["iterations"]
+    assert torch.equal(xg, xe)
+    _, info = O.OracleHierarchy(A).pcg(b)
+    assert abs(rg["iterations"] - info["iterations"]) <= 1
+    zg = hg.precond_apply(bt)
+    ze = he.precond_apply(bt)
+    assert torch.equal(zg, ze)
+
+
+def test_loopback_replicated_levels_run_the_single_rank_fused_forms(ctx):
+    """Replicated levels compute every row on every rank, so they use the same compact /
+    collapsed level forms as one rank (W5); level 0 uses the fused direction update with the
+    z-halo unpack forming p_new at the halo (no separate p-update kernel)."""
+    import paper_2006_16147_b200 as amg
+    A, b, _ = config_problem(4, grid=(96, 96, 96))  # levels ... -> 1.7k (compact) -> 220 (collapsed) -> 28
+    h = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=4))
+    names = [k["name"] for k in h.profile_vcycle(1)]
+    assert "collapsed" in names and "prolong_post_c" in names, names
+    it = [k["name"] for k in h.profile_iteration(torch.tensor(b, device="cuda:0"), 2)]
+    assert "spmv_dot_pupd" in it and "pupdate" not in it, it
+    ho = O.OracleHierarchy(A)
+    r = uniform_pm1(77, A.n_global)
+    z = h.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    zo = ho.vcycle(r)
+    assert np.linalg.norm(z - zo) <= 1e-12 * np.linalg.norm(zo)
+    bt = torch.tensor(b, device="cuda:0")
+    x, rep = h.solve(bt)
+    xo, info = ho.pcg(b)
+    assert abs(rep["iterations"] - info["iterations"]) <= 1
+    k = min(rep["iterations"], info["iterations"])
+    x, _ = h.solve(bt, rtol=0.0, maxit=k)
+    xo, _ = ho.pcg(b, rtol=0.0, maxit=k)
+    assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-8 * np.linalg.norm(xo)

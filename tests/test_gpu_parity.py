@@ -7,6 +7,8 @@ Bars (BASELINE.json north_star):
   * x within 1e-8 relative, compared at EQUAL iteration counts (fixed-count mode,
     rtol = 0, maxit = min of the two natural counts; SURVEY.md §4 protocol).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -99,12 +101,16 @@ def _case(name):
     if name == "n1":
         A = diagonal_spd(1)
         return A, np.array([3.0]), {}, {}
+    if name == "va4_48":  # VA4: 4 matching sweeps per level (aggregates <= 16), smoothed P
+        A = poisson7(48, 48, 48)
+        kw = dict(sweeps_per_level=4)
+        return A, uniform01(28, A.n_global), kw, kw
     raise KeyError(name)
 
 
 CASES = ["c1", "c2", "c3_64", "c4_64x64x128", "c5_32", "ragged_17x13x11", "unsmoothed_24",
          "omega_text_32", "single_level", "irregular_hubs", "irregular_narrow", "line_1d_100k",
-         "plane_2d_300", "diagonal", "n1", "c5_72", "irregular_400k"]
+         "plane_2d_300", "diagonal", "n1", "c5_72", "irregular_400k", "va4_48"]
 _cache = {}
 
 
@@ -273,11 +279,36 @@ def test_full_c3_anisotropic_properties(ctx):
     assert (torch.linalg.norm(res) / torch.linalg.norm(bt)).item() <= 1.5e-6
 
 
-def test_full_c4_hierarchy_and_vcycle_vs_oracle(ctx):
-    """BASELINE config 4 at full size (256^3) exactly as bench.py builds it (GPU setup,
-    default config): every level's aggregate map equals the oracle's bit for bit and one
-    V-cycle on a seeded vector agrees with the oracle's to 1e-12 (the oracle runs the
-    full-size V-cycle once, single-threaded)."""
+def _full_size_parity(h, ho, A, b, seed, threads=1):
+    """V-cycle <= 1e-12; PCG iterations +-1; x <= 1e-8 at equal counts.  threads > 1 runs the
+    oracle's solve with its OpenMP row loops (only the dot summation order differs)."""
+    r = uniform_pm1(seed, A.n_global)
+    z = h.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    zo = ho.vcycle(r)
+    rel = np.linalg.norm(z - zo) / np.linalg.norm(zo)
+    assert rel <= VCYCLE_TOL, rel
+    bt = torch.tensor(b, device="cuda:0")
+    x, rep = h.solve(bt, rtol=1e-6)
+    O.OracleHierarchy.set_threads(threads)
+    try:
+        xo, info = ho.pcg(b, rtol=1e-6)
+        assert rep["converged"] == 1 and info["status"] == O.OR_OK
+        assert abs(rep["iterations"] - info["iterations"]) <= 1, (rep["iterations"], info["iterations"])
+        k = min(rep["iterations"], info["iterations"])
+        x, _ = h.solve(bt, rtol=0.0, maxit=k)
+        if k != info["iterations"]:
+            xo, _ = ho.pcg(b, rtol=0.0, maxit=k)
+    finally:
+        O.OracleHierarchy.set_threads(1)
+    relx = np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo)
+    assert relx <= X_TOL, relx
+
+
+def test_full_c4_hierarchy_vcycle_and_pcg_vs_oracle(ctx):
+    """BASELINE config 4 at full size (256^3) exactly as bench.py builds and solves it (GPU
+    setup, default config): every level's aggregate map equals the oracle's bit for bit, one
+    V-cycle agrees to 1e-12, the PCG iteration counts agree +-1 and x agrees to 1e-8 at equal
+    iteration counts (the oracle runs single-threaded: the sequential parity reference)."""
     amg = _amg()
     A, b, meta = config_problem(4)
     h = amg.Hierarchy(ctx, A)
@@ -285,11 +316,54 @@ def test_full_c4_hierarchy_and_vcycle_vs_oracle(ctx):
     assert h.sizes() == ho.sizes()
     for l in range(h.nlevels - 1):
         assert np.array_equal(h.level_aggregates(l), ho.agg(l)), f"level {l}"
-    r = uniform_pm1(1004, A.n_global)
-    z = h.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
-    zo = ho.vcycle(r)
-    rel = np.linalg.norm(z - zo) / np.linalg.norm(zo)
-    assert rel <= VCYCLE_TOL, rel
+    _full_size_parity(h, ho, A, b, 1004)
+
+
+def test_full_c3_hierarchy_vcycle_and_pcg_vs_oracle(ctx):
+    """BASELINE config 3 at full size (256^3 anisotropic, 2/2 sweeps) as bench.py --config 3
+    runs it: aggregates bit-exact, V-cycle <= 1e-12, iterations +-1, x <= 1e-8 at equal counts.
+    The oracle's solve uses its OpenMP row loops here to bound the test's time."""
+    amg = _amg()
+    A, b, meta = config_problem(3)
+    kw = dict(pre_sweeps=2, post_sweeps=2)
+    h = amg.Hierarchy(ctx, A, cfg=amg.make_config(**kw))
+    ho = O.OracleHierarchy(A, **kw)
+    assert h.sizes() == ho.sizes()
+    for l in range(h.nlevels - 1):
+        assert np.array_equal(h.level_aggregates(l), ho.agg(l)), f"level {l}"
+    _full_size_parity(h, ho, A, b, 1003, threads=os.cpu_count() or 1)
+
+
+def test_breakdown_on_an_indefinite_matrix(ctx):
+    """O11 / SPEC.md:468: p^T A p <= 0 stops PCG with AMG_ERR_BREAKDOWN (x = the last
+    iterate).  tridiag(1.5, 2, 1.5) has a positive diagonal (the build accepts it; its
+    Galerkin coarse operators are s.p.d.) but eigenvalues 2 + 3 cos(k pi/(n+1)) of both signs;
+    the oracle breaks down at the same iteration."""
+    import ctypes as C
+    import scipy.sparse as sp
+    from inputs.problems import CSR
+    amg = _amg()
+    n = 1000
+    M = sp.diags([1.5 * np.ones(n - 1), 2.0 * np.ones(n), 1.5 * np.ones(n - 1)], [-1, 0, 1]).tocsr()
+    A = CSR(n_global=n, row_begin=0, row_end=n, rowptr=M.indptr.astype(np.int64),
+            colind=M.indices.astype(np.int64), values=M.data.astype(np.float64))
+    b = np.ones(n)
+    ho = O.OracleHierarchy(A, max_coarse_size=10)
+    xo, info = ho.pcg(b, rtol=1e-8, maxit=100)
+    assert info["status"] == O.OR_BREAKDOWN
+    for graphs in (1, 0):
+        h = amg.Hierarchy(ctx, A, cfg=amg.make_config(max_coarse_size=10, use_graphs=graphs))
+        bt = torch.tensor(b, device="cuda:0")
+        x = torch.empty_like(bt)
+        rep = amg.amg_report_t()
+        code = amg.lib.amg_solve(h.h, C.c_void_p(bt.data_ptr()), C.c_void_p(x.data_ptr()), 1e-8, 100,
+                                 C.byref(rep))
+        assert code == amg.AMG_ERR_BREAKDOWN and rep.status == amg.AMG_ERR_BREAKDOWN
+        assert rep.iterations == info["iterations"] and rep.converged == 0
+        assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-10 * np.linalg.norm(xo)
+        with pytest.raises(amg.AmgError) as e:
+            h.solve(bt, rtol=1e-8, maxit=100)
+        assert e.value.code == amg.AMG_ERR_BREAKDOWN
 
 
 def test_compact_and_collapsed_levels_are_taken(ctx):
