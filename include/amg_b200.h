@@ -95,7 +95,8 @@ typedef struct {
                                      correction of every level whose coarse level is not the
                                      coarsest is two FCG(1) iterations preconditioned by the cycle
                                      rooted there.  Nonlinear:
-                                     use krylov = 1.  Single-rank contexts only (AMG_ERR_ARG). */
+                                     use krylov = 1.  Several ranks: the inner FCG exchanges p halos
+                                     and finishes its dots in rank order on every rank. */
     int32_t setup_device;         /* 1 = build the hierarchy on the context's GPU (default; SURVEY.md
                                      §8f NEXT-1: suitor matching, expand-sort-compress canonical
                                      SpGEMM), bit-identical to 0 = the host build (C++/OpenMP).
@@ -279,6 +280,18 @@ int amg_host_level_aggregates(amg_host_hier_t h, int32_t lvl, int64_t* agg_out);
  * int64 rowptr (n_l+1), int64 colind and fp64 values (nnz entries). */
 int amg_host_level_matrix(amg_host_hier_t h, int32_t lvl, int32_t which, int64_t* rowptr,
                           int64_t* colind, double* values);
+
+/* The DISTRIBUTED setup run by `nranks` ranks emulated as
+ * threads of this process (an in-process transport): rank g owns level-0 rows
+ * [n g/nranks, n (g+1)/nranks), builds only its rows of every level (cross-rank matching rounds,
+ * remote-row-gather Galerkin products, all-reduced omega) and its own plan (windows, halos,
+ * replicated levels all-gathered), with no rank ever holding the whole matrix of a distributed
+ * level.  The result is inspected with the amg_host_level_* calls (levels concatenated in rank
+ * order) and amg_host_plan_* (every rank's plan); it must equal amg_host_hierarchy_build +
+ * amg_host_partition bit for bit.  Host only (no device needed). */
+int amg_host_dist_build(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values,
+                        const double* w, const amg_config_t* cfg, int32_t nranks, int64_t replicate_below_bytes,
+                        amg_host_hier_t* out);
 
 /* Partition plan of the host hierarchy over `nranks` ranks with level-0 row blocks
  * row_bounds[0..nranks] (coarse rows owned by the rank of their

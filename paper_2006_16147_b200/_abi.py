@@ -78,6 +78,8 @@ _SIG = {
     "amg_host_level_aggregates": (C.c_int, [_vp, C.c_int32, _vp]),
     "amg_host_level_matrix": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp]),
     "amg_host_partition": (C.c_int, [_vp, C.c_int32, _vp, C.c_int64]),
+    "amg_host_dist_build": (C.c_int, [C.c_int64, _vp, _vp, _vp, _vp, C.POINTER(amg_config_t), C.c_int32,
+                                      C.c_int64, C.POINTER(_vp)]),
     "amg_host_plan_level": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
     "amg_host_plan_array": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp]),
 }

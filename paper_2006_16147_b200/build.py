@@ -23,12 +23,13 @@ def _nccl_dir():
     import nvidia.nccl
     return list(nvidia.nccl.__path__)[0]
 
-SOURCES_CXX = [os.path.join(CSRC, "setup", "setup.cpp"), os.path.join(CSRC, "setup", "partition.cpp")]
+SOURCES_CXX = [os.path.join(CSRC, "setup", "setup.cpp"), os.path.join(CSRC, "setup", "partition.cpp"),
+               os.path.join(CSRC, "setup", "dist_setup.cpp")]
 SOURCES_CU = [os.path.join(CSRC, "amg_api.cu")]
 # the GPU setup must follow the canonical arithmetic contract C1 (no FMA contraction)
 SOURCES_CU_NOFMA = [os.path.join(CSRC, "setup", "setup_gpu.cu")]
 HEADERS = [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "setup", "setup.hpp"),
-           os.path.join(CSRC, "setup", "partition.hpp"),
+           os.path.join(CSRC, "setup", "partition.hpp"), os.path.join(CSRC, "setup", "dist_setup.hpp"),
            os.path.join(ROOT, "include", "amg_b200.h")]
 
 

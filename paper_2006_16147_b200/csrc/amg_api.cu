@@ -39,6 +39,7 @@
 
 #include "../../include/amg_b200.h"
 #include "kernels.cuh"
+#include "setup/dist_setup.hpp"
 #include "setup/partition.hpp"
 #include "setup/setup.hpp"
 
@@ -507,6 +508,26 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0)
     }
 }
 
+// Several ranks, K-cycle: the same gather, finished into each rank's level-lvl K state.
+void dot_finish_k(amg_hier_s* h, Launch& L, int kind, int lvl) {
+    if (!h->multi()) return;
+    if (h->loopback) {
+        for (auto& Rd : h->ranks)
+            for (auto& Rs : h->ranks)
+                cudaMemcpyAsync(Rd.dot_all + kDotSlots * Rs.rank, Rs.dot_local, kDotSlots * sizeof(double),
+                                cudaMemcpyDeviceToDevice, L.s);
+    } else {
+        RankState& R = h->ranks[0];
+        nccl_note(h, ncclAllGather(R.dot_local, R.dot_all, kDotSlots, ncclDouble, h->ctx->nccl, L.s),
+                  "ncclAllGather (K-cycle dot totals)");
+    }
+    for (auto& R : h->ranks) {
+        RedCtx rc{nullptr, nullptr, nullptr, nullptr, 0ull, kind, R.lv[lvl].kst};
+        launch_k(k_finish, 1, 32, L.s, R.dot_all, kDotSlots * h->np, rc);
+        cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
+    }
+}
+
 using VecOf = std::function<double*(RankState&)>;
 // custom unpack of a received halo (rank, its exchange plan, stream); null: v[idx] = buf
 using UnpackFn = std::function<void(RankState&, const Exch&, cudaStream_t)>;
@@ -881,21 +902,33 @@ void launch_tail(amg_hier_s* h, Launch& L) {
 void enqueue_fcg2(amg_hier_s* h, Launch& L, int l);
 // K-cycle inner FCG without the vector-update kernel (one pre-sweep, l1-Jacobi): the
 // second application forms r = b - alpha_1 q_1 itself, the consumer forms x (GXap2)
-inline bool kcycle_fused(const amg_hier_s* h) { return h->cfg.pre_sweeps == 1 && h->cfg.smoother == 0; }
+// (single rank: several ranks form the inner x explicitly, so a consumer gathers ONE vector)
+inline bool kcycle_fused(const amg_hier_s* h) {
+    return h->cfg.pre_sweeps == 1 && h->cfg.smoother == 0 && !h->multi();
+}
 // Where a cycle's fused dot goes: the PCG state (default) or a K-cycle level state.
 struct DotSink {
-    double* ks;
+    double* ks;  // single rank: the level's K state (ranks[0]); several ranks use lvl
     int kind;
     // K-cycle, s1 == 1: the application's right-hand side is b - alpha q (k = ks), formed by
     // its first kernel, which also writes it to the application's b vector
     const double* kb = nullptr;
     const double* kq = nullptr;
+    int lvl = -1;  // the level whose K state {p^T r, p^T q, alpha, beta, stop} receives the dot
 };
 void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const VecOf* mbvec, const VecOf& outv,
                    bool dot, const VecOf* dwv, const DotSink* sink = nullptr);
-RedCtx sink_red(amg_hier_s* h, RankState& R, int dkind, const DotSink* sink) {
-    if (sink) return RedCtx{R.partials, R.ticket, nullptr, nullptr, 0ull, sink->kind, sink->ks};
-    return dot_red(h, R, dkind, 0);
+// Several ranks: every dot (PCG or K state) goes to the rank's local slots; end_dot all-gathers
+// them and finishes into the PCG state or each rank's level-K state in rank order.
+RedCtx sink_red(amg_hier_s* h, RankState& R, int dkind, const DotSink* sink, int part = 0) {
+    if (sink && !h->multi()) return RedCtx{R.partials, R.ticket, nullptr, nullptr, 0ull, sink->kind, sink->ks};
+    return dot_red(h, R, dkind, 0, part);
+}
+void dot_finish_k(amg_hier_s* h, Launch& L, int kind, int lvl);
+void end_dot(amg_hier_s* h, Launch& L, bool dot, int dkind, const DotSink* sink) {
+    if (!dot || !h->multi()) return;
+    if (sink) dot_finish_k(h, L, sink->kind, sink->lvl);
+    else dot_finish(h, L, dkind);
 }
 
 // Level l of the cycle with the INVK smoother (cfg.smoother == 1): M^{-1} r = Z (Wd r),
@@ -962,7 +995,7 @@ void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, cons
         DevLevel& D = R.lv[l];
         DevLevel& C = R.lv[l + 1];
         double* x = outv(R) + D.ep_off;
-        if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
+        if (kfcg && !h->multi())  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
             launch_mat(L, D.P, GXap{C.kx, C.kp2, C.kst}, EProlongAdd{x, x}, no_red(), "prolong",
                        2 * n8(R) + 16.0 * (double)C.comp_n, part);
         else
@@ -973,7 +1006,7 @@ void enqueue_level_invk(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, cons
         resid("invk_resid");
         precond(rv, true, dot && sw == s2 - 1);
     }
-    if (dot && !sink) dot_finish(h, L, dkind);
+    end_dot(h, L, dot, dkind, sink);
 }
 
 // Collapsed level (compact, above a direct coarsest solve): out = S2(b) + M b in ONE kernel.
@@ -1003,7 +1036,7 @@ void enqueue_level_collapsed(amg_hier_s* h, Launch& L, int l, const VecOf& bvec,
         }
         L.end();
     }
-    if (dot && !sink) dot_finish(h, L, dkind);
+    end_dot(h, L, dot, dkind, sink);
 }
 
 // Compact small level (see compact_level_ok): s = S2(b) = m b + m (b - A (m b)) into r;
@@ -1068,10 +1101,10 @@ void enqueue_level_compact(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, c
                 launch_mat(L, D.Pc, g, EAddDot<false>{D.r, out}, no_red(), "prolong_post_c", 2 * n8 + nc8);
         };
         if (kfcg && kcycle_fused(h) && !tailc) post(GXap2{C.kp, C.kp2, C.kst});
-        else if (kfcg) post(GXap{C.kx, tailc ? C.kp : C.kp2, C.kst});
+        else if (kfcg && !h->multi()) post(GXap{C.kx, tailc ? C.kp : C.kp2, C.kst});
         else post(GVec{ev(R)});
     }
-    if (dot && !sink) dot_finish(h, L, dkind);
+    end_dot(h, L, dot, dkind, sink);
 }
 
 // out = B_l b: the part of the cycle rooted at level l (Eq. 3.1;
@@ -1104,7 +1137,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
                 L.end();
             }
         }
-        if (dot && !sink) dot_finish(h, L, dkind);
+        end_dot(h, L, dot, dkind, sink);
         return;
     }
     if (h->ranks[0].lv[l].Mc) {
@@ -1216,7 +1249,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             if (kfcg && kfused(C))  // e = alpha_1 p_1 + alpha_2 p_2 of the inner FCG, formed in the gather
                 launch_mat(L, D.P, GXap2{C.kp, C.kp2, C.kst}, EStore{dst + D.ep_off}, no_red(), "prolong",
                            n8 + 2 * nc8, part);
-            else if (kfcg)  // e = x + alpha p of the inner FCG, formed in the gather (its last update)
+            else if (kfcg && !h->multi())  // e = x + alpha p of the inner FCG, formed in the gather
                 launch_mat(L, D.P, GXap{C.kx, kpfin(C), C.kst}, EStore{dst + D.ep_off}, no_red(), "prolong",
                            n8 + 2 * nc8, part);
             else
@@ -1225,7 +1258,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             if (kfcg && kfused(C))
                 launch_mat(L, D.P, GXap2{C.kp, C.kp2, C.kst}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off},
                            no_red(), "prolong", 2 * n8 + 2 * nc8, part);
-            else if (kfcg)
+            else if (kfcg && !h->multi())
                 launch_mat(L, D.P, GXap{C.kx, kpfin(C), C.kst}, EProlongAdd{xpre[ri] + D.ep_off, dst + D.ep_off},
                            no_red(), "prolong", 2 * n8 + 2 * nc8, part);
             else
@@ -1250,7 +1283,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
             const double mb8 = abs ? 0.0 : n8;
             double* m = D.m + D.ep_off;
-            auto red = [&]() { return sink ? sink_red(h, R, dkind, sink) : dot_red(h, R, dkind, 0, part); };
+            auto red = [&]() { return sink_red(h, R, dkind, sink, part); };
             if (s == 0 && s1 == 1) {
                 const double* bo = !mbvec ? b + D.ep_off : (*mbvec)(R) + D.ep_off;
                 const double* rr = D.r + D.ep_off;
@@ -1293,7 +1326,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
         });
         cur = nxt;
     }
-    if (dot && !sink) dot_finish(h, L, dkind);
+    end_dot(h, L, dot, dkind, sink);
 }
 
 // K-cycle coarse correction at level l (oracle kcycle_fcg2): two
@@ -1301,7 +1334,68 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
 // at level l, no residual test.  Single rank.  Scalars live in the level's
 // device-side K state {p^T r, p^T q, alpha, beta, stop}; every dot is fused into
 // the kernel that produces its operand and reduced deterministically.
+// Several ranks (each level distributed or replicated): the same two FCG(1) iterations with
+// the halo of p exchanged before each q = A p (overlapped with the interior rows), every dot
+// reduced into the rank's local slots and finished into each rank's K state in rank order
+// (dot_finish_k), and the inner solution x = x + alpha p formed explicitly (k_kupd2), so the
+// consumer (the coarser level's prolongation) gathers, and exchanges, one vector.
+void enqueue_fcg2_multi(amg_hier_s* h, Launch& L, int l) {
+    const int nsm = h->ctx->nsm;
+    const bool dist = !h->ranks[0].lv[l].replicated;
+    const VecOf bv = [l](RankState& R) { return R.lv[l].b; };
+    const VecOf mbv = [l](RankState& R) { return R.lv[l].mb; };
+    const VecOf kp = [l](RankState& R) { return R.lv[l].kp; };
+    const VecOf kr = [l](RankState& R) { return R.lv[l].kr; };
+    const VecOf kmb = [l](RankState& R) { return R.lv[l].kmb; };
+    const VecOf kz = [l](RankState& R) { return R.lv[l].kz; };
+    const VecOf kq = [l](RankState& R) { return R.lv[l].kq; };
+    auto spmv_alpha = [&]() {  // q = A p, p^T q -> alpha (FIN_KALPHA)
+        overlapped(h, L, l, kp, dist, [&](RankState& R, int part) {
+            DevLevel& D = R.lv[l];
+            launch_mat(L, D.A, GVec{D.kp}, ESpmvDot{D.kp + D.ep_off, D.kq + D.ep_off}, dot_red(h, R, FIN_NONE, 0, part),
+                       "kfcg_spmv", 16.0 * (double)D.comp_n, part);
+        });
+        dot_finish_k(h, L, FIN_KALPHA, l);
+    };
+    // iteration 1: p = z = B_l b with p^T b fused into the cycle's last step (a new inner solve)
+    const DotSink s1{nullptr, FIN_KPR0, nullptr, nullptr, l};
+    enqueue_level(h, L, l, bv, &mbv, kp, true, nullptr, &s1);
+    spmv_alpha();
+    for (auto& R : h->ranks) {  // x = alpha p ; r = b - alpha q ; m o r
+        DevLevel& D = R.lv[l];
+        const int64_t o = D.ep_off, n = D.comp_n;
+        L.begin("kfcg_upd1", 56.0 * (double)n);
+        launch_k(k_kupd1, vec_grid(n, nsm), kBlock, L.s, D.kx + o, D.kr + o, D.kmb + o, (const double*)D.kp + o,
+                 (const double*)D.kq + o, (const double*)D.b + o, (const double*)D.m + o, n, (const double*)D.kst);
+        L.end();
+    }
+    // iteration 2: z = B_l r with z^T q -> beta ; p = z + beta p, p^T r ; q = A p -> alpha ; x += alpha p
+    const DotSink s2{nullptr, FIN_KBETA, nullptr, nullptr, l};
+    enqueue_level(h, L, l, kr, &kmb, kz, true, &kq, &s2);
+    for (auto& R : h->ranks) {
+        DevLevel& D = R.lv[l];
+        const int64_t o = D.ep_off, n = D.comp_n;
+        L.begin("kfcg_pupd", 32.0 * (double)n);
+        launch_k(k_kpupd, vec_grid(n, nsm), kBlock, L.s, D.kp + o, (const double*)D.kz + o, (const double*)D.kr + o,
+                 n, (const double*)D.kst, dot_red(h, R, FIN_NONE, 0));
+        L.end();
+    }
+    dot_finish_k(h, L, FIN_KPR, l);
+    spmv_alpha();
+    for (auto& R : h->ranks) {
+        DevLevel& D = R.lv[l];
+        const int64_t o = D.ep_off, n = D.comp_n;
+        L.begin("kfcg_upd2", 24.0 * (double)n);
+        launch_k(k_kupd2, vec_grid(n, nsm), kBlock, L.s, D.kx + o, (const double*)D.kp + o, n, (const double*)D.kst);
+        L.end();
+    }
+}
+
 void enqueue_fcg2(amg_hier_s* h, Launch& L, int l) {
+    if (h->multi()) {
+        enqueue_fcg2_multi(h, L, l);
+        return;
+    }
     const int nsm = h->ctx->nsm;
     RankState& R = h->ranks[0];
     DevLevel& D = R.lv[l];
@@ -1315,7 +1409,7 @@ void enqueue_fcg2(amg_hier_s* h, Launch& L, int l) {
     const VecOf kmb = [l](RankState& R) { return R.lv[l].kmb; };
     const VecOf kz = [l](RankState& R) { return R.lv[l].kz; };
     // iteration 1: p = z = B_l b with p^T r (r = b) fused into the cycle's last step
-    const DotSink s1{D.kst, FIN_KPR0};
+    const DotSink s1{D.kst, FIN_KPR0, nullptr, nullptr, l};
     const bool fused = kcycle_fused(h);
     if (D.AMc && fused) {  // collapsed level: p = B b and q = (A B) b in one kernel
         L.begin("collapsed_kq", 16.0 * (double)n * (double)n + 24.0 * (double)n);
@@ -1337,7 +1431,7 @@ void enqueue_fcg2(amg_hier_s* h, Launch& L, int l) {
     // The final x += alpha p is formed by the consumer (the prolongation gathers x + alpha p).
     // fused: r = b - alpha_1 q_1 is formed (and stored in kr) by the application's first kernel,
     // x = alpha_1 p_1 + alpha_2 p_2 by the consumer (GXap2)
-    const DotSink s2{D.kst, FIN_KBETA, fused ? D.b : nullptr, fused ? D.kq : nullptr};
+    const DotSink s2{D.kst, FIN_KBETA, fused ? D.b : nullptr, fused ? D.kq : nullptr, l};
     const VecOf kq = [l](RankState& R) { return R.lv[l].kq; };
     if (D.AMc && fused) {  // collapsed level: z = B r1, w = A z = (AB) r1, then p2 / q2 by vectors
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, kMaxPartials));
@@ -2520,6 +2614,21 @@ void fill_report(amg_hier_s* h, amg_report_t* rep) {
     rep->iteration_bytes_model = h->bytes_it;
 }
 
+amgsetup::Config setup_config(const amg_config_t& cfg) {
+    amgsetup::Config sc;
+    sc.sweeps_per_level = cfg.sweeps_per_level;
+    sc.smooth_prolongator = cfg.smooth_prolongator;
+    sc.prol_omega_scale = cfg.prol_omega_scale;
+    sc.max_coarse_size = cfg.max_coarse_size;
+    sc.max_levels = cfg.max_levels;
+    sc.min_coarsening_ratio = cfg.min_coarsening_ratio;
+    sc.pre_sweeps = cfg.pre_sweeps;
+    sc.post_sweeps = cfg.post_sweeps;
+    sc.threads = cfg.setup_threads;
+    sc.device = cfg.setup_device;
+    return sc;
+}
+
 // Copies the caller's CSR into the setup's form and runs the host setup.
 int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values, const double* w,
                const amg_config_t& cfg, amgsetup::Hierarchy& H) {
@@ -2560,17 +2669,7 @@ int host_setup(int64_t n, const int64_t* rowptr, const int64_t* colind, const do
     }
     std::vector<double> wv(n, 1.0);
     if (w) std::copy(w, w + n, wv.begin());
-    amgsetup::Config sc;
-    sc.sweeps_per_level = cfg.sweeps_per_level;
-    sc.smooth_prolongator = cfg.smooth_prolongator;
-    sc.prol_omega_scale = cfg.prol_omega_scale;
-    sc.max_coarse_size = cfg.max_coarse_size;
-    sc.max_levels = cfg.max_levels;
-    sc.min_coarsening_ratio = cfg.min_coarsening_ratio;
-    sc.pre_sweeps = cfg.pre_sweeps;
-    sc.post_sweeps = cfg.post_sweeps;
-    sc.threads = cfg.setup_threads;
-    sc.device = cfg.setup_device;
+    amgsetup::Config sc = setup_config(cfg);
     if (sc.device) {
         // capacity: A_0 and the level-0 Galerkin operands and results (A P-bar, its
         // per-entry product offsets, P-bar^T, the kept device hierarchy: <= ~64 B per
@@ -2907,10 +3006,6 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
             set_err("amg_hierarchy_build: with several ranks the INVK blocks are the ranks' (invk_blocks 0 or np)");
             return AMG_ERR_ARG;
         }
-    }
-    if (cfg.cycle == 1 && (ctx->nranks > 1 || cfg.emulate_ranks > 1)) {
-        set_err("amg_hierarchy_build: the K-cycle is implemented for single-rank contexts only");
-        return AMG_ERR_ARG;
     }
     CK(cudaSetDevice(ctx->device));
     const int nr = ctx->nranks;
@@ -3539,6 +3634,101 @@ int amg_host_hierarchy_build(int64_t n, const int64_t* rowptr, const int64_t* co
         set_err("amg_host_hierarchy_build: " + g_err);
         return st;
     }
+    *out = h;
+    return AMG_OK;
+}
+
+int amg_host_dist_build(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values,
+                        const double* w, const amg_config_t* cfg_in, int32_t nranks, int64_t replicate_below_bytes,
+                        amg_host_hier_t* out) {
+    if (!out || nranks < 1 || !rowptr || !colind || !values || n <= 0 || n >= (int64_t)INT32_MAX) {
+        set_err("amg_host_dist_build: bad argument");
+        return AMG_ERR_ARG;
+    }
+    *out = nullptr;
+    amg_config_t cfg;
+    amg_config_default(&cfg);
+    if (cfg_in) cfg = *cfg_in;
+    // the same validation as the single-process build (the whole matrix is at hand here)
+    amgsetup::Csr A;
+    A.nrows = A.ncols = n;
+    A.rp.assign(rowptr, rowptr + n + 1);
+    A.ci.resize(rowptr[n]);
+    for (int64_t k = 0; k < rowptr[n]; ++k) {
+        if (colind[k] < 0 || colind[k] >= n) {
+            set_err("amg_host_dist_build: column index out of range");
+            return AMG_ERR_ARG;
+        }
+        A.ci[k] = (int32_t)colind[k];
+    }
+    A.v.assign(values, values + rowptr[n]);
+    std::vector<double> wv(n, 1.0);
+    if (w) std::copy(w, w + n, wv.begin());
+    std::string err;
+    int vst = amgsetup::validate(A, wv, err);
+    if (vst != amgsetup::SETUP_OK) {
+        set_err("amg_host_dist_build: " + err);
+        return vst == amgsetup::SETUP_ERR_ARG ? AMG_ERR_ARG : AMG_ERR_NOT_SPD;
+    }
+    std::vector<int64_t> b0(nranks + 1);
+    for (int g = 0; g <= nranks; ++g) b0[g] = n * g / nranks;
+    amgsetup::Config sc = setup_config(cfg);
+    std::vector<amgsetup::DistHierarchy> DH(nranks);
+    std::vector<amgsetup::RankPlan> plans(nranks);
+    std::vector<int> rst(nranks, AMG_OK);
+    std::vector<std::string> rerr(nranks);
+    amgsetup::run_loopback(nranks, [&](amgsetup::Comm& c) {
+        const int r = c.rank();
+        amgsetup::Csr Al;
+        Al.nrows = b0[r + 1] - b0[r];
+        Al.ncols = n;
+        Al.rp.resize(Al.nrows + 1);
+        for (int64_t i = 0; i <= Al.nrows; ++i) Al.rp[i] = A.rp[b0[r] + i] - A.rp[b0[r]];
+        Al.ci.assign(A.ci.begin() + A.rp[b0[r]], A.ci.begin() + A.rp[b0[r + 1]]);
+        Al.v.assign(A.v.begin() + A.rp[b0[r]], A.v.begin() + A.rp[b0[r + 1]]);
+        std::vector<double> wl(wv.begin() + b0[r], wv.begin() + b0[r + 1]);
+        const int st = amgsetup::build_distributed(c, b0, std::move(Al), std::move(wl), sc, DH[r], rerr[r]);
+        if (st != amgsetup::SETUP_OK) {
+            rst[r] = st == amgsetup::SETUP_ERR_ARG ? AMG_ERR_ARG : AMG_ERR_NOT_SPD;
+            return;
+        }
+        if (!amgsetup::partition_distributed(c, DH[r], replicate_below_bytes, plans[r], rerr[r])) rst[r] = AMG_ERR_ARG;
+    });
+    for (int r = 0; r < nranks; ++r)
+        if (rst[r] != AMG_OK) {
+            set_err("amg_host_dist_build: rank " + std::to_string(r) + ": " + rerr[r]);
+            return rst[r];
+        }
+    // the global view for inspection: every level's rows concatenated in rank order
+    auto* h = new amg_host_hier_s();
+    const size_t nl = DH[0].lv.size();
+    h->H.lv.resize(nl);
+    for (size_t l = 0; l < nl; ++l) {
+        amgsetup::Level& L = h->H.lv[l];
+        const int64_t nn = DH[0].lv[l].n;
+        auto cat = [&](auto get, int64_t ncols) {
+            amgsetup::Csr M;
+            M.nrows = nn;
+            M.ncols = ncols;
+            M.rp.assign(1, 0);
+            for (int r = 0; r < nranks; ++r) {
+                const amgsetup::Csr& X = get(DH[r].lv[l]);
+                for (int64_t i = 0; i < X.nrows; ++i) M.rp.push_back(M.rp.back() + (X.rp[i + 1] - X.rp[i]));
+                M.ci.insert(M.ci.end(), X.ci.begin(), X.ci.end());
+                M.v.insert(M.v.end(), X.v.begin(), X.v.end());
+            }
+            return M;
+        };
+        L.A = cat([](const amgsetup::DistLevel& D) -> const amgsetup::Csr& { return D.A; }, nn);
+        if (l + 1 < nl) {
+            L.P = cat([](const amgsetup::DistLevel& D) -> const amgsetup::Csr& { return D.P; }, DH[0].lv[l + 1].n);
+            for (int r = 0; r < nranks; ++r) L.agg.insert(L.agg.end(), DH[r].lv[l].agg.begin(), DH[r].lv[l].agg.end());
+            L.omega = DH[0].lv[l].omega;
+            L.sweeps = DH[0].lv[l].sweeps;
+        }
+    }
+    h->H.coarse_inv = DH[0].coarse_inv;
+    h->plans = std::move(plans);
     *out = h;
     return AMG_OK;
 }

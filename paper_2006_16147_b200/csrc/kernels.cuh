@@ -1226,6 +1226,29 @@ __global__ void __launch_bounds__(kBlock) k_kupd1(double* __restrict__ x, double
         mb[i] = m[i] * ri;
     }
 }
+// K-cycle inner FCG, several ranks (own rows): p = z + beta p, p^T r -> rc (the rank's dot
+// slot; beta = k[3]); x += alpha p (alpha = k[2]), the inner solve's last update.
+__global__ void __launch_bounds__(kBlock) k_kpupd(double* __restrict__ p, const double* __restrict__ z,
+                                                  const double* __restrict__ r, int64_t n,
+                                                  const double* __restrict__ k, RedCtx rc) {
+    pdl_begin();
+    const double beta = k[3];
+    double d = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        const double pi = z[i] + beta * p[i];
+        p[i] = pi;
+        d += pi * r[i];
+    }
+    grid_reduce(d, rc);
+}
+__global__ void __launch_bounds__(kBlock) k_kupd2(double* __restrict__ x, const double* __restrict__ p, int64_t n,
+                                                  const double* __restrict__ k) {
+    pdl_begin();
+    const double alpha = k[2];
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        x[i] = x[i] + alpha * p[i];
+}
+
 // ------------------------------------------------------- coarsest iterative solve
 // The paper's coarsest solver for the GPU runs: CG
 // preconditioned by the l1-Jacobi diagonal of A_L, x0 = 0, stopped as soon as

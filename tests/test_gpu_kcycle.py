@@ -59,10 +59,23 @@ def _case(name):
     if name == "k_jump27_24":
         A = jump27(24)
         return A, uniform01(5, A.n_global), dict(smooth_prolongator=0), K, False
+    # several ranks (loopback): the inner FCG exchanges p halos, finishes its dots in rank order
+    if name == "ka1_48_loop2":
+        A = poisson7(48, 48, 48)
+        return A, uniform01(2, A.n_global), dict(smooth_prolongator=0), dict(K, emulate_ranks=2), False
+    if name == "ka1_64_loop4_dist":  # replicate nothing but the coarsest: inner FCG on distributed levels
+        A = poisson7(64, 64, 64)
+        return (A, np.ones(A.n_global), dict(smooth_prolongator=0),
+                dict(K, emulate_ranks=4, replicate_below_bytes=0), False)
+    if name == "k_aniso22_loop3":
+        A, b, _ = config_problem(3, grid=(36, 36, 36))
+        return (A, b, dict(smooth_prolongator=0, pre_sweeps=2, post_sweeps=2),
+                dict(K, emulate_ranks=3, replicate_below_bytes=1 << 18), False)
     raise KeyError(name)
 
 
-CASES = ["ka1_c1", "ka1_48", "ka2_64", "k_smoothed_32", "k_aniso_coarse_cg", "k_jump27_24"]
+CASES = ["ka1_c1", "ka1_48", "ka2_64", "k_smoothed_32", "k_aniso_coarse_cg", "k_jump27_24", "ka1_48_loop2",
+         "ka1_64_loop4_dist", "k_aniso22_loop3"]
 _cache = {}
 
 
@@ -130,7 +143,20 @@ def test_kcycle_eager_equals_graph_and_is_deterministic(ctx):
     assert r1["iterations"] == r2["iterations"] and torch.equal(x1, x2)
 
 
-def test_kcycle_rejects_multirank(ctx):
+def test_kcycle_multirank_graph_equals_eager_and_single_rank(ctx):
+    """Loopback K-cycle: the WHILE-graph solve equals the eager one bitwise, and both agree with
+    the single-rank K-cycle to rounding (same iterations)."""
     amg = _amg()
-    with pytest.raises(amg.AmgError):
-        amg.Hierarchy(ctx, poisson7(16, 16, 16), cfg=amg.make_config(cycle=1, emulate_ranks=2))
+    A = poisson7(40, 40, 40)
+    cfg = dict(smooth_prolongator=0, cycle=1, krylov=1)
+    h1 = amg.Hierarchy(ctx, A, cfg=amg.make_config(**cfg))
+    hg = amg.Hierarchy(ctx, A, cfg=amg.make_config(**cfg, emulate_ranks=2, replicate_below_bytes=0))
+    he = amg.Hierarchy(ctx, A, cfg=amg.make_config(**cfg, emulate_ranks=2, replicate_below_bytes=0,
+                                                      use_graphs=0))
+    b = torch.tensor(uniform01(90, A.n_global), device="cuda:0")
+    x1, r1 = h1.solve(b, rtol=1e-8)
+    xg, rg = hg.solve(b, rtol=1e-8)
+    xe, re_ = he.solve(b, rtol=1e-8)
+    assert rg["iterations"] == re_["iterations"] and torch.equal(xg, xe)
+    assert rg["iterations"] == r1["iterations"]
+    assert (torch.linalg.norm(xg - x1) / torch.linalg.norm(x1)).item() <= 1e-10
