@@ -143,6 +143,12 @@ typedef struct {
                                      with the smoother's blocks / l1 / fill (VA3S3CS1: "we apply HINVK also
                                      as preconditioner of the CG method at the coarsest level",
                                      PAPER.md:420) */
+    int32_t setup_distributed;    /* several ranks: 1 = the DISTRIBUTED setup: every
+                                     rank builds only its rows of every level and its own plan (cross-rank
+                                     matching rounds, remote-row-gather Galerkin products, all-reduced
+                                     omega), bit-identical to the single-process build; 0 = rank 0 gathers
+                                     the matrix, builds the whole hierarchy and scatters the plans; -1
+                                     (default) = 1 for NCCL contexts, 0 for emulate_ranks (loopback) */
 } amg_config_t;
 
 /* Solve report (SPEC.md:440-443 SolveReport). */
@@ -292,6 +298,20 @@ int amg_host_level_matrix(amg_host_hier_t h, int32_t lvl, int32_t which, int64_t
 int amg_host_dist_build(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values,
                         const double* w, const amg_config_t* cfg, int32_t nranks, int64_t replicate_below_bytes,
                         amg_host_hier_t* out);
+
+/* The same distributed setup for ONE rank of a caller-provided transport (e.g. torch.distributed over
+ * gloo, one process per rank): `exchange` is called collectively; with phase 0 it exchanges byte
+ * counts (send_counts[q] bytes go to rank q, recv_counts[q] receives rank q's count), with phase 1 the
+ * payloads, concatenated in rank order (send_buf holds sum(send_counts) bytes, recv_buf has room for
+ * sum(recv_counts)); it returns 0 on success (non-zero: AMG_ERR_NCCL).  rowptr / colind / values / w
+ * hold this rank's rows [row_begin, row_end) (global column ids).  The result holds this rank's plan
+ * (amg_host_plan_level / amg_host_plan_array with this rank) and level sizes.  Host only. */
+typedef int (*amg_exchange_fn)(void* user, int32_t phase, const int64_t* send_counts, int64_t* recv_counts,
+                               const void* send_buf, void* recv_buf);
+int amg_host_dist_build_rank(int64_t n, int64_t row_begin, int64_t row_end, const int64_t* rowptr,
+                             const int64_t* colind, const double* values, const double* w, const amg_config_t* cfg,
+                             int32_t nranks, int32_t rank, int64_t replicate_below_bytes,
+                             amg_exchange_fn exchange, void* user, amg_host_hier_t* out);
 
 /* Partition plan of the host hierarchy over `nranks` ranks with level-0 row blocks
  * row_bounds[0..nranks] (coarse rows owned by the rank of their

@@ -28,7 +28,7 @@ class amg_config_t(C.Structure):
                 ("coarse_rtol", C.c_double), ("cycle", C.c_int32), ("setup_device", C.c_int32),
                 ("tail_rows", C.c_int64), ("smoother", C.c_int32), ("invk_fill", C.c_int32),
                 ("tail_bytes", C.c_int64), ("invk_l1", C.c_int32), ("invk_blocks", C.c_int32),
-                ("invk_dense_cut", C.c_int32), ("coarse_prec", C.c_int32)]
+                ("invk_dense_cut", C.c_int32), ("coarse_prec", C.c_int32), ("setup_distributed", C.c_int32)]
 
 
 class amg_report_t(C.Structure):
@@ -80,6 +80,9 @@ _SIG = {
     "amg_host_partition": (C.c_int, [_vp, C.c_int32, _vp, C.c_int64]),
     "amg_host_dist_build": (C.c_int, [C.c_int64, _vp, _vp, _vp, _vp, C.POINTER(amg_config_t), C.c_int32,
                                       C.c_int64, C.POINTER(_vp)]),
+    "amg_host_dist_build_rank": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp, _vp,
+                                           C.POINTER(amg_config_t), C.c_int32, C.c_int32, C.c_int64,
+                                           _vp, _vp, C.POINTER(_vp)]),
     "amg_host_plan_level": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp]),
     "amg_host_plan_array": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp]),
 }
@@ -89,6 +92,10 @@ for _name, (_res, _args) in _SIG.items():
     _f.argtypes = _args
 
 EXPORTED = tuple(_SIG)
+
+# amg_exchange_fn (include/amg_b200.h): the distributed setup's transport callback
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                          C.c_void_p, C.c_void_p)
 
 
 class AmgError(RuntimeError):

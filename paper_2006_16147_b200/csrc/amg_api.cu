@@ -2414,47 +2414,57 @@ int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<do
 // runs 2^l times (l <= nl-2; the coarsest 2^(nl-2) times) and each of the 2^(l-1)
 // inner FCG solves at level l >= 1 adds two SpMVs and its vector updates
 // (176 B per row: p^T b, kupd1, z^T q, p-update, kupd2 and the SpMV p/q).
-void byte_model(amg_hier_s* h, const amgsetup::Hierarchy& H) {
+// Global level statistics (rows, nnz(A_l), nnz(P-bar_l), nnz(Wd_l) + nnz(Z_l)).
+struct LevelStats {
+    std::vector<int64_t> n, nnzA, nnzP, nnzWZ;
+};
+LevelStats stats_of(const amgsetup::Hierarchy& H) {
+    LevelStats S;
+    for (auto& L : H.lv) {
+        S.n.push_back(L.A.nrows);
+        S.nnzA.push_back(L.A.nnz());
+        S.nnzP.push_back(L.P.nnz());
+        S.nnzWZ.push_back(L.Wd.nnz() + L.Z.nnz());
+    }
+    return S;
+}
+
+void byte_model(amg_hier_s* h, const LevelStats& S) {
     const double s1 = h->cfg.pre_sweeps, s2 = h->cfg.post_sweeps;
     const bool kc = h->cfg.cycle == 1;
     double bv = 0.0;
-    const size_t nl = H.lv.size();
+    const size_t nl = S.n.size();
     for (size_t l = 0; l + 1 < nl; ++l) {
-        const double n = (double)H.lv[l].A.nrows, nc = (double)H.lv[l + 1].A.nrows;
-        const double MA = 12.0 * (double)H.lv[l].A.nnz() + 4.0 * (n + 1);
-        const double MP = 12.0 * (double)H.lv[l].P.nnz() + 4.0 * (n + 1);
+        const double n = (double)S.n[l], nc = (double)S.n[l + 1];
+        const double MA = 12.0 * (double)S.nnzA[l] + 4.0 * (n + 1);
+        const double MP = 12.0 * (double)S.nnzP[l] + 4.0 * (n + 1);
         const double visits = kc ? std::ldexp(1.0, (int)l) : 1.0;
         bv += visits * ((s1 + s2) * MA + 2 * MP + 8 * n * ((s1 + s2) + 2 + 3 * (s1 - 1) + 2 + 2 + 3 * s2) + 16 * nc);
         if (h->cfg.smoother == 1)  // INVK: every smoothing step also streams Wd and Z (+ t write/read)
-            bv += visits * (s1 + s2) *
-                  (12.0 * (double)(H.lv[l].Wd.nnz() + H.lv[l].Z.nnz()) + 8.0 * (n + 1) + 16.0 * n);
+            bv += visits * (s1 + s2) * (12.0 * (double)S.nnzWZ[l] + 8.0 * (n + 1) + 16.0 * n);
         if (kc && l >= 1) bv += std::ldexp(1.0, (int)l - 1) * (2 * MA + 176.0 * n);
     }
-    const double nL = (double)H.lv.back().A.nrows;
+    const double nL = (double)S.n.back();
     bv += (kc && nl >= 2 ? std::ldexp(1.0, (int)nl - 2) : 1.0) * (8 * nL * nL + 16 * nL);
     h->bytes_v = bv;
-    const double n0 = (double)H.lv[0].A.nrows;
-    h->bytes_it = bv + 12.0 * (double)H.lv[0].A.nnz() + 4.0 * (n0 + 1) + 88.0 * n0;
+    const double n0 = (double)S.n[0];
+    h->bytes_it = bv + 12.0 * (double)S.nnzA[0] + 4.0 * (n0 + 1) + 88.0 * n0;
 }
 
-void hier_stats(amg_hier_s* h, const amgsetup::Hierarchy& H) {
-    const size_t nl = H.lv.size();
+void hier_stats(amg_hier_s* h, const LevelStats& S) {
+    const size_t nl = S.n.size();
     double s = 0.0;
-    for (auto& L : H.lv) s += (double)L.A.nnz();
-    h->opc = s / (double)H.lv[0].A.nnz();
+    for (int64_t x : S.nnzA) s += (double)x;
+    h->opc = s / (double)S.nnzA[0];
     double cr = 0.0;
-    for (size_t l = 0; l + 1 < nl; ++l) cr += (double)H.lv[l].A.nrows / (double)H.lv[l + 1].A.nrows;
+    for (size_t l = 0; l + 1 < nl; ++l) cr += (double)S.n[l] / (double)S.n[l + 1];
     h->avg_cr = nl > 1 ? cr / (double)(nl - 1) : 1.0;
-    h->lvl_n.resize(nl);
-    h->lvl_nnzA.resize(nl);
-    h->lvl_nnzP.resize(nl);
-    for (size_t l = 0; l < nl; ++l) {
-        h->lvl_n[l] = H.lv[l].A.nrows;
-        h->lvl_nnzA[l] = H.lv[l].A.nnz();
-        h->lvl_nnzP[l] = H.lv[l].P.nnz();
-    }
-    byte_model(h, H);
+    h->lvl_n = S.n;
+    h->lvl_nnzA = S.nnzA;
+    h->lvl_nnzP = S.nnzP;
+    byte_model(h, S);
 }
+void hier_stats(amg_hier_s* h, const amgsetup::Hierarchy& H) { hier_stats(h, stats_of(H)); }
 
 int build_solve_exec(amg_hier_s* h, const double* b, double* x, cudaGraphExec_t* out);
 enum { GM_WHILE = 0, GM_ITER = 1 };
@@ -2876,6 +2886,307 @@ void blob_put_array(Blob& B, const T* p, int64_t n) {
     B.b.insert(B.b.end(), c, c + n * sizeof(T));
 }
 
+
+// ---------------------------------------------------- distributed setup (NEXT-1)
+// NCCL transport of the distributed setup: an all-to-all of host byte buffers through device
+// staging (sizes all-gathered, payloads by grouped send/recv on the context stream).
+struct NcclComm : amgsetup::Comm {
+    amg_ctx_s* c = nullptr;
+    bool ok = true;
+    std::string what;
+    int rank() const override { return c->rank; }
+    int size() const override { return c->nranks; }
+    bool fail(const std::string& w) {
+        if (ok) what = w;
+        ok = false;
+        return false;
+    }
+    bool alltoallv(const std::vector<std::vector<char>>& out, std::vector<std::vector<char>>& in) override {
+        const int np = c->nranks, me = c->rank;
+        in.assign(np, {});
+        if (!ok) return false;
+        std::vector<int64_t> mine(np), all((size_t)np * np);
+        for (int q = 0; q < np; ++q) mine[q] = (int64_t)out[q].size();
+        int64_t* dsz = nullptr;
+        if (cudaMalloc(&dsz, sizeof(int64_t) * (size_t)np * (np + 1)) != cudaSuccess) return fail("cudaMalloc");
+        cudaMemcpy(dsz, mine.data(), sizeof(int64_t) * np, cudaMemcpyHostToDevice);
+        if (ncclAllGather(dsz, dsz + np, np, ncclInt64, c->nccl, c->stream) != ncclSuccess)
+            return cudaFree(dsz), fail("ncclAllGather (setup sizes)");
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cudaFree(dsz), fail("setup sizes sync");
+        cudaMemcpy(all.data(), dsz + np, sizeof(int64_t) * (size_t)np * np, cudaMemcpyDeviceToHost);
+        cudaFree(dsz);
+        int64_t stot = 0, rtot = 0;
+        std::vector<int64_t> soff(np + 1, 0), roff(np + 1, 0);
+        for (int q = 0; q < np; ++q) {
+            const int64_t sq = q == me ? 0 : mine[q], rq = q == me ? 0 : all[(size_t)q * np + me];
+            soff[q + 1] = soff[q] + sq;
+            roff[q + 1] = roff[q] + rq;
+        }
+        stot = soff[np];
+        rtot = roff[np];
+        char *ds = nullptr, *dr = nullptr;
+        if (cudaMalloc(&ds, std::max<int64_t>(stot, 8)) != cudaSuccess ||
+            cudaMalloc(&dr, std::max<int64_t>(rtot, 8)) != cudaSuccess)
+            return cudaFree(ds), fail("cudaMalloc (setup payload)");
+        for (int q = 0; q < np; ++q)
+            if (q != me && mine[q]) cudaMemcpy(ds + soff[q], out[q].data(), mine[q], cudaMemcpyHostToDevice);
+        bool nok = ncclGroupStart() == ncclSuccess;
+        for (int q = 0; q < np; ++q) {
+            if (q == me) continue;
+            if (soff[q + 1] > soff[q])
+                nok &= ncclSend(ds + soff[q], soff[q + 1] - soff[q], ncclChar, q, c->nccl, c->stream) == ncclSuccess;
+            if (roff[q + 1] > roff[q])
+                nok &= ncclRecv(dr + roff[q], roff[q + 1] - roff[q], ncclChar, q, c->nccl, c->stream) == ncclSuccess;
+        }
+        nok &= ncclGroupEnd() == ncclSuccess;
+        nok &= cudaStreamSynchronize(c->stream) == cudaSuccess;
+        for (int q = 0; q < np && nok; ++q) {
+            if (q == me) {
+                in[q] = out[q];
+                continue;
+            }
+            in[q].resize(roff[q + 1] - roff[q]);
+            if (!in[q].empty()) cudaMemcpy(in[q].data(), dr + roff[q], in[q].size(), cudaMemcpyDeviceToHost);
+        }
+        cudaFree(ds);
+        cudaFree(dr);
+        if (!nok) return fail("ncclSend/ncclRecv (setup payload)");
+        return true;
+    }
+};
+
+// The INVK factors of a rank's plan (smoother == 1 / the coarse CG's HINVK): block-diagonal over
+// the ranks (HINVK / l1-INVK), so a distributed level factors its own diagonal
+// block (its rows, its columns) and a replicated level the whole level with the owners' blocks --
+// the same numbers as invk_build on the whole hierarchy sliced by partition().
+int plan_invk(const amg_config_t& cfg, amgsetup::RankPlan& P, const std::vector<std::vector<int64_t>>& bounds,
+              const LevelStats& S) {
+    const int nl = (int)P.lv.size();
+    const bool smooth = cfg.smoother == 1, coarse = cfg.coarse_solver == 1 && cfg.coarse_prec == 1;
+    for (int l = 0; l < nl; ++l) {
+        if (l == nl - 1 ? !coarse : !smooth) continue;
+        amgsetup::RankLevel& L = P.lv[l];
+        const int f = (cfg.invk_dense_cut > 0 && (double)S.nnzA[l] > (double)cfg.invk_dense_cut * (double)S.n[l])
+                          ? 0 : cfg.invk_fill;
+        if (L.replicated) {  // win = [0, n): global frame; blocks = the owners of this level
+            std::vector<int32_t> own(L.n_global);
+            for (size_t g = 0; g + 1 < bounds[l].size(); ++g)
+                for (int64_t i = bounds[l][g]; i < bounds[l][g + 1]; ++i) own[i] = (int32_t)g;
+            const amgsetup::Csr B = amgsetup::block_diagonal_part(L.A, bounds[l].size() > 2 ? own : std::vector<int32_t>(),
+                                                                  cfg.invk_l1 == 1);
+            if (!amgsetup::invk_factors(B, f, L.Wd, L.Z)) return AMG_ERR_NOT_SPD;
+            continue;
+        }
+        // own diagonal block in local indices (window columns [o0, o1) are the owned rows)
+        const int64_t n = L.own_end - L.own_begin, o0 = L.own_begin - L.win_begin, o1 = o0 + n;
+        amgsetup::Csr B;
+        B.nrows = B.ncols = n;
+        B.rp.assign(n + 1, 0);
+        for (int64_t r = 0; r < n; ++r) {
+            double dl1 = 0.0;
+            if (cfg.invk_l1 == 1)
+                for (int64_t k = L.A.rp[r]; k < L.A.rp[r + 1]; ++k)
+                    if (L.A.ci[k] < o0 || L.A.ci[k] >= o1) dl1 = dl1 + std::fabs(L.A.v[k]);
+            for (int64_t k = L.A.rp[r]; k < L.A.rp[r + 1]; ++k) {
+                const int64_t cc = L.A.ci[k];
+                if (cc < o0 || cc >= o1) continue;
+                B.ci.push_back((int32_t)(cc - o0));
+                B.v.push_back((cfg.invk_l1 == 1 && cc - o0 == r) ? L.A.v[k] + dl1 : L.A.v[k]);
+            }
+            B.rp[r + 1] = (int64_t)B.ci.size();
+        }
+        amgsetup::Csr Wd, Z;
+        if (!amgsetup::invk_factors(B, f, Wd, Z)) return AMG_ERR_NOT_SPD;
+        for (amgsetup::Csr* M : {&Wd, &Z}) {
+            for (auto& cc : M->ci) cc = (int32_t)(cc + o0);
+            M->ncols = L.win_end - L.win_begin;
+        }
+        L.Wd = std::move(Wd);
+        L.Z = std::move(Z);
+    }
+    return AMG_OK;
+}
+
+struct DistOut {
+    amgsetup::RankPlan plan;
+    std::vector<double> cinv;
+    std::vector<std::vector<int32_t>> agg;  // owned rows of every non-coarsest level
+    LevelStats S;
+    int st = AMG_OK;
+    std::string err;
+};
+
+// One rank of the distributed setup: validation, build, plan, INVK factors, statistics.
+void dist_rank(amgsetup::Comm& c, const amg_config_t& cfg, const std::vector<int64_t>& b0, amgsetup::Csr&& Al,
+               std::vector<double>&& wl, bool validate, DistOut& o) {
+    if (validate) {
+        const int v = amgsetup::validate_distributed(c, b0, Al, wl, o.err);
+        if (v != amgsetup::SETUP_OK) {
+            o.st = v == amgsetup::SETUP_ERR_ARG ? AMG_ERR_ARG : AMG_ERR_NOT_SPD;
+            return;
+        }
+    }
+    amgsetup::DistHierarchy H;
+    const int st = amgsetup::build_distributed(c, b0, std::move(Al), std::move(wl), setup_config(cfg), H, o.err);
+    if (st != amgsetup::SETUP_OK) {
+        o.st = st == amgsetup::SETUP_ERR_ARG ? AMG_ERR_ARG : AMG_ERR_NOT_SPD;
+        return;
+    }
+    const int nl = (int)H.lv.size();
+    std::vector<std::vector<int64_t>> bounds;
+    for (auto& L : H.lv) {
+        o.S.n.push_back(L.n);
+        o.S.nnzA.push_back(L.nnzA);
+        o.S.nnzP.push_back(L.nnzP);
+        bounds.push_back(L.bounds);
+    }
+    for (int l = 0; l + 1 < nl; ++l) o.agg.push_back(H.lv[l].agg);
+    o.cinv = H.coarse_inv;
+    if (!amgsetup::partition_distributed(c, H, cfg.replicate_below_bytes, o.plan, o.err)) {
+        o.st = AMG_ERR_ARG;
+        return;
+    }
+    const int ist = plan_invk(cfg, o.plan, bounds, o.S);
+    if (amgsetup::comm_allreduce_sum(c, ist ? 1 : 0)) {  // collective: every rank stops
+        o.st = AMG_ERR_NOT_SPD;
+        o.err = "INVK: non-positive IC(0) pivot";
+        return;
+    }
+    // global nnz of the INVK factors (replicated levels: every rank holds all rows, count once)
+    o.S.nnzWZ.assign(nl, 0);
+    for (int l = 0; l < nl; ++l) {
+        const auto& L = o.plan.lv[l];
+        const int64_t mine = L.replicated ? (c.rank() == 0 ? L.Wd.nnz() + L.Z.nnz() : 0) : L.Wd.nnz() + L.Z.nnz();
+        o.S.nnzWZ[l] = amgsetup::comm_allreduce_sum(c, mine);
+    }
+}
+
+// amg_hierarchy_build's distributed path: loopback (one process, np threads) or NCCL ranks.
+int build_dist_path(amg_hier_s* h, amg_ctx_s* ctx, const amg_config_t& cfg, int64_t n_global, int64_t row_begin,
+                    int64_t row_end, const int64_t* rowptr, const int64_t* colind, const double* values,
+                    const double* w) {
+    const int np = h->np;
+    auto to_local = [&](int64_t r0, int64_t r1, int64_t base, amgsetup::Csr& A, std::vector<double>& wl) -> bool {
+        A.nrows = r1 - r0;
+        A.ncols = n_global;
+        A.rp.resize(A.nrows + 1);
+        const int64_t k0 = rowptr[r0 - base];
+        for (int64_t i = 0; i <= A.nrows; ++i) A.rp[i] = rowptr[r0 - base + i] - k0;
+        const int64_t nnz = A.rp[A.nrows];
+        A.ci.resize(nnz);
+        A.v.assign(values + k0, values + k0 + nnz);
+        bool ok = true;
+        for (int64_t k = 0; k < nnz; ++k) {
+            const int64_t cc = colind[k0 + k];
+            ok &= (cc >= 0 && cc < n_global);
+            A.ci[k] = (int32_t)cc;
+        }
+        wl.assign(A.nrows, 1.0);
+        if (w) std::copy(w + (r0 - base), w + (r1 - base), wl.begin());
+        return ok;
+    };
+    std::vector<DistOut> outs;
+    if (h->loopback) {
+        if (rowptr[0] != 0) {
+            set_err("amg_hierarchy_build: rowptr[0] must be 0");
+            return AMG_ERR_ARG;
+        }
+        std::vector<int64_t> b0(np + 1);
+        for (int g = 0; g <= np; ++g) b0[g] = n_global * g / np;
+        outs.resize(np);
+        std::vector<char> okc(np, 1);
+        amgsetup::run_loopback(np, [&](amgsetup::Comm& c) {
+            const int r = c.rank();
+            amgsetup::Csr A;
+            std::vector<double> wl;
+            okc[r] = to_local(b0[r], b0[r + 1], 0, A, wl);
+            dist_rank(c, cfg, b0, std::move(A), std::move(wl), true, outs[r]);
+        });
+        for (int r = 0; r < np; ++r)
+            if (!okc[r] || outs[r].st != AMG_OK) {
+                set_err("amg_hierarchy_build (distributed setup, rank " + std::to_string(r) +
+                        "): " + (okc[r] ? outs[r].err : std::string("column index out of range")));
+                return okc[r] ? outs[r].st : AMG_ERR_ARG;
+            }
+    } else {
+        NcclComm c;
+        c.c = ctx;
+        std::vector<int64_t> mine{row_begin, row_end};
+        // the row blocks of all ranks (rank order, contiguous, covering [0, n))
+        std::vector<std::vector<char>> out(np), in;
+        for (int q = 0; q < np; ++q) {
+            out[q].resize(16);
+            std::memcpy(out[q].data(), mine.data(), 16);
+        }
+        c.alltoallv(out, in);
+        if (!c.ok) {
+            set_err("amg_hierarchy_build: " + c.what);
+            return AMG_ERR_NCCL;
+        }
+        std::vector<int64_t> b0(np + 1, 0);
+        bool okb = true;
+        for (int q = 0; q < np; ++q) {
+            int64_t rb, re;
+            std::memcpy(&rb, in[q].data(), 8);
+            std::memcpy(&re, in[q].data() + 8, 8);
+            okb &= (rb == b0[q] && re >= rb);
+            b0[q + 1] = re;
+        }
+        if (!okb || b0[np] != n_global) {
+            set_err("amg_hierarchy_build: row blocks must be contiguous, in rank order and cover [0, n_global)");
+            return AMG_ERR_ARG;
+        }
+        if (rowptr[0] != 0) {
+            set_err("amg_hierarchy_build: rowptr[0] must be 0");
+            return AMG_ERR_ARG;
+        }
+        amgsetup::Csr A;
+        std::vector<double> wl;
+        if (!to_local(row_begin, row_end, row_begin, A, wl)) {
+            set_err("amg_hierarchy_build: column index out of range");
+            return AMG_ERR_ARG;
+        }
+        outs.resize(1);
+        dist_rank(c, cfg, b0, std::move(A), std::move(wl), true, outs[0]);
+        if (!c.ok) {
+            set_err("amg_hierarchy_build (distributed setup): " + c.what);
+            return AMG_ERR_NCCL;
+        }
+        if (outs[0].st != AMG_OK) {
+            set_err("amg_hierarchy_build (distributed setup): " + outs[0].err);
+            return outs[0].st;
+        }
+    }
+    amgsetup::tmark("distributed setup + plans");
+    hier_stats(h, outs[0].S);
+    const int nl = (int)outs[0].S.n.size();
+    h->ranks.resize(outs.size());
+    int st;
+    for (size_t g = 0; g < outs.size(); ++g)
+        if ((st = upload_rank(h, outs[g].plan, outs[g].cinv, h->ranks[g]))) return st;
+    amgsetup::tmark("device formats + upload");
+    h->agg.assign(nl > 0 ? nl - 1 : 0, {});
+    for (int l = 0; l + 1 < nl; ++l)
+        for (auto& o : outs) h->agg[l].insert(h->agg[l].end(), o.agg[l].begin(), o.agg[l].end());
+    if (h->loopback) {
+        for (size_t g = 0; g < outs.size(); ++g) h->ranks[g].user_off = outs[g].plan.lv[0].own_begin;
+        h->lvl_own_begin.assign(nl, 0);
+        h->lvl_own_end = h->lvl_n;
+        h->n0_local = n_global;
+    } else {
+        h->ranks[0].user_off = 0;
+        for (auto& L : outs[0].plan.lv) {
+            h->lvl_own_begin.push_back(L.own_begin);
+            h->lvl_own_end.push_back(L.own_end);
+        }
+        h->n0_local = row_end - row_begin;
+    }
+    for (int l = 0; l < nl; ++l)
+        h->lvl_fmt.push_back(l + 1 < nl ? (h->ranks[0].lv[l].A.perm ? FMT_SELL_SIGMA : h->ranks[0].lv[l].A.fmt)
+                                        : FMT_DENSE);
+    return AMG_OK;
+}
+
 }  // namespace
 
 // ===================================================================== ABI
@@ -2911,6 +3222,7 @@ void amg_config_default(amg_config_t* c) {
     c->invk_blocks = 0;
     c->invk_dense_cut = 0;
     c->coarse_prec = 0;
+    c->setup_distributed = -1;
 }
 
 int amg_nccl_unique_id(void* out128) {
@@ -3028,7 +3340,12 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         return code;
     };
     int st = AMG_OK;
-    if (nr == 1) {
+    // the distributed setup (NEXT-1): default for NCCL contexts, opt-in for loopback
+    const bool dist_setup = np > 1 && (cfg.setup_distributed == 1 || (cfg.setup_distributed < 0 && nr > 1));
+    if (dist_setup) {
+        if ((st = build_dist_path(h, ctx, cfg, n_global, row_begin, row_end, rowptr, colind, values, w)))
+            return fail(st);
+    } else if (nr == 1) {
         amgsetup::Hierarchy H;
         // one process, l1-Jacobi: a GPU-built hierarchy stays on the device (formats converted there)
         H.keep_device = (np == 1 && cfg.smoother == 0 && !(cfg.coarse_solver == 1 && cfg.coarse_prec == 1));
@@ -3729,6 +4046,119 @@ int amg_host_dist_build(int64_t n, const int64_t* rowptr, const int64_t* colind,
     }
     h->H.coarse_inv = DH[0].coarse_inv;
     h->plans = std::move(plans);
+    *out = h;
+    return AMG_OK;
+}
+
+namespace {
+// A caller-supplied transport (amg_exchange_fn): counts, then payloads concatenated in rank order.
+struct CallbackComm : amgsetup::Comm {
+    amg_exchange_fn fn = nullptr;
+    void* user = nullptr;
+    int me = 0, np = 1;
+    bool ok = true;
+    int rank() const override { return me; }
+    int size() const override { return np; }
+    bool alltoallv(const std::vector<std::vector<char>>& out, std::vector<std::vector<char>>& in) override {
+        in.assign(np, {});
+        if (!ok) return false;
+        std::vector<int64_t> sc(np), rc(np, 0);
+        int64_t stot = 0, rtot = 0;
+        for (int q = 0; q < np; ++q) stot += (sc[q] = (int64_t)out[q].size());
+        if (fn(user, 0, sc.data(), rc.data(), nullptr, nullptr) != 0) return ok = false;
+        for (int q = 0; q < np; ++q) rtot += rc[q];
+        std::vector<char> sb((size_t)std::max<int64_t>(stot, 1)), rb((size_t)std::max<int64_t>(rtot, 1));
+        int64_t o = 0;
+        for (int q = 0; q < np; ++q) {
+            if (sc[q]) std::memcpy(sb.data() + o, out[q].data(), sc[q]);
+            o += sc[q];
+        }
+        if (fn(user, 1, sc.data(), rc.data(), sb.data(), rb.data()) != 0) return ok = false;
+        o = 0;
+        for (int q = 0; q < np; ++q) {
+            in[q].assign(rb.data() + o, rb.data() + o + rc[q]);
+            o += rc[q];
+        }
+        return true;
+    }
+};
+}  // namespace
+
+int amg_host_dist_build_rank(int64_t n, int64_t row_begin, int64_t row_end, const int64_t* rowptr,
+                             const int64_t* colind, const double* values, const double* w, const amg_config_t* cfg_in,
+                             int32_t nranks, int32_t rank, int64_t replicate_below_bytes, amg_exchange_fn exchange,
+                             void* user, amg_host_hier_t* out) {
+    if (!out || !exchange || nranks < 1 || rank < 0 || rank >= nranks || !rowptr || !colind || !values || n <= 0 ||
+        n >= (int64_t)INT32_MAX || row_begin < 0 || row_end < row_begin || row_end > n || rowptr[0] != 0) {
+        set_err("amg_host_dist_build_rank: bad argument");
+        return AMG_ERR_ARG;
+    }
+    *out = nullptr;
+    amg_config_t cfg;
+    amg_config_default(&cfg);
+    if (cfg_in) cfg = *cfg_in;
+    CallbackComm c;
+    c.fn = exchange;
+    c.user = user;
+    c.me = rank;
+    c.np = nranks;
+    // the row blocks of all ranks (contiguous, in rank order, covering [0, n))
+    std::vector<std::vector<char>> ob(nranks, std::vector<char>(16)), ib;
+    for (auto& b : ob) {
+        std::memcpy(b.data(), &row_begin, 8);
+        std::memcpy(b.data() + 8, &row_end, 8);
+    }
+    c.alltoallv(ob, ib);
+    std::vector<int64_t> b0(nranks + 1, 0);
+    bool okb = c.ok;
+    for (int q = 0; q < nranks && okb; ++q) {
+        int64_t rb, re;
+        std::memcpy(&rb, ib[q].data(), 8);
+        std::memcpy(&re, ib[q].data() + 8, 8);
+        okb &= (rb == b0[q] && re >= rb);
+        b0[q + 1] = re;
+    }
+    if (!okb || b0[nranks] != n) {
+        set_err(c.ok ? "amg_host_dist_build_rank: row blocks must be contiguous, in rank order and cover [0, n)"
+                     : "amg_host_dist_build_rank: exchange callback failed");
+        return c.ok ? AMG_ERR_ARG : AMG_ERR_NCCL;
+    }
+    amgsetup::Csr A;
+    A.nrows = row_end - row_begin;
+    A.ncols = n;
+    A.rp.assign(rowptr, rowptr + A.nrows + 1);
+    A.ci.resize(rowptr[A.nrows]);
+    for (int64_t k = 0; k < rowptr[A.nrows]; ++k) {
+        if (colind[k] < 0 || colind[k] >= n) {
+            set_err("amg_host_dist_build_rank: column index out of range");
+            return AMG_ERR_ARG;
+        }
+        A.ci[k] = (int32_t)colind[k];
+    }
+    A.v.assign(values, values + rowptr[A.nrows]);
+    std::vector<double> wl(A.nrows, 1.0);
+    if (w) std::copy(w, w + A.nrows, wl.begin());
+    cfg.replicate_below_bytes = replicate_below_bytes;
+    DistOut o;
+    dist_rank(c, cfg, b0, std::move(A), std::move(wl), true, o);
+    if (!c.ok) {
+        set_err("amg_host_dist_build_rank: exchange callback failed");
+        return AMG_ERR_NCCL;
+    }
+    if (o.st != AMG_OK) {
+        set_err("amg_host_dist_build_rank: " + o.err);
+        return o.st;
+    }
+    auto* h = new amg_host_hier_s();
+    h->plans.resize(nranks);
+    h->plans[rank] = std::move(o.plan);
+    h->H.lv.resize(o.S.n.size());
+    for (size_t l = 0; l < o.S.n.size(); ++l) {
+        h->H.lv[l].A.nrows = o.S.n[l];  // sizes only: the rank holds its own rows (see the plan)
+        h->H.lv[l].A.rp.assign(1, 0);
+        if (l + 1 < o.S.n.size()) h->H.lv[l].agg = o.agg[l];
+    }
+    h->H.coarse_inv = std::move(o.cinv);
     *out = h;
     return AMG_OK;
 }

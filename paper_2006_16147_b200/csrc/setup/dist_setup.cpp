@@ -1121,6 +1121,103 @@ bool partition_distributed(Comm& c, const DistHierarchy& H, int64_t rep_bytes, R
     return true;
 }
 
+
+// ====================================================================== validation
+int validate_distributed(Comm& c, const std::vector<int64_t>& bounds, const Csr& A, const std::vector<double>& w,
+                         std::string& err) {
+    const int me = c.rank(), np = c.size();
+    const int64_t b0 = bounds[me], b1 = bounds[me + 1], n = bounds[np];
+    int bad = 0;
+    int64_t badrow = -1;
+    std::vector<std::vector<int64_t>> req(np), got;
+    auto lookup = [&](int64_t row, int64_t col, double& v) {
+        const int64_t r = row - b0;
+        const int32_t* b = A.ci.data() + A.rp[r];
+        const int32_t* e = A.ci.data() + A.rp[r + 1];
+        const int32_t* p = std::lower_bound(b, e, (int32_t)col);
+        if (p != e && *p == col) {
+            v = A.v[p - A.ci.data()];
+            return true;
+        }
+        return false;
+    };
+    for (int64_t r = 0; r < A.nrows && bad < 3; ++r) {
+        const int64_t i = b0 + r;
+        bool has_d = false;
+        for (int64_t k = A.rp[r]; k < A.rp[r + 1]; ++k) {
+            const int64_t col = A.ci[k];
+            if (col < 0 || col >= n || (k > A.rp[r] && col <= A.ci[k - 1])) {
+                bad = 3;
+                badrow = i;
+                break;
+            }
+            if (col == i) {
+                has_d = true;
+                if (!(A.v[k] > 0.0)) bad = std::max(bad, 1), badrow = i;
+            }
+            if (col >= b0 && col < b1) {
+                double t;
+                if (!lookup(col, i, t) || t != A.v[k]) bad = std::max(bad, 2), badrow = i;
+            } else {
+                const int o = owner_of(bounds, col);
+                req[o].push_back(col);
+                req[o].push_back(i);
+            }
+        }
+        if (!has_d && bad < 3) bad = std::max(bad, 1), badrow = i;
+    }
+    // the transposed entries of the off-rank couplings, answered by their owners
+    std::vector<std::vector<double>> ans(np), vals;
+    std::vector<std::vector<int64_t>> hit(np), hits;
+    a2a_vec(c, req, got);
+    for (int q = 0; q < np; ++q)
+        for (size_t k = 0; k + 1 < got[q].size(); k += 2) {
+            double v = 0.0;
+            const bool f = got[q][k] >= b0 && got[q][k] < b1 && lookup(got[q][k], got[q][k + 1], v);
+            ans[q].push_back(v);
+            hit[q].push_back(f ? 1 : 0);
+        }
+    a2a_vec(c, ans, vals);
+    a2a_vec(c, hit, hits);
+    if (bad < 3) {
+        std::vector<size_t> pos(np, 0);
+        for (int64_t r = 0; r < A.nrows; ++r)
+            for (int64_t k = A.rp[r]; k < A.rp[r + 1]; ++k) {
+                const int64_t col = A.ci[k];
+                if (col >= b0 && col < b1) continue;
+                const int o = owner_of(bounds, col);
+                const size_t p = pos[o]++;
+                if (!hits[o][p] || vals[o][p] != A.v[k]) bad = std::max(bad, 2), badrow = b0 + r;
+            }
+    }
+    int64_t anyw = 0;
+    for (double x : w) anyw |= (x != 0.0);
+    const std::vector<int64_t> bads = allgatherv(c, std::vector<int64_t>{bad, badrow});
+    int worst = 0;
+    int64_t wrow = -1;
+    for (int q = 0; q < np; ++q)
+        if (bads[2 * q] > worst) worst = (int)bads[2 * q], wrow = bads[2 * q + 1];
+    if (worst == 3) {
+        err = "column indices must be in range and strictly ascending (row " + std::to_string(wrow) + ")";
+        return SETUP_ERR_ARG;
+    }
+    if (worst == 2) {
+        err = "matrix is not exactly symmetric (row " + std::to_string(wrow) + ")";
+        return SETUP_ERR_ARG;
+    }
+    if (worst == 1) {
+        err = "non-positive or missing diagonal (row " + std::to_string(wrow) + ")";
+        return SETUP_ERR_NOT_SPD;
+    }
+    if (allreduce_sum(c, anyw) == 0) {
+        err = "weight vector w is identically zero";
+        return SETUP_ERR_NOT_SPD;
+    }
+    return SETUP_OK;
+}
+
+int64_t comm_allreduce_sum(Comm& c, int64_t v) { return allreduce_sum(c, v); }
+
 // ====================================================================== loopback transport
 namespace {
 struct Hub {

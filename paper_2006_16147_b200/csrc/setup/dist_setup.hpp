@@ -70,6 +70,12 @@ int build_distributed(Comm& comm, const std::vector<int64_t>& bounds0, Csr&& A_l
 bool partition_distributed(Comm& comm, const DistHierarchy& H, int64_t replicate_bytes, RankPlan& plan,
                            std::string& err);
 
+// The checks of validate() on a row-distributed matrix (symmetry through the owners of the
+// off-rank couplings); the same error on every rank.
+int validate_distributed(Comm& comm, const std::vector<int64_t>& bounds, const Csr& A_loc,
+                         const std::vector<double>& w_loc, std::string& err);
+int64_t comm_allreduce_sum(Comm& comm, int64_t v);
+
 // Runs fn(comm) on nranks threads of this process, each with its own LoopbackComm.
 void run_loopback(int nranks, const std::function<void(Comm&)>& fn);
 

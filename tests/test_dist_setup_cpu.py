@@ -9,6 +9,7 @@ aggregate map and omega, and every rank's plan (windows, halo lists, local opera
 frames, l1 diagonal) -- and hence, by the single build's tests, the oracle's aggregate maps.
 """
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -156,3 +157,116 @@ def test_distributed_build_rejects_bad_input():
     A.values[1] = -2.0   # asymmetric
     with pytest.raises(amg.AmgError):
         _build(A, amg.make_config(setup_device=0), nranks=2)
+
+
+# ------------------------------------------------------------ one process per rank (gloo)
+def _gloo_rank(rank, world, port, q):
+    """One rank of the distributed setup in its own process, the transport being
+    torch.distributed all_to_all over gloo; compares its plan with partition() of the
+    single-process build of the same matrix (each process builds that reference itself)."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        amg = _amg()
+        A, kw, w = _case("c5_jump27_24")
+        cfg = amg.make_config(setup_device=0, **kw)
+        n = A.n_global
+        b = [n * g // world for g in range(world + 1)]
+        r0, r1 = b[rank], b[rank + 1]
+        rp = np.ascontiguousarray(A.rowptr[r0:r1 + 1] - A.rowptr[r0], np.int64)
+        ci = np.ascontiguousarray(A.colind[A.rowptr[r0]:A.rowptr[r1]], np.int64)
+        v = np.ascontiguousarray(A.values[A.rowptr[r0]:A.rowptr[r1]], np.float64)
+        state = {}
+
+        def exchange(user, phase, sc, rc, sbuf, rbuf):
+            try:
+                if phase == 0:
+                    send = torch.tensor([sc[k] for k in range(world)], dtype=torch.int64)
+                    recv = torch.zeros(world, dtype=torch.int64)
+                    dist.all_to_all_single(recv, send)
+                    for k in range(world):
+                        rc[k] = int(recv[k])
+                    state["sc"], state["rc"] = send.tolist(), recv.tolist()
+                else:
+                    ns, nr = sum(state["sc"]), sum(state["rc"])
+                    send = torch.frombuffer(C.string_at(sbuf, ns), dtype=torch.uint8) if ns else \
+                        torch.zeros(0, dtype=torch.uint8)
+                    recv = torch.zeros(nr, dtype=torch.uint8)
+                    dist.all_to_all_single(recv, send, output_split_sizes=state["rc"],
+                                           input_split_sizes=state["sc"])
+                    if nr:
+                        C.memmove(rbuf, recv.numpy().ctypes.data, nr)
+                return 0
+            except Exception as e:  # pragma: no cover - reported through the status code
+                state["err"] = repr(e)
+                return 1
+
+        cb = amg._abi.EXCHANGE_FN(exchange)
+        h = C.c_void_p()
+        code = amg.lib.amg_host_dist_build_rank(n, r0, r1, C.c_void_p(rp.ctypes.data), C.c_void_p(ci.ctypes.data),
+                                                C.c_void_p(v.ctypes.data), None, C.byref(cfg), world, rank, 0,
+                                                C.cast(cb, C.c_void_p), None, C.byref(h))
+        assert code == 0, (amg.amg_last_error(), state.get("err"))
+        hs = _build(A, cfg)
+        bb = np.array(b, np.int64)
+        amg.check(amg.lib.amg_host_partition(hs, world, C.c_void_p(bb.ctypes.data), 0), "partition")
+        nl = len(_levels(hs))
+        mine = _plans_of_rank(h, rank, world, nl)
+        ref = _plans_of_rank(hs, rank, world, nl)
+        same = all(np.array_equal(p.view(np.int64) if p.dtype == np.float64 else p,
+                                  r.view(np.int64) if r.dtype == np.float64 else r)
+                   for x, y in zip(mine, ref) for p, r in zip(x, y))
+        q.put((rank, same, nl))
+    finally:
+        dist.destroy_process_group()
+
+
+def _plans_of_rank(h, r, nr, nl):
+    return _plans_one(h, r, nr, nl)
+
+
+def _plans_one(h, r, nr, nl):
+    amg = _amg()
+    out = []
+    for l in range(nl):
+        info = np.zeros(16, np.int64)
+        amg.check(amg.lib.amg_host_plan_level(h, r, l, C.c_void_p(info.ctypes.data)), "plan level")
+        rec = [info.copy()]
+        win, comp, rst = info[7] - info[6], info[5] - info[4], info[9] - info[8]
+        sizes = {0: nr + 1, 1: info[10], 2: nr + 1, 3: info[11], 4: comp + 1, 5: info[12], 6: info[12],
+                 7: comp + 1, 8: info[13], 9: info[13], 10: rst + 1, 11: info[14], 12: info[14], 13: win}
+        for which in range(14):
+            if which in (7, 8, 9, 10, 11, 12) and l == nl - 1:
+                continue
+            dt = np.float64 if which in (6, 9, 12, 13) else np.int64
+            a = np.zeros(max(1, int(sizes[which])), dt)
+            amg.check(amg.lib.amg_host_plan_array(h, r, l, which, C.c_void_p(a.ctypes.data)), "plan array")
+            rec.append(a)
+        out.append(rec)
+    return out
+
+
+@pytest.mark.slow
+def test_gloo_world2_distributed_setup_equals_partition():
+    """Two processes (torch.distributed over gloo): each builds only its own rows and plan through
+    amg_host_dist_build_rank; both plans equal partition() of the single-process build bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[0] for r in res] == [0, 1] and all(r[1] for r in res) and res[0][2] >= 3

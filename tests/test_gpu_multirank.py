@@ -171,3 +171,32 @@ def test_loopback_replicated_levels_run_the_single_rank_fused_forms(ctx):
     x, _ = h.solve(bt, rtol=0.0, maxit=k)
     xo, _ = ho.pcg(b, rtol=0.0, maxit=k)
     assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("np_,extra", [(2, {}), (4, dict(replicate_below_bytes=0)), (3, dict(smoother=1)),
+                                       (2, dict(smooth_prolongator=0, cycle=1, krylov=1)),
+                                       (2, dict(smoother=1, invk_l1=1, krylov=1, coarse_solver=1, coarse_prec=1,
+                                                max_coarse_size=2400))])
+def test_distributed_setup_solves_exactly_like_the_gathered_setup(ctx, np_, extra):
+    """setup_distributed = 1 (NEXT-1): every rank builds only its rows and its own plan (loopback:
+    np threads of this process with an in-process transport).  The plans are bit-identical to
+    the gathered build's (tests/test_dist_setup_cpu.py), so the solves are bitwise equal; the
+    aggregate maps equal the oracle's.  Covers HINVK / l1-INVK factors built per rank and the
+    K-cycle on the distributed hierarchy."""
+    import paper_2006_16147_b200 as amg
+    A, b, _ = config_problem(4, grid=(32, 32, 96))
+    bt = torch.tensor(b, device="cuda:0")
+    kw = dict(emulate_ranks=np_, **extra)
+    hg = amg.Hierarchy(ctx, A, cfg=amg.make_config(setup_distributed=0, **kw))
+    hd = amg.Hierarchy(ctx, A, cfg=amg.make_config(setup_distributed=1, **kw))
+    assert hd.sizes() == hg.sizes()
+    okw = {k: v for k, v in extra.items() if k in ("smooth_prolongator", "max_coarse_size")}
+    ho = O.OracleHierarchy(A, **okw)
+    for l in range(hd.nlevels - 1):
+        assert np.array_equal(hd.level_aggregates(l), ho.agg(l)), l
+    assert hd.report()["opc"] == hg.report()["opc"]
+    xg, rg = hg.solve(bt)
+    xd, rd = hd.solve(bt)
+    assert rg["iterations"] == rd["iterations"] and torch.equal(xg, xd)
+    r = torch.tensor(uniform_pm1(31, A.n_global), device="cuda:0")
+    assert torch.equal(hg.precond_apply(r), hd.precond_apply(r))
