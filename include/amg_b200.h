@@ -181,6 +181,7 @@ int amg_nccl_unique_id(void* out128);
  * AMG_ERR_NCCL when the device or communicator cannot be initialised. */
 int amg_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
                    void* cuda_stream, amg_ctx_t* out);
+/* Destroy the hierarchies built on a context before the context itself. */
 int amg_ctx_destroy(amg_ctx_t ctx);
 
 /* Builds the hierarchy for the s.p.d. matrix A.

@@ -266,6 +266,7 @@ struct amg_ctx_s {
 
 struct amg_hier_s {
     amg_ctx_s* ctx = nullptr;
+    int device = 0;  // the context's device, kept for amg_hierarchy_destroy
     amg_config_t cfg{};
     int np = 1;                 // ranks of the partition
     bool loopback = false;      // all ranks in this process (emulate_ranks)
@@ -3332,6 +3333,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     const int np = nr > 1 ? nr : std::max(1, cfg.emulate_ranks);
     auto* h = new amg_hier_s();
     h->ctx = ctx;
+    h->device = ctx->device;
     h->cfg = cfg;
     h->np = np;
     h->loopback = (nr == 1 && np > 1);
@@ -3568,8 +3570,11 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
 
 int amg_hierarchy_destroy(amg_hier_t h) {
     if (h) {
-        cudaSetDevice(h->ctx->device);
+        // h->ctx may already be destroyed (a caller error the Python binding can hit at garbage
+        // collection): use the device recorded at build time, and leave no error behind
+        cudaSetDevice(h->device);
         delete h;
+        cudaGetLastError();
     }
     return AMG_OK;
 }

@@ -842,6 +842,9 @@ void DeviceKeep::free_all() {
 // Full GPU build with the same results as amgsetup::build (validated input A0 on the
 // host; the hierarchy is copied back into `out` for partitioning / format upload).
 int build_gpu(Csr&& A0, std::vector<double>&& w0, const Config& cfg, Hierarchy& out, std::string& err) {
+    // a non-sticky error left by an unrelated earlier runtime call of this thread would be
+    // reported by the first CUB call below (CUB peeks at the last error): clear it first
+    cudaGetLastError();
     cudaStream_t s;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
         err = "build_gpu: cudaStreamCreate failed";
