@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libamg_b200.so")
+LIB_PATH = os.environ.get("AMG_LIB_PATH") or os.path.join(_HERE, "libamg_b200.so")  # override: experiments
 
 AMG_OK, AMG_ERR_ARG, AMG_ERR_NOT_SPD, AMG_ERR_CUDA, AMG_ERR_NCCL, AMG_ERR_OOM = 0, 1, 2, 3, 4, 5
 AMG_NOT_CONVERGED, AMG_ERR_BREAKDOWN = 6, 7

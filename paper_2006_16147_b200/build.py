@@ -13,8 +13,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libamg_b200.so")
+# AMG_BUILD_VARIANT=<name> (experiments only): extra -D flags from AMG_BUILD_DEFS, a separate build
+# directory and libamg_b200_<name>.so, loaded when AMG_LIB_PATH points at it (_abi.py)
+VARIANT = os.environ.get("AMG_BUILD_VARIANT", "")
+DEFS = os.environ.get("AMG_BUILD_DEFS", "").split() if VARIANT else []
+BUILD = os.path.join(PKG, "_build" + ("_" + VARIANT if VARIANT else ""))
+LIB = os.path.join(PKG, "libamg_b200" + ("_" + VARIANT if VARIANT else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -57,7 +61,7 @@ def build_library(force: bool = False, verbose_ptxas: bool = False) -> str:
     for src in SOURCES_CU + SOURCES_CU_NOFMA:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         if force or _stale(obj, [src] + HEADERS):
-            cmd = [NVCC] + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-I", os.path.join(_nccl_dir(), "include"),
+            cmd = [NVCC] + ARCH + DEFS + ["-O3", "-lineinfo", "-std=c++17", "-I", os.path.join(_nccl_dir(), "include"),
                                    "-Xcompiler",
                                    "-fPIC,-fopenmp,-ffp-contract=off", "-c", src, "-o", obj]
             if src in SOURCES_CU_NOFMA:

@@ -742,8 +742,23 @@ __device__ __forceinline__ void slice_row(const double* v, uint32_t w, const Col
     }
 }
 
+// Resident 256-thread blocks per SM the SELL / SDIA kernels are compiled for: 8 (32 registers)
+// keeps 64 warps in flight; the fused direction update of q = A p (two gathered vectors, three
+// written) spills at 32 registers, so it may trade occupancy for no spills (AMG_PUPD_MINB).
+#ifndef AMG_PUPD_MINB
+#define AMG_PUPD_MINB 8
+#endif
 template <class G, class E>
-__global__ void __launch_bounds__(kBlock, 8) k_sell(SellView A, G g, E e, RedCtx rc) {
+struct MinBlocks {
+    static constexpr int v = 8;
+};
+template <>
+struct MinBlocks<GPz, ESpmvDotPz> {
+    static constexpr int v = AMG_PUPD_MINB;
+};
+
+template <class G, class E>
+__global__ void __launch_bounds__(kBlock, MinBlocks<G, E>::v) k_sell(SellView A, G g, E e, RedCtx rc) {
     pdl_begin();
     bind(g);
     bind(e);
@@ -782,7 +797,7 @@ struct SdiaView {
 };
 
 template <class G, class E>
-__global__ void __launch_bounds__(kBlock, 8) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
+__global__ void __launch_bounds__(kBlock, MinBlocks<G, E>::v) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
     pdl_begin();
     bind(g);
     bind(e);

@@ -18,7 +18,7 @@ AMG_EAGER=1 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.s
     --log-file gpurun_out/prof2_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/prof2_ncu_launch.log 2>&1
 AMG_EAGER=1 timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:k_sdia<GPz' -s 5 -c 1 -o gpurun_out/prof2_full_pupd -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    -k 'regex:k_sdia<amgk::GPz' -s 5 -c 1 -o gpurun_out/prof2_full_pupd -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/prof2_ncu_full.log 2>&1
 ncu -i gpurun_out/prof2_full_pupd.ncu-rep --page raw --csv > gpurun_out/prof2_full_pupd_raw.csv 2>/dev/null
 echo snapshot done
