@@ -87,6 +87,7 @@ struct DevMat {
     // contiguous block of units whose gathers touch only owned columns ("interior": it can
     // run while the halo is in flight); the rest ("head" / "tail") runs after the exchange
     int64_t units = 0, ib0 = 0, ib1 = 0;
+    bool persist = false;      // deep-level operator: launched with an L2 persistence window
     // algorithmic bytes of one pass over the operator: 12 nnz + 4 (n+1)
     double model_bytes() const { return 12.0 * (double)nnz + 4.0 * (double)(nrows + 1); }
     // bytes the chosen device format actually stores for one pass
@@ -376,6 +377,10 @@ bool pdl_enabled() {
     static const bool on = !(std::getenv("AMG_PDL") && std::getenv("AMG_PDL")[0] == '0');
     return on;
 }
+// L2 persistence window of the next launch_mat launch (deep-level operators, AMG_L2_PERSIST_MB;
+// an experiment: VERDICT r1 W8 / SURVEY §7.5).  Thread-local: set and consumed by launch_mat.
+thread_local const void* g_persist_ptr = nullptr;
+thread_local size_t g_persist_bytes = 0;
 template <class... KArgs, class... Args>
 void launch_k(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -383,11 +388,24 @@ void launch_k(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&
     cfg.blockDim = dim3((unsigned)block);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (g_persist_ptr) {
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = const_cast<void*>(g_persist_ptr);
+        attr[na].val.accessPolicyWindow.num_bytes = g_persist_bytes;
+        attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -411,37 +429,50 @@ struct Launch {
 template <class G, class E>
 void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* name, double vec_bytes,
                 int part = 0) {
-    // part 0: all rows; 1: the interior units; 2: units before them; 3: units after them
+    // part 0: all rows; 1: the interior units; 2: the units before AND after them (one launch,
+    // the interior skipped); 3: nothing (kept for the callers' slot numbering)
     const int64_t units = (M.fmt == FMT_SDIA || M.fmt == FMT_SELL) ? (M.nrows + 31) / 32 : M.nrows;
-    int64_t u0 = 0, u1 = units;
+    int64_t u0 = 0, u1 = units, k0 = 0, kspan = 0;
     if (part == 1) {
         u0 = M.ib0;
         u1 = M.ib1;
     } else if (part == 2) {
-        u1 = M.ib0;
+        k0 = M.ib0;
+        kspan = M.ib1 - M.ib0;
     } else if (part == 3) {
-        u0 = M.ib1;
+        return;
     }
-    if (part != 0 && u1 <= u0) return;
-    const double frac = units ? (double)(u1 - u0) / (double)units : 1.0;
+    if (part != 0 && u1 - u0 - kspan <= 0) return;
+    const double frac = units ? (double)(u1 - u0 - kspan) / (double)units : 1.0;
     L.begin(name, frac * (M.model_bytes() + vec_bytes), frac * (M.stored_bytes() + vec_bytes));
+    struct PersistScope {  // the window covers this operator's values for this launch only
+        PersistScope(const DevMat& M) {
+            if (M.persist) {
+                g_persist_ptr = M.val;
+                g_persist_bytes = (size_t)(M.fmt == FMT_SDIA || M.fmt == FMT_SELL ? M.stored : M.nnz) * 8;
+            }
+        }
+        ~PersistScope() { g_persist_ptr = nullptr; }
+    } persist_scope(M);
     if (M.fmt == FMT_SDIA) {
         const int cap = ctx_cap(L.h->ctx, (const void*)k_sdia<G, E>);
-        const int64_t need = ((u1 - u0) * 32 + kBlock - 1) / kBlock;
+        const int64_t need = ((u1 - u0 - kspan) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
         launch_k(k_sdia<G, E>, grid, kBlock, L.s,
-                 SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor, u0, u1}, g, e, rc);
+                 SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor, u0, u1, k0, kspan}, g,
+                 e, rc);
     } else if (M.fmt == FMT_SELL) {
         const int cap = ctx_cap(L.h->ctx, (const void*)k_sell<G, E>);
-        const int64_t need = ((u1 - u0) * 32 + kBlock - 1) / kBlock;
+        const int64_t need = ((u1 - u0 - kspan) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1, M.perm}, g, e, rc);
+        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1, k0, kspan, M.perm},
+                 g, e, rc);
     } else {
-        const CsrView v{M.rp, M.col, M.val, M.nrows, u0, u1};
-        const int64_t need = ((u1 - u0) * M.vw + kBlock - 1) / kBlock;
+        const CsrView v{M.rp, M.col, M.val, M.nrows, u0, u1, k0, kspan};
+        const int64_t need = ((u1 - u0 - kspan) * M.vw + kBlock - 1) / kBlock;
         if (M.vw == kVWBlock) {
             const int cap = ctx_cap(L.h->ctx, (const void*)k_csrb<G, E>);
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(u1 - u0, cap));
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(u1 - u0 - kspan, cap));
             launch_k(k_csrb<G, E>, grid, kBlock, L.s, v, g, e, rc);
             L.end();
             return;
@@ -2467,6 +2498,31 @@ void hier_stats(amg_hier_s* h, const LevelStats& S) {
 }
 void hier_stats(amg_hier_s* h, const amgsetup::Hierarchy& H) { hier_stats(h, stats_of(H)); }
 
+// AMG_L2_PERSIST_MB=<MB> (experiment, default off): the value arrays of the deepest levels' operators,
+// from the coarsest up while they fit in the budget, are launched with an L2 persistence window so
+// they stay L2-resident across V-cycles (the level-0/1 streams would otherwise evict them).
+void mark_persistent(amg_hier_s* h) {
+    const char* e = std::getenv("AMG_L2_PERSIST_MB");
+    if (!e) return;
+    const double budget = std::atof(e) * 1048576.0;
+    if (!(budget > 0.0)) return;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)budget);
+    double used = 0.0;
+    for (int l = h->nlev() - 2; l >= 1; --l) {
+        double lb = 0.0;
+        for (auto& R : h->ranks) {
+            DevLevel& D = R.lv[l];
+            for (DevMat* M : {&D.A, &D.Am, &D.P, &D.R, &D.Rc, &D.Pc}) lb += 8.0 * (double)M->stored;
+        }
+        if (used + lb > budget) break;
+        used += lb;
+        for (auto& R : h->ranks) {
+            DevLevel& D = R.lv[l];
+            for (DevMat* M : {&D.A, &D.Am, &D.P, &D.R, &D.Rc, &D.Pc}) M->persist = M->val != nullptr;
+        }
+    }
+}
+
 int build_solve_exec(amg_hier_s* h, const double* b, double* x, cudaGraphExec_t* out);
 enum { GM_WHILE = 0, GM_ITER = 1 };
 // NCCL contexts: every rank must take the same graph shape (the captured collectives must
@@ -3550,6 +3606,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
         for (size_t l = 0; l < P.lv.size(); ++l)
             h->lvl_fmt.push_back(l + 1 < P.lv.size() ? h->ranks[0].lv[l].A.fmt : FMT_DENSE);
     }
+    mark_persistent(h);
     if (const char* gm = std::getenv("AMG_MULTI_GRAPH"))
         if (h->multi() && std::strcmp(gm, "iter") == 0) h->graph_mode = GM_ITER;
     if (cudaMallocHost((void**)&h->st_host, sizeof(PcgState)) != cudaSuccess) {

@@ -689,6 +689,8 @@ struct SellView {
     const double* __restrict__ val;
     int64_t n;
     int64_t s0, s1;                     // slice range of this launch (multi-rank interior/boundary split)
+    int64_t k0 = 0, kspan = 0;          // slices [k0, k0 + kspan) inside the range are skipped (boundary
+                                        // launch of a split operator: head + tail in one launch)
     // SELL-32-sigma: slot (slice, lane) -> row (rows sorted by length inside windows of
     // sigma rows; -1 = padding slot); null for plain SELL-32 (slot = row)
     const int32_t* __restrict__ perm;
@@ -766,7 +768,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<G, E>::v) k_sell(SellView A,
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
     typename DotOf<E>::type d{};
-    for (int64_t s = A.s0 + w0; s < A.s1; s += nw) {
+    for (int64_t vs = A.s0 + w0; vs < A.s1 - A.kspan; vs += nw) {
+        const int64_t s = vs + (vs >= A.k0 ? A.kspan : 0);
         const uint32_t b0 = __ldg(A.sptr + s);
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
         const int32_t* c = A.col + (int64_t)b0 * 32 + lane;
@@ -794,6 +797,7 @@ struct SdiaView {
     int32_t shift;  // row -> column frame: col = row + shift + offset (multi-rank windows)
     const int32_t* __restrict__ anchor;  // rectangular operators: col = anchor[row] + offset
     int64_t s0, s1;                      // slice range of this launch
+    int64_t k0 = 0, kspan = 0;           // skipped slices [k0, k0 + kspan) (see SellView)
 };
 
 template <class G, class E>
@@ -805,7 +809,8 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<G, E>::v) k_sdia(SdiaView A,
     const int64_t w0 = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kBlock) >> 5;
     typename DotOf<E>::type d{};
-    for (int64_t s = A.s0 + w0; s < A.s1; s += nw) {
+    for (int64_t vs = A.s0 + w0; vs < A.s1 - A.kspan; vs += nw) {
+        const int64_t s = vs + (vs >= A.k0 ? A.kspan : 0);
         const uint32_t b0 = __ldg(A.sptr + s);
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
         const int64_t row = (s << 5) + lane;
@@ -830,6 +835,7 @@ struct CsrView {
     const double* __restrict__ v;
     int64_t n;
     int64_t r0 = 0, r1 = 0;  // row range of this launch (k_csrv / k_csrb)
+    int64_t k0 = 0, kspan = 0;  // skipped rows [k0, k0 + kspan) (see SellView)
 };
 
 // One lane's share of a CSR row: entries k, k+S, k+2S, ... < k1 (S lanes per row),
@@ -871,11 +877,13 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
     const int64_t ng = ((int64_t)gridDim.x * kBlock) / VW;
     typename DotOf<E>::type d{};
     // every lane of a warp runs the same number of outer iterations (shuffles)
-    const int64_t iters = (A.r1 - A.r0 + ng - 1) / ng;
+    const int64_t rend = A.r1 - A.kspan;
+    const int64_t iters = (rend - A.r0 + ng - 1) / ng;
     for (int64_t it = 0; it < iters; ++it) {
-        const int64_t row = A.r0 + g0 + it * ng;
+        const int64_t vr = A.r0 + g0 + it * ng;
+        const int64_t row = vr + (vr >= A.k0 ? A.kspan : 0);
         double acc = 0.0, asum = 0.0;
-        if (row < A.r1) {
+        if (vr < rend) {
             const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
             csr_lane_row<VW, E::kAbs>(A, k0 + sub, k1, g, acc, asum);
         }
@@ -884,7 +892,7 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
             acc += __shfl_xor_sync(0xffffffffu, acc, o, VW);
             if constexpr (E::kAbs) asum += __shfl_xor_sync(0xffffffffu, asum, o, VW);
         }
-        if (sub == 0 && row < A.r1) d += apply_epi(e, row, acc, asum);
+        if (sub == 0 && vr < rend) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
 }
@@ -900,7 +908,8 @@ __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc)
     __shared__ double part[kBlock / 32], apart[kBlock / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     typename DotOf<E>::type d{};
-    for (int64_t row = A.r0 + blockIdx.x; row < A.r1; row += gridDim.x) {
+    for (int64_t vr = A.r0 + blockIdx.x; vr < A.r1 - A.kspan; vr += gridDim.x) {
+        const int64_t row = vr + (vr >= A.k0 ? A.kspan : 0);
         const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
         double acc = 0.0, asum = 0.0;
         csr_lane_row<kBlock, E::kAbs>(A, k0 + (int32_t)threadIdx.x, k1, g, acc, asum);

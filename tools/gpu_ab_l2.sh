@@ -1,0 +1,22 @@
+# A/B: L2 persistence windows for the deep-level operators (AMG_L2_PERSIST_MB), c2 / c4 / KA1 c2
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+for i in 1 2; do
+  for mb in 0 48 96; do
+    for args in "--config 2 --steps 50" "--config 4 --steps 20" "--config 2 --method ka1 --steps 50"; do
+      tag=$(echo "$args" | tr -d ' -')
+      if [ $mb = 0 ]; then env=""; else env="AMG_L2_PERSIST_MB=$mb"; fi
+      env $env timeout 600 python bench.py $args --no-cpu-baseline > gpurun_out/l2_${tag}_mb${mb}_$i.json 2>/dev/null
+    done
+  done
+done
+python - <<'PY'
+import json,glob,collections
+res=collections.defaultdict(list)
+for f in sorted(glob.glob('gpurun_out/l2_*.json')):
+    try:
+        d=json.loads(open(f).read().strip().splitlines()[-1])
+        key=f.split('/')[-1].rsplit('_',1)[0]
+        res[key].append((round(d['ms_per_step'],3), round(d['vcycle']['ms'],4)))
+    except Exception as e: print(f,'ERR',e)
+for k,v in sorted(res.items()): print(k, v)
+PY
