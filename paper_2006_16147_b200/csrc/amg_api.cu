@@ -426,6 +426,21 @@ struct Launch {
     }
 };
 
+// Experiment knob (AMG_SMALL_GRID="<rows>:<blocks per SM>"): operators of at most <rows> rows launch at
+// most <blocks per SM> x #SM blocks, leaving SM slots free so that the next kernel's blocks (PDL) can
+// become resident -- and wait -- before this one finishes.  Off by default.
+int small_cap(amg_hier_s* h, const DevMat& M, int cap) {
+    static const std::pair<int64_t, int> knob = [] {
+        const char* e = std::getenv("AMG_SMALL_GRID");
+        long long rows = 0;
+        int bps = 0;
+        if (e && std::sscanf(e, "%lld:%d", &rows, &bps) == 2 && rows > 0 && bps > 0) return std::make_pair((int64_t)rows, bps);
+        return std::make_pair((int64_t)0, 0);
+    }();
+    if (knob.first > 0 && M.nrows <= knob.first) return std::min(cap, knob.second * h->ctx->nsm);
+    return cap;
+}
+
 template <class G, class E>
 void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* name, double vec_bytes,
                 int part = 0) {
@@ -455,14 +470,14 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         ~PersistScope() { g_persist_ptr = nullptr; }
     } persist_scope(M);
     if (M.fmt == FMT_SDIA) {
-        const int cap = ctx_cap(L.h->ctx, (const void*)k_sdia<G, E>);
+        const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)k_sdia<G, E>));
         const int64_t need = ((u1 - u0 - kspan) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
         launch_k(k_sdia<G, E>, grid, kBlock, L.s,
                  SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor, u0, u1, k0, kspan}, g,
                  e, rc);
     } else if (M.fmt == FMT_SELL) {
-        const int cap = ctx_cap(L.h->ctx, (const void*)k_sell<G, E>);
+        const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)k_sell<G, E>));
         const int64_t need = ((u1 - u0 - kspan) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
         launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1, k0, kspan, M.perm},
@@ -471,7 +486,7 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         const CsrView v{M.rp, M.col, M.val, M.nrows, u0, u1, k0, kspan};
         const int64_t need = ((u1 - u0 - kspan) * M.vw + kBlock - 1) / kBlock;
         if (M.vw == kVWBlock) {
-            const int cap = ctx_cap(L.h->ctx, (const void*)k_csrb<G, E>);
+            const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)k_csrb<G, E>));
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(u1 - u0 - kspan, cap));
             launch_k(k_csrb<G, E>, grid, kBlock, L.s, v, g, e, rc);
             L.end();
@@ -480,7 +495,7 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         switch (M.vw) {
 #define VWCASE(W)                                                                 \
     case W: {                                                                     \
-        const int cap = ctx_cap(L.h->ctx, (const void*)k_csrv<W, G, E>);           \
+        const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)k_csrv<W, G, E>)); \
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap)); \
         launch_k(k_csrv<W, G, E>, grid, kBlock, L.s, v, g, e, rc);                   \
         break;                                                                    \
