@@ -550,7 +550,9 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0)
     for (auto& R : h->ranks) {
         // every rank computes the same status; in loopback each sets the (shared) WHILE condition
         RedCtx rc{nullptr, nullptr, nullptr, R.st, cond, kind, nullptr};
+        L.begin("dot_finish", 8.0 * kDotSlots * h->np);
         launch_k(k_finish, 1, 32, L.s, R.dot_all, kDotSlots * h->np, rc);
+        L.end();
         cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);  // slots of skipped parts stay 0
     }
 }
@@ -570,7 +572,9 @@ void dot_finish_k(amg_hier_s* h, Launch& L, int kind, int lvl) {
     }
     for (auto& R : h->ranks) {
         RedCtx rc{nullptr, nullptr, nullptr, nullptr, 0ull, kind, R.lv[lvl].kst};
+        L.begin("dot_finish", 8.0 * kDotSlots * h->np);
         launch_k(k_finish, 1, 32, L.s, R.dot_all, kDotSlots * h->np, rc);
+        L.end();
         cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
     }
 }
@@ -580,15 +584,16 @@ using VecOf = std::function<double*(RankState&)>;
 using UnpackFn = std::function<void(RankState&, const Exch&, cudaStream_t)>;
 
 // Halo exchange of a level-l vector (window base pointer given per rank) on stream `st`.
-void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const UnpackFn* unpack = nullptr);
+// pack_st: stream of the pack kernels (null: st).  The overlapped form packs on the context stream
+// BEFORE the interior kernel takes every SM, so the transfer runs during it.
+void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const UnpackFn* unpack = nullptr,
+                 cudaStream_t pack_st = nullptr);
 void exchange(amg_hier_s* h, Launch& L, int l, const VecOf& vec) { exchange_on(h, L.s, l, vec); }
 
 // Overlapped exchange: fork the comm stream off the context stream, exchange there,
 // and let the caller launch the interior rows before exchange_end joins the streams.
 void exchange_begin(amg_hier_s* h, Launch& L, int l, const VecOf& vec, const UnpackFn* unpack = nullptr) {
-    cudaEventRecord(h->ev_fork, L.s);
-    cudaStreamWaitEvent(h->comm, h->ev_fork, 0);
-    exchange_on(h, h->comm, l, vec, unpack);
+    exchange_on(h, h->comm, l, vec, unpack, L.s);
     cudaEventRecord(h->ev_join, h->comm);
 }
 void exchange_end(amg_hier_s* h, Launch& L) { cudaStreamWaitEvent(L.s, h->ev_join, 0); }
@@ -621,16 +626,33 @@ void overlapped(amg_hier_s* h, Launch& L, int lx, const VecOf& xv, bool dist, co
     }
 }
 
-void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const UnpackFn* unpack) {
+void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const UnpackFn* unpack,
+                 cudaStream_t pack_st) {
     if (!h->multi()) return;
-    struct { cudaStream_t s; } L{st};
+    Launch L{h, st};
     const int nsm = h->ctx->nsm;
     bool any = false;
     for (auto& R : h->ranks) any |= (R.lv[l].ex.nsend > 0 || R.lv[l].ex.nrecv > 0);
-    if (!any && h->loopback) return;
-    for (auto& R : h->ranks) {
-        const Exch& E = R.lv[l].ex;
-        if (E.nsend) launch_k(k_pack, vec_grid(E.nsend, nsm), kBlock, L.s, vec(R), E.send_idx, E.sbuf, E.nsend);
+    if (!any && h->loopback) {
+        if (pack_st) {  // keep the fork/join structure of the caller (ev_join recorded on st)
+            cudaEventRecord(h->ev_fork, pack_st);
+            cudaStreamWaitEvent(st, h->ev_fork, 0);
+        }
+        return;
+    }
+    {
+        Launch Lp{h, pack_st ? pack_st : st};
+        for (auto& R : h->ranks) {
+            const Exch& E = R.lv[l].ex;
+            if (!E.nsend) continue;
+            Lp.begin("halo_pack", 20.0 * (double)E.nsend);
+            launch_k(k_pack, vec_grid(E.nsend, nsm), kBlock, Lp.s, vec(R), E.send_idx, E.sbuf, E.nsend);
+            Lp.end();
+        }
+    }
+    if (pack_st) {  // the transfer and the unpack follow the packs on st
+        cudaEventRecord(h->ev_fork, pack_st);
+        cudaStreamWaitEvent(st, h->ev_fork, 0);
     }
     if (h->loopback) {
         for (auto& Rd : h->ranks) {
@@ -658,8 +680,10 @@ void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const 
     for (auto& R : h->ranks) {
         const Exch& E = R.lv[l].ex;
         if (!E.nrecv) continue;
+        L.begin("halo_unpack", 20.0 * (double)E.nrecv);
         if (unpack) (*unpack)(R, E, L.s);
         else launch_k(k_unpack, vec_grid(E.nrecv, nsm), kBlock, L.s, vec(R), E.recv_idx, E.rbuf, E.nrecv);
+        L.end();
     }
 }
 

@@ -6,8 +6,8 @@ ctx=amg.Context(device=0)
 res={}
 for np_ in (1, 8):
     A,b,_=config_problem(4,grid=(256,256,256*np_))
-    h=amg.Hierarchy(ctx,A,cfg=amg.make_config(max_coarse_size=200*np_,emulate_ranks=np_))
-    prof=h.profile_iteration(torch.tensor(b,device='cuda:0'),5)
+    h=amg.Hierarchy(ctx,A,cfg=amg.make_config(max_coarse_size=200*np_,emulate_ranks=np_,replicate_below_bytes=int(sys.argv[1]) if len(sys.argv)>1 else 64<<20))
+    prof=h.profile_iteration(torch.tensor(b,device='cuda:0'),5,cap=4096)
     agg=collections.OrderedDict()
     for k in prof:
         agg.setdefault(k['name'],[0,0.0]); agg[k['name']][0]+=1; agg[k['name']][1]+=k['ms']

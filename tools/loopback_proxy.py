@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--weak", action="store_true",
                     help="weak scaling: np ranks hold np x the grid (z extent x np), as on np GPUs; "
                          "reports t_loop(np) / (np t(1)), the per-rank share of the serialised loopback time")
+    ap.add_argument("--rep", type=int, default=None, help="replicate_below_bytes (default: the library's)")
     args = ap.parse_args()
     grid0 = tuple(int(v) for v in args.grid.split("x"))
     ctx = amg.Context(device=0)
@@ -47,7 +48,8 @@ def main():
             cache[grid] = (A, torch.tensor(b, device="cuda:0"))
         A, bt = cache[grid]
         for graphs in ([1, 0] if args.eager else [1]):
-            cfg = amg.make_config(max_coarse_size=200 * np_, emulate_ranks=np_, use_graphs=graphs)
+            extra = {} if args.rep is None else {"replicate_below_bytes": args.rep}
+            cfg = amg.make_config(max_coarse_size=200 * np_, emulate_ranks=np_, use_graphs=graphs, **extra)
             h = amg.Hierarchy(ctx, A, cfg=cfg)
             for _ in range(3):
                 h.solve(bt)
@@ -57,7 +59,7 @@ def main():
                 ts.append(rep["solve_s"])
                 its = rep["iterations"]
             t = sorted(ts)[len(ts) // 2]
-            prof = h.profile_iteration(bt, 3)
+            prof = h.profile_iteration(bt, 3, cap=4096)
             rec = {"np": np_, "graphs": graphs, "grid": list(grid), "solve_ms": t * 1e3, "iterations": its,
                    "ms_per_iter": t * 1e3 / its, "launches_per_iter": len(prof), "levels": h.sizes()}
             if np_ == 1 and graphs == 1:
