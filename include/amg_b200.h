@@ -222,7 +222,7 @@ int amg_solve_host(amg_hier_t h, const double* b_host, double* x_host, double rt
  * be pinned (cudaHostAlloc / cudaHostRegister); pageable buffers still give correct results.
  * `reps` may be NULL or hold nrhs reports (solve_s of each = the batch time / nrhs).  Returns
  * the first non-AMG_OK status of the batch (AMG_NOT_CONVERGED / AMG_ERR_BREAKDOWN: x valid).
- * Multi-rank contexts or use_graphs = 0: the solves run one after another (amg_solve_host). */
+ * NCCL contexts or use_graphs = 0: the solves run one after another (amg_solve_host). */
 int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, double* X_host, double rtol,
                          int32_t maxit, amg_report_t* reps);
 

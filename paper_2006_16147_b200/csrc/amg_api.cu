@@ -3758,7 +3758,8 @@ int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, doubl
     CK(cudaSetDevice(h->ctx->device));
     const int64_t n = h->n0_local;
     int code = AMG_OK;
-    if (h->multi() || !h->cfg.use_graphs) {  // no pipelining: one solve after another
+    // NCCL ranks / eager launches: one solve after another (loopback pipelines like one rank)
+    if ((h->multi() && !h->loopback) || !h->cfg.use_graphs) {
         for (int32_t k = 0; k < nrhs; ++k) {
             const int c = amg_solve_host(h, B_host + k * n, X_host + k * n, rtol, maxit, reps ? reps + k : nullptr);
             if (c != AMG_OK && c != AMG_NOT_CONVERGED && c != AMG_ERR_BREAKDOWN) return c;
@@ -3819,7 +3820,7 @@ int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, doubl
         // solve k once b_k is there and x_{k-2} has left bx[q]
         CK(cudaStreamWaitEvent(s, h2d[q], 0));
         if (k >= 2) CK(cudaStreamWaitEvent(s, d2h[q], 0));
-        CK(cudaMemcpyAsync(R.st, &sts[0], sizeof(PcgState), cudaMemcpyHostToDevice, s));
+        for (auto& Rk : h->ranks) CK(cudaMemcpyAsync(Rk.st, &sts[0], sizeof(PcgState), cudaMemcpyHostToDevice, s));
         CK(cudaGraphLaunch(h->batch_exec[q], s));
         CK(cudaMemcpyAsync(&sts[1 + k], R.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(solved[q], s));

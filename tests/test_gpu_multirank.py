@@ -200,3 +200,20 @@ def test_distributed_setup_solves_exactly_like_the_gathered_setup(ctx, np_, extr
     assert rg["iterations"] == rd["iterations"] and torch.equal(xg, xd)
     r = torch.tensor(uniform_pm1(31, A.n_global), device="cuda:0")
     assert torch.equal(hg.precond_apply(r), hd.precond_apply(r))
+
+
+def test_loopback_host_batch_equals_single_solves(ctx):
+    """amg_solve_host_batch pipelines the copies with the (WHILE-graph) solves on a loopback
+    multi-rank hierarchy too: bitwise the solutions and reports of one amg_solve_host each."""
+    import paper_2006_16147_b200 as amg
+    A, _, _ = config_problem(4, grid=(32, 32, 64))
+    h = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=2))
+    n = A.n_global
+    B = np.stack([uniform01(400 + k, n) for k in range(4)])
+    B[2] = 0.0
+    X, reps = h.solve_host_batch(B.copy(), rtol=1e-6)
+    for k in range(B.shape[0]):
+        xk, rk = h.solve_host(B[k].copy(), rtol=1e-6)
+        assert np.array_equal(X[k], xk), k
+        assert reps[k]["iterations"] == rk["iterations"]
+    assert reps[2]["iterations"] == 0 and not X[2].any()
