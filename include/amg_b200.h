@@ -73,9 +73,11 @@ typedef struct {
     int64_t replicate_below_bytes;/* multi-rank: levels whose A_l + P-bar_l bytes are below
                                      this are held whole on every rank (default 64 MiB) */
     int32_t setup_threads;        /* host OpenMP threads for setup; 0 = all available */
-    int32_t use_graphs;           /* 1 (default): solve/apply run as CUDA graphs; 0: eager
-                                     launches (debug / per-kernel timing).  Multi-rank solves
-                                     always run eagerly with one status read per iteration. */
+    int32_t use_graphs;           /* 1 (default): a solve is ONE CUDA graph (a device-side WHILE node over
+                                     the iteration, on one or several ranks; NCCL contexts fall back,
+                                     collectively, to one graph per iteration if the WHILE graph cannot be
+                                     built); 0: eager launches with one status read per iteration (debug /
+                                     per-kernel timing). */
     int32_t emulate_ranks;        /* single-rank contexts only: > 1 partitions the hierarchy into
                                      this many equal row blocks held by ONE process on one GPU and
                                      runs the multi-rank kernels with in-process halo copies
