@@ -4295,6 +4295,10 @@ int amg_host_level_aggregates(amg_host_hier_t h, int32_t l, int64_t* agg) {
         return AMG_ERR_ARG;
     }
     const auto& a = h->H.lv[l].agg;
+    if ((int64_t)a.size() != h->H.lv[l].A.nrows) {  // a rank's view holds its own rows only
+        set_err("amg_host_level_aggregates: this host hierarchy holds one rank's rows only");
+        return AMG_ERR_ARG;
+    }
     for (size_t i = 0; i < a.size(); ++i) agg[i] = a[i];
     return AMG_OK;
 }
@@ -4307,6 +4311,10 @@ int amg_host_level_matrix(amg_host_hier_t h, int32_t l, int32_t which, int64_t* 
         return AMG_ERR_ARG;
     }
     const amgsetup::Csr& M = which == 0 ? h->H.lv[l].A : h->H.lv[l].P;
+    if ((int64_t)M.rp.size() != M.nrows + 1) {  // amg_host_dist_build_rank keeps only its plan
+        set_err("amg_host_level_matrix: this host hierarchy holds one rank's plan, not the level matrices");
+        return AMG_ERR_ARG;
+    }
     for (int64_t i = 0; i <= M.nrows; ++i) rowptr[i] = M.rp[i];
     for (int64_t k = 0; k < M.nnz(); ++k) {
         colind[k] = M.ci[k];

@@ -17,7 +17,7 @@ struct Csr {
     std::vector<int64_t> rp;   // nrows+1
     std::vector<int32_t> ci;   // ascending within a row
     std::vector<double> v;
-    int64_t nnz() const { return rp.empty() ? 0 : rp[nrows]; }
+    int64_t nnz() const { return (int64_t)rp.size() <= nrows ? 0 : rp[nrows]; }
 };
 
 struct Config {
