@@ -642,7 +642,6 @@ __device__ __forceinline__ void bind(ESpmvDotPz& e) {
     e.pnew = (it & 1) ? e.p0 : e.p1;
 }
 
-__device__ __forceinline__ void epi_prefetch(const EResid& e, int64_t i) { pf_l2(e.b + i); }
 template <bool DOT, bool ABS>
 __device__ __forceinline__ void epi_prefetch(const ESweep<DOT, ABS>& e, int64_t i) {
     pf_l2(e.x + i);
@@ -656,13 +655,9 @@ __device__ __forceinline__ void epi_prefetch(const EPost1<DOT, MB, ABS>& e, int6
     pf_l2(e.bmb + i);
     if constexpr (!ABS) pf_l2(e.m + i);
 }
-__device__ __forceinline__ void epi_prefetch(const ESpmvDotPz& e, int64_t i) {
-    pf_l2(e.z + i);
-    if (!e.first) {
-        pf_l2(e.pold + i);
-        pf_l2(e.x + i);
-    }
-}
+// (measured: prefetching for the residual and for q = A p with the fused direction update makes
+// them 1-3 % slower -- their epilogues read one / three vectors the gathers already touch -- while the
+// sweeps gain 1.5-4 % on c3; profiles/r02_ab_epi_prefetch.txt)
 __device__ __forceinline__ void epi_prefetch(const EProlongAdd& e, int64_t i) { pf_l2(e.x + i); }
 
 // x' = x + s, returns dw_i x'_i (DOT)       (INVK: x' = x + Z (D^-1 W r); the level-0
