@@ -152,10 +152,22 @@ def test_loopback_replicated_levels_run_the_single_rank_fused_forms(ctx):
     collapsed level forms as one rank (W5); level 0 uses the fused direction update with the
     z-halo unpack forming p_new at the halo (no separate p-update kernel)."""
     import paper_2006_16147_b200 as amg
+    import os
     A, b, _ = config_problem(4, grid=(96, 96, 96))  # levels ... -> 1.7k (compact) -> 220 (collapsed) -> 28
-    h = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=4))
+    os.environ["AMG_NO_COLLAPSE2"] = "1"  # keep the compact level visible (else it collapses as well)
+    try:
+        h = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=4))
+    finally:
+        os.environ.pop("AMG_NO_COLLAPSE2", None)
     names = [k["name"] for k in h.profile_vcycle(1)]
     assert "collapsed" in names and "prolong_post_c" in names, names
+    os.environ["AMG_FORCE_COLLAPSE2"] = "1"  # second collapse on the replicated levels
+    try:
+        h2 = amg.Hierarchy(ctx, A, cfg=amg.make_config(emulate_ranks=4))
+    finally:
+        os.environ.pop("AMG_FORCE_COLLAPSE2", None)
+    n2 = [k["name"] for k in h2.profile_vcycle(1)]
+    assert n2.count("collapsed") == 4 and "prolong_post_c" not in n2, n2  # one per loopback rank
     it = [k["name"] for k in h.profile_iteration(torch.tensor(b, device="cuda:0"), 2)]
     assert "spmv_dot_pupd" in it and "pupdate" not in it, it
     ho = O.OracleHierarchy(A)
@@ -171,6 +183,8 @@ def test_loopback_replicated_levels_run_the_single_rank_fused_forms(ctx):
     x, _ = h.solve(bt, rtol=0.0, maxit=k)
     xo, _ = ho.pcg(b, rtol=0.0, maxit=k)
     assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-8 * np.linalg.norm(xo)
+    z2 = h2.precond_apply(torch.tensor(r, device="cuda:0")).cpu().numpy()
+    assert np.linalg.norm(z2 - zo) <= 1e-12 * np.linalg.norm(zo)
 
 
 @pytest.mark.parametrize("np_,extra", [(2, {}), (4, dict(replicate_below_bytes=0)), (3, dict(smoother=1)),

@@ -372,10 +372,28 @@ def test_compact_and_collapsed_levels_are_taken(ctx):
     above check their numbers against the oracle, this checks the paths are actually used."""
     amg = _amg()
     A, b, _ = config_problem(2)
+    ho2 = O.OracleHierarchy(A)
+    r2 = uniform_pm1(4243, A.n_global)
+    zo2 = ho2.vcycle(r2)
+    # forced second collapse: the compact 4147-row level above the collapsed 522-row level becomes
+    # one dense GEMV for the whole cycle below level 2 (by default c2 keeps it compact: the dense
+    # operator would move 3x the bytes)
+    os.environ["AMG_FORCE_COLLAPSE2"] = "1"
+    try:
+        h = amg.Hierarchy(ctx, A)
+    finally:
+        os.environ.pop("AMG_FORCE_COLLAPSE2", None)
+    names = [k["name"] for k in h.profile_vcycle(1)]
+    assert names.count("collapsed") == 1 and "coarse_gemv" not in names and "restrict_c" not in names, names
+    z = h.precond_apply(torch.tensor(r2, device="cuda:0")).cpu().numpy()
+    assert np.linalg.norm(z - zo2) / np.linalg.norm(zo2) <= VCYCLE_TOL
+    # default (byte rule): the compact level runs its three kernels
     h = amg.Hierarchy(ctx, A)
     names = [k["name"] for k in h.profile_vcycle(1)]
     assert "collapsed" in names and "restrict_c" in names and "sweep0_c" in names
     assert names.count("collapsed") == 1 and "coarse_gemv" not in names
+    z = h.precond_apply(torch.tensor(r2, device="cuda:0")).cpu().numpy()
+    assert np.linalg.norm(z - zo2) / np.linalg.norm(zo2) <= VCYCLE_TOL
     # and 2/2 sweeps collapse too (general dense level operator)
     A3 = poisson7(32, 32, 32, (1.0, 1.0, 0.01))
     h3 = amg.Hierarchy(ctx, A3, cfg=amg.make_config(pre_sweeps=2, post_sweeps=2))
