@@ -71,7 +71,8 @@ typedef struct {
     int32_t pre_sweeps;           /* l1-Jacobi pre-smoothing sweeps, >= 1 (default 1) */
     int32_t post_sweeps;          /* l1-Jacobi post-smoothing sweeps, >= 1 (default 1) */
     int64_t replicate_below_bytes;/* multi-rank: levels whose A_l + P-bar_l bytes are below
-                                     this are held whole on every rank (default 64 MiB) */
+                                     this are held whole on every rank (default 128 MiB: at c4 np = 8 the
+                                     4k-row level, ~0.1 GB, whose rows would otherwise be ~500 per rank) */
     int32_t setup_threads;        /* host OpenMP threads for setup; 0 = all available */
     int32_t use_graphs;           /* 1 (default): a solve is ONE CUDA graph (a device-side WHILE node over
                                      the iteration, on one or several ranks; NCCL contexts fall back,

@@ -3361,7 +3361,7 @@ void amg_config_default(amg_config_t* c) {
     c->min_coarsening_ratio = 1.2;
     c->pre_sweeps = 1;
     c->post_sweeps = 1;
-    c->replicate_below_bytes = 64ll << 20;
+    c->replicate_below_bytes = 128ll << 20;
     c->setup_threads = 0;
     c->use_graphs = 1;
     c->emulate_ranks = 1;
