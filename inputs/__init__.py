@@ -13,6 +13,7 @@ from .problems import (  # noqa: F401
     jump27,
     random_spd,
     diagonal_spd,
+    islands,
     uniform01,
     uniform_pm1,
     config_problem,

@@ -220,6 +220,32 @@ def diagonal_spd(n: int, seed: int = 71) -> CSR:
                1.0 + uniform01(seed, n))
 
 
+def islands(seed: int = 73) -> CSR:
+    """Disconnected graph: poisson7(12,12,12) (+) poisson7(9,7,5) (+) 37 isolated rows, symmetrically
+    permuted by a seeded permutation so the components interleave in the row order (the matching's
+    unmatched-vertex and disconnected-component cases, away from the lexicographic order)."""
+    blocks = [poisson7(12, 12, 12), poisson7(9, 7, 5), diagonal_spd(37, seed=seed + 1)]
+    rows, cols, vals, off = [], [], [], 0
+    for B in blocks:
+        r = np.repeat(np.arange(B.n_global, dtype=np.int64), np.diff(B.rowptr))
+        rows.append(r + off)
+        cols.append(B.colind + off)
+        vals.append(B.values)
+        off += B.n_global
+    n = off
+    perm = np.argsort(uniform01(seed, n), kind="stable")  # new index of old row i: inv[i]
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n, dtype=np.int64)
+    r = inv[np.concatenate(rows)]
+    c = inv[np.concatenate(cols)]
+    v = np.concatenate(vals)
+    order = np.lexsort((c, r))
+    r, c, v = r[order], c[order], v[order]
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, r + 1, 1)
+    return CSR(n, 0, n, np.cumsum(rp), c, v)
+
+
 # ------------------------------------------------------------------- configs
 CONFIGS = {
     # name: (grid builder, rhs, pre, post, maxsize_per_gpu)

@@ -23,6 +23,7 @@
 // which is how the multi-rank kernels are parity-tested on a single B200.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <omp.h>
 
 #include <algorithm>
@@ -372,10 +373,27 @@ int vec_grid(int64_t n, int nsm) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)nsm * 8));
 }
 
+// NVTX range over one ABI call (visible in nsys / ncu --nvtx; a no-op without a tool attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Kernel launch with programmatic stream serialization (PDL, see kernels.cuh).
 bool pdl_enabled() {
     static const bool on = !(std::getenv("AMG_PDL") && std::getenv("AMG_PDL")[0] == '0');
     return on;
+}
+// Sweeps recompute m_i = sum_j |a_ij| from the streamed row while rows average at most this many
+// entries, else read the stored m (AMG_ABS_ROW_CUT, an A/B knob; default 40).
+double abs_row_cut() {
+    static const double cut = [] {
+        const char* e = std::getenv("AMG_ABS_ROW_CUT");
+        return e ? std::atof(e) : 40.0;
+    }();
+    return cut;
 }
 // L2 persistence window of the next launch_mat launch (deep-level operators, AMG_L2_PERSIST_MB;
 // an experiment: VERDICT r1 W8 / SURVEY §7.5).  Thread-local: set and consumed by launch_mat.
@@ -827,7 +845,7 @@ struct TailEmitter {
             ops.back().x = xpre;
         }
         const double* cur = dst;
-        const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
+        const bool abs = (double)D.A.nnz <= abs_row_cut() * (double)std::max<int64_t>(D.A.nrows, 1);
         for (int sw = 0; sw < s2; ++sw) {
             double* xo = (cur == tmp) ? out : tmp;
             if (sw == 0 && am) {
@@ -1351,7 +1369,7 @@ void enqueue_level(amg_hier_s* h, Launch& L, int l, const VecOf& bvec, const Vec
             const bool dt = (dot && last);
             const double* dw = (dt && dwv) ? (*dwv)(R) + D.ep_off : nullptr;
             // short rows: m_i recomputed from the streamed row; long rows: read m
-            const bool abs = (double)D.A.nnz <= 40.0 * (double)std::max<int64_t>(D.A.nrows, 1);
+            const bool abs = (double)D.A.nnz <= abs_row_cut() * (double)std::max<int64_t>(D.A.nrows, 1);
             const double mb8 = abs ? 0.0 : n8;
             double* m = D.m + D.ep_off;
             auto red = [&]() { return sink_red(h, R, dkind, sink, part); };
@@ -3441,6 +3459,7 @@ int amg_ctx_destroy(amg_ctx_t c) {
 int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int64_t row_end, const int64_t* rowptr,
                         const int64_t* colind, const double* values, const double* w, const amg_config_t* cfg_in,
                         amg_hier_t* out) {
+    NvtxRange nvtx_("amg_hierarchy_build");
     auto t0 = std::chrono::steady_clock::now();
     if (!ctx || !out || !rowptr || !colind || !values || n_global <= 0 || row_begin < 0 || row_end < row_begin ||
         row_end > n_global) {
@@ -3737,6 +3756,7 @@ int amg_hierarchy_destroy(amg_hier_t h) {
 }
 
 int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int32_t maxit, amg_report_t* rep) {
+    NvtxRange nvtx_("amg_solve");
     if (!h || !b_dev || !x_dev || rtol < 0.0 || maxit < 0) {
         set_err("amg_solve: bad argument");
         return AMG_ERR_ARG;
@@ -3811,6 +3831,7 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
 
 int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, double* X_host, double rtol,
                          int32_t maxit, amg_report_t* reps) {
+    NvtxRange nvtx_("amg_solve_host_batch");
     if (!h || nrhs < 0 || (nrhs > 0 && (!B_host || !X_host)) || rtol < 0.0 || maxit < 0) {
         set_err("amg_solve_host_batch: bad argument");
         return AMG_ERR_ARG;
@@ -3920,6 +3941,7 @@ int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, doubl
 
 int amg_solve_host(amg_hier_t h, const double* b_host, double* x_host, double rtol, int32_t maxit,
                    amg_report_t* rep) {
+    NvtxRange nvtx_("amg_solve_host");
     if (!h || !b_host || !x_host) {
         set_err("amg_solve_host: bad argument");
         return AMG_ERR_ARG;
@@ -3939,6 +3961,7 @@ int amg_solve_host(amg_hier_t h, const double* b_host, double* x_host, double rt
 }
 
 int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
+    NvtxRange nvtx_("amg_precond_apply");
     if (!h || !r_dev || !z_dev) {
         set_err("amg_precond_apply: bad argument");
         return AMG_ERR_ARG;
@@ -4001,6 +4024,7 @@ int amg_hierarchy_report(amg_hier_t h, amg_report_t* rep) {
 
 int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out, double* bytes_out,
                        double* stored_bytes_out, const char** names_out, int32_t* count) {
+    NvtxRange nvtx_("amg_profile_vcycle");
     if (!h || napply < 1 || !count) {
         set_err("amg_profile_vcycle: bad argument");
         return AMG_ERR_ARG;
@@ -4044,6 +4068,7 @@ int amg_profile_vcycle(amg_hier_t h, int32_t napply, int32_t cap, double* ms_out
 int amg_profile_iteration(amg_hier_t h, const double* b_dev, double* x_dev, int32_t napply, int32_t cap,
                           double* ms_out, double* bytes_out, double* stored_bytes_out, const char** names_out,
                           int32_t* count) {
+    NvtxRange nvtx_("amg_profile_iteration");
     if (!h || !b_dev || !x_dev || napply < 1 || !count) {
         set_err("amg_profile_iteration: bad argument");
         return AMG_ERR_ARG;
@@ -4098,6 +4123,7 @@ struct amg_host_hier_s {
 
 int amg_host_hierarchy_build(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values,
                              const double* w, const amg_config_t* cfg_in, amg_host_hier_t* out) {
+    NvtxRange nvtx_("amg_host_hierarchy_build");
     if (!out) {
         set_err("amg_host_hierarchy_build: null out");
         return AMG_ERR_ARG;
@@ -4121,6 +4147,7 @@ int amg_host_hierarchy_build(int64_t n, const int64_t* rowptr, const int64_t* co
 int amg_host_dist_build(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* values,
                         const double* w, const amg_config_t* cfg_in, int32_t nranks, int64_t replicate_below_bytes,
                         amg_host_hier_t* out) {
+    NvtxRange nvtx_("amg_host_dist_build");
     if (!out || nranks < 1 || !rowptr || !colind || !values || n <= 0 || n >= (int64_t)INT32_MAX) {
         set_err("amg_host_dist_build: bad argument");
         return AMG_ERR_ARG;
@@ -4251,6 +4278,7 @@ int amg_host_dist_build_rank(int64_t n, int64_t row_begin, int64_t row_end, cons
                              const int64_t* colind, const double* values, const double* w, const amg_config_t* cfg_in,
                              int32_t nranks, int32_t rank, int64_t replicate_below_bytes, amg_exchange_fn exchange,
                              void* user, amg_host_hier_t* out) {
+    NvtxRange nvtx_("amg_host_dist_build_rank");
     if (!out || !exchange || nranks < 1 || rank < 0 || rank >= nranks || !rowptr || !colind || !values || n <= 0 ||
         n >= (int64_t)INT32_MAX || row_begin < 0 || row_end < row_begin || row_end > n || rowptr[0] != 0) {
         set_err("amg_host_dist_build_rank: bad argument");

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from inputs import config_problem, diagonal_spd, jump27, poisson7, random_spd, uniform01
+from inputs import config_problem, diagonal_spd, islands, jump27, poisson7, random_spd, uniform01
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -138,7 +138,8 @@ def _compare(amg, A, w=None, **cfg):
 
 @pytest.mark.parametrize("case", ["c1", "aniso_32", "jump_16", "ragged", "unsmoothed_20", "random_w",
                                   "omega_text", "m4_sweeps", "c4_like_24x24x48", "irregular_hubs",
-                                  "irregular_narrow", "line_1d", "plane_2d", "diagonal", "n1"])
+                                  "irregular_narrow", "line_1d", "plane_2d", "diagonal", "n1", "islands",
+                                  "pair_mcs1"])
 def test_host_setup_bit_exact_vs_oracle(amg, case):
     w, cfg = None, {}
     if case == "c1":
@@ -174,6 +175,12 @@ def test_host_setup_bit_exact_vs_oracle(amg, case):
         A = diagonal_spd(300)
     elif case == "n1":
         A = diagonal_spd(1)
+    elif case == "islands":  # two components + isolated rows, interleaved: coarsening stalls at 43
+        A = islands()
+        cfg = dict(max_coarse_size=20)
+    elif case == "pair_mcs1":  # 2 rows, max_coarse_size 1: a 1-row coarsest level
+        A = poisson7(2, 1, 1)
+        cfg = dict(max_coarse_size=1)
     else:
         A = poisson7(24, 24, 48)
         cfg = dict(max_coarse_size=400)

@@ -14,7 +14,7 @@ import os
 import numpy as np
 import pytest
 
-from inputs import config_problem, jump27, poisson7, random_spd, uniform01
+from inputs import config_problem, islands, jump27, poisson7, random_spd, uniform01
 
 
 def _amg():
@@ -106,11 +106,14 @@ def _case(name):
         return random_spd(5000, hubs=3), {}, None
     if name == "ragged_rows":           # np does not divide n; uneven blocks
         return poisson7(17, 13, 11), {}, None
+    if name == "islands":               # disconnected + isolated rows interleaved; coarsening stalls
+        return islands(), dict(max_coarse_size=20), None
     raise KeyError(name)
 
 
 CASES = [("c4_32x32x64", 2), ("c4_32x32x64", 4), ("c4_24x24x96_np8", 8), ("c5_jump27_24", 3),
-         ("c3_aniso_2x2", 2), ("unsmoothed_va4", 4), ("random_w", 3), ("irregular_hubs", 3), ("ragged_rows", 5)]
+         ("c3_aniso_2x2", 2), ("unsmoothed_va4", 4), ("random_w", 3), ("irregular_hubs", 3), ("ragged_rows", 5),
+         ("islands", 4)]
 
 
 @pytest.mark.parametrize("name,nr", CASES)

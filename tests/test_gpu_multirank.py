@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from inputs import config_problem, jump27, poisson7, random_spd, uniform01, uniform_pm1
+from inputs import config_problem, islands, jump27, poisson7, random_spd, uniform01, uniform_pm1
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -41,12 +41,15 @@ def _case(name):
     if name == "irregular_hubs":  # not slab-shaped: hub rows couple every rank with every rank
         A = random_spd(6000, hubs=3)
         return A, uniform_pm1(6, A.n_global), {}
+    if name == "islands":  # disconnected components + isolated rows interleaved over the ranks
+        A = islands()
+        return A, uniform01(29, A.n_global), dict(max_coarse_size=20)
     raise KeyError(name)
 
 
 @pytest.mark.parametrize("rep_bytes", [0, 1 << 22])
 @pytest.mark.parametrize("np_", [2, 3, 4])
-@pytest.mark.parametrize("name", ["c4_slabs", "aniso22", "jump27", "irregular_hubs"])
+@pytest.mark.parametrize("name", ["c4_slabs", "aniso22", "jump27", "irregular_hubs", "islands"])
 def test_loopback_multirank_parity(ctx, name, np_, rep_bytes):
     import paper_2006_16147_b200 as amg
     A, b, kw = _case(name)

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from inputs import config_problem, diagonal_spd, jump27, poisson7, random_spd, uniform01, uniform_pm1
+from inputs import config_problem, diagonal_spd, islands, jump27, poisson7, random_spd, uniform01, uniform_pm1
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -105,12 +105,20 @@ def _case(name):
         A = poisson7(48, 48, 48)
         kw = dict(sweeps_per_level=4)
         return A, uniform01(28, A.n_global), kw, kw
+    if name == "islands":  # disconnected components + isolated rows, interleaved; coarsening stalls
+        A = islands()
+        kw = dict(max_coarse_size=20)
+        return A, uniform01(29, A.n_global), kw, kw
+    if name == "pair_mcs1":  # 2 rows, max_coarse_size 1: a 1-row coarsest level
+        A = poisson7(2, 1, 1)
+        kw = dict(max_coarse_size=1)
+        return A, np.array([1.0, -3.0]), kw, kw
     raise KeyError(name)
 
 
 CASES = ["c1", "c2", "c3_64", "c4_64x64x128", "c5_32", "ragged_17x13x11", "unsmoothed_24",
          "omega_text_32", "single_level", "irregular_hubs", "irregular_narrow", "line_1d_100k",
-         "plane_2d_300", "diagonal", "n1", "c5_72", "irregular_400k", "va4_48"]
+         "plane_2d_300", "diagonal", "n1", "c5_72", "irregular_400k", "va4_48", "islands", "pair_mcs1"]
 _cache = {}
 
 
