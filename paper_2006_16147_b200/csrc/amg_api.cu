@@ -84,6 +84,10 @@ struct DevMat {
     int32_t* col = nullptr;
     double* val = nullptr;
     int32_t* perm = nullptr;   // SELL-32-sigma: slot -> row (null: plain SELL-32)
+    // 16-bit columns (SELL / CSR whose every row spans < 2^16 columns): col = cbase[row or slot]
+    // + c16[k]; `col` is then null.  10 instead of 12 B per stored entry (+ 4 B per row)
+    uint16_t* c16 = nullptr;
+    int32_t* cbase = nullptr;
     // multi-rank overlap: launch units (slices for SELL/SDIA, rows for CSR) and the largest
     // contiguous block of units whose gathers touch only owned columns ("interior": it can
     // run while the halo is in flight); the rest ("head" / "tail") runs after the exchange
@@ -95,11 +99,13 @@ struct DevMat {
     double stored_bytes() const {
         const double nsl = (double)((nrows + 31) / 32);
         switch (fmt) {
-            case FMT_SELL: return 12.0 * (double)stored + 4.0 * (nsl + 1) + (perm ? 128.0 * nsl : 0.0);
+            case FMT_SELL:
+                return (c16 ? 10.0 : 12.0) * (double)stored + 4.0 * (nsl + 1) + (perm ? 128.0 * nsl : 0.0) +
+                       (c16 ? 128.0 * nsl : 0.0);
             case FMT_SDIA:
                 return 8.0 * (double)stored + 4.0 * (double)stored / 32.0 + 4.0 * (nsl + 1) +
                        (anchor ? 4.0 * (double)nrows : 0.0);
-            default: return 12.0 * (double)nnz + 4.0 * (double)(nrows + 1);
+            default: return (c16 ? 10.0 : 12.0) * (double)nnz + 4.0 * (double)(nrows + 1) + (c16 ? 4.0 * nrows : 0.0);
         }
     }
     void release() {
@@ -110,6 +116,10 @@ struct DevMat {
         cudaFree(col);
         cudaFree(val);
         cudaFree(perm);
+        cudaFree(c16);
+        cudaFree(cbase);
+        c16 = nullptr;
+        cbase = nullptr;
         sptr = nullptr;
         offs = nullptr;
         anchor = nullptr;
@@ -498,10 +508,10 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)k_sell<G, E>));
         const int64_t need = ((u1 - u0 - kspan) * 32 + kBlock - 1) / kBlock;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1, k0, kspan, M.perm},
+        launch_k(k_sell<G, E>, grid, kBlock, L.s, SellView{M.sptr, M.col, M.val, M.nrows, u0, u1, k0, kspan, M.perm, M.c16, M.cbase},
                  g, e, rc);
     } else {
-        const CsrView v{M.rp, M.col, M.val, M.nrows, u0, u1, k0, kspan};
+        const CsrView v{M.rp, M.col, M.val, M.nrows, u0, u1, k0, kspan, M.c16, M.cbase};
         const int64_t need = ((u1 - u0 - kspan) * M.vw + kBlock - 1) / kBlock;
         if (M.vw == kVWBlock) {
             const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)k_csrb<G, E>));
@@ -767,6 +777,7 @@ struct TailEmitter {
         return o;
     }
     void spmv(const DevMat& M, int epi, const double* g, double* y, int64_t nvec) {
+        if (M.c16) std::abort();  // the tail's levels are uploaded with 32-bit columns (C16Scope)
         TailOp o = op(TK_SPMV, epi);
         o.rp = M.rp;
         o.ci = M.col;
@@ -1673,8 +1684,109 @@ void interior_run(const std::vector<char>& flag, int64_t& b0, int64_t& b1) {
 
 // own_lo/own_hi: columns (window frame) owned by this rank for the gathered vector;
 // own_lo < 0: no split (single rank, replicated levels)
-int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bool force_csr = false,
-               int64_t own_lo = -1, int64_t own_hi = -1) {
+// ------------------------------------------------------------- 16-bit columns
+// A SELL / CSR operator whose rows each span fewer than 2^16 columns stores col - cbase as
+// uint16 (cbase = the row's smallest column; per slot for SELL, per row for CSR): 10 instead of
+// 12 bytes per entry on the deep aggregation levels (c4 A_2 / A_3: 168 / 735 entries per row,
+// spans <= 33k).  Same entries, same order: results bitwise equal.  Off with AMG_NO_C16=1, and
+// for levels of the persistent tail (its TailOp reads 32-bit columns).
+thread_local bool g_c16_allowed = true;
+struct C16Scope {
+    bool saved;
+    explicit C16Scope(bool allow) : saved(g_c16_allowed) {
+        const char* e = std::getenv("AMG_NO_C16");
+        g_c16_allowed = allow && !(e && e[0] == '1');
+    }
+    ~C16Scope() { g_c16_allowed = saved; }
+};
+// per unit (SELL slot / CSR row): smallest column -> base, largest span -> atomicMax(*span)
+__global__ void kc_c16_span(const uint32_t* __restrict__ sptr, const int32_t* __restrict__ rp,
+                            const int32_t* __restrict__ col, int64_t nunits, int32_t* base, int* span) {
+    int mx = 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nunits; q += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k0, k1, stride;
+        if (sptr) {
+            k0 = (int64_t)sptr[q >> 5] * 32 + (q & 31);
+            k1 = (int64_t)sptr[(q >> 5) + 1] * 32 + (q & 31);
+            stride = 32;
+        } else {
+            k0 = rp[q];
+            k1 = rp[q + 1];
+            stride = 1;
+        }
+        int32_t lo = INT32_MAX, hi = INT32_MIN;
+        for (int64_t k = k0; k < k1; k += stride) {
+            lo = min(lo, col[k]);
+            hi = max(hi, col[k]);
+        }
+        if (k1 <= k0) lo = hi = 0;
+        base[q] = lo;
+        mx = max(mx, hi - lo);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(span, mx);
+}
+__global__ void kc_c16_fill(const uint32_t* __restrict__ sptr, const int32_t* __restrict__ rp,
+                            const int32_t* __restrict__ col, int64_t nunits, const int32_t* __restrict__ base,
+                            uint16_t* c16) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nunits; q += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k0, k1, stride;
+        if (sptr) {
+            k0 = (int64_t)sptr[q >> 5] * 32 + (q & 31);
+            k1 = (int64_t)sptr[(q >> 5) + 1] * 32 + (q & 31);
+            stride = 32;
+        } else {
+            k0 = rp[q];
+            k1 = rp[q + 1];
+            stride = 1;
+        }
+        for (int64_t k = k0; k < k1; k += stride) c16[k] = (uint16_t)(col[k] - base[q]);
+    }
+}
+// SELL / CSR-vector operator with 32-bit columns -> 16-bit columns when every unit's span fits
+// (and rows are long enough, >= 4 entries on average, for the 4 B per-row base to pay)
+int compress_cols(DevMat& D, cudaStream_t s) {
+    if (!g_c16_allowed || !D.col || (D.fmt != FMT_SELL && D.fmt != FMT_CSRV) || D.nrows <= 0 ||
+        (double)D.nnz < 4.0 * (double)D.nrows)
+        return AMG_OK;
+    const bool sell = D.fmt == FMT_SELL;
+    const int64_t nunits = sell ? D.units * 32 : D.nrows;
+    const int64_t ncol = sell ? D.stored : D.nnz;
+    int32_t* base = nullptr;
+    int* dspan = nullptr;
+    int st;
+    if ((st = dev_alloc(&base, (size_t)nunits))) return st;
+    if ((st = dev_alloc(&dspan, 1))) {
+        cudaFree(base);
+        return st;
+    }
+    const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((nunits + 255) / 256, 148 * 16));
+    CK(cudaMemsetAsync(dspan, 0, sizeof(int), s));
+    kc_c16_span<<<gs, 256, 0, s>>>(sell ? D.sptr : nullptr, D.rp, D.col, nunits, base, dspan);
+    int span = 0;
+    CK(cudaMemcpyAsync(&span, dspan, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(dspan);
+    if (span >= 65536) {
+        cudaFree(base);
+        return AMG_OK;
+    }
+    uint16_t* c16 = nullptr;
+    if ((st = dev_alloc(&c16, (size_t)std::max<int64_t>(1, ncol)))) {
+        cudaFree(base);
+        return st;
+    }
+    kc_c16_fill<<<gs, 256, 0, s>>>(sell ? D.sptr : nullptr, D.rp, D.col, nunits, base, c16);
+    CK(cudaStreamSynchronize(s));
+    cudaFree(D.col);
+    D.col = nullptr;
+    D.c16 = c16;
+    D.cbase = base;
+    return AMG_OK;
+}
+
+int upload_mat_fmt(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bool force_csr,
+                   int64_t own_lo, int64_t own_hi) {
     const int64_t n = M.nrows, nnz = M.nnz();
     D.nrows = n;
     D.ncols = M.ncols;
@@ -1839,6 +1951,11 @@ int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bo
     if ((st = dev_copy(&D.val, M.v.data(), M.v.size()))) return st;
     return AMG_OK;
 }
+int upload_mat(const amgsetup::Csr& M, DevMat& D, bool square, int64_t shift, bool force_csr = false,
+               int64_t own_lo = -1, int64_t own_hi = -1) {
+    int st = upload_mat_fmt(M, D, square, shift, force_csr, own_lo, own_hi);
+    return st ? st : compress_cols(D, 0);
+}
 
 
 // ------------------------------------------------------------- device-side formats
@@ -1966,7 +2083,7 @@ static double sigma_mean_max() {  // AMG_SIGMA_MEAN_MAX: experiment knob (defaul
     return e ? std::atof(e) : 128.0;
 }
 
-int convert_mat(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t shift, bool force_csr, cudaStream_t s) {
+int convert_mat_fmt(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t shift, bool force_csr, cudaStream_t s) {
     const int64_t n = M.nrows, nnz = M.nnz;
     D.nrows = n;
     D.ncols = M.ncols;
@@ -2100,6 +2217,10 @@ int convert_mat(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t sh
     }
     CK(cudaStreamSynchronize(s));
     return AMG_OK;
+}
+int convert_mat(const amgsetup::DevCsrRaw& M, DevMat& D, bool square, int64_t shift, bool force_csr, cudaStream_t s) {
+    int st = convert_mat_fmt(M, D, square, shift, force_csr, s);
+    return st ? st : compress_cols(D, s);
 }
 
 // Coarse CG (cfg.coarse_solver == 1): CSR of the replicated A_L, its l1 diagonal,
@@ -2378,6 +2499,7 @@ std::vector<double> collapse_above(const CompactHost& c, const std::vector<doubl
 
 int upload_rank(amg_hier_s* h, const amgsetup::RankPlan& P, const std::vector<double>& coarse_inv, RankState& R,
                 const amgsetup::DeviceKeep* dk = nullptr) {
+    const C16Scope c16_scope(h->tail_level < 0);
     const int nl = (int)P.lv.size();
     R.rank = P.rank;
     R.lv.resize(nl);

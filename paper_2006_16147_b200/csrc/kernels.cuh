@@ -295,6 +295,11 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
+__device__ __forceinline__ int32_t ld_stream(const uint16_t* p) {
+    unsigned short r;
+    asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+    return (int32_t)r;
+}
 
 // --------------------------------------------------------------- gathers
 struct GVec {  // x_j
@@ -723,6 +728,9 @@ struct SellView {
     // SELL-32-sigma: slot (slice, lane) -> row (rows sorted by length inside windows of
     // sigma rows; -1 = padding slot); null for plain SELL-32 (slot = row)
     const int32_t* __restrict__ perm;
+    // 16-bit columns (col null): column = cbase[slot] + c16[k]
+    const uint16_t* __restrict__ c16 = nullptr;
+    const int32_t* __restrict__ cbase = nullptr;
 };
 
 // Row-chunk of exactly W entries of one slice (lane = row): the W value loads are
@@ -804,12 +812,19 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<G, E>::v) k_sell(SellView A,
         const int64_t s = vs + (vs >= A.k0 ? A.kspan : 0);
         const uint32_t b0 = __ldg(A.sptr + s);
         const uint32_t w = __ldg(A.sptr + s + 1) - b0;
-        const int32_t* c = A.col + (int64_t)b0 * 32 + lane;
         const double* v = A.val + (int64_t)b0 * 32 + lane;
         double acc = 0.0, asum = 0.0;
         const int64_t row = A.perm ? (int64_t)__ldg(A.perm + (s << 5) + lane) : (s << 5) + lane;
         if (AMG_EPI_PREFETCH && row >= 0 && row < A.n) epi_prefetch(e, row);
-        slice_row<G::kChunk, E::kAbs>(v, w, [&](uint32_t k) { return ld_stream(c + 32 * k); }, g, acc, asum);
+        if (A.c16) {
+            const int32_t cb = __ldg(A.cbase + (s << 5) + lane);
+            const uint16_t* c = A.c16 + (int64_t)b0 * 32 + lane;
+            slice_row<G::kChunk, E::kAbs>(v, w, [&](uint32_t k) { return cb + ld_stream(c + 32 * k); }, g, acc,
+                                          asum);
+        } else {
+            const int32_t* c = A.col + (int64_t)b0 * 32 + lane;
+            slice_row<G::kChunk, E::kAbs>(v, w, [&](uint32_t k) { return ld_stream(c + 32 * k); }, g, acc, asum);
+        }
         if (row >= 0 && row < A.n) d += apply_epi(e, row, acc, asum);
     }
     if constexpr (E::kDot) grid_reduce(d, rc);
@@ -870,21 +885,28 @@ struct CsrView {
     int64_t n;
     int64_t r0 = 0, r1 = 0;  // row range of this launch (k_csrv / k_csrb)
     int64_t k0 = 0, kspan = 0;  // skipped rows [k0, k0 + kspan) (see SellView)
+    // 16-bit columns (ci null): column = cbase[row] + c16[k]
+    const uint16_t* __restrict__ c16 = nullptr;
+    const int32_t* __restrict__ cbase = nullptr;
 };
 
 // One lane's share of a CSR row: entries k, k+S, k+2S, ... < k1 (S lanes per row),
 // in chunks of 4 whose loads are all issued before the FMAs (cf. row_chunk), then
 // at most 3 single entries.  Ascending order per lane, as before.
-template <int S, bool ABS, class G>
+template <int S, bool ABS, bool C16 = false, class G>
 __device__ __forceinline__ void csr_lane_row(const CsrView& A, int32_t k, int32_t k1, const G& g, double& acc,
-                                             double& asum) {
+                                             double& asum, int32_t cb = 0) {
+    auto col = [&](int32_t t) -> int32_t {
+        if constexpr (C16) return cb + ld_stream(A.c16 + t);
+        else return ld_stream(A.ci + t);
+    };
     for (; k + 3 * S < k1; k += 4 * S) {
         double a[4], x[4];
         int32_t c[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) a[j] = ld_stream(A.v + k + j * S);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) c[j] = ld_stream(A.ci + k + j * S);
+        for (int j = 0; j < 4; ++j) c[j] = col(k + j * S);
 #pragma unroll
         for (int j = 0; j < 4; ++j) x[j] = g(c[j]);
 #pragma unroll
@@ -895,7 +917,7 @@ __device__ __forceinline__ void csr_lane_row(const CsrView& A, int32_t k, int32_
     }
     for (; k < k1; k += S) {
         const double a = ld_stream(A.v + k);
-        acc += a * g(ld_stream(A.ci + k));
+        acc += a * g(col(k));
         if constexpr (ABS) asum += fabs(a);
     }
 }
@@ -919,7 +941,8 @@ __global__ void __launch_bounds__(kBlock) k_csrv(CsrView A, G g, E e, RedCtx rc)
         double acc = 0.0, asum = 0.0;
         if (vr < rend) {
             const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
-            csr_lane_row<VW, E::kAbs>(A, k0 + sub, k1, g, acc, asum);
+            if (A.c16) csr_lane_row<VW, E::kAbs, true>(A, k0 + sub, k1, g, acc, asum, __ldg(A.cbase + row));
+            else csr_lane_row<VW, E::kAbs>(A, k0 + sub, k1, g, acc, asum);
         }
 #pragma unroll
         for (int o = VW / 2; o > 0; o >>= 1) {
@@ -946,7 +969,10 @@ __global__ void __launch_bounds__(kBlock) k_csrb(CsrView A, G g, E e, RedCtx rc)
         const int64_t row = vr + (vr >= A.k0 ? A.kspan : 0);
         const int32_t k0 = __ldg(A.rp + row), k1 = __ldg(A.rp + row + 1);
         double acc = 0.0, asum = 0.0;
-        csr_lane_row<kBlock, E::kAbs>(A, k0 + (int32_t)threadIdx.x, k1, g, acc, asum);
+        if (A.c16)
+            csr_lane_row<kBlock, E::kAbs, true>(A, k0 + (int32_t)threadIdx.x, k1, g, acc, asum, __ldg(A.cbase + row));
+        else
+            csr_lane_row<kBlock, E::kAbs>(A, k0 + (int32_t)threadIdx.x, k1, g, acc, asum);
         for (int o = 16; o > 0; o >>= 1) {
             acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if constexpr (E::kAbs) asum += __shfl_xor_sync(0xffffffffu, asum, o);

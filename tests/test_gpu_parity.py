@@ -413,6 +413,31 @@ def test_compact_and_collapsed_levels_are_taken(ctx):
     assert np.linalg.norm(z - zo) / np.linalg.norm(zo) <= VCYCLE_TOL
 
 
+@pytest.mark.parametrize("name", ["c2", "c5_72", "islands"])
+def test_16bit_columns_bitwise_equal_to_32bit(ctx, name):
+    """Operators whose rows span < 2^16 columns store 16-bit column offsets from a per-row (per
+    SELL slot) base instead of int32 columns: the same entries in the same order, so the V-cycle
+    and the PCG iterates are bitwise equal to the 32-bit form (AMG_NO_C16=1), with fewer bytes."""
+    amg = _amg()
+    A, b, _, lkw = _case(name)
+    h16 = amg.Hierarchy(ctx, A, cfg=_cfg(**lkw))
+    os.environ["AMG_NO_C16"] = "1"
+    try:
+        h32 = amg.Hierarchy(ctx, A, cfg=_cfg(**lkw))
+    finally:
+        os.environ.pop("AMG_NO_C16", None)
+    p16, p32 = h16.profile_vcycle(1), h32.profile_vcycle(1)
+    assert [k["name"] for k in p16] == [k["name"] for k in p32]
+    s16, s32 = sum(k["stored_bytes"] for k in p16), sum(k["stored_bytes"] for k in p32)
+    assert s16 < s32, (s16, s32)
+    r = torch.tensor(uniform_pm1(77, A.n_global), device="cuda:0")
+    assert torch.equal(h16.precond_apply(r), h32.precond_apply(r))
+    bt = torch.tensor(b, device="cuda:0")
+    x16, r16 = h16.solve(bt, rtol=1e-8)
+    x32, r32 = h32.solve(bt, rtol=1e-8)
+    assert r16["iterations"] == r32["iterations"] and torch.equal(x16, x32)
+
+
 def test_solve_host_batch_equals_single_solves(ctx):
     """amg_solve_host_batch (copies pipelined with the solves over two device buffer pairs)
     returns exactly the solutions and reports of one amg_solve_host per right-hand side."""
