@@ -848,6 +848,18 @@ struct SdiaView {
     int64_t k0 = 0, kspan = 0;           // skipped slices [k0, k0 + kspan) (see SellView)
 };
 
+#ifndef AMG_SDIA_GPZ_CHUNK
+#define AMG_SDIA_GPZ_CHUNK 8
+#endif
+template <class G>
+struct SdiaChunk {
+    static constexpr int v = 8;
+};
+template <>
+struct SdiaChunk<GPz> {
+    static constexpr int v = AMG_SDIA_GPZ_CHUNK;
+};
+
 template <class G, class E>
 __global__ void __launch_bounds__(kBlock, MinBlocks<G, E>::v) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
     pdl_begin();
@@ -869,8 +881,9 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<G, E>::v) k_sdia(SdiaView A,
         const int32_t rmax = A.ncols - 1;
         double acc = 0.0, asum = 0.0;
         // SDIA needs no registers for column indices: full chunks of 8 for every gather
+        // (AMG_SDIA_GPZ_CHUNK: the chunk of the two-vector gather of q = A p, an A/B knob)
         if (AMG_EPI_PREFETCH && row < A.n) epi_prefetch(e, row);
-        slice_row<8, E::kAbs>(v, w, [&](uint32_t k) { return min(max(base + __ldg(o + k), 0), rmax); }, g, acc,
+        slice_row<SdiaChunk<G>::v, E::kAbs>(v, w, [&](uint32_t k) { return min(max(base + __ldg(o + k), 0), rmax); }, g, acc,
                               asum);
         if (row < A.n) d += apply_epi(e, row, acc, asum);
     }
