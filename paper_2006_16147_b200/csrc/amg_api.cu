@@ -1746,8 +1746,12 @@ __global__ void kc_c16_fill(const uint32_t* __restrict__ sptr, const int32_t* __
 // SELL / CSR-vector operator with 32-bit columns -> 16-bit columns when every unit's span fits
 // (and rows are long enough, >= 4 entries on average, for the 4 B per-row base to pay)
 int compress_cols(DevMat& D, cudaStream_t s) {
+    static const double min_mean = [] {  // AMG_C16_MIN_MEAN: an A/B knob (default 4 entries per row)
+        const char* e = std::getenv("AMG_C16_MIN_MEAN");
+        return e ? std::atof(e) : 4.0;
+    }();
     if (!g_c16_allowed || !D.col || (D.fmt != FMT_SELL && D.fmt != FMT_CSRV) || D.nrows <= 0 ||
-        (double)D.nnz < 4.0 * (double)D.nrows)
+        (double)D.nnz < min_mean * (double)D.nrows)
         return AMG_OK;
     const bool sell = D.fmt == FMT_SELL;
     const int64_t nunits = sell ? D.units * 32 : D.nrows;
