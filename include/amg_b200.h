@@ -179,9 +179,14 @@ int amg_nccl_unique_id(void* out128);
  * (a cudaStream_t; NULL = a non-blocking stream created and owned by the context —
  * CUDA graphs cannot be captured on the legacy default stream).  For nranks > 1,
  * `nccl_unique_id` points to the 128-byte ncclUniqueId produced by rank 0 and
- * broadcast by the caller (e.g. through torch.distributed); it is ignored when
- * nranks == 1.  Returns AMG_ERR_ARG for rank/nranks out of range, AMG_ERR_CUDA /
- * AMG_ERR_NCCL when the device or communicator cannot be initialised. */
+ * broadcast by the caller (e.g. through torch.distributed).  With nranks == 1 a
+ * non-NULL id creates a ONE-rank communicator: hierarchies built with emulate_ranks > 1
+ * on that context then move every halo and dot slot by NCCL self send/recv instead of
+ * device copies ("NCCL loopback"), taking the real ranks' code path -- graph capture of
+ * the collectives and its collective fallback included -- on one GPU (testing aid; the
+ * arithmetic is unchanged, results are bitwise those of the device-copy loopback).
+ * Returns AMG_ERR_ARG for rank/nranks out of range, AMG_ERR_CUDA / AMG_ERR_NCCL when
+ * the device or communicator cannot be initialised. */
 int amg_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
                    void* cuda_stream, amg_ctx_t* out);
 /* Destroy the hierarchies built on a context before the context itself. */
@@ -240,6 +245,12 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev);
  * rows aligned by column offset, no per-entry column index, 4 = SELL-32-sigma: SELL-32
  * over rows sorted by length inside windows of 256 rows, with a slot -> row map). */
 int amg_num_levels(amg_hier_t h, int32_t* nlevels);
+/* Shape the solves of h currently take (use_graphs = 1): 0 = one CUDA graph per solve
+ * with a device-side WHILE node over the iteration; 1 = one graph per iteration from a
+ * host loop (NCCL transports fall back to it, collectively, when a collective cannot be
+ * captured into the WHILE body; AMG_MULTI_GRAPH=iter forces it); 2 = eager launches
+ * (use_graphs = 0, or no graph could be captured).  Set by the first solve. */
+int amg_solve_graph_mode(amg_hier_t h, int32_t* mode);
 int amg_level_info(amg_hier_t h, int32_t lvl, int64_t* n_global, int64_t* nnzA_global,
                    int64_t* nnzP_global, int64_t* row_begin, int64_t* row_end, int32_t* format);
 /* Aggregate map of level lvl (lvl < nlevels-1): for each local row of level lvl the

@@ -110,6 +110,12 @@ class Hierarchy:
         check(lib.amg_level_aggregates(self.h, l, _ptr(out)), "amg_level_aggregates")
         return out
 
+    def graph_mode(self) -> str:
+        """amg_solve_graph_mode: 'while' (one graph per solve), 'iter' (one per iteration) or 'eager'."""
+        m = C.c_int32()
+        check(lib.amg_solve_graph_mode(self.h, C.byref(m)), "amg_solve_graph_mode")
+        return ("while", "iter", "eager")[m.value]
+
     def report(self) -> dict:
         r = amg_report_t()
         check(lib.amg_hierarchy_report(self.h, C.byref(r)), "amg_hierarchy_report")

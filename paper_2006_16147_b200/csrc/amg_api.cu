@@ -34,6 +34,7 @@
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <set>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -274,6 +275,10 @@ struct amg_ctx_s {
     // launch caps (SM count x resident blocks) per kernel, computed once per context
     std::unordered_map<const void*, int> caps;
     std::mutex caps_mu;
+    // live hierarchies built on this context: amg_ctx_destroy releases their CUDA graphs before
+    // destroying the communicator (graphs holding captured NCCL work would block it forever)
+    std::set<struct amg_hier_s*> hiers;
+    std::mutex hiers_mu;
 };
 
 struct amg_hier_s {
@@ -332,20 +337,36 @@ struct amg_hier_s {
     std::string nccl_what;
 
     bool multi() const { return np > 1; }
+    // halos and dot slots travel through NCCL: real ranks, or loopback on a context that holds a
+    // one-rank communicator (every transfer a self send/recv -- the captured NCCL transport
+    // exercised on one GPU, no kernel waiting on another rank)
+    bool nccl_xport() const { return multi() && ctx->nccl != nullptr; }
+    bool loop_nccl() const { return loopback && nccl_xport(); }
     int nlev() const { return (int)ranks[0].lv.size(); }
+    void release_graphs() {
+        if (solve_exec) cudaGraphExecDestroy(solve_exec);
+        solve_exec = nullptr;
+        solve_b = nullptr;
+        solve_x = nullptr;
+        for (int q = 0; q < 2; ++q) {
+            if (batch_exec[q]) cudaGraphExecDestroy(batch_exec[q]);
+            batch_exec[q] = nullptr;
+        }
+        if (apply_exec) cudaGraphExecDestroy(apply_exec);
+        apply_exec = nullptr;
+        if (iter_exec) cudaGraphExecDestroy(iter_exec);
+        iter_exec = nullptr;
+    }
     ~amg_hier_s() {
         cudaFree(tail_prog);
         cudaFree(tail_partials);
-        if (solve_exec) cudaGraphExecDestroy(solve_exec);
+        release_graphs();
         for (int q = 0; q < 2; ++q) {
-            if (batch_exec[q]) cudaGraphExecDestroy(batch_exec[q]);
             cudaFree(bb[q]);
             cudaFree(bx[q]);
         }
         if (cstream) cudaStreamDestroy(cstream);
         if (dstream) cudaStreamDestroy(dstream);
-        if (apply_exec) cudaGraphExecDestroy(apply_exec);
-        if (iter_exec) cudaGraphExecDestroy(iter_exec);
         for (auto& R : ranks) R.release();
         cudaFree(hb);
         cudaFree(hx);
@@ -562,10 +583,25 @@ void nccl_note(amg_hier_s* h, ncclResult_t r, const char* what) {
     }
 }
 
+// Loopback over a one-rank NCCL communicator: every (destination, source) rank pair's dot slots
+// as one self send/recv of a group (NCCL matches a peer's sends and receives in issue order).
+void loop_nccl_dots(amg_hier_s* h, cudaStream_t s) {
+    nccl_note(h, ncclGroupStart(), "ncclGroupStart (loopback dots)");
+    for (auto& Rd : h->ranks)
+        for (auto& Rs : h->ranks) {
+            nccl_note(h, ncclSend(Rs.dot_local, kDotSlots, ncclDouble, 0, h->ctx->nccl, s), "ncclSend (loopback dots)");
+            nccl_note(h, ncclRecv(Rd.dot_all + kDotSlots * Rs.rank, kDotSlots, ncclDouble, 0, h->ctx->nccl, s),
+                      "ncclRecv (loopback dots)");
+        }
+    nccl_note(h, ncclGroupEnd(), "ncclGroupEnd (loopback dots)");
+}
+
 // Multi-rank: gather every rank's dot total to every rank, then finish in rank order.
 void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0) {
     if (!h->multi()) return;
-    if (h->loopback) {
+    if (h->loop_nccl()) {
+        loop_nccl_dots(h, L.s);
+    } else if (h->loopback) {
         for (auto& Rd : h->ranks)
             for (auto& Rs : h->ranks)
                 cudaMemcpyAsync(Rd.dot_all + kDotSlots * Rs.rank, Rs.dot_local, kDotSlots * sizeof(double),
@@ -588,7 +624,9 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0)
 // Several ranks, K-cycle: the same gather, finished into each rank's level-lvl K state.
 void dot_finish_k(amg_hier_s* h, Launch& L, int kind, int lvl) {
     if (!h->multi()) return;
-    if (h->loopback) {
+    if (h->loop_nccl()) {
+        loop_nccl_dots(h, L.s);
+    } else if (h->loopback) {
         for (auto& Rd : h->ranks)
             for (auto& Rs : h->ranks)
                 cudaMemcpyAsync(Rd.dot_all + kDotSlots * Rs.rank, Rs.dot_local, kDotSlots * sizeof(double),
@@ -683,16 +721,26 @@ void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const 
         cudaStreamWaitEvent(st, h->ev_fork, 0);
     }
     if (h->loopback) {
+        const bool nc = h->loop_nccl();
+        if (nc) nccl_note(h, ncclGroupStart(), "ncclGroupStart (loopback halo)");
         for (auto& Rd : h->ranks) {
             const Exch& Ed = Rd.lv[l].ex;
             for (auto& Rs : h->ranks) {
                 const int64_t cnt = Ed.recv_off[Rs.rank + 1] - Ed.recv_off[Rs.rank];
                 if (!cnt) continue;
                 const Exch& Es = Rs.lv[l].ex;
-                cudaMemcpyAsync(Ed.rbuf + Ed.recv_off[Rs.rank], Es.sbuf + Es.send_off[Rd.rank], cnt * sizeof(double),
-                                cudaMemcpyDeviceToDevice, L.s);
+                if (nc) {
+                    nccl_note(h, ncclSend(Es.sbuf + Es.send_off[Rd.rank], cnt, ncclDouble, 0, h->ctx->nccl, L.s),
+                              "ncclSend (loopback halo)");
+                    nccl_note(h, ncclRecv(Ed.rbuf + Ed.recv_off[Rs.rank], cnt, ncclDouble, 0, h->ctx->nccl, L.s),
+                              "ncclRecv (loopback halo)");
+                } else {
+                    cudaMemcpyAsync(Ed.rbuf + Ed.recv_off[Rs.rank], Es.sbuf + Es.send_off[Rd.rank],
+                                    cnt * sizeof(double), cudaMemcpyDeviceToDevice, L.s);
+                }
             }
         }
+        if (nc) nccl_note(h, ncclGroupEnd(), "ncclGroupEnd (loopback halo)");
     } else {
         RankState& R = h->ranks[0];
         const Exch& E = R.lv[l].ex;
@@ -2773,7 +2821,7 @@ enum { GM_WHILE = 0, GM_ITER = 1 };
 // match), so a local failure is agreed on with an eager all-reduce (min) of the success flags.
 int agree_ok(amg_hier_s* h, int ok_local, int* ok_all) {
     *ok_all = ok_local;
-    if (!h->multi() || h->loopback) return AMG_OK;
+    if (!h->nccl_xport()) return AMG_OK;
     int* d = nullptr;
     CK(cudaMalloc(&d, sizeof(int)));
     CK(cudaMemcpy(d, &ok_local, sizeof(int), cudaMemcpyHostToDevice));
@@ -2790,7 +2838,14 @@ int ensure_solve_graph(amg_hier_s* h, const double* b, double* x) {
         h->solve_exec = nullptr;
     }
     int st = build_solve_exec(h, b, x, &h->solve_exec);
-    if (h->multi() && !h->loopback) {  // NCCL: collective decision, fall back to one graph per iteration
+    if (h->nccl_xport()) {  // NCCL: collective decision, fall back to one graph per iteration
+        if (st == AMG_OK && h->nccl_status != ncclSuccess) st = AMG_ERR_NCCL;  // a collective refused capture
+        if (st != AMG_OK) {
+            std::fprintf(stderr, "amg: the NCCL solve could not be captured as one WHILE graph (%s); "
+                         "falling back to one graph per iteration\n",
+                         h->nccl_status != ncclSuccess ? h->nccl_what.c_str() : amg_last_error());
+            h->nccl_status = ncclSuccess;
+        }
         int all = 0, e;
         if ((e = agree_ok(h, st == AMG_OK ? 1 : 0, &all))) return e;
         if (!all) {
@@ -2822,8 +2877,14 @@ int ensure_iter_graph(amg_hier_s* h, double* x) {
     cudaError_t ei = cudaErrorUnknown;
     if (ec == cudaSuccess) ei = cudaGraphInstantiate(&h->iter_exec, g, 0);
     if (g) cudaGraphDestroy(g);
+    const bool nok = h->nccl_status != ncclSuccess;  // a collective refused capture: discard the graph
+    if (ec != cudaSuccess || ei != cudaSuccess || nok) {
+        std::fprintf(stderr, "amg: the iteration could not be captured as a graph (%s); eager launches\n",
+                     nok ? h->nccl_what.c_str() : cudaGetErrorString(ec != cudaSuccess ? ec : ei));
+        h->nccl_status = ncclSuccess;
+    }
     int all = 0, e;
-    if ((e = agree_ok(h, (ec == cudaSuccess && ei == cudaSuccess) ? 1 : 0, &all))) return e;
+    if ((e = agree_ok(h, (ec == cudaSuccess && ei == cudaSuccess && !nok) ? 1 : 0, &all))) return e;
     if (!all) {
         if (h->iter_exec && ei == cudaSuccess) cudaGraphExecDestroy(h->iter_exec);
         h->iter_exec = nullptr;
@@ -2835,10 +2896,19 @@ int ensure_iter_graph(amg_hier_s* h, double* x) {
     return AMG_OK;
 }
 // the whole solve as one graph: prologue, WHILE node over the PCG body, final x update
+// (every exit destroys the graph: a leaked graph that captured NCCL collectives keeps the
+// communicator's persistent references alive, and ncclCommDestroy then waits forever)
+struct GraphGuard {
+    cudaGraph_t g = nullptr;
+    ~GraphGuard() {
+        if (g) cudaGraphDestroy(g);
+    }
+};
 int build_solve_exec(amg_hier_s* h, const double* b, double* x, cudaGraphExec_t* out) {
     cudaStream_t s = h->ctx->stream;
-    cudaGraph_t g;
-    CK(cudaGraphCreate(&g, 0));
+    GraphGuard gg;
+    CK(cudaGraphCreate(&gg.g, 0));
+    cudaGraph_t g = gg.g;  // capture-to-graph hands the same graph back
     cudaGraphConditionalHandle cond;
     CK(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
     Launch L{h, s};
@@ -2864,8 +2934,29 @@ int build_solve_exec(amg_hier_s* h, const double* b, double* x, cudaGraphExec_t*
     CK(cudaStreamBeginCaptureToGraph(s, g, &wnode, nullptr, 1, cudaStreamCaptureModeThreadLocal));
     enqueue_pcg_final(h, L, x);
     CK(cudaStreamEndCapture(s, &g));
-    CK(cudaGraphInstantiate(out, g, 0));
-    CK(cudaGraphDestroy(g));
+    cudaGraphInstantiateParams ip = {};
+    const cudaError_t ei = cudaGraphInstantiateWithParams(out, g, &ip);
+    if (ei != cudaSuccess) {
+        // name the node the driver refused (NCCL collectives inside the WHILE body, B200 / CUDA 12.9:
+        // tests/test_gpu_nccl_loopback.py records what it is)
+        std::string what = std::string("cudaGraphInstantiate (WHILE graph): ") + cudaGetErrorString(ei) +
+                           ", result " + std::to_string((int)ip.result_out);
+        if (ip.errNode_out) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(ip.errNode_out, &t) == cudaSuccess) {
+                what += ", node type " + std::to_string((int)t);
+                cudaKernelNodeParams kp = {};
+                const char* fname = nullptr;
+                if (t == cudaGraphNodeTypeKernel && cudaGraphKernelNodeGetParams(ip.errNode_out, &kp) == cudaSuccess &&
+                    cudaFuncGetName(&fname, kp.func) == cudaSuccess && fname)
+                    what += std::string(" (kernel ") + fname + ")";
+            }
+        }
+        cudaGetLastError();
+        *out = nullptr;
+        set_err(what);
+        return AMG_ERR_CUDA;
+    }
     return AMG_OK;
 }
 
@@ -2897,12 +2988,11 @@ int ensure_apply_graph(amg_hier_s* h, const double* r, double* z) {
     }
     cudaStream_t s = h->ctx->stream;
     Launch L{h, s};
-    cudaGraph_t g;
+    GraphGuard gg;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     enqueue_apply(h, L, r, z);
-    CK(cudaStreamEndCapture(s, &g));
-    CK(cudaGraphInstantiate(&h->apply_exec, g, 0));
-    CK(cudaGraphDestroy(g));
+    CK(cudaStreamEndCapture(s, &gg.g));
+    CK(cudaGraphInstantiate(&h->apply_exec, gg.g, 0));
     h->apply_r = r;
     h->apply_z = z;
     return AMG_OK;
@@ -3559,7 +3649,7 @@ int amg_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
         }
         c->own_stream = true;
     }
-    if (nranks > 1) {
+    if (nranks > 1 || nccl_unique_id) {  // nranks == 1 with an id: a one-rank communicator (loopback transport)
         ncclUniqueId id;
         std::memcpy(&id, nccl_unique_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
@@ -3576,6 +3666,20 @@ int amg_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
 
 int amg_ctx_destroy(amg_ctx_t c) {
     if (!c) return AMG_OK;
+    {
+        // hierarchies still alive (a caller error the header warns about, and a garbage-collection
+        // order Python can produce): release their graphs now and orphan them, so the communicator
+        // is not held by captured NCCL work; amg_hierarchy_destroy still frees them later
+        std::lock_guard<std::mutex> g(c->hiers_mu);
+        for (amg_hier_s* h : c->hiers) {
+            std::lock_guard<std::recursive_mutex> hg(h->mu);
+            cudaSetDevice(h->device);
+            cudaStreamSynchronize(c->stream);
+            h->release_graphs();
+            h->ctx = nullptr;
+        }
+        c->hiers.clear();
+    }
     if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -3866,15 +3970,24 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     CK(cudaDeviceSynchronize());
     h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    {
+        std::lock_guard<std::mutex> g(ctx->hiers_mu);
+        ctx->hiers.insert(h);
+    }
     *out = h;
     return AMG_OK;
 }
 
 int amg_hierarchy_destroy(amg_hier_t h) {
     if (h) {
-        // h->ctx may already be destroyed (a caller error the Python binding can hit at garbage
-        // collection): use the device recorded at build time, and leave no error behind
+        // the context may already be destroyed (a caller error the Python binding can hit at garbage
+        // collection; amg_ctx_destroy then orphaned h, ctx = null): use the device recorded at build
+        // time, and leave no error behind
         cudaSetDevice(h->device);
+        if (amg_ctx_s* c = h->ctx) {
+            std::lock_guard<std::mutex> g(c->hiers_mu);
+            c->hiers.erase(h);
+        }
         delete h;
         cudaGetLastError();
     }
@@ -3967,7 +4080,7 @@ int amg_solve_host_batch(amg_hier_t h, int32_t nrhs, const double* B_host, doubl
     const int64_t n = h->n0_local;
     int code = AMG_OK;
     // NCCL ranks / eager launches: one solve after another (loopback pipelines like one rank)
-    if ((h->multi() && !h->loopback) || !h->cfg.use_graphs) {
+    if (h->nccl_xport() || !h->cfg.use_graphs) {
         for (int32_t k = 0; k < nrhs; ++k) {
             const int c = amg_solve_host(h, B_host + k * n, X_host + k * n, rtol, maxit, reps ? reps + k : nullptr);
             if (c != AMG_OK && c != AMG_NOT_CONVERGED && c != AMG_ERR_BREAKDOWN) return c;
@@ -4096,7 +4209,7 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
     CK(cudaSetDevice(h->ctx->device));
     cudaStream_t s = h->ctx->stream;
     h->nccl_status = ncclSuccess;
-    if (h->cfg.use_graphs && (!h->multi() || h->loopback)) {
+    if (h->cfg.use_graphs && !h->nccl_xport()) {
         int e = ensure_apply_graph(h, r_dev, z_dev);
         if (e) return e;
         CK(cudaGraphLaunch(h->apply_exec, s));
@@ -4107,6 +4220,16 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
     }
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
+    return AMG_OK;
+}
+
+int amg_solve_graph_mode(amg_hier_t h, int32_t* mode) {
+    if (!h || !mode) {
+        set_err("amg_solve_graph_mode: null argument");
+        return AMG_ERR_ARG;
+    }
+    std::lock_guard<std::recursive_mutex> guard(h->mu);
+    *mode = h->cfg.use_graphs ? (int32_t)h->graph_mode : 2;
     return AMG_OK;
 }
 
