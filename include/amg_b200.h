@@ -251,6 +251,16 @@ int amg_num_levels(amg_hier_t h, int32_t* nlevels);
  * captured into the WHILE body; AMG_MULTI_GRAPH=iter forces it); 2 = eager launches
  * (use_graphs = 0, or no graph could be captured).  Set by the first solve. */
 int amg_solve_graph_mode(amg_hier_t h, int32_t* mode);
+/* How h moves halos and dot slots between ranks: 0 = one rank (nothing to move); 1 = device
+ * copies (loopback without a communicator); 2 = NCCL send/recv + all-gather (the fallback);
+ * 3 = peer memory over an NCCL symmetric window ("LSA": the sending kernel stores halo values
+ * and dot slots straight into the receivers' windows over NVLink, then a flag barrier with
+ * system-scope release/acquire; no NCCL call inside the solve, so it stays one WHILE graph).
+ * NCCL contexts take 3 when the window can be registered, every rank is in one load/store
+ * domain and an end-to-end check passes on every rank (decided collectively at build);
+ * AMG_TRANSPORT=nccl forces 2.  A barrier that waits 60 s for a peer makes the solve return
+ * AMG_ERR_NCCL instead of hanging. */
+int amg_comm_transport(amg_hier_t h, int32_t* transport);
 int amg_level_info(amg_hier_t h, int32_t lvl, int64_t* n_global, int64_t* nnzA_global,
                    int64_t* nnzP_global, int64_t* row_begin, int64_t* row_end, int32_t* format);
 /* Aggregate map of level lvl (lvl < nlevels-1): for each local row of level lvl the

@@ -116,6 +116,12 @@ class Hierarchy:
         check(lib.amg_solve_graph_mode(self.h, C.byref(m)), "amg_solve_graph_mode")
         return ("while", "iter", "eager")[m.value]
 
+    def transport(self) -> str:
+        """amg_comm_transport: 'none', 'copies', 'nccl' or 'lsa' (peer memory)."""
+        t = C.c_int32()
+        check(lib.amg_comm_transport(self.h, C.byref(t)), "amg_comm_transport")
+        return ("none", "copies", "nccl", "lsa")[t.value]
+
     def report(self) -> dict:
         r = amg_report_t()
         check(lib.amg_hierarchy_report(self.h, C.byref(r)), "amg_hierarchy_report")

@@ -61,6 +61,7 @@ _SIG = {
     "amg_precond_apply": (C.c_int, [_vp, _vp, _vp]),
     "amg_num_levels": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "amg_solve_graph_mode": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
+    "amg_comm_transport": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "amg_level_info": (C.c_int, [_vp, C.c_int32, _i64p, _i64p, _i64p, _i64p, _i64p,
                                  C.POINTER(C.c_int32)]),
     "amg_level_aggregates": (C.c_int, [_vp, C.c_int32, _vp]),

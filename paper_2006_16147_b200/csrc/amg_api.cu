@@ -23,6 +23,7 @@
 // which is how the multi-rank kernels are parity-tested on a single B200.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 #include <nvtx3/nvToolsExt.h>
 #include <omp.h>
 
@@ -137,14 +138,22 @@ struct Exch {
     int32_t* send_idx = nullptr;              // window positions to pack
     int32_t* recv_idx = nullptr;              // window positions to unpack into
     double* sbuf = nullptr;
-    double* rbuf = nullptr;
+    double* rbuf = nullptr;       // LSA transport: region 0 of this level in the rank's window segment
+    int64_t* d_send_off = nullptr;  // LSA: device copy of send_off
+    int64_t* d_dst_off = nullptr;   // LSA: np byte offsets of my data in each destination's region 0
+    bool rbuf_in_window = false;
+    const unsigned long long* rx_seq = nullptr;  // LSA: the receiver's barrier count (region parity)
+    int64_t rx_stride = 0;                        // LSA: doubles between the region's two parities
     void release() {
         cudaFree(send_idx);
         cudaFree(recv_idx);
         cudaFree(sbuf);
-        cudaFree(rbuf);
+        if (!rbuf_in_window) cudaFree(rbuf);
+        cudaFree(d_send_off);
+        cudaFree(d_dst_off);
         send_idx = recv_idx = nullptr;
         sbuf = rbuf = nullptr;
+        d_send_off = d_dst_off = nullptr;
     }
 };
 
@@ -229,6 +238,12 @@ struct RankState {
     unsigned int* ticket = nullptr;
     double* dot_local = nullptr;  // this rank's dot total
     double* dot_all = nullptr;    // all-gathered totals (np)
+    // LSA transport: barriers completed by this rank, the push kernel's block counter, the dot
+    // region (region 0) and the barrier flags in this rank's window segment
+    unsigned long long* lsa_seq = nullptr;
+    unsigned int* lsa_count = nullptr;
+    double* lsa_dots = nullptr;
+    unsigned long long* lsa_flags = nullptr;
     // coarsest iterative solve (cfg.coarse_solver == 1): CSR of A_L, its l1 diagonal,
     // the per-CTA row split and the cluster launch shape of k_coarse_cg
     int32_t *cg_rp = nullptr, *cg_ci = nullptr, *cg_split = nullptr;
@@ -260,6 +275,8 @@ struct RankState {
         cudaFree(ticket);
         cudaFree(dot_local);
         cudaFree(dot_all);
+        cudaFree(lsa_seq);
+        cudaFree(lsa_count);
     }
     const DevLevel& L0() const { return lv[0]; }
 };
@@ -332,6 +349,29 @@ struct amg_hier_s {
     // one solve / apply at a time per hierarchy: the graphs, PCG vectors and staging buffers
     // are per-hierarchy state (include/amg_b200.h, "Threads")
     std::recursive_mutex mu;
+    // peer-memory (LSA) transport over an NCCL symmetric window (include/amg_b200.h "Transport"):
+    // one segment per rank (np segments on a one-rank loopback communicator) holding the barrier
+    // flags, the double-buffered dot region and every distributed level's double-buffered receive region
+    bool lsa = false;
+    ncclComm_t lsa_comm = nullptr;
+    void* lsa_mem = nullptr;
+    ncclWindow_t lsa_win = nullptr;
+    int64_t lsa_seg = 0, lsa_flag_off = 0, lsa_dot_off = 0, lsa_dot_stride = 0;
+    std::vector<int64_t> lsa_lvl_stride;  // bytes between the parities of a level's region
+    char** lsa_peer = nullptr;            // device: np segment bases as this GPU addresses them
+    int* lsa_err = nullptr;               // device: a barrier timed out (sticky)
+    unsigned long long lsa_timeout_ns = 60ull * 1000000000ull;
+    void release_lsa() {
+        if (lsa_win && lsa_comm) ncclCommWindowDeregister(lsa_comm, lsa_win);
+        if (lsa_mem) ncclMemFree(lsa_mem);
+        cudaFree(lsa_peer);
+        cudaFree(lsa_err);
+        lsa_win = nullptr;
+        lsa_mem = nullptr;
+        lsa_peer = nullptr;
+        lsa_err = nullptr;
+        lsa = false;
+    }
     // first NCCL failure of an enqueue pass (exchange / all-gather), reported as AMG_ERR_NCCL
     ncclResult_t nccl_status = ncclSuccess;
     std::string nccl_what;
@@ -358,6 +398,7 @@ struct amg_hier_s {
         iter_exec = nullptr;
     }
     ~amg_hier_s() {
+        release_lsa();
         cudaFree(tail_prog);
         cudaFree(tail_partials);
         release_graphs();
@@ -596,9 +637,53 @@ void loop_nccl_dots(amg_hier_s* h, cudaStream_t s) {
     nccl_note(h, ncclGroupEnd(), "ncclGroupEnd (loopback dots)");
 }
 
+// ------------------------------------------------------ peer-memory (LSA) transport
+LsaPush lsa_args(amg_hier_s* h, RankState& R, const Exch* E, int l) {
+    LsaPush P{};
+    P.peer_base = h->lsa_peer;
+    P.send_off = E ? E->d_send_off : nullptr;
+    P.dst_off = E ? E->d_dst_off : nullptr;
+    P.stride = l >= 0 ? h->lsa_lvl_stride[l] : 0;
+    P.seq = R.lsa_seq;
+    P.count = R.lsa_count;
+    P.np = h->np;
+    P.me = R.rank;
+    P.flag_off = h->lsa_flag_off;
+    P.dots = nullptr;
+    P.kdot = kDotSlots;
+    P.dot_off = h->lsa_dot_off;
+    P.dot_stride = h->lsa_dot_stride;
+    return P;
+}
+void lsa_wait(amg_hier_s* h, RankState& R, cudaStream_t s) {
+    launch_k(k_lsa_wait, 1, kBlock, s, (const unsigned long long*)R.lsa_flags, h->np, R.lsa_seq, h->lsa_err,
+             h->lsa_timeout_ns);
+}
+// every rank's dot slots to every rank (slot rank), one barrier
+void lsa_dot_gather(amg_hier_s* h, cudaStream_t s) {
+    for (auto& R : h->ranks) {
+        LsaPush P = lsa_args(h, R, nullptr, -1);
+        P.dots = R.dot_local;
+        launch_k(k_lsa_push, 1, kBlock, s, (const double*)nullptr, (const int32_t*)nullptr, (int64_t)0, P);
+    }
+    for (auto& R : h->ranks) lsa_wait(h, R, s);  // loopback: every rank arrived before any waits
+}
+
 // Multi-rank: gather every rank's dot total to every rank, then finish in rank order.
 void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0) {
     if (!h->multi()) return;
+    if (h->lsa) {
+        lsa_dot_gather(h, L.s);
+        for (auto& R : h->ranks) {
+            RedCtx rc{nullptr, nullptr, nullptr, R.st, cond, kind, nullptr};
+            L.begin("dot_finish", 8.0 * kDotSlots * h->np);
+            launch_k(k_finish, 1, 32, L.s, (const double*)R.lsa_dots, kDotSlots * h->np, rc,
+                     (const unsigned long long*)R.lsa_seq, h->lsa_dot_stride / 8);
+            L.end();
+            cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
+        }
+        return;
+    }
     if (h->loop_nccl()) {
         loop_nccl_dots(h, L.s);
     } else if (h->loopback) {
@@ -615,7 +700,8 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0)
         // every rank computes the same status; in loopback each sets the (shared) WHILE condition
         RedCtx rc{nullptr, nullptr, nullptr, R.st, cond, kind, nullptr};
         L.begin("dot_finish", 8.0 * kDotSlots * h->np);
-        launch_k(k_finish, 1, 32, L.s, R.dot_all, kDotSlots * h->np, rc);
+        launch_k(k_finish, 1, 32, L.s, (const double*)R.dot_all, kDotSlots * h->np, rc,
+                 (const unsigned long long*)nullptr, (int64_t)0);
         L.end();
         cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);  // slots of skipped parts stay 0
     }
@@ -624,6 +710,18 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0)
 // Several ranks, K-cycle: the same gather, finished into each rank's level-lvl K state.
 void dot_finish_k(amg_hier_s* h, Launch& L, int kind, int lvl) {
     if (!h->multi()) return;
+    if (h->lsa) {
+        lsa_dot_gather(h, L.s);
+        for (auto& R : h->ranks) {
+            RedCtx rc{nullptr, nullptr, nullptr, nullptr, 0ull, kind, R.lv[lvl].kst};
+            L.begin("dot_finish", 8.0 * kDotSlots * h->np);
+            launch_k(k_finish, 1, 32, L.s, (const double*)R.lsa_dots, kDotSlots * h->np, rc,
+                     (const unsigned long long*)R.lsa_seq, h->lsa_dot_stride / 8);
+            L.end();
+            cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
+        }
+        return;
+    }
     if (h->loop_nccl()) {
         loop_nccl_dots(h, L.s);
     } else if (h->loopback) {
@@ -639,7 +737,8 @@ void dot_finish_k(amg_hier_s* h, Launch& L, int kind, int lvl) {
     for (auto& R : h->ranks) {
         RedCtx rc{nullptr, nullptr, nullptr, nullptr, 0ull, kind, R.lv[lvl].kst};
         L.begin("dot_finish", 8.0 * kDotSlots * h->np);
-        launch_k(k_finish, 1, 32, L.s, R.dot_all, kDotSlots * h->np, rc);
+        launch_k(k_finish, 1, 32, L.s, (const double*)R.dot_all, kDotSlots * h->np, rc,
+                 (const unsigned long long*)nullptr, (int64_t)0);
         L.end();
         cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
     }
@@ -706,6 +805,27 @@ void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const 
         }
         return;
     }
+    if (h->lsa) {
+        // push + arrive on the pack stream (ahead of the interior kernel), wait + unpack on st; every
+        // rank arrives at every exchange, with or without entries for its peers
+        Launch Lp{h, pack_st ? pack_st : st};
+        for (auto& R : h->ranks) {
+            const Exch& E = R.lv[l].ex;
+            Lp.begin("halo_push", 16.0 * (double)E.nsend);
+            launch_k(k_lsa_push, E.nsend ? vec_grid(E.nsend, nsm) : 1, kBlock, Lp.s, (const double*)vec(R),
+                     (const int32_t*)E.send_idx, E.nsend, lsa_args(h, R, &E, l));
+            Lp.end();
+        }
+        if (pack_st) {
+            cudaEventRecord(h->ev_fork, pack_st);
+            cudaStreamWaitEvent(st, h->ev_fork, 0);
+        }
+        for (auto& R : h->ranks) {
+            L.begin("halo_wait", 8.0 * h->np);
+            lsa_wait(h, R, L.s);
+            L.end();
+        }
+    } else {
     {
         Launch Lp{h, pack_st ? pack_st : st};
         for (auto& R : h->ranks) {
@@ -753,12 +873,14 @@ void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const 
         }
         nccl_note(h, ncclGroupEnd(), "ncclGroupEnd (halo)");
     }
+    }  // transports
     for (auto& R : h->ranks) {
         const Exch& E = R.lv[l].ex;
         if (!E.nrecv) continue;
         L.begin("halo_unpack", 20.0 * (double)E.nrecv);
         if (unpack) (*unpack)(R, E, L.s);
-        else launch_k(k_unpack, vec_grid(E.nrecv, nsm), kBlock, L.s, vec(R), E.recv_idx, E.rbuf, E.nrecv);
+        else launch_k(k_unpack, vec_grid(E.nrecv, nsm), kBlock, L.s, vec(R), (const int32_t*)E.recv_idx,
+                      (const double*)E.rbuf, E.nrecv, E.rx_seq, E.rx_stride);  // rx_seq null: plain buffer
         L.end();
     }
 }
@@ -1625,8 +1747,8 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
         // positions (p_old's halo arrived with the previous iteration's z), so the gathers see
         // the same p_new as the owners write.
         const UnpackFn pz_unpack = [&](RankState& R, const Exch& E, cudaStream_t s) {
-            launch_k(k_unpack_pz, vec_grid(E.nrecv, nsm), kBlock, s, R.pz, R.pp, R.pp2, E.recv_idx, E.rbuf, E.nrecv,
-                     (const PcgState*)R.st);
+            launch_k(k_unpack_pz, vec_grid(E.nrecv, nsm), kBlock, s, R.pz, R.pp, R.pp2, (const int32_t*)E.recv_idx,
+                     (const double*)E.rbuf, E.nrecv, (const PcgState*)R.st, E.rx_seq, E.rx_stride);
         };
         overlapped(h, L, 0, [](RankState& R) { return R.pz; }, true, [&](RankState& R, int part) {
             const DevLevel& D = R.L0();
@@ -2998,6 +3120,200 @@ int ensure_apply_graph(amg_hier_s* h, const double* r, double* z) {
     return AMG_OK;
 }
 
+// ------------------------------------------------ LSA transport setup (NCCL symmetric window)
+__global__ void k_lsa_bases(ncclWindow_t win, int np, int loopback, int64_t seg, char** out) {
+    const int q = threadIdx.x;
+    if (q >= np) return;
+    out[q] = loopback ? (char*)ncclGetLsaPointer(win, 0, 0) + (int64_t)q * seg : (char*)ncclGetLsaPointer(win, 0, q);
+}
+
+// All ranks agree (NCCL contexts; min over ranks) -- on the context stream, outside any capture.
+int lsa_agree(amg_hier_s* h, int ok_local, int* ok_all) {
+    *ok_all = ok_local;
+    if (h->loopback) return AMG_OK;  // one process: the local decision is everyone's
+    int* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(int)));
+    CK(cudaMemcpy(d, &ok_local, sizeof(int), cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(d, d, 1, ncclInt, ncclMin, h->ctx->nccl, h->ctx->stream));
+    CK(cudaStreamSynchronize(h->ctx->stream));
+    CK(cudaMemcpy(ok_all, d, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return AMG_OK;
+}
+
+// Sets up the peer-memory transport for a hierarchy on an NCCL context (real ranks, or loopback on a
+// one-rank communicator): lays out one window segment per rank (flags | 2 x dots | 2 x receive region
+// per level), allocates it with ncclMemAlloc, registers it as a symmetric window, resolves every
+// segment's address (ncclGetLsaPointer), checks one dot gather end to end (values and a bounded
+// barrier) and only then points the levels' receive buffers into the window.  Any failure on any
+// rank keeps every rank on the NCCL send/recv transport (decided collectively).  AMG_TRANSPORT=nccl
+// skips it.
+int lsa_setup(amg_hier_s* h) {
+    const char* tr = std::getenv("AMG_TRANSPORT");
+    if ((tr && std::strcmp(tr, "nccl") == 0) || !h->nccl_xport()) return AMG_OK;
+    ncclComm_t comm = h->ctx->nccl;
+    const int np = h->np, nl = h->nlev();
+    const bool lb = h->loopback;
+    cudaStream_t s = h->ctx->stream;
+    int ok = np <= kBlock ? 1 : 0;
+    if (!lb && ok) {
+        const ncclTeam_t t = ncclTeamLsa(comm);
+        if (t.nRanks != np) ok = 0;  // not one NVLink (load/store) domain
+    }
+    // every rank's recv_off per level: [rank][level][np+1]
+    const size_t per = (size_t)nl * (np + 1);
+    std::vector<int64_t> ro((size_t)np * per, 0);
+    auto mine = [&](RankState& R, int64_t* out) {
+        for (int l = 0; l < nl; ++l) {
+            const auto& v = R.lv[l].ex.recv_off;
+            for (int q = 0; q <= np; ++q) out[(size_t)l * (np + 1) + q] = v.size() == (size_t)np + 1 ? v[q] : 0;
+        }
+    };
+    if (lb) {
+        for (auto& R : h->ranks) mine(R, ro.data() + (size_t)R.rank * per);
+    } else {
+        std::vector<int64_t> m(per);
+        mine(h->ranks[0], m.data());
+        int64_t* d = nullptr;
+        CK(cudaMalloc(&d, sizeof(int64_t) * per * (np + 1)));
+        CK(cudaMemcpy(d, m.data(), sizeof(int64_t) * per, cudaMemcpyHostToDevice));
+        NK(ncclAllGather(d, d + per, per, ncclInt64, comm, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpy(ro.data(), d + per, sizeof(int64_t) * per * np, cudaMemcpyDeviceToHost));
+        cudaFree(d);
+    }
+    auto al = [](int64_t x, int64_t a) { return (x + a - 1) / a * a; };
+    int64_t off = al(8 * (int64_t)np, 256);
+    h->lsa_flag_off = 0;
+    h->lsa_dot_off = off;
+    h->lsa_dot_stride = al(8 * (int64_t)kDotSlots * np, 256);
+    off += 2 * h->lsa_dot_stride;
+    std::vector<int64_t> lvl_off(nl, 0);
+    h->lsa_lvl_stride.assign(nl, 0);
+    for (int l = 0; l < nl; ++l) {
+        int64_t mx = 0;
+        for (int q = 0; q < np; ++q) mx = std::max(mx, ro[(size_t)q * per + (size_t)l * (np + 1) + np]);
+        if (!mx) continue;
+        lvl_off[l] = off;
+        h->lsa_lvl_stride[l] = al(8 * mx, 256);
+        off += 2 * h->lsa_lvl_stride[l];
+    }
+    h->lsa_seg = al(off, NCCL_WIN_REQUIRED_ALIGNMENT);
+    const size_t total = (size_t)h->lsa_seg * (lb ? np : 1);
+    if (ok && ncclMemAlloc(&h->lsa_mem, total) != ncclSuccess) {
+        h->lsa_mem = nullptr;
+        ok = 0;
+    }
+    if (ok && cudaMemset(h->lsa_mem, 0, total) != cudaSuccess) ok = 0;
+    int all = 0, e;
+    if ((e = lsa_agree(h, ok, &all))) return e;
+    if (all) {  // collective registration, every rank takes part
+        h->lsa_comm = comm;
+        if (ncclCommWindowRegister(comm, h->lsa_mem, total, &h->lsa_win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) {
+            h->lsa_win = nullptr;
+            ok = 0;
+        }
+        if ((e = lsa_agree(h, ok, &all))) return e;
+    }
+    std::string why = "ncclMemAlloc / window registration / LSA team";
+    if (all) {
+        if (cudaMalloc(&h->lsa_peer, sizeof(char*) * np) != cudaSuccess || cudaMalloc(&h->lsa_err, sizeof(int)) != cudaSuccess ||
+            cudaMemset(h->lsa_err, 0, sizeof(int)) != cudaSuccess)
+            ok = 0;
+        if (ok) {
+            k_lsa_bases<<<1, kBlock, 0, s>>>(h->lsa_win, np, lb ? 1 : 0, h->lsa_seg, h->lsa_peer);
+            for (auto& R : h->ranks) {
+                char* mine_seg = (char*)h->lsa_mem + (lb ? (int64_t)R.rank * h->lsa_seg : 0);
+                R.lsa_flags = (unsigned long long*)(mine_seg + h->lsa_flag_off);
+                R.lsa_dots = (double*)(mine_seg + h->lsa_dot_off);
+                if (cudaMalloc(&R.lsa_seq, sizeof(unsigned long long)) != cudaSuccess ||
+                    cudaMalloc(&R.lsa_count, sizeof(unsigned int)) != cudaSuccess ||
+                    cudaMemset(R.lsa_seq, 0, sizeof(unsigned long long)) != cudaSuccess ||
+                    cudaMemset(R.lsa_count, 0, sizeof(unsigned int)) != cudaSuccess)
+                    ok = 0;
+            }
+        }
+        // end-to-end check: one dot gather of known values through the window (a bounded barrier)
+        if (ok) {
+            for (auto& R : h->ranks) {
+                const double v[kDotSlots] = {(double)R.rank + 1.0, -2.0 * R.rank, 0.5};
+                cudaMemcpy(R.dot_local, v, sizeof(v), cudaMemcpyHostToDevice);
+            }
+            const unsigned long long t = h->lsa_timeout_ns;
+            h->lsa_timeout_ns = 30ull * 1000000000ull;
+            lsa_dot_gather(h, s);
+            h->lsa_timeout_ns = t;
+            int err = 1;
+            if (cudaStreamSynchronize(s) != cudaSuccess) ok = 0;
+            if (ok) cudaMemcpy(&err, h->lsa_err, sizeof(int), cudaMemcpyDeviceToHost);
+            if (err) {
+                ok = 0;
+                why = "barrier check timed out";
+            }
+            for (auto& R : h->ranks) {
+                std::vector<double> got((size_t)kDotSlots * np);
+                if (ok && cudaMemcpy(got.data(), R.lsa_dots, sizeof(double) * got.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+                    ok = 0;
+                for (int q = 0; q < np && ok; ++q)
+                    if (got[(size_t)q * kDotSlots] != q + 1.0 || got[(size_t)q * kDotSlots + 1] != -2.0 * q ||
+                        got[(size_t)q * kDotSlots + 2] != 0.5) {
+                        ok = 0;
+                        why = "dot gather check read wrong values";
+                    }
+                cudaMemset(R.dot_local, 0, kDotSlots * sizeof(double));
+            }
+        }
+        if ((e = lsa_agree(h, ok, &all))) return e;
+    }
+    if (!all) {
+        std::fprintf(stderr, "amg: peer-memory (LSA) transport unavailable (%s); NCCL send/recv transport\n",
+                     why.c_str());
+        for (auto& R : h->ranks) {
+            cudaFree(R.lsa_seq);
+            cudaFree(R.lsa_count);
+            R.lsa_seq = nullptr;
+            R.lsa_count = nullptr;
+            R.lsa_flags = nullptr;
+            R.lsa_dots = nullptr;
+        }
+        h->release_lsa();
+        cudaGetLastError();
+        return AMG_OK;
+    }
+    // point every distributed level's receive buffer into the window (double-buffered regions)
+    for (auto& R : h->ranks) {
+        char* mine_seg = (char*)h->lsa_mem + (lb ? (int64_t)R.rank * h->lsa_seg : 0);
+        for (int l = 0; l < nl; ++l) {
+            Exch& E = R.lv[l].ex;
+            if (!h->lsa_lvl_stride[l]) continue;
+            if (!E.rbuf_in_window) cudaFree(E.rbuf);
+            E.rbuf = (double*)(mine_seg + lvl_off[l]);
+            E.rbuf_in_window = true;
+            E.rx_seq = R.lsa_seq;
+            E.rx_stride = h->lsa_lvl_stride[l] / 8;
+            std::vector<int64_t> so(np + 1, 0), dst(np, 0);
+            for (int q = 0; q <= np; ++q) so[q] = E.send_off.size() == (size_t)np + 1 ? E.send_off[q] : 0;
+            for (int q = 0; q < np; ++q) dst[q] = lvl_off[l] + 8 * ro[(size_t)q * per + (size_t)l * (np + 1) + R.rank];
+            int st;
+            if ((st = dev_copy(&E.d_send_off, so.data(), so.size()))) return st;
+            if ((st = dev_copy(&E.d_dst_off, dst.data(), dst.size()))) return st;
+        }
+    }
+    h->lsa = true;
+    return AMG_OK;
+}
+
+// AMG_ERR_NCCL if an LSA barrier timed out (a peer rank never arrived; sticky).
+int take_lsa_err(amg_hier_s* h) {
+    if (!h->lsa) return AMG_OK;
+    int err = 0;
+    CK(cudaMemcpy(&err, h->lsa_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!err) return AMG_OK;
+    set_err("peer-memory transport: a peer rank did not arrive at a barrier within " +
+            std::to_string(h->lsa_timeout_ns / 1000000000ull) + " s");
+    return AMG_ERR_NCCL;
+}
+
 // AMG_ERR_NCCL if an enqueue pass since the last call recorded an NCCL failure.
 int take_nccl_status(amg_hier_s* h) {
     if (h->nccl_status == ncclSuccess) return AMG_OK;
@@ -3676,6 +3992,7 @@ int amg_ctx_destroy(amg_ctx_t c) {
             cudaSetDevice(h->device);
             cudaStreamSynchronize(c->stream);
             h->release_graphs();
+            h->release_lsa();  // the window belongs to the communicator
             h->ctx = nullptr;
         }
         c->hiers.clear();
@@ -3969,6 +4286,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     CK(cudaDeviceSynchronize());
+    if (int e = lsa_setup(h)) return fail(e);
     h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     {
         std::lock_guard<std::mutex> g(ctx->hiers_mu);
@@ -4048,6 +4366,7 @@ int amg_solve(amg_hier_t h, const double* b_dev, double* x_dev, double rtol, int
         CK(cudaStreamSynchronize(s));
     }
     CK(cudaGetLastError());
+    if (int e = take_lsa_err(h)) return e;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h->ev0, h->ev1);
     const PcgState& S = *h->st_host;
@@ -4220,7 +4539,7 @@ int amg_precond_apply(amg_hier_t h, const double* r_dev, double* z_dev) {
     }
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
-    return AMG_OK;
+    return take_lsa_err(h);
 }
 
 int amg_solve_graph_mode(amg_hier_t h, int32_t* mode) {
@@ -4230,6 +4549,15 @@ int amg_solve_graph_mode(amg_hier_t h, int32_t* mode) {
     }
     std::lock_guard<std::recursive_mutex> guard(h->mu);
     *mode = h->cfg.use_graphs ? (int32_t)h->graph_mode : 2;
+    return AMG_OK;
+}
+
+int amg_comm_transport(amg_hier_t h, int32_t* transport) {
+    if (!h || !transport) {
+        set_err("amg_comm_transport: null argument");
+        return AMG_ERR_ARG;
+    }
+    *transport = !h->multi() ? 0 : h->lsa ? 3 : h->nccl_xport() ? 2 : 1;
     return AMG_OK;
 }
 

@@ -240,6 +240,7 @@ def test_null_handles_and_bad_arguments_are_status_codes(amg):
         "amg_precond_apply": lambda: L.amg_precond_apply(null, p, p),
         "amg_num_levels": lambda: L.amg_num_levels(null, C.byref(i32)),
         "amg_solve_graph_mode": lambda: L.amg_solve_graph_mode(null, C.byref(i32)),
+        "amg_comm_transport": lambda: L.amg_comm_transport(null, C.byref(i32)),
         "amg_level_info": lambda: L.amg_level_info(null, 0, C.byref(i64), C.byref(i64), C.byref(i64),
                                                    C.byref(i64), C.byref(i64), C.byref(i32)),
         "amg_level_aggregates": lambda: L.amg_level_aggregates(null, 0, p),

@@ -1,4 +1,8 @@
-"""The NCCL transport of the multi-rank path, exercised on ONE GPU.
+"""The NCCL transports of the multi-rank path, exercised on ONE GPU.
+
+Two transports run on NCCL contexts: peer memory over an NCCL symmetric window ("lsa", the
+default: push kernels store halo values and dot slots straight into the receivers' window
+segments, then a flag barrier) and NCCL send/recv (AMG_TRANSPORT=nccl, the fallback).
 
 A single-rank context given an ncclUniqueId holds a one-rank NCCL communicator; loopback
 hierarchies (cfg.emulate_ranks = np) built on it move every halo and every rank's dot slots
@@ -52,21 +56,26 @@ def _case(name):
     raise KeyError(name)
 
 
+@pytest.mark.parametrize("transport", ["lsa", "nccl"])
 @pytest.mark.parametrize("np_", [2, 3])
 @pytest.mark.parametrize("name", ["c4_slabs", "jump27", "kcycle", "hinvk_va3s3cs1"])
-def test_nccl_loopback_bitwise_equals_copy_loopback(ctxs, name, np_):
+def test_nccl_loopback_bitwise_equals_copy_loopback(ctxs, name, np_, transport, monkeypatch):
     import paper_2006_16147_b200 as amg
     plain, nccl = ctxs
     A, b, kw = _case(name)
     cfg = dict(emulate_ranks=np_, replicate_below_bytes=0, **kw)
     hc = amg.Hierarchy(plain, A, cfg=amg.make_config(**cfg))
+    monkeypatch.setenv("AMG_TRANSPORT", transport)
     hn = amg.Hierarchy(nccl, A, cfg=amg.make_config(**cfg))
+    assert hc.transport() == "copies" and hn.transport() == transport
     bt = torch.tensor(b, device="cuda:0")
     xc, rc = hc.solve(bt)
     xn, rn = hn.solve(bt)
     mode = hn.graph_mode()
-    print(f"{name} np={np_}: NCCL loopback solve graph mode = {mode}, its {rn['iterations']}")
-    assert mode in ("while", "iter")
+    print(f"{name} np={np_} {transport}: solve graph mode = {mode}, its {rn['iterations']}")
+    # peer memory keeps NCCL out of the solve: one WHILE graph; NCCL send/recv cannot sit in the
+    # WHILE body (wait-event nodes) and falls back to one graph per iteration
+    assert mode == ("while" if transport == "lsa" else "iter")
     assert rn["converged"] == 1 and rn["iterations"] == rc["iterations"]
     assert torch.equal(xn, xc)
     xn2, _ = hn.solve(bt)  # the cached graph (or the fallback) again
@@ -76,11 +85,14 @@ def test_nccl_loopback_bitwise_equals_copy_loopback(ctxs, name, np_):
     assert torch.equal(zn, zc)
 
 
-def test_nccl_loopback_vs_oracle_and_host_batch(ctxs):
+@pytest.mark.parametrize("transport", ["lsa", "nccl"])
+def test_nccl_loopback_vs_oracle_and_host_batch(ctxs, transport, monkeypatch):
     import paper_2006_16147_b200 as amg
     _, nccl = ctxs
     A, b, _ = config_problem(4, grid=(32, 32, 64))
+    monkeypatch.setenv("AMG_TRANSPORT", transport)
     h = amg.Hierarchy(nccl, A, cfg=amg.make_config(emulate_ranks=2))
+    assert h.transport() == transport
     ho = O.OracleHierarchy(A)
     bt = torch.tensor(b, device="cuda:0")
     x, rep = h.solve(bt)
@@ -114,11 +126,13 @@ print("MODE", h.graph_mode())
 """
 
 
+@pytest.mark.parametrize("transport", ["lsa", "nccl"])
 @pytest.mark.parametrize("forced,ug,expect", [("iter", 1, "iter"), ("", 0, "eager")])
-def test_nccl_loopback_fallback_shapes(forced, ug, expect):
-    """The fallback shapes a real NCCL job may take (one graph per iteration, eager launches),
-    run with NCCL collectives, give the same x bitwise."""
+def test_nccl_loopback_fallback_shapes(forced, ug, expect, transport):
+    """The other shapes a real NCCL job may take (one graph per iteration, eager launches), on
+    either transport, give the same x bitwise."""
     env = dict(os.environ)
+    env["AMG_TRANSPORT"] = transport
     if forced:
         env["AMG_MULTI_GRAPH"] = forced
     out = subprocess.run([sys.executable, "-c", _FORCED.format(root=ROOT, ug=ug)], env=env, cwd=ROOT,
@@ -142,11 +156,27 @@ print("CLOSED", rep["iterations"])
 """
 
 
-def test_ctx_destroy_with_live_hierarchy_does_not_hang():
+@pytest.mark.parametrize("transport", ["lsa", "nccl"])
+def test_ctx_destroy_with_live_hierarchy_does_not_hang(transport):
     """A graph that captured NCCL collectives holds the communicator: amg_ctx_destroy must release
     the graphs of hierarchies still alive before ncclCommDestroy, or it waits forever (what a
     garbage-collection order at interpreter exit produces under torchrun)."""
+    env = dict(os.environ, AMG_TRANSPORT=transport)
     out = subprocess.run([sys.executable, "-c", _ORPHAN.format(root=ROOT)], cwd=ROOT, capture_output=True,
-                         text=True, timeout=300)
+                         text=True, timeout=300, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     assert "CLOSED" in out.stdout
+
+
+def test_lsa_profiled_kernels_and_overlap(ctxs, monkeypatch):
+    """On the peer-memory transport an exchange is push (+arrive) / wait / unpack kernels and the
+    split operators still run interior + boundary launches; the profiled V-cycle names them."""
+    import paper_2006_16147_b200 as amg
+    _, nccl = ctxs
+    A, b, _ = config_problem(4, grid=(64, 64, 128))
+    monkeypatch.setenv("AMG_TRANSPORT", "lsa")
+    h = amg.Hierarchy(nccl, A, cfg=amg.make_config(emulate_ranks=2, replicate_below_bytes=0))
+    assert h.transport() == "lsa"
+    names = [k["name"] for k in h.profile_vcycle(1)]
+    assert "halo_push" in names and "halo_wait" in names and "halo_unpack" in names
+    assert "halo_pack" not in names
