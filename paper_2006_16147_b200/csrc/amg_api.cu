@@ -142,8 +142,7 @@ struct Exch {
     int64_t* d_send_off = nullptr;  // LSA: device copy of send_off
     int64_t* d_dst_off = nullptr;   // LSA: np byte offsets of my data in each destination's region 0
     bool rbuf_in_window = false;
-    const unsigned long long* rx_seq = nullptr;  // LSA: the receiver's barrier count (region parity)
-    int64_t rx_stride = 0;                        // LSA: doubles between the region's two parities
+    RxWait rx{};                    // LSA: the receive side's barrier wait + region parity (flags null: none)
     void release() {
         cudaFree(send_idx);
         cudaFree(recv_idx);
@@ -655,33 +654,41 @@ LsaPush lsa_args(amg_hier_s* h, RankState& R, const Exch* E, int l) {
     P.dot_stride = h->lsa_dot_stride;
     return P;
 }
-void lsa_wait(amg_hier_s* h, RankState& R, cudaStream_t s) {
-    launch_k(k_lsa_wait, 1, kBlock, s, (const unsigned long long*)R.lsa_flags, h->np, R.lsa_seq, h->lsa_err,
-             h->lsa_timeout_ns);
+RxWait lsa_rx(amg_hier_s* h, RankState& R, int64_t stride_doubles) {
+    RxWait w;
+    w.flags = R.lsa_flags;
+    w.seq = R.lsa_seq;
+    w.err = h->lsa_err;
+    w.timeout_ns = h->lsa_timeout_ns;
+    w.np = h->np;
+    w.stride = stride_doubles;
+    return w;
 }
-// every rank's dot slots to every rank (slot rank), one barrier
-void lsa_dot_gather(amg_hier_s* h, cudaStream_t s) {
+// every rank's dot slots to every rank (slot rank), one barrier (the receive side: k_finish)
+void lsa_dot_push(amg_hier_s* h, cudaStream_t s) {
     for (auto& R : h->ranks) {
         LsaPush P = lsa_args(h, R, nullptr, -1);
         P.dots = R.dot_local;
         launch_k(k_lsa_push, 1, kBlock, s, (const double*)nullptr, (const int32_t*)nullptr, (int64_t)0, P);
     }
-    for (auto& R : h->ranks) lsa_wait(h, R, s);  // loopback: every rank arrived before any waits
+}
+// finish every rank's gathered dots (loopback: every rank pushed before any waits)
+void lsa_dot_finish(amg_hier_s* h, Launch& L, const std::function<RedCtx(RankState&)>& rc) {
+    lsa_dot_push(h, L.s);
+    for (auto& R : h->ranks) {
+        L.begin("dot_finish", 8.0 * kDotSlots * h->np);
+        launch_k(k_finish, 1, kBlock, L.s, (const double*)R.lsa_dots, kDotSlots * h->np, rc(R),
+                 lsa_rx(h, R, h->lsa_dot_stride / 8));
+        L.end();
+        cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
+    }
 }
 
 // Multi-rank: gather every rank's dot total to every rank, then finish in rank order.
 void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0) {
     if (!h->multi()) return;
     if (h->lsa) {
-        lsa_dot_gather(h, L.s);
-        for (auto& R : h->ranks) {
-            RedCtx rc{nullptr, nullptr, nullptr, R.st, cond, kind, nullptr};
-            L.begin("dot_finish", 8.0 * kDotSlots * h->np);
-            launch_k(k_finish, 1, 32, L.s, (const double*)R.lsa_dots, kDotSlots * h->np, rc,
-                     (const unsigned long long*)R.lsa_seq, h->lsa_dot_stride / 8);
-            L.end();
-            cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
-        }
+        lsa_dot_finish(h, L, [&](RankState& R) { return RedCtx{nullptr, nullptr, nullptr, R.st, cond, kind, nullptr}; });
         return;
     }
     if (h->loop_nccl()) {
@@ -700,8 +707,7 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0)
         // every rank computes the same status; in loopback each sets the (shared) WHILE condition
         RedCtx rc{nullptr, nullptr, nullptr, R.st, cond, kind, nullptr};
         L.begin("dot_finish", 8.0 * kDotSlots * h->np);
-        launch_k(k_finish, 1, 32, L.s, (const double*)R.dot_all, kDotSlots * h->np, rc,
-                 (const unsigned long long*)nullptr, (int64_t)0);
+        launch_k(k_finish, 1, 32, L.s, (const double*)R.dot_all, kDotSlots * h->np, rc, RxWait{});
         L.end();
         cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);  // slots of skipped parts stay 0
     }
@@ -711,15 +717,9 @@ void dot_finish(amg_hier_s* h, Launch& L, int kind, unsigned long long cond = 0)
 void dot_finish_k(amg_hier_s* h, Launch& L, int kind, int lvl) {
     if (!h->multi()) return;
     if (h->lsa) {
-        lsa_dot_gather(h, L.s);
-        for (auto& R : h->ranks) {
-            RedCtx rc{nullptr, nullptr, nullptr, nullptr, 0ull, kind, R.lv[lvl].kst};
-            L.begin("dot_finish", 8.0 * kDotSlots * h->np);
-            launch_k(k_finish, 1, 32, L.s, (const double*)R.lsa_dots, kDotSlots * h->np, rc,
-                     (const unsigned long long*)R.lsa_seq, h->lsa_dot_stride / 8);
-            L.end();
-            cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
-        }
+        lsa_dot_finish(h, L, [&](RankState& R) {
+            return RedCtx{nullptr, nullptr, nullptr, nullptr, 0ull, kind, R.lv[lvl].kst};
+        });
         return;
     }
     if (h->loop_nccl()) {
@@ -737,8 +737,7 @@ void dot_finish_k(amg_hier_s* h, Launch& L, int kind, int lvl) {
     for (auto& R : h->ranks) {
         RedCtx rc{nullptr, nullptr, nullptr, nullptr, 0ull, kind, R.lv[lvl].kst};
         L.begin("dot_finish", 8.0 * kDotSlots * h->np);
-        launch_k(k_finish, 1, 32, L.s, (const double*)R.dot_all, kDotSlots * h->np, rc,
-                 (const unsigned long long*)nullptr, (int64_t)0);
+        launch_k(k_finish, 1, 32, L.s, (const double*)R.dot_all, kDotSlots * h->np, rc, RxWait{});
         L.end();
         cudaMemsetAsync(R.dot_local, 0, kDotSlots * sizeof(double), L.s);
     }
@@ -820,9 +819,10 @@ void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const 
             cudaEventRecord(h->ev_fork, pack_st);
             cudaStreamWaitEvent(st, h->ev_fork, 0);
         }
-        for (auto& R : h->ranks) {
+        for (auto& R : h->ranks) {  // ranks with something to receive wait inside their unpack (below)
+            if (R.lv[l].ex.nrecv) continue;
             L.begin("halo_wait", 8.0 * h->np);
-            lsa_wait(h, R, L.s);
+            launch_k(k_lsa_wait, 1, kBlock, L.s, R.lv[l].ex.rx);
             L.end();
         }
     } else {
@@ -880,7 +880,7 @@ void exchange_on(amg_hier_s* h, cudaStream_t st, int l, const VecOf& vec, const 
         L.begin("halo_unpack", 20.0 * (double)E.nrecv);
         if (unpack) (*unpack)(R, E, L.s);
         else launch_k(k_unpack, vec_grid(E.nrecv, nsm), kBlock, L.s, vec(R), (const int32_t*)E.recv_idx,
-                      (const double*)E.rbuf, E.nrecv, E.rx_seq, E.rx_stride);  // rx_seq null: plain buffer
+                      (const double*)E.rbuf, E.nrecv, E.rx);  // rx.flags null: plain buffer
         L.end();
     }
 }
@@ -1748,7 +1748,7 @@ void enqueue_pcg_body(amg_hier_s* h, Launch& L, double* x_user, unsigned long lo
         // the same p_new as the owners write.
         const UnpackFn pz_unpack = [&](RankState& R, const Exch& E, cudaStream_t s) {
             launch_k(k_unpack_pz, vec_grid(E.nrecv, nsm), kBlock, s, R.pz, R.pp, R.pp2, (const int32_t*)E.recv_idx,
-                     (const double*)E.rbuf, E.nrecv, (const PcgState*)R.st, E.rx_seq, E.rx_stride);
+                     (const double*)E.rbuf, E.nrecv, (const PcgState*)R.st, E.rx);
         };
         overlapped(h, L, 0, [](RankState& R) { return R.pz; }, true, [&](RankState& R, int part) {
             const DevLevel& D = R.L0();
@@ -3239,10 +3239,12 @@ int lsa_setup(amg_hier_s* h) {
                 const double v[kDotSlots] = {(double)R.rank + 1.0, -2.0 * R.rank, 0.5};
                 cudaMemcpy(R.dot_local, v, sizeof(v), cudaMemcpyHostToDevice);
             }
-            const unsigned long long t = h->lsa_timeout_ns;
-            h->lsa_timeout_ns = 30ull * 1000000000ull;
-            lsa_dot_gather(h, s);
-            h->lsa_timeout_ns = t;
+            lsa_dot_push(h, s);
+            for (auto& R : h->ranks) {
+                RxWait w = lsa_rx(h, R, 0);
+                w.timeout_ns = 30ull * 1000000000ull;
+                k_lsa_wait<<<1, kBlock, 0, s>>>(w);
+            }
             int err = 1;
             if (cudaStreamSynchronize(s) != cudaSuccess) ok = 0;
             if (ok) cudaMemcpy(&err, h->lsa_err, sizeof(int), cudaMemcpyDeviceToHost);
@@ -3285,12 +3287,11 @@ int lsa_setup(amg_hier_s* h) {
         char* mine_seg = (char*)h->lsa_mem + (lb ? (int64_t)R.rank * h->lsa_seg : 0);
         for (int l = 0; l < nl; ++l) {
             Exch& E = R.lv[l].ex;
+            E.rx = lsa_rx(h, R, h->lsa_lvl_stride[l] / 8);  // every level: ranks without entries wait too
             if (!h->lsa_lvl_stride[l]) continue;
             if (!E.rbuf_in_window) cudaFree(E.rbuf);
             E.rbuf = (double*)(mine_seg + lvl_off[l]);
             E.rbuf_in_window = true;
-            E.rx_seq = R.lsa_seq;
-            E.rx_stride = h->lsa_lvl_stride[l] / 8;
             std::vector<int64_t> so(np + 1, 0), dst(np, 0);
             for (int q = 0; q <= np; ++q) so[q] = E.send_off.size() == (size_t)np + 1 ? E.send_off[q] : 0;
             for (int q = 0; q < np; ++q) dst[q] = lvl_off[l] + 8 * ro[(size_t)q * per + (size_t)l * (np + 1) + R.rank];

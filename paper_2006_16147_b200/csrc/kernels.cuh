@@ -1079,19 +1079,52 @@ __global__ void __launch_bounds__(kBlock) k_xfinal(double* __restrict__ x, const
         x[i] = x[i] + alpha * p[i];
 }
 
-// Receive buffers of the peer-memory (LSA) transport are double-buffered by the parity of the
-// barrier that delivered them: `seq` counts this rank's completed barriers, so after barrier k+1
-// the data of barrier k sits at buf + ((seq - 1) & 1) * stride (seq null: a plain buffer).
-__device__ __forceinline__ const double* rx_sel(const double* buf, const unsigned long long* seq, int64_t stride) {
-    return seq ? buf + (((*seq) - 1ull) & 1ull) * stride : buf;
+// Receive side of a peer-memory (LSA) barrier, fused into the kernel that consumes the data.
+// Receive regions are double-buffered by the parity of the barrier that filled them; `seq` counts
+// the barriers this rank has pushed (k_lsa_push advances it), so the data of the barrier just
+// pushed sits at buf + ((seq - 1) & 1) * stride.  Every block's threads q < np wait (acquire, system
+// scope) for rank q's flag to reach seq, bounded by timeout_ns of %globaltimer: a peer that never
+// arrives sets *err and every later wait returns at once (the solve reports AMG_ERR_NCCL instead of
+// hanging).  flags null: a plain buffer, no wait.
+struct RxWait {
+    const unsigned long long* flags = nullptr;
+    const unsigned long long* seq = nullptr;
+    int* err = nullptr;
+    unsigned long long timeout_ns = 0;
+    int np = 0;
+    int64_t stride = 0;  // doubles between the two parities
+};
+__device__ __forceinline__ void rx_wait(const RxWait& w) {
+    if (!w.flags) return;
+    const unsigned long long e = *w.seq;
+    const int q = threadIdx.x;
+    if (q < w.np && !*(volatile int*)w.err) {
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(w.flags + q) : "memory");
+            if (v >= e) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > w.timeout_ns) {
+                atomicExch(w.err, 1);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ const double* rx_buf(const double* buf, const RxWait& w) {
+    return w.flags ? buf + (int64_t)(((*w.seq) - 1ull) & 1ull) * w.stride : buf;
 }
 
 // Multi-rank dot finisher: sum the all-gathered per-rank totals in rank order.
-__global__ void k_finish(const double* __restrict__ totals, int np, RedCtx rc, const unsigned long long* seq = nullptr,
-                         int64_t stride = 0) {
+__global__ void k_finish(const double* __restrict__ totals, int np, RedCtx rc, RxWait w) {
     pdl_begin();
+    rx_wait(w);
     if (threadIdx.x == 0 && blockIdx.x == 0) {
-        const double* t = rx_sel(totals, seq, stride);
+        const double* t = rx_buf(totals, w);
         double s = 0.0;
         for (int g = 0; g < np; ++g) s += t[g];
         finish(rc, s);
@@ -1106,10 +1139,10 @@ __global__ void __launch_bounds__(kBlock) k_pack(const double* __restrict__ v, c
         buf[k] = v[idx[k]];
 }
 __global__ void __launch_bounds__(kBlock) k_unpack(double* __restrict__ v, const int32_t* __restrict__ idx,
-                                                   const double* __restrict__ buf0, int64_t n,
-                                                   const unsigned long long* seq = nullptr, int64_t stride = 0) {
+                                                   const double* __restrict__ buf0, int64_t n, RxWait w) {
     pdl_begin();
-    const double* __restrict__ buf = rx_sel(buf0, seq, stride);
+    rx_wait(w);
+    const double* __restrict__ buf = rx_buf(buf0, w);
     for (int64_t k = (int64_t)blockIdx.x * kBlock + threadIdx.x; k < n; k += (int64_t)gridDim.x * kBlock)
         v[idx[k]] = buf[k];
 }
@@ -1119,13 +1152,13 @@ __global__ void __launch_bounds__(kBlock) k_unpack(double* __restrict__ v, const
 // segment as this GPU addresses it over NVLink (ncclGetLsaPointer).  A halo exchange is: push
 // and arrive (k_lsa_push: gather v at the send positions and STORE straight into each destination's
 // receive region -- no send buffer, no copy engine -- then flag stores), wait (flag loads), unpack.
-// The region is chosen by the parity of the barrier about to complete (see rx_sel).
+// The region is chosen by the parity of the barrier being pushed (see RxWait).
 struct LsaPush {
     char* const* peer_base;           // np window segments
     const int64_t* send_off;          // np+1: entries for peer q are [send_off[q], send_off[q+1])
     const int64_t* dst_off;           // np: byte offset, inside q's segment, of my data in q's region 0
     int64_t stride;                   // bytes between a region's two parities
-    const unsigned long long* seq;    // this rank's completed barriers
+    unsigned long long* seq;          // barriers this rank has pushed (advanced by the last block)
     unsigned int* count;              // blocks done (last-block pattern; reset by the last block)
     int np, me;
     int64_t flag_off;                 // byte offset of the np barrier flags in every segment
@@ -1134,8 +1167,8 @@ struct LsaPush {
     int64_t dot_off, dot_stride;      // dot region (slot me) and its parity stride, in bytes
 };
 // Push + arrive in one launch: every thread stores its halo entries straight into the destination
-// ranks' receive regions and fences them (system scope); the last block to finish (threadfence-
-// reduction pattern) pushes the dot slots, if any, and release-stores the barrier epoch into flag
+// ranks' receive regions; each block fences them once (system scope); the last block to finish
+// (threadfence-reduction pattern) pushes the dot slots, if any, and release-stores the barrier epoch into flag
 // `me` of every rank's segment.  n = 0 with one block: a dot gather / plain barrier arrival.
 __global__ void __launch_bounds__(kBlock) k_lsa_push(const double* __restrict__ v, const int32_t* __restrict__ idx,
                                                      int64_t n, LsaPush P) {
@@ -1148,10 +1181,15 @@ __global__ void __launch_bounds__(kBlock) k_lsa_push(const double* __restrict__ 
         double* dst = (double*)(P.peer_base[q] + P.dst_off[q] + par) + (k - P.send_off[q]);
         *dst = v[idx[k]];
     }
-    __threadfence_system();
+    // the block's stores happen-before thread 0's fence and arrival count (bar.sync, then a cumulative
+    // GPU-scope fence: the grid-sync pattern); the last block observes every block's count, and its
+    // system-scope release stores below are cumulative over all of them
     __shared__ bool last;
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(P.count, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(P.count, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (!last) return;
     const int q = threadIdx.x;
@@ -1160,40 +1198,23 @@ __global__ void __launch_bounds__(kBlock) k_lsa_push(const double* __restrict__ 
             double* d = (double*)(P.peer_base[q] + P.dot_off + (int64_t)(s & 1ull) * P.dot_stride) + (int64_t)P.me * P.kdot;
             for (int j = 0; j < P.kdot; ++j) d[j] = P.dots[j];
         }
-        __threadfence_system();
         unsigned long long* f = (unsigned long long*)(P.peer_base[q] + P.flag_off) + P.me;
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(s + 1ull) : "memory");
     }
-    if (q == 0) *P.count = 0u;
+    if (q == 0) {
+        *P.count = 0u;
+        *P.seq = s + 1ull;  // read by this rank's receive side (stream-ordered after this launch)
+    }
 }
 
-// Wait: thread q (< np) spins until rank q's flag in this rank's segment reaches the epoch
-// (acquire, system scope), bounded by timeout_ns of %globaltimer: a peer that never arrives sets
-// *err and every later wait returns at once (the solve then reports AMG_ERR_NCCL instead of
-// hanging).  Then seq advances.
-__global__ void k_lsa_wait(const unsigned long long* my_flags, int np, unsigned long long* seq, int* err,
-                           unsigned long long timeout_ns) {
+// A rank with nothing to receive at an exchange still waits at its barrier (so no rank runs two
+// barriers ahead of a peer still reading the other parity).
+__global__ void k_lsa_wait(RxWait w) {
     pdl_begin();
-    const int q = threadIdx.x;
-    const unsigned long long e = *seq + 1ull;
-    if (q < np && !*(volatile int*)err) {
-        unsigned long long t0, t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        for (;;) {
-            unsigned long long v;
-            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + q) : "memory");
-            if (v >= e) break;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > timeout_ns) {
-                atomicExch(err, 1);
-                break;
-            }
-            __nanosleep(64);
-        }
-    }
-    __syncthreads();
-    if (q == 0) *seq = e;
+    rx_wait(w);
 }
+
+
 
 // Halo unpack of z for the fused direction update (several ranks): z[idx] = buf and, at the
 // same halo positions, p_new = z + beta p_old (p_new = z on the first iteration), with the p
@@ -1201,10 +1222,10 @@ __global__ void k_lsa_wait(const unsigned long long* my_flags, int np, unsigned 
 __global__ void __launch_bounds__(kBlock) k_unpack_pz(double* __restrict__ z, double* p0, double* p1,
                                                       const int32_t* __restrict__ idx,
                                                       const double* __restrict__ buf0, int64_t n,
-                                                      const PcgState* __restrict__ st,
-                                                      const unsigned long long* seq = nullptr, int64_t stride = 0) {
+                                                      const PcgState* __restrict__ st, RxWait w) {
     pdl_begin();
-    const double* __restrict__ buf = rx_sel(buf0, seq, stride);
+    rx_wait(w);
+    const double* __restrict__ buf = rx_buf(buf0, w);
     const int32_t it = st->iter;
     const bool first = (it == 0);
     const double beta = st->beta;

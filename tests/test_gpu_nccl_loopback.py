@@ -169,8 +169,9 @@ def test_ctx_destroy_with_live_hierarchy_does_not_hang(transport):
 
 
 def test_lsa_profiled_kernels_and_overlap(ctxs, monkeypatch):
-    """On the peer-memory transport an exchange is push (+arrive) / wait / unpack kernels and the
-    split operators still run interior + boundary launches; the profiled V-cycle names them."""
+    """On the peer-memory transport an exchange is a push (+ arrive) kernel and an unpack kernel that
+    waits for the barrier itself (a rank with nothing to receive launches a bare wait); no pack
+    into a send buffer."""
     import paper_2006_16147_b200 as amg
     _, nccl = ctxs
     A, b, _ = config_problem(4, grid=(64, 64, 128))
@@ -178,5 +179,5 @@ def test_lsa_profiled_kernels_and_overlap(ctxs, monkeypatch):
     h = amg.Hierarchy(nccl, A, cfg=amg.make_config(emulate_ranks=2, replicate_below_bytes=0))
     assert h.transport() == "lsa"
     names = [k["name"] for k in h.profile_vcycle(1)]
-    assert "halo_push" in names and "halo_wait" in names and "halo_unpack" in names
+    assert "halo_push" in names and "halo_unpack" in names
     assert "halo_pack" not in names

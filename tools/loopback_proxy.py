@@ -35,9 +35,12 @@ def main():
                          "reports t_loop(np) / (np t(1)), the per-rank share of the serialised loopback time")
     ap.add_argument("--rep", type=int, default=None, help="replicate_below_bytes (default: the library's)")
     ap.add_argument("--nccl", action="store_true",
-                    help="move halos and dot slots through a one-rank NCCL communicator (self send/recv): "
-                         "the real ranks' transport and graph shape (one graph per iteration) on one GPU")
+                    help="build on a one-rank NCCL communicator: the real ranks' transport on one GPU "
+                         "(--transport lsa: peer memory through the symmetric window, one WHILE graph; "
+                         "nccl: self send/recv, one graph per iteration)")
+    ap.add_argument("--transport", default="lsa", choices=["lsa", "nccl"])
     args = ap.parse_args()
+    os.environ["AMG_TRANSPORT"] = args.transport
     grid0 = tuple(int(v) for v in args.grid.split("x"))
     ctx = amg.Context(device=0, nranks=1, nccl_uid=amg.nccl_unique_id()) if args.nccl else amg.Context(device=0)
     out = {"grid": list(grid0), "weak": args.weak, "what": __doc__.strip().splitlines()[0], "runs": []}
@@ -64,7 +67,7 @@ def main():
             t = sorted(ts)[len(ts) // 2]
             prof = h.profile_iteration(bt, 3, cap=4096)
             rec = {"np": np_, "graphs": graphs, "graph_mode": h.graph_mode(), "transport":
-                   ("nccl" if args.nccl and np_ > 1 else "copies"), "grid": list(grid), "solve_ms": t * 1e3, "iterations": its,
+                   h.transport(), "grid": list(grid), "solve_ms": t * 1e3, "iterations": its,
                    "ms_per_iter": t * 1e3 / its, "launches_per_iter": len(prof), "levels": h.sizes()}
             if np_ == 1 and graphs == 1:
                 base = rec
