@@ -431,7 +431,10 @@ def run_ours(args):
                        "hierarchy": method["desc"],
                        "max_coarse_size": method["cfg"]["max_coarse_size"], "rhs": meta["rhs"],
                        "l2_policy": "inputs larger than L2 (hierarchy >> 126 MB), no flush",
-                       "parallelism": f"rowblock{world}"},
+                       "parallelism": f"rowblock{world}",
+                       # how halos / dots move between ranks and the solve's graph shape
+                       # (amg_comm_transport / amg_solve_graph_mode)
+                       "transport": h.transport(), "solve_graph": h.graph_mode()},
             "solve_s": ms_per_step * 1e-3, "device_solve_s": dev_solve_ms * 1e-3, "iterations": iters,
             "ms_per_iter": ms_per_step / max(iters, 1), "setup_s": setup_s,
             "levels": h.sizes(), "opc": hrep["opc"],
