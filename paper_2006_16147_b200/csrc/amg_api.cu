@@ -439,6 +439,22 @@ int ctx_cap(amg_ctx_s* c, const void* fn) {
     return v;
 }
 
+// The synchronous-API cudaMemcpy / cudaMemset run on the legacy default stream, which the library's
+// non-blocking streams (the context's, the GPU setup's) do NOT wait for, and a host-to-device copy
+// from pageable memory or a device memset may return before the device has finished it.  A kernel
+// launched next on the context stream could then read the buffer before (or while) it is written:
+// a rare, build-to-build race (found on the SELL-32-sigma slot map of c5's A_1, zeroed by dev_alloc
+// and written by the next kernel: one build in ~10 took 500 iterations).  Every such call goes
+// through these helpers, which wait for the legacy stream before returning.
+cudaError_t h2d_sync(void* dst, const void* src, size_t bytes) {
+    cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? cudaStreamSynchronize(cudaStreamLegacy) : e;
+}
+cudaError_t memset_sync(void* dst, int v, size_t bytes) {
+    cudaError_t e = cudaMemset(dst, v, bytes);
+    return e == cudaSuccess ? cudaStreamSynchronize(cudaStreamLegacy) : e;
+}
+
 int vec_grid(int64_t n, int nsm) {
     const int64_t need = (n + kBlock - 1) / kBlock;
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)nsm * 8));
@@ -1819,14 +1835,14 @@ void enqueue_pcg_init(amg_hier_s* h, Launch& L, const double* b_user, double* x_
 template <class T>
 int dev_copy(T** dst, const T* src, size_t count) {
     CK(cudaMalloc((void**)dst, std::max<size_t>(1, count) * sizeof(T)));
-    if (count) CK(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    if (count) CK(h2d_sync(*dst, src, count * sizeof(T)));
     return AMG_OK;
 }
 
 template <class T>
 int dev_alloc(T** dst, size_t count) {
     CK(cudaMalloc((void**)dst, std::max<size_t>(1, count) * sizeof(T)));
-    CK(cudaMemset(*dst, 0, std::max<size_t>(1, count) * sizeof(T)));
+    CK(memset_sync(*dst, 0, std::max<size_t>(1, count) * sizeof(T)));
     return AMG_OK;
 }
 
@@ -2946,7 +2962,7 @@ int agree_ok(amg_hier_s* h, int ok_local, int* ok_all) {
     if (!h->nccl_xport()) return AMG_OK;
     int* d = nullptr;
     CK(cudaMalloc(&d, sizeof(int)));
-    CK(cudaMemcpy(d, &ok_local, sizeof(int), cudaMemcpyHostToDevice));
+    CK(h2d_sync(d, &ok_local, sizeof(int)));
     NK(ncclAllReduce(d, d, 1, ncclInt, ncclMin, h->ctx->nccl, h->ctx->stream));
     CK(cudaStreamSynchronize(h->ctx->stream));
     CK(cudaMemcpy(ok_all, d, sizeof(int), cudaMemcpyDeviceToHost));
@@ -3133,7 +3149,7 @@ int lsa_agree(amg_hier_s* h, int ok_local, int* ok_all) {
     if (h->loopback) return AMG_OK;  // one process: the local decision is everyone's
     int* d = nullptr;
     CK(cudaMalloc(&d, sizeof(int)));
-    CK(cudaMemcpy(d, &ok_local, sizeof(int), cudaMemcpyHostToDevice));
+    CK(h2d_sync(d, &ok_local, sizeof(int)));
     NK(ncclAllReduce(d, d, 1, ncclInt, ncclMin, h->ctx->nccl, h->ctx->stream));
     CK(cudaStreamSynchronize(h->ctx->stream));
     CK(cudaMemcpy(ok_all, d, sizeof(int), cudaMemcpyDeviceToHost));
@@ -3176,7 +3192,7 @@ int lsa_setup(amg_hier_s* h) {
         mine(h->ranks[0], m.data());
         int64_t* d = nullptr;
         CK(cudaMalloc(&d, sizeof(int64_t) * per * (np + 1)));
-        CK(cudaMemcpy(d, m.data(), sizeof(int64_t) * per, cudaMemcpyHostToDevice));
+        CK(h2d_sync(d, m.data(), sizeof(int64_t) * per));
         NK(ncclAllGather(d, d + per, per, ncclInt64, comm, s));
         CK(cudaStreamSynchronize(s));
         CK(cudaMemcpy(ro.data(), d + per, sizeof(int64_t) * per * np, cudaMemcpyDeviceToHost));
@@ -3204,7 +3220,7 @@ int lsa_setup(amg_hier_s* h) {
         h->lsa_mem = nullptr;
         ok = 0;
     }
-    if (ok && cudaMemset(h->lsa_mem, 0, total) != cudaSuccess) ok = 0;
+    if (ok && memset_sync(h->lsa_mem, 0, total) != cudaSuccess) ok = 0;
     int all = 0, e;
     if ((e = lsa_agree(h, ok, &all))) return e;
     if (all) {  // collective registration, every rank takes part
@@ -3218,7 +3234,7 @@ int lsa_setup(amg_hier_s* h) {
     std::string why = "ncclMemAlloc / window registration / LSA team";
     if (all) {
         if (cudaMalloc(&h->lsa_peer, sizeof(char*) * np) != cudaSuccess || cudaMalloc(&h->lsa_err, sizeof(int)) != cudaSuccess ||
-            cudaMemset(h->lsa_err, 0, sizeof(int)) != cudaSuccess)
+            memset_sync(h->lsa_err, 0, sizeof(int)) != cudaSuccess)
             ok = 0;
         if (ok) {
             k_lsa_bases<<<1, kBlock, 0, s>>>(h->lsa_win, np, lb ? 1 : 0, h->lsa_seg, h->lsa_peer);
@@ -3228,8 +3244,8 @@ int lsa_setup(amg_hier_s* h) {
                 R.lsa_dots = (double*)(mine_seg + h->lsa_dot_off);
                 if (cudaMalloc(&R.lsa_seq, sizeof(unsigned long long)) != cudaSuccess ||
                     cudaMalloc(&R.lsa_count, sizeof(unsigned int)) != cudaSuccess ||
-                    cudaMemset(R.lsa_seq, 0, sizeof(unsigned long long)) != cudaSuccess ||
-                    cudaMemset(R.lsa_count, 0, sizeof(unsigned int)) != cudaSuccess)
+                    memset_sync(R.lsa_seq, 0, sizeof(unsigned long long)) != cudaSuccess ||
+                    memset_sync(R.lsa_count, 0, sizeof(unsigned int)) != cudaSuccess)
                     ok = 0;
             }
         }
@@ -3237,7 +3253,7 @@ int lsa_setup(amg_hier_s* h) {
         if (ok) {
             for (auto& R : h->ranks) {
                 const double v[kDotSlots] = {(double)R.rank + 1.0, -2.0 * R.rank, 0.5};
-                cudaMemcpy(R.dot_local, v, sizeof(v), cudaMemcpyHostToDevice);
+                h2d_sync(R.dot_local, v, sizeof(v));
             }
             lsa_dot_push(h, s);
             for (auto& R : h->ranks) {
@@ -3262,7 +3278,7 @@ int lsa_setup(amg_hier_s* h) {
                         ok = 0;
                         why = "dot gather check read wrong values";
                     }
-                cudaMemset(R.dot_local, 0, kDotSlots * sizeof(double));
+                memset_sync(R.dot_local, 0, kDotSlots * sizeof(double));
             }
         }
         if ((e = lsa_agree(h, ok, &all))) return e;
@@ -3302,6 +3318,55 @@ int lsa_setup(amg_hier_s* h) {
     }
     h->lsa = true;
     return AMG_OK;
+}
+
+// AMG_DEBUG_CHECKSUM=1 (diagnostics): FNV-1a of every device array of rank 0's hierarchy on stderr,
+// one line per level and operator, so two builds of the same matrix can be compared array by array.
+uint64_t dev_fnv(const void* p, size_t bytes) {
+    if (!p || !bytes) return 0;
+    std::vector<unsigned char> hbuf(bytes);
+    if (cudaMemcpy(hbuf.data(), p, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+    uint64_t x = 1469598103934665603ull;
+    for (unsigned char c : hbuf) x = (x ^ c) * 1099511628211ull;
+    return x;
+}
+void debug_checksums(amg_hier_s* h) {
+    cudaDeviceSynchronize();
+    RankState& R = h->ranks[0];
+    auto mat = [&](int l, const char* name, const DevMat& M) {
+        if (!M.nrows) return;
+        const int64_t nsl = M.units;
+        const bool sell = M.fmt == FMT_SELL, sdia = M.fmt == FMT_SDIA;
+        const int64_t ne = (sell || sdia) ? M.stored : M.nnz;
+        std::fprintf(stderr,
+                     "amg-checksum L%d %s fmt %d n %lld stored %lld sptr %016llx offs %016llx anchor %016llx rp %016llx "
+                     "col %016llx val %016llx perm %016llx c16 %016llx cbase %016llx\n",
+                     l, name, M.fmt, (long long)M.nrows, (long long)ne,
+                     (unsigned long long)dev_fnv(M.sptr, (sell || sdia) ? (nsl + 1) * 4 : 0),
+                     (unsigned long long)dev_fnv(M.offs, sdia ? ne / 32 * 4 : 0),
+                     (unsigned long long)dev_fnv(M.anchor, M.anchor ? M.nrows * 4 : 0),
+                     (unsigned long long)dev_fnv(M.rp, M.rp ? (M.nrows + 1) * 4 : 0),
+                     (unsigned long long)dev_fnv(M.col, M.col ? ne * 4 : 0),
+                     (unsigned long long)dev_fnv(M.val, ne * 8),
+                     (unsigned long long)dev_fnv(M.perm, M.perm ? nsl * 32 * 4 : 0),
+                     (unsigned long long)dev_fnv(M.c16, M.c16 ? ne * 2 : 0),
+                     (unsigned long long)dev_fnv(M.cbase, M.cbase ? (sell ? nsl * 32 : M.nrows) * 4 : 0));
+    };
+    for (int l = 0; l < (int)R.lv.size(); ++l) {
+        DevLevel& D = R.lv[l];
+        mat(l, "A", D.A);
+        mat(l, "Am", D.Am);
+        mat(l, "P", D.P);
+        mat(l, "R", D.R);
+        mat(l, "Rc", D.Rc);
+        mat(l, "Pc", D.Pc);
+        const int64_t nc = l + 1 < (int)R.lv.size() ? R.lv[l + 1].win_n : 0;
+        std::fprintf(stderr, "amg-checksum L%d vec m %016llx Mc %016llx (n %lld)\n", l,
+                     (unsigned long long)dev_fnv(D.m, D.m ? D.win_n * 8 : 0),
+                     (unsigned long long)dev_fnv(D.Mc, D.Mc ? D.comp_n * D.comp_n * 8 : 0), (long long)nc);
+    }
+    std::fprintf(stderr, "amg-checksum cinv %016llx (nL %lld)\n", (unsigned long long)dev_fnv(R.cinv, R.nL * R.nL * 8),
+                 (long long)R.nL);
 }
 
 // AMG_ERR_NCCL if an LSA barrier timed out (a peer rank never arrived; sticky).
@@ -3558,8 +3623,8 @@ int nccl_send_bytes(amg_ctx_s* c, const std::vector<char>& buf, int peer) {
     int64_t n = (int64_t)buf.size();
     char* d = nullptr;
     CK(cudaMalloc(&d, std::max<int64_t>(n, 8) + 8));
-    CK(cudaMemcpy(d, &n, 8, cudaMemcpyHostToDevice));
-    if (n) CK(cudaMemcpy(d + 8, buf.data(), n, cudaMemcpyHostToDevice));
+    CK(h2d_sync(d, &n, 8));
+    if (n) CK(h2d_sync(d + 8, buf.data(), n));
     NK(ncclSend(d, 8, ncclChar, peer, c->nccl, c->stream));
     if (n) NK(ncclSend(d + 8, n, ncclChar, peer, c->nccl, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -3617,7 +3682,7 @@ struct NcclComm : amgsetup::Comm {
         for (int q = 0; q < np; ++q) mine[q] = (int64_t)out[q].size();
         int64_t* dsz = nullptr;
         if (cudaMalloc(&dsz, sizeof(int64_t) * (size_t)np * (np + 1)) != cudaSuccess) return fail("cudaMalloc");
-        cudaMemcpy(dsz, mine.data(), sizeof(int64_t) * np, cudaMemcpyHostToDevice);
+        h2d_sync(dsz, mine.data(), sizeof(int64_t) * np);
         if (ncclAllGather(dsz, dsz + np, np, ncclInt64, c->nccl, c->stream) != ncclSuccess)
             return cudaFree(dsz), fail("ncclAllGather (setup sizes)");
         if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cudaFree(dsz), fail("setup sizes sync");
@@ -3637,7 +3702,7 @@ struct NcclComm : amgsetup::Comm {
             cudaMalloc(&dr, std::max<int64_t>(rtot, 8)) != cudaSuccess)
             return cudaFree(ds), fail("cudaMalloc (setup payload)");
         for (int q = 0; q < np; ++q)
-            if (q != me && mine[q]) cudaMemcpy(ds + soff[q], out[q].data(), mine[q], cudaMemcpyHostToDevice);
+            if (q != me && mine[q]) h2d_sync(ds + soff[q], out[q].data(), mine[q]);
         bool nok = ncclGroupStart() == ncclSuccess;
         for (int q = 0; q < np; ++q) {
             if (q == me) continue;
@@ -4288,6 +4353,7 @@ int amg_hierarchy_build(amg_ctx_t ctx, int64_t n_global, int64_t row_begin, int6
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     CK(cudaDeviceSynchronize());
     if (int e = lsa_setup(h)) return fail(e);
+    if (std::getenv("AMG_DEBUG_CHECKSUM")) debug_checksums(h);
     h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     {
         std::lock_guard<std::mutex> g(ctx->hiers_mu);

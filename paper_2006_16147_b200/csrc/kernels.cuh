@@ -790,9 +790,17 @@ __device__ __forceinline__ void slice_row(const double* v, uint32_t w, const Col
 #ifndef AMG_PUPD_MINB
 #define AMG_PUPD_MINB 8
 #endif
+// Sweeps / updates that also reduce a dot (the level-0 last post-sweep r^T z, FCG's q^T z): the
+// reduction's accumulator is one more live register across the row loop, and at 32 registers
+// ptxas then serialises the chunk's loads (tools/tma_lab.cu, the EPost1 sweep on 256^3: with the
+// dot, 8 blocks/SM run the 27-point operator 18 % and the 7-point 8 % slower than without; 6 blocks
+// at 40 registers recover it: 6.30 vs 5.42 TB/s and 6.32 vs 6.15 TB/s).  AMG_DOT_MINB: an A/B knob.
+#ifndef AMG_DOT_MINB
+#define AMG_DOT_MINB 6
+#endif
 template <class G, class E>
 struct MinBlocks {
-    static constexpr int v = 8;
+    static constexpr int v = E::kDot ? AMG_DOT_MINB : 8;
 };
 template <>
 struct MinBlocks<GPz, ESpmvDotPz> {

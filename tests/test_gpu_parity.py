@@ -458,3 +458,24 @@ def test_solve_host_batch_equals_single_solves(ctx):
     # pageable buffers: same results
     X2, _ = h.solve_host_batch(B.copy(), rtol=1e-6)
     assert np.array_equal(X2, X)
+
+
+def test_repeated_builds_are_bitwise_identical(ctx):
+    """Builds of the same matrix in one process give the same solve bit for bit (round 2 found a
+    build-to-build race: device buffers zeroed by a synchronous-API memset on the legacy default
+    stream were written by the next kernel on the context's non-blocking stream; ~1 build in 10 of
+    the c5 256^3 analogue then had a corrupt SELL-32-sigma slot map, profiles/r02_race_legacy_stream_fix.txt).
+    The 27-point jump operator at 96^3 takes the SELL-32-sigma path on level 1."""
+    import hashlib
+    import paper_2006_16147_b200 as amg
+    A = jump27(96)
+    b = uniform01(5, A.n_global)
+    bt = torch.tensor(b, device="cuda:0")
+    ref = None
+    for _ in range(4):
+        h = amg.Hierarchy(ctx, A)
+        x, rep = h.solve(bt)
+        got = (rep["iterations"], hashlib.sha1(x.cpu().numpy().tobytes()).hexdigest())
+        ref = ref or got
+        assert got == ref
+        h.close()
