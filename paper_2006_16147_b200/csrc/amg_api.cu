@@ -575,12 +575,24 @@ void launch_mat(Launch& L, const DevMat& M, G g, E e, RedCtx rc, const char* nam
         ~PersistScope() { g_persist_ptr = nullptr; }
     } persist_scope(M);
     if (M.fmt == FMT_SDIA) {
-        const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)k_sdia<G, E>));
-        const int64_t need = ((u1 - u0 - kspan) * 32 + kBlock - 1) / kBlock;
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
-        launch_k(k_sdia<G, E>, grid, kBlock, L.s,
-                 SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor, u0, u1, k0, kspan}, g,
-                 e, rc);
+        auto go = [&](auto kern) {
+            const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)kern));
+            const int64_t need = ((u1 - u0 - kspan) * 32 + kBlock - 1) / kBlock;
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
+            launch_k(kern, grid, kBlock, L.s,
+                     SdiaView{M.sptr, M.offs, M.val, M.nrows, (int32_t)M.ncols, M.shift, M.anchor, u0, u1, k0, kspan},
+                     g, e, rc);
+        };
+        // dot-fused kernels over wide rows: the 40-register instance (kernels.cuh, kDotWideEntries)
+        bool wide = false;
+        // (the q = A p kernels with the fused direction update gather two vectors and stay at 8 blocks:
+        // c5's spmv_dot_pupd ran 0.82 -> 1.21 ms at 6)
+        if constexpr (E::kDot && !std::is_same<G, GPz>::value && !std::is_same<G, GKpz>::value) {
+            static const bool wide_off = std::getenv("AMG_DOT_WIDE_OFF") != nullptr;  // A/B switch
+            wide = !wide_off && M.stored > (int64_t)kDotWideEntries * M.nrows;
+            if (wide) go(k_sdia<G, E, AMG_DOT_MINB>);
+        }
+        if (!wide) go(k_sdia<G, E>);
     } else if (M.fmt == FMT_SELL) {
         const int cap = small_cap(L.h, M, ctx_cap(L.h->ctx, (const void*)k_sell<G, E>));
         const int64_t need = ((u1 - u0 - kspan) * 32 + kBlock - 1) / kBlock;

@@ -790,17 +790,21 @@ __device__ __forceinline__ void slice_row(const double* v, uint32_t w, const Col
 #ifndef AMG_PUPD_MINB
 #define AMG_PUPD_MINB 8
 #endif
-// Sweeps / updates that also reduce a dot (the level-0 last post-sweep r^T z, FCG's q^T z): the
-// reduction's accumulator is one more live register across the row loop, and at 32 registers
-// ptxas then serialises the chunk's loads (tools/tma_lab.cu, the EPost1 sweep on 256^3: with the
-// dot, 8 blocks/SM run the 27-point operator 18 % and the 7-point 8 % slower than without; 6 blocks
-// at 40 registers recover it: 6.30 vs 5.42 TB/s and 6.32 vs 6.15 TB/s).  AMG_DOT_MINB: an A/B knob.
+// SDIA sweeps / updates that also reduce a dot (the level-0 last post-sweep r^T z, FCG's q^T z) over
+// WIDE rows (> kDotWideEntries stored entries per row, the 27-point operators): the reduction's
+// accumulator is one more live register across the row loop, and at 32 registers ptxas then
+// serialises the chunk's loads (tools/tma_lab.cu, the EPost1 sweep on 256^3 27-point: 5.42 TB/s
+// with the dot vs 6.38 without at 8 blocks/SM; 6 blocks at 40 registers: 6.30).  In the library the
+// 7-point operators lose 0.3-2 % with 6 blocks (c4 / c2 / KA1 c2) while c5's post-sweep gains 15 %
+// (0.82 -> 0.70 ms; profiles/r02_ab_dot_minb.txt), so launch_mat picks the 6-block instance for wide
+// operators only.  AMG_DOT_MINB: an A/B knob.
 #ifndef AMG_DOT_MINB
 #define AMG_DOT_MINB 6
 #endif
+constexpr int kDotWideEntries = 16;
 template <class G, class E>
 struct MinBlocks {
-    static constexpr int v = E::kDot ? AMG_DOT_MINB : 8;
+    static constexpr int v = 8;
 };
 template <>
 struct MinBlocks<GPz, ESpmvDotPz> {
@@ -868,8 +872,8 @@ struct SdiaChunk<GPz> {
     static constexpr int v = AMG_SDIA_GPZ_CHUNK;
 };
 
-template <class G, class E>
-__global__ void __launch_bounds__(kBlock, MinBlocks<G, E>::v) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
+template <class G, class E, int MB = MinBlocks<G, E>::v>
+__global__ void __launch_bounds__(kBlock, MB) k_sdia(SdiaView A, G g, E e, RedCtx rc) {
     pdl_begin();
     bind(g);
     bind(e);
