@@ -1071,10 +1071,42 @@ __global__ void __launch_bounds__(kBlock) k_axpy_rr(double* __restrict__ r, cons
     pdl_begin();
     const double alpha = st->alpha;
     double d = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
-        const double ri = r[i] - alpha * q[i];
-        r[i] = ri;
-        d += ri * ri;
+    const int64_t t0 = (int64_t)blockIdx.x * kBlock + threadIdx.x, nt = (int64_t)gridDim.x * kBlock;
+    if (((reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(q)) & 15) == 0) {
+        // 16-byte accesses, two pairs in flight per thread; the odd last element by thread 0
+        double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
+        const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q);
+        const int64_t m = n >> 1;
+        int64_t i = t0;
+        for (; i + nt < m; i += 2 * nt) {
+            const double2 a = r2[i], b = __ldg(q2 + i), c = r2[i + nt], e = __ldg(q2 + i + nt);
+            const double2 u = make_double2(a.x - alpha * b.x, a.y - alpha * b.y);
+            const double2 v = make_double2(c.x - alpha * e.x, c.y - alpha * e.y);
+            r2[i] = u;
+            r2[i + nt] = v;
+            d += u.x * u.x;
+            d += u.y * u.y;
+            d += v.x * v.x;
+            d += v.y * v.y;
+        }
+        if (i < m) {
+            const double2 a = r2[i], b = __ldg(q2 + i);
+            const double2 u = make_double2(a.x - alpha * b.x, a.y - alpha * b.y);
+            r2[i] = u;
+            d += u.x * u.x;
+            d += u.y * u.y;
+        }
+        if ((n & 1) && t0 == 0) {
+            const double ri = r[n - 1] - alpha * q[n - 1];
+            r[n - 1] = ri;
+            d += ri * ri;
+        }
+    } else {
+        for (int64_t i = t0; i < n; i += nt) {
+            const double ri = r[i] - alpha * q[i];
+            r[i] = ri;
+            d += ri * ri;
+        }
     }
     grid_reduce(d, rc);
 }
